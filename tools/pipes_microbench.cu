@@ -1,0 +1,92 @@
+// Integer pipe-rate microbenchmark for sm_100a: the denominators of the
+// round kernel's roofline (SURVEY.md §8d asks to confirm POPC / LOP3 issue
+// rates on the box instead of trusting the cc<=9.0 throughput table).
+//
+// Each kernel runs NCH independent dependency chains per thread of a single
+// instruction class, long enough that issue throughput (not latency) binds.
+// ops/clk/SM = (threads * iters * NCH) / (elapsed_s * f_sm * SMs), with f_sm
+// measured in-kernel from clock64() against the CUDA-event wall time.
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o pipes tools/pipes_microbench.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define NCH 16
+
+__device__ unsigned long long g_sink;
+__device__ long long g_clk[2048];
+
+template <int OP>
+__global__ void pipe_kernel(uint32_t seed, int iters) {
+    uint32_t a[NCH];
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) a[i] = seed * (threadIdx.x + 1) + i * 0x9E3779B9u;
+    uint32_t b = seed ^ 0x5bd1e995u, c = seed * 3u + 1u;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) {
+            if (OP == 0) {        // LOP3: 3-input xor
+                asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[i]) : "r"(b), "r"(c));
+            } else if (OP == 1) { // POPC chain
+                asm volatile("popc.b32 %0, %0;" : "+r"(a[i]));
+            } else if (OP == 2) { // IADD3
+                asm volatile("add.u32 %0, %0, %1;" : "+r"(a[i]) : "r"(b));
+            } else if (OP == 3) { // IMNMX
+                asm volatile("min.u32 %0, %0, %1;" : "+r"(a[i]) : "r"(b));
+            } else if (OP == 4) { // IMAD (fma pipe)
+                asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[i]) : "r"(b), "r"(c));
+            } else if (OP == 5) { // POPC of a 64-bit value (2x POPC + add)
+                uint64_t v = ((uint64_t)a[i] << 32) | b;
+                uint32_t r;
+                asm volatile("popc.b64 %0, %1;" : "=r"(r) : "l"(v));
+                a[i] = r;
+            }
+        }
+    }
+    long long t1 = clock64();
+    uint32_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) acc ^= a[i];
+    if (acc == 0xFFFFFFFFu) g_sink = acc;
+    if (threadIdx.x == 0 && blockIdx.x < 2048) g_clk[blockIdx.x] = t1 - t0;
+}
+
+template <int OP>
+void run(const char* name, int sms) {
+    int threads = 512, blocks = sms * 4, iters = 4096;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    pipe_kernel<OP><<<blocks, threads>>>(1u, 64); // warm-up
+    cudaDeviceSynchronize();
+    cudaEventRecord(e0);
+    pipe_kernel<OP><<<blocks, threads>>>(7u, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
+    long long clk[1];
+    cudaMemcpyFromSymbol(clk, g_clk, sizeof(long long));
+    double f_mhz = clk[0] / (ms * 1e3); // lower bound on clock (block 0 ran ~whole kernel)
+    double ops = (double)threads * blocks * iters * NCH;
+    double per_clk_sm = ops / (ms * 1e-3) / (f_mhz * 1e6) / sms;
+    printf("{\"op\": \"%s\", \"ms\": %.3f, \"f_mhz_est\": %.0f, \"ops_per_clk_per_sm\": %.2f, \"Gops\": %.1f}\n",
+           name, ms, f_mhz, per_clk_sm, ops / (ms * 1e-3) / 1e9);
+}
+
+int main() {
+    cudaDeviceProp p;
+    cudaGetDeviceProperties(&p, 0);
+    int clk_khz = 0;
+    cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+    printf("{\"device\": \"%s\", \"sms\": %d, \"cc\": \"%d.%d\", \"clock_khz_attr\": %d}\n",
+           p.name, p.multiProcessorCount, p.major, p.minor, clk_khz);
+    int sms = p.multiProcessorCount;
+    run<0>("lop3", sms);
+    run<1>("popc32", sms);
+    run<2>("iadd", sms);
+    run<3>("imnmx", sms);
+    run<4>("imad", sms);
+    run<5>("popc64", sms);
+    return 0;
+}
