@@ -1,0 +1,230 @@
+/*
+ * mdg — B200-native Brouwer–Zimmermann minimum-distance engine: C ABI.
+ *
+ * The reference (arXiv 1911.08963, /root/reference/proj) is a C++20 library
+ * with no FFI; its seam for this path is the round runner
+ *   using RoundRunner = std::function<uint32_t(uint32_t gamma_index, uint32_t g, RoundStats&)>;
+ *   EngineResult run_bz_loop(const GammaSet&, Bounds, const RoundRunner&);
+ * (proj/include/mindist/engines.hpp:151-152, proj/src/engines.cpp:447-476)
+ * and its front door  md::min_weight(const BitMatrix&, const EngineConfig&)
+ * (engines.hpp:164-166, engines.cpp:617-648). Each entry point below names the
+ * reference interface it replaces. Plain pointers and sizes only.
+ *
+ * Bit layout of every matrix crossing this boundary: row-major, W = ceil(n/64)
+ * u64 words per row, bit i of a row in word i/64 at bit position i%64
+ * (LSB-first — the same bit order as the reference's u32 words,
+ * f2core.hpp:9-12), padding bits zero.
+ *
+ * Status codes: 0 OK; MDG_EINVAL (-2) bad argument / input (the reference's
+ * std::invalid_argument family, CLI exit 2); MDG_EOVERFLOW (-3) 64-bit
+ * overflow (std::overflow_error, exit 2); MDG_ECUDA (-4) device failure and
+ * MDG_EINTERNAL (-1) anything else (std::exception, exit 1). The message of
+ * the last failure on the calling thread: mdg_last_error().
+ */
+#ifndef MDG_H
+#define MDG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MDG_OK 0
+#define MDG_EINTERNAL (-1)
+#define MDG_EINVAL (-2)
+#define MDG_EOVERFLOW (-3)
+#define MDG_ECUDA (-4)
+
+/* Round kernel selector. MDG_KERNEL_TAB: pivot-split Cartesian enumeration
+ * (saved suffix table in HBM x prefix chunk in shared memory; the default).
+ * MDG_KERNEL_RD: per-thread revolving-door walk of a contiguous rank range. */
+#define MDG_KERNEL_TAB 0
+#define MDG_KERNEL_RD 1
+
+const char* mdg_last_error(void);
+const char* mdg_version(void);
+
+/* ---------------------------------------------------------------- device */
+typedef struct mdg_ctx mdg_ctx;
+
+/* Open a device context (one CUDA stream, device buffers). Replaces the
+ * reference's per-engine state (SavedAdditions tables, engines.hpp:94-125). */
+int mdg_open(int device, mdg_ctx** out);
+void mdg_close(mdg_ctx* ctx);
+
+/* Upload m Gamma matrices (m*k rows of W words). ranks[j] = rank of block j
+ * (GammaSet::ranks, gamma.hpp:14-24): Gamma j carries the identity on rows
+ * [0, ranks[j]) in columns [j*k, j*k + ranks[j]), which the kernels elide
+ * (weight = |S ∩ [0,ranks[j])| + weight of the other columns). ranks == NULL
+ * loads raw matrices with no identity structure (config 5). */
+int mdg_load_gammas(mdg_ctx* ctx, uint32_t m, uint32_t k, uint32_t n, const uint64_t* rows,
+                    const uint32_t* ranks);
+
+typedef struct {
+    uint32_t min_weight;      /* UINT32_MAX when nothing was evaluated */
+    uint32_t stopped_early;   /* 1 when the early-exit bound fired */
+    uint64_t argmin_key;      /* opaque (weight << 40 | task); input of mdg_round_witness */
+    uint64_t combinations;    /* C(k,c): the reference's RoundStats.combinations */
+    uint64_t evaluated;       /* codewords actually evaluated on this device */
+    uint64_t task_lo, task_hi;/* task range this call covered (partition units) */
+    double device_ms;         /* CUDA-event time of the round's kernels */
+} mdg_round_out;
+
+/* One (c, Gamma_j) round: min weight of all XOR-sums of c rows of Gamma_j.
+ * Replaces round_saved / round_stack / round_saved_parallel
+ * (engines.hpp:140-146, engines.cpp:175-443) behind RoundRunner
+ * (engines.hpp:151). stop_at: stop as soon as a weight <= stop_at is found
+ * (pass L_prev of the level loop; 0 = enumerate everything). */
+int mdg_round(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t stop_at, mdg_round_out* out);
+
+/* Number of partition tasks of round (j, c) and the same round restricted to
+ * tasks [task_lo, task_hi) — the unit the multi-GPU path splits across ranks
+ * (parallel.cpp:72-88 prefix tasks / engines.cpp:508-557 contiguous blocks). */
+int mdg_round_tasks(mdg_ctx* ctx, uint32_t j, uint32_t c, uint64_t* n_tasks);
+int mdg_round_range(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t stop_at, uint64_t task_lo,
+                    uint64_t task_hi, mdg_round_out* out);
+
+/* Full weight histogram of round (j, c) (no early exit): hist[0..n] (config 5;
+ * no reference counterpart). Returns the min in out. */
+int mdg_round_hist(mdg_ctx* ctx, uint32_t j, uint32_t c, uint64_t* hist, mdg_round_out* out);
+
+/* Combination (c sorted row indices) achieving out->min_weight in the task
+ * named by out->argmin_key — the witness of that round. */
+int mdg_round_witness(mdg_ctx* ctx, uint32_t j, uint32_t c, const mdg_round_out* out,
+                      uint32_t* idx);
+
+/* Kernel selection and launch geometry (0 = keep the current value). */
+int mdg_set_kernel(mdg_ctx* ctx, int kernel);
+
+/* ----------------------------------------------------------- host objects */
+typedef struct mdg_gset mdg_gset;   /* GammaSet (gamma.hpp:14-24) */
+
+/* best_gamma_over_permutations(row_basis(G), trials, seed) (gamma.cpp:77-94,
+ * f2core.cpp:92-97): rank-deficient G is row-reduced first, as min_weight
+ * does (engines.cpp:619). */
+int mdg_gset_build(const uint64_t* G, uint32_t k, uint32_t n, uint32_t trials, uint64_t seed,
+                   mdg_gset** out);
+/* compute_gamma_matrices on a full-rank G (gamma.cpp:32-75). */
+int mdg_gset_compute(const uint64_t* G, uint32_t k, uint32_t n, mdg_gset** out);
+void mdg_gset_free(mdg_gset* gs);
+/* m, k (effective), n, k_last */
+int mdg_gset_info(const mdg_gset* gs, uint32_t* m, uint32_t* k, uint32_t* n, uint32_t* k_last);
+/* rows of Gamma j (k*W words), ranks (m), column_perm (n), FNV-1a hash of Gamma j */
+int mdg_gset_gamma(const mdg_gset* gs, uint32_t j, uint64_t* rows);
+int mdg_gset_ranks(const mdg_gset* gs, uint32_t* ranks);
+int mdg_gset_perm(const mdg_gset* gs, uint32_t* perm);
+uint64_t mdg_gset_hash(const mdg_gset* gs, uint32_t j);
+int mdg_load_gset(mdg_ctx* ctx, const mdg_gset* gs);
+
+/* gamma.cpp:96-100 and :102-106 */
+uint32_t mdg_lower_bound(uint32_t m, uint32_t g, uint32_t k, uint32_t k_last);
+uint32_t mdg_singleton_upper(uint32_t n, uint32_t k);
+
+/* -------------------------------------------------------------- the loop */
+typedef struct { uint32_t c, j, w, U_after; } mdg_round_rec;
+typedef struct { uint32_t c, L_after, U_after, pad; } mdg_level_rec;
+
+/* RoundRunner as a C callback (engines.hpp:151): return 0 and set *w, or a
+ * status. stop_at is the loop's current lower bound (early-exit hint). */
+typedef int (*mdg_round_fn)(void* user, uint32_t j, uint32_t c, uint32_t stop_at, uint32_t* w);
+
+typedef struct mdg_run mdg_run;     /* result of one BZ run */
+
+/* Cross-rank reduction: replace keys[0..count) by their elementwise minimum over ranks. */
+typedef int (*mdg_reduce_fn)(void* user, uint64_t* keys, uint32_t count); /* in-place min */
+
+/* run_bz_loop (engines.cpp:447-476) with the reference's exact semantics,
+ * a level cap (0 = none) and the round trace, driving a caller-supplied
+ * round. Used for host-logic tests and custom engines. */
+int mdg_bz_loop_cb(const mdg_gset* gs, uint32_t lower, uint32_t upper, uint32_t level_cap,
+                   mdg_round_fn fn, void* user, mdg_run** out);
+
+/* Front door: min_weight(G, cfg) with the GPU engine (engines.cpp:617-648):
+ * row_basis -> Gamma search -> Singleton U -> level loop on the device ->
+ * witness. ctx == NULL opens a context on device 0 for the call. */
+typedef struct {
+    uint32_t trials;      /* permutation_trials, default 10 (engines.hpp:64) */
+    uint64_t seed;        /* EngineConfig.seed */
+    uint32_t level_cap;   /* 0 = run to termination */
+    int kernel;           /* MDG_KERNEL_TAB | MDG_KERNEL_RD */
+    int want_witness;     /* 1 = reconstruct and verify a minimum-weight codeword */
+} mdg_config;
+void mdg_config_default(mdg_config* cfg);
+int mdg_min_weight(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n, const mdg_config* cfg,
+                   mdg_run** out);
+
+/* The level loop over the Gamma set already loaded into ctx (mdg_load_gset):
+ * the device-resident variant of the front door (no Gamma search, no upload). */
+int mdg_bz_loop_device(mdg_ctx* ctx, const mdg_gset* gs, const mdg_config* cfg, mdg_run** out);
+int mdg_bz_loop_device_dist(mdg_ctx* ctx, const mdg_gset* gs, const mdg_config* cfg,
+                            uint32_t rank, uint32_t world, mdg_reduce_fn reduce_min, void* user,
+                            mdg_run** out);
+
+/* CUDA-event timer on the context's stream (includes host gaps between
+ * launches), and the context's counters: kernel launches, H2D / D2H bytes. */
+int mdg_timer_start(mdg_ctx* ctx);
+int mdg_timer_stop(mdg_ctx* ctx, double* ms);
+int mdg_ctx_counters(mdg_ctx* ctx, uint64_t* launches, uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+int mdg_device_info(mdg_ctx* ctx, int* sm_count, int* device);
+
+/* Multi-GPU (one process per GPU): every rank runs the same
+ * host loop; each round's task range is split contiguously across ranks and
+ * the per-round minimum key is combined with reduce_min (an NCCL
+ * allreduce(min) in mdg_dist_*, or any callback). */
+int mdg_min_weight_dist(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n,
+                        const mdg_config* cfg, uint32_t rank, uint32_t world,
+                        mdg_reduce_fn reduce_min, void* user, mdg_run** out);
+/* NCCL reducer owned by the context (libnccl.so.2 loaded at runtime). */
+int mdg_nccl_unique_id(uint8_t id[128]);
+int mdg_nccl_init(mdg_ctx* ctx, const uint8_t id[128], uint32_t rank, uint32_t world);
+int mdg_nccl_reduce_min(void* ctx, uint64_t* keys, uint32_t count); /* mdg_reduce_fn; user = ctx */
+
+/* Result accessors. */
+typedef struct {
+    uint32_t d;              /* U at termination, or at the level cap */
+    uint32_t capped;         /* 1 when level_cap stopped the loop (d = upper bound) */
+    uint32_t n, k, m, k_last, g_final;
+    uint32_t n_rounds, n_levels;
+    uint32_t witness_ok;     /* 1: witness weight == d and it lies in the code */
+    uint64_t combinations;   /* sum of C(k,c) over executed rounds (reference counter) */
+    uint64_t evaluated;      /* codewords evaluated on the device(s) */
+    uint64_t row_additions;  /* one row XOR per evaluated codeword */
+    double wall_seconds;     /* whole call */
+    double device_seconds;   /* sum of round kernel times */
+    double gamma_seconds;    /* Gamma search on the host */
+    double loop_seconds;     /* CUDA-event time of the whole level loop (host gaps included) */
+    uint64_t launches;       /* kernels launched by the call */
+    uint64_t h2d_bytes, d2h_bytes; /* host<->device traffic of the call */
+} mdg_run_info;
+int mdg_run_info_get(const mdg_run* r, mdg_run_info* info);
+int mdg_run_rounds(const mdg_run* r, mdg_round_rec* out);     /* n_rounds entries */
+int mdg_run_levels(const mdg_run* r, mdg_level_rec* out);     /* n_levels entries */
+int mdg_run_witness(const mdg_run* r, uint64_t* row);         /* W words, original columns */
+int mdg_run_perm(const mdg_run* r, uint32_t* perm);           /* column_perm (n) */
+uint64_t mdg_run_gamma_hash(const mdg_run* r, uint32_t j);
+/* The reference CLI's JSON record (cli.cpp:223-238) plus the new keys. */
+long mdg_run_json(const mdg_run* r, char* buf, size_t cap);
+void mdg_run_free(mdg_run* r);
+
+/* ----------------------------------------------------------- misc / I/O */
+/* parse_matrix (io.cpp:33-73): rows_out NULL to query k, n. Errors carry
+ * "line L, column C: ..." like ParseError (io.cpp:8-12). */
+int mdg_parse_matrix(const char* text, uint32_t* k, uint32_t* n, uint64_t* rows_out);
+long mdg_serialize_matrix(const uint64_t* rows, uint32_t k, uint32_t n, char* buf, size_t cap);
+/* Config input generator: std::mt19937_64(seed), one draw
+ * per bit, bit = draw & 1, row-major; identity != 0 gives G = (I_k | A). */
+int mdg_gen_matrix(uint32_t n, uint32_t k, uint64_t seed, int identity, uint64_t* rows);
+uint32_t mdg_rank(const uint64_t* rows, uint32_t k, uint32_t n);
+uint64_t mdg_hash_rows(const uint64_t* rows, uint32_t k, uint32_t n);
+/* Exact binomial (enumeration.cpp:9-20); returns MDG_EOVERFLOW past 64 bits. */
+int mdg_binomial(uint32_t p, uint32_t q, uint64_t* out);
+/* Revolving-door order (Knuth 7.2.1.3 Alg. R): rank <-> combination. */
+int mdg_rd_unrank(uint32_t c, uint64_t rank, uint32_t* idx);
+uint64_t mdg_rd_rank(uint32_t c, const uint32_t* idx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MDG_H */

@@ -87,6 +87,13 @@ def rank(rows: np.ndarray, n: int) -> int:
     return int(lib().mdo_rank(rows, rows.shape[0], n))
 
 
+def row_basis(rows: np.ndarray, n: int) -> np.ndarray:
+    rows = np.ascontiguousarray(rows, dtype=np.uint64)
+    out = np.zeros_like(rows)
+    r = lib().mdo_row_basis(rows, rows.shape[0], n, out)
+    return out[:r]
+
+
 def round_min(rows: np.ndarray, n: int, c: int) -> tuple[int, int]:
     rows = np.ascontiguousarray(rows, dtype=np.uint64)
     combos = C.c_uint64(0)

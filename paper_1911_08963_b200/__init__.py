@@ -1,0 +1,592 @@
+"""B200-native Brouwer–Zimmermann minimum-distance engine (arXiv 1911.08963 hot path).
+
+Python mirror of the reference's C++ interface for this path, over the C ABI
+``include/mdg.h`` of ``lib/libmdg.so`` (ctypes). Names follow the reference
+(``md::min_weight``, ``GammaSet``, ``run_bz_loop``, ``round_*``,
+``lower_bound``, ``singleton_upper``, ``parse_matrix``); see the per-function
+docstrings for the reference file:line each mirrors.
+
+Matrices are numpy ``uint64`` arrays of shape (k, W), W = ceil(n/64), bit i of
+a row in word i//64 at bit position i%64 (LSB-first, the reference's bit order).
+
+There is no CPU fallback: every compute call goes to the CUDA engine, and
+importing this package raises if ``libmdg.so`` is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+__all__ = [
+    "MdgError", "InvalidArgument", "OverflowError_", "CudaFailure", "lib", "Device", "GammaSet",
+    "RoundOut", "RunResult", "min_weight", "min_weight_dist", "run_bz_loop", "lower_bound",
+    "singleton_upper", "parse_matrix", "serialize_matrix", "gen_matrix", "binomial",
+    "rd_unrank", "rd_rank", "hash_rows", "rank_of", "words", "KERNEL_TAB", "KERNEL_RD",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libmdg.so")
+KERNEL_TAB, KERNEL_RD = 0, 1
+
+
+class MdgError(RuntimeError):
+    """Internal / device failure (the reference's CLI exit code 1)."""
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument family (ParseError, caps, bad config) — exit code 2."""
+
+
+class OverflowError_(OverflowError):
+    """std::overflow_error (binomial beyond 64 bits) — exit code 2."""
+
+
+class CudaFailure(MdgError):
+    """CUDA runtime failure."""
+
+
+def words(n: int) -> int:
+    return (n + 63) // 64
+
+
+u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+
+
+class _RoundOut(C.Structure):
+    _fields_ = [("min_weight", C.c_uint32), ("stopped_early", C.c_uint32),
+                ("argmin_key", C.c_uint64), ("combinations", C.c_uint64),
+                ("evaluated", C.c_uint64), ("task_lo", C.c_uint64), ("task_hi", C.c_uint64),
+                ("device_ms", C.c_double)]
+
+
+class _Config(C.Structure):
+    _fields_ = [("trials", C.c_uint32), ("seed", C.c_uint64), ("level_cap", C.c_uint32),
+                ("kernel", C.c_int), ("want_witness", C.c_int)]
+
+
+class _RunInfo(C.Structure):
+    _fields_ = [(f, C.c_uint32) for f in ("d", "capped", "n", "k", "m", "k_last", "g_final",
+                                          "n_rounds", "n_levels", "witness_ok")] + \
+               [("combinations", C.c_uint64), ("evaluated", C.c_uint64),
+                ("row_additions", C.c_uint64), ("wall_seconds", C.c_double),
+                ("device_seconds", C.c_double), ("gamma_seconds", C.c_double),
+                ("loop_seconds", C.c_double), ("launches", C.c_uint64), ("h2d_bytes", C.c_uint64),
+                ("d2h_bytes", C.c_uint64)]
+
+
+class _RoundRec(C.Structure):
+    _fields_ = [("c", C.c_uint32), ("j", C.c_uint32), ("w", C.c_uint32), ("U_after", C.c_uint32)]
+
+
+class _LevelRec(C.Structure):
+    _fields_ = [("c", C.c_uint32), ("L_after", C.c_uint32), ("U_after", C.c_uint32),
+                ("pad", C.c_uint32)]
+
+
+ROUND_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32,
+                       C.POINTER(C.c_uint32))
+REDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_uint32)
+
+_LIB = None
+
+# exported symbols of include/mdg.h (tests check the .so exports exactly these)
+SYMBOLS = {
+    "mdg_last_error": (C.c_char_p, []),
+    "mdg_version": (C.c_char_p, []),
+    "mdg_open": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "mdg_close": (None, [C.c_void_p]),
+    "mdg_load_gammas": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, u64p, C.c_void_p]),
+    "mdg_round": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(_RoundOut)]),
+    "mdg_round_tasks": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64)]),
+    "mdg_round_range": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
+                                  C.c_uint64, C.POINTER(_RoundOut)]),
+    "mdg_round_hist": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, u64p, C.POINTER(_RoundOut)]),
+    "mdg_round_witness": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(_RoundOut), u32p]),
+    "mdg_set_kernel": (C.c_int, [C.c_void_p, C.c_int]),
+    "mdg_gset_build": (C.c_int, [u64p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
+                                 C.POINTER(C.c_void_p)]),
+    "mdg_gset_compute": (C.c_int, [u64p, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "mdg_gset_free": (None, [C.c_void_p]),
+    "mdg_gset_info": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_uint32)] * 4),
+    "mdg_gset_gamma": (C.c_int, [C.c_void_p, C.c_uint32, u64p]),
+    "mdg_gset_ranks": (C.c_int, [C.c_void_p, u32p]),
+    "mdg_gset_perm": (C.c_int, [C.c_void_p, u32p]),
+    "mdg_gset_hash": (C.c_uint64, [C.c_void_p, C.c_uint32]),
+    "mdg_load_gset": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "mdg_lower_bound": (C.c_uint32, [C.c_uint32] * 4),
+    "mdg_singleton_upper": (C.c_uint32, [C.c_uint32] * 2),
+    "mdg_bz_loop_cb": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, ROUND_FN,
+                                 C.c_void_p, C.POINTER(C.c_void_p)]),
+    "mdg_config_default": (None, [C.POINTER(_Config)]),
+    "mdg_min_weight": (C.c_int, [C.c_void_p, u64p, C.c_uint32, C.c_uint32, C.POINTER(_Config),
+                                 C.POINTER(C.c_void_p)]),
+    "mdg_min_weight_dist": (C.c_int, [C.c_void_p, u64p, C.c_uint32, C.c_uint32,
+                                      C.POINTER(_Config), C.c_uint32, C.c_uint32, C.c_void_p,
+                                      C.c_void_p, C.POINTER(C.c_void_p)]),
+    "mdg_bz_loop_device": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(_Config),
+                                     C.POINTER(C.c_void_p)]),
+    "mdg_bz_loop_device_dist": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(_Config), C.c_uint32,
+                                          C.c_uint32, C.c_void_p, C.c_void_p,
+                                          C.POINTER(C.c_void_p)]),
+    "mdg_timer_start": (C.c_int, [C.c_void_p]),
+    "mdg_timer_stop": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
+    "mdg_ctx_counters": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_uint64)] * 3),
+    "mdg_device_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "mdg_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "mdg_nccl_init": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint32, C.c_uint32]),
+    "mdg_nccl_reduce_min": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_uint32]),
+    "mdg_run_info_get": (C.c_int, [C.c_void_p, C.POINTER(_RunInfo)]),
+    "mdg_run_rounds": (C.c_int, [C.c_void_p, C.POINTER(_RoundRec)]),
+    "mdg_run_levels": (C.c_int, [C.c_void_p, C.POINTER(_LevelRec)]),
+    "mdg_run_witness": (C.c_int, [C.c_void_p, u64p]),
+    "mdg_run_perm": (C.c_int, [C.c_void_p, u32p]),
+    "mdg_run_gamma_hash": (C.c_uint64, [C.c_void_p, C.c_uint32]),
+    "mdg_run_json": (C.c_long, [C.c_void_p, C.c_char_p, C.c_size_t]),
+    "mdg_run_free": (None, [C.c_void_p]),
+    "mdg_parse_matrix": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                   C.c_void_p]),
+    "mdg_serialize_matrix": (C.c_long, [u64p, C.c_uint32, C.c_uint32, C.c_char_p, C.c_size_t]),
+    "mdg_gen_matrix": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint64, C.c_int, u64p]),
+    "mdg_rank": (C.c_uint32, [u64p, C.c_uint32, C.c_uint32]),
+    "mdg_hash_rows": (C.c_uint64, [u64p, C.c_uint32, C.c_uint32]),
+    "mdg_binomial": (C.c_int, [C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64)]),
+    "mdg_rd_unrank": (C.c_int, [C.c_uint32, C.c_uint64, u32p]),
+    "mdg_rd_rank": (C.c_uint64, [C.c_uint32, u32p]),
+}
+
+
+def lib():
+    """Load lib/libmdg.so (built by ``__graft_entry__.build()``); raise if absent."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with "
+                              "`python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SYMBOLS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def _check(rc: int):
+    if rc == 0:
+        return
+    msg = lib().mdg_last_error().decode(errors="replace")
+    if rc == -2:
+        raise InvalidArgument(msg)
+    if rc == -3:
+        raise OverflowError_(msg)
+    if rc == -4:
+        raise CudaFailure(msg)
+    raise MdgError(msg)
+
+
+def _rows(G: np.ndarray) -> np.ndarray:
+    G = np.ascontiguousarray(G, dtype=np.uint64)
+    if G.ndim != 2:
+        raise InvalidArgument("matrix must be a 2-D uint64 array (k, W)")
+    return G
+
+
+# ----------------------------------------------------------------- helpers
+def lower_bound(m: int, g: int, k: int, k_last: int) -> int:
+    """gamma.cpp:96-100: (m-1)(g+1) + max(0, g+1-k+k_last)."""
+    return int(lib().mdg_lower_bound(m, g, k, k_last))
+
+
+def singleton_upper(n: int, k: int) -> int:
+    """gamma.cpp:102-106: n - k + 1; raises on n < k or k < 1."""
+    if k < 1 or n < k:
+        raise InvalidArgument("singleton_upper: need n >= k >= 1")
+    return int(lib().mdg_singleton_upper(n, k))
+
+
+def binomial(p: int, q: int) -> int:
+    """enumeration.cpp:9-20 (raises OverflowError_ past 64 bits)."""
+    out = C.c_uint64(0)
+    _check(lib().mdg_binomial(p, q, C.byref(out)))
+    return int(out.value)
+
+
+def rd_unrank(c: int, rank: int) -> list:
+    idx = np.zeros(c, dtype=np.uint32)
+    _check(lib().mdg_rd_unrank(c, rank, idx))
+    return [int(x) for x in idx]
+
+
+def rd_rank(idx) -> int:
+    a = np.ascontiguousarray(idx, dtype=np.uint32)
+    return int(lib().mdg_rd_rank(len(a), a))
+
+
+def parse_matrix(text: str) -> tuple[np.ndarray, int]:
+    """io.cpp:33-73 — returns (rows, n); raises InvalidArgument('line L, column C: ...')."""
+    k, n = C.c_uint32(0), C.c_uint32(0)
+    b = text.encode()
+    _check(lib().mdg_parse_matrix(b, C.byref(k), C.byref(n), None))
+    rows = np.zeros((k.value, words(n.value)), dtype=np.uint64)
+    _check(lib().mdg_parse_matrix(b, None, None, rows.ctypes.data))
+    return rows, int(n.value)
+
+
+def serialize_matrix(rows: np.ndarray, n: int) -> str:
+    """io.cpp:81-88."""
+    rows = _rows(rows)
+    cap = rows.shape[0] * (n + 1) + 64
+    buf = C.create_string_buffer(cap)
+    ln = lib().mdg_serialize_matrix(rows, rows.shape[0], n, buf, cap)
+    if ln < 0:
+        _check(int(ln))
+    return buf.value.decode()
+
+
+def gen_matrix(n: int, k: int, seed: int, identity: bool = True) -> np.ndarray:
+    """SURVEY.md §8d input generator: std::mt19937_64(seed), bit = draw & 1, row-major."""
+    out = np.zeros((k, words(n)), dtype=np.uint64)
+    _check(lib().mdg_gen_matrix(n, k, seed, 1 if identity else 0, out))
+    return out
+
+
+def rank_of(rows: np.ndarray, n: int) -> int:
+    rows = _rows(rows)
+    return int(lib().mdg_rank(rows, rows.shape[0], n))
+
+
+def hash_rows(rows: np.ndarray, n: int) -> str:
+    rows = _rows(rows)
+    return "%016x" % lib().mdg_hash_rows(rows, rows.shape[0], n)
+
+
+# --------------------------------------------------------------- GammaSet
+class GammaSet:
+    """gamma.hpp:14-24. ``GammaSet.build`` = best_gamma_over_permutations(row_basis(G))."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle)
+        m, k, n, kl = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+        _check(lib().mdg_gset_info(self._h, C.byref(m), C.byref(k), C.byref(n), C.byref(kl)))
+        self.m, self.k, self.n, self.k_last = int(m.value), int(k.value), int(n.value), int(kl.value)
+
+    @classmethod
+    def build(cls, G: np.ndarray, n: int, trials: int = 10, seed: int = 0) -> "GammaSet":
+        """gamma.cpp:77-94 over row_basis(G) (f2core.cpp:92-97)."""
+        G = _rows(G)
+        h = C.c_void_p()
+        _check(lib().mdg_gset_build(G, G.shape[0], n, trials, seed, C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def compute(cls, G: np.ndarray, n: int) -> "GammaSet":
+        """gamma.cpp:32-75 (identity permutation only)."""
+        G = _rows(G)
+        h = C.c_void_p()
+        _check(lib().mdg_gset_compute(G, G.shape[0], n, C.byref(h)))
+        return cls(h.value)
+
+    def gamma(self, j: int) -> np.ndarray:
+        out = np.zeros((self.k, words(self.n)), dtype=np.uint64)
+        _check(lib().mdg_gset_gamma(self._h, j, out))
+        return out
+
+    @property
+    def gammas(self) -> np.ndarray:
+        return np.stack([self.gamma(j) for j in range(self.m)])
+
+    @property
+    def ranks(self) -> list:
+        out = np.zeros(self.m, dtype=np.uint32)
+        _check(lib().mdg_gset_ranks(self._h, out))
+        return [int(x) for x in out]
+
+    @property
+    def column_perm(self) -> list:
+        out = np.zeros(self.n, dtype=np.uint32)
+        _check(lib().mdg_gset_perm(self._h, out))
+        return [int(x) for x in out]
+
+    def hash(self, j: int) -> str:
+        return "%016x" % lib().mdg_gset_hash(self._h, j)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value and _LIB is not None:
+            _LIB.mdg_gset_free(self._h)
+            self._h = C.c_void_p()
+
+
+# ------------------------------------------------------------------ device
+@dataclass
+class RoundOut:
+    min_weight: int
+    stopped_early: bool
+    argmin_key: int
+    combinations: int
+    evaluated: int
+    task_lo: int
+    task_hi: int
+    device_ms: float
+    _raw: object = field(default=None, repr=False)
+
+
+def _round_out(o: _RoundOut) -> RoundOut:
+    raw = _RoundOut()
+    C.pointer(raw)[0] = o
+    return RoundOut(int(o.min_weight), bool(o.stopped_early), int(o.argmin_key),
+                    int(o.combinations), int(o.evaluated), int(o.task_lo), int(o.task_hi),
+                    float(o.device_ms), raw)
+
+
+class Device:
+    """A CUDA context of the engine (mdg_open). Rounds mirror round_* (engines.hpp:140-146)."""
+
+    def __init__(self, device: int = 0):
+        self._h = C.c_void_p()
+        _check(lib().mdg_open(device, C.byref(self._h)))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h and self._h.value:
+            lib().mdg_close(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load_gammas(self, gammas: np.ndarray, n: int, ranks: Optional[list] = None):
+        """mdg_load_gammas: gammas (m, k, W); ranks None = raw matrices (no identity elision)."""
+        g = np.ascontiguousarray(gammas, dtype=np.uint64)
+        if g.ndim == 2:
+            g = g[None]
+        m, k = g.shape[0], g.shape[1]
+        flat = g.reshape(-1)
+        r = None if ranks is None else np.ascontiguousarray(ranks, dtype=np.uint32)
+        _check(lib().mdg_load_gammas(self._h, m, k, n, flat, None if r is None else r.ctypes.data))
+        self._keep = r
+
+    def load_gset(self, gs: GammaSet):
+        _check(lib().mdg_load_gset(self._h, gs._h))
+
+    def set_kernel(self, kernel: int):
+        _check(lib().mdg_set_kernel(self._h, kernel))
+
+    def round(self, j: int, c: int, stop_at: int = 0) -> RoundOut:
+        o = _RoundOut()
+        _check(lib().mdg_round(self._h, j, c, stop_at, C.byref(o)))
+        return _round_out(o)
+
+    def tasks(self, j: int, c: int) -> int:
+        t = C.c_uint64(0)
+        _check(lib().mdg_round_tasks(self._h, j, c, C.byref(t)))
+        return int(t.value)
+
+    def round_range(self, j: int, c: int, task_lo: int, task_hi: int, stop_at: int = 0) -> RoundOut:
+        o = _RoundOut()
+        _check(lib().mdg_round_range(self._h, j, c, stop_at, task_lo, task_hi, C.byref(o)))
+        return _round_out(o)
+
+    def round_hist(self, j: int, c: int, n: int) -> tuple[RoundOut, np.ndarray]:
+        hist = np.zeros(n + 1, dtype=np.uint64)
+        o = _RoundOut()
+        _check(lib().mdg_round_hist(self._h, j, c, hist, C.byref(o)))
+        return _round_out(o), hist
+
+    def round_witness(self, j: int, c: int, out: RoundOut) -> list:
+        idx = np.zeros(c, dtype=np.uint32)
+        _check(lib().mdg_round_witness(self._h, j, c, C.byref(out._raw), idx))
+        return [int(x) for x in idx]
+
+    def timer_start(self):
+        _check(lib().mdg_timer_start(self._h))
+
+    def timer_stop(self) -> float:
+        """Milliseconds on the context's stream since timer_start (CUDA events)."""
+        ms = C.c_double(0)
+        _check(lib().mdg_timer_stop(self._h, C.byref(ms)))
+        return float(ms.value)
+
+    def counters(self) -> dict:
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib().mdg_ctx_counters(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"launches": int(a.value), "h2d_bytes": int(b.value), "d2h_bytes": int(c.value)}
+
+    def info(self) -> dict:
+        sms, dev = C.c_int(), C.c_int()
+        _check(lib().mdg_device_info(self._h, C.byref(sms), C.byref(dev)))
+        return {"sm_count": int(sms.value), "device": int(dev.value)}
+
+    def bz_loop(self, gs: "GammaSet", level_cap: int = 0, kernel: int = KERNEL_TAB,
+                witness: bool = True, rank: int = 0, world: int = 1,
+                reduce_min: Callable | str | None = None) -> "RunResult":
+        """run_bz_loop on the device over the Gamma set loaded with load_gset (no search,
+        no upload): the device-resident level loop (+ witness)."""
+        cfg = _config(0, 0, level_cap, kernel, witness)
+        h = C.c_void_p()
+        if world == 1:
+            _check(lib().mdg_bz_loop_device(self._h, gs._h, C.byref(cfg), C.byref(h)))
+        else:
+            fn, user, keep = _reducer(reduce_min, self)
+            _check(lib().mdg_bz_loop_device_dist(self._h, gs._h, C.byref(cfg), rank, world, fn,
+                                                 user, C.byref(h)))
+            del keep
+        return _collect(h)
+
+    def nccl_init(self, uid: bytes, rank: int, world: int):
+        _check(lib().mdg_nccl_init(self._h, uid, rank, world))
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().mdg_nccl_unique_id(buf))
+    return buf.raw
+
+
+# ------------------------------------------------------------------ runs
+@dataclass
+class RunResult:
+    d: int
+    capped: bool
+    n: int
+    k: int
+    m: int
+    k_last: int
+    g_final: int
+    witness_ok: bool
+    combinations: int
+    evaluated: int
+    row_additions: int
+    wall_seconds: float
+    device_seconds: float
+    gamma_seconds: float
+    loop_seconds: float
+    launches: int
+    h2d_bytes: int
+    d2h_bytes: int
+    rounds: list            # [c, j, w, U_after]
+    levels: list            # [c, L_after, U_after]
+    column_perm: list
+    gamma_hash: list
+    witness: Optional[np.ndarray]
+    json: str
+
+
+def _collect(h) -> RunResult:
+    L = lib()
+    info = _RunInfo()
+    _check(L.mdg_run_info_get(h, C.byref(info)))
+    rr = (_RoundRec * max(1, info.n_rounds))()
+    ll = (_LevelRec * max(1, info.n_levels))()
+    _check(L.mdg_run_rounds(h, rr))
+    _check(L.mdg_run_levels(h, ll))
+    perm = np.zeros(max(1, info.n), dtype=np.uint32)
+    _check(L.mdg_run_perm(h, perm))
+    wit = np.zeros(words(info.n), dtype=np.uint64)
+    has_w = L.mdg_run_witness(h, wit) == 0
+    cap = 1 << 16
+    while True:
+        buf = C.create_string_buffer(cap)
+        ln = L.mdg_run_json(h, buf, cap)
+        if ln >= 0:
+            break
+        cap = -ln + 16
+    res = RunResult(
+        d=info.d, capped=bool(info.capped), n=info.n, k=info.k, m=info.m, k_last=info.k_last,
+        g_final=info.g_final, witness_ok=bool(info.witness_ok), combinations=info.combinations,
+        evaluated=info.evaluated, row_additions=info.row_additions,
+        wall_seconds=info.wall_seconds, device_seconds=info.device_seconds,
+        gamma_seconds=info.gamma_seconds, loop_seconds=info.loop_seconds,
+        launches=info.launches, h2d_bytes=info.h2d_bytes, d2h_bytes=info.d2h_bytes,
+        rounds=[[r.c, r.j, r.w, r.U_after] for r in rr[: info.n_rounds]],
+        levels=[[x.c, x.L_after, x.U_after] for x in ll[: info.n_levels]],
+        column_perm=[int(x) for x in perm[: info.n]],
+        gamma_hash=["%016x" % L.mdg_run_gamma_hash(h, j) for j in range(info.m)],
+        witness=wit if has_w else None,
+        json=buf.value.decode(),
+    )
+    L.mdg_run_free(h)
+    return res
+
+
+def _config(trials, seed, level_cap, kernel, witness) -> _Config:
+    cfg = _Config()
+    lib().mdg_config_default(C.byref(cfg))
+    cfg.trials, cfg.seed, cfg.level_cap = trials, seed, level_cap
+    cfg.kernel, cfg.want_witness = kernel, 1 if witness else 0
+    return cfg
+
+
+def min_weight(G: np.ndarray, n: int, trials: int = 10, seed: int = 0, level_cap: int = 0,
+               kernel: int = KERNEL_TAB, witness: bool = True,
+               device: Optional[Device] = None) -> RunResult:
+    """md::min_weight (engines.cpp:617-648) with the GPU engine, plus trace and witness."""
+    G = _rows(G)
+    h = C.c_void_p()
+    cfg = _config(trials, seed, level_cap, kernel, witness)
+    _check(lib().mdg_min_weight(device.handle if device else None, G, G.shape[0], n,
+                                C.byref(cfg), C.byref(h)))
+    return _collect(h)
+
+
+def min_weight_dist(G: np.ndarray, n: int, rank: int, world: int,
+                    reduce_min: Callable[[np.ndarray], np.ndarray] | str = "nccl",
+                    trials: int = 10, seed: int = 0, level_cap: int = 0,
+                    kernel: int = KERNEL_TAB, witness: bool = True,
+                    device: Optional[Device] = None) -> RunResult:
+    """Multi-GPU min_weight: each rank evaluates a contiguous task range of every round;
+    the per-round key is combined by NCCL allreduce(min) (reduce_min='nccl', device must have
+    called nccl_init) or by a Python callable (numpy uint64 array -> elementwise global min)."""
+    G = _rows(G)
+    h = C.c_void_p()
+    cfg = _config(trials, seed, level_cap, kernel, witness)
+    fn, user, keep = _reducer(reduce_min, device)
+    _check(lib().mdg_min_weight_dist(device.handle if device else None, G, G.shape[0], n,
+                                     C.byref(cfg), rank, world, fn, user, C.byref(h)))
+    del keep
+    return _collect(h)
+
+
+def _reducer(reduce_min, device):
+    if reduce_min == "nccl":
+        return C.cast(lib().mdg_nccl_reduce_min, C.c_void_p), device.handle, None
+
+    def _cb(_user, keys, count):
+        try:
+            arr = np.ctypeslib.as_array(keys, shape=(count,))
+            arr[:] = reduce_min(arr.copy())
+            return 0
+        except Exception:  # surfaced as a status
+            return -1
+    keep = REDUCE_FN(_cb)
+    return C.cast(keep, C.c_void_p), None, keep
+
+
+def run_bz_loop(gs: GammaSet, round_fn: Callable[[int, int, int], int], lower: int = 1,
+                upper: Optional[int] = None, level_cap: int = 0) -> RunResult:
+    """run_bz_loop (engines.cpp:447-476) in the native host library, driving a Python round
+    ``round_fn(j, c, stop_at) -> w`` (the RoundRunner seam, engines.hpp:151)."""
+    if upper is None:
+        upper = singleton_upper(gs.n, gs.k)
+
+    def _cb(_user, j, c, stop_at, w_out):
+        try:
+            w_out[0] = int(round_fn(int(j), int(c), int(stop_at)))
+            return 0
+        except Exception:
+            return -1
+
+    cb = ROUND_FN(_cb)
+    h = C.c_void_p()
+    _check(lib().mdg_bz_loop_cb(gs._h, lower, upper, level_cap, cb, None, C.byref(h)))
+    return _collect(h)

@@ -1,0 +1,738 @@
+// C ABI of the B200 Brouwer–Zimmermann engine (include/mdg.h) and the GPU
+// front door min_weight (reference: engines.cpp:617-648 + cli.cpp:69-112).
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "mdg.h"
+#include "mdg.hpp"
+
+using namespace mdg;
+
+struct mdg_ctx {
+    std::unique_ptr<Engine> eng;
+};
+
+struct mdg_gset {
+    GammaSet gs;
+};
+
+struct mdg_run {
+    EngineResult er;
+    uint32_t n = 0, k = 0, m = 0, k_last = 0;
+    uint32_t level_cap = 0, trials = 0, devices = 1;
+    uint64_t seed = 0;
+    std::string algorithm = "gpu", kernel = "tab";
+    std::vector<uint32_t> perm;
+    std::vector<uint64_t> gamma_hash;
+    std::vector<uint64_t> witness;      // W words, original column order
+    std::vector<uint32_t> witness_idx;  // row indices into Gamma witness_gamma
+    int32_t witness_gamma = -1;
+    uint32_t witness_level = 0;
+    bool witness_ok = false;
+    bool witness_from_trace = true;
+    double wall = 0, gamma_s = 0, loop_s = 0;
+    Engine::Counters cnt;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return MDG_OK;
+    } catch (const std::overflow_error& e) {
+        g_err = e.what();
+        return MDG_EOVERFLOW;
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return MDG_ECUDA;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return MDG_EINVAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return MDG_EINTERNAL;
+    } catch (...) {
+        g_err = "unknown error";
+        return MDG_EINTERNAL;
+    }
+}
+
+BitMatrix from_rows(const uint64_t* rows, uint32_t k, uint32_t n) {
+    if (!rows) throw std::invalid_argument("null matrix");
+    if (k < 1 || n < 1) throw std::invalid_argument("empty matrix");
+    BitMatrix M(k, n);
+    std::memcpy(M.data(), rows, size_t(k) * M.words() * 8);
+    // padding bits must be zero (f2core.hpp:9-12)
+    if (n % 64)
+        for (uint32_t r = 0; r < k; ++r) M.row(r)[M.words() - 1] &= (uint64_t{1} << (n % 64)) - 1;
+    return M;
+}
+
+uint32_t weight_of(const std::vector<uint64_t>& v) {
+    uint32_t w = 0;
+    for (uint64_t x : v) w += static_cast<uint32_t>(__builtin_popcountll(x));
+    return w;
+}
+
+// XOR of Gamma_j rows idx, mapped back to the original column order with
+// column_perm (the semantics of unpermute_columns, gamma.cpp:24-30).
+std::vector<uint64_t> codeword(const GammaSet& gs, uint32_t j, const std::vector<uint32_t>& idx) {
+    const BitMatrix& Gm = gs.gammas[j];
+    std::vector<uint64_t> acc(Gm.words(), 0);
+    for (uint32_t r : idx)
+        for (uint32_t i = 0; i < Gm.words(); ++i) acc[i] ^= Gm.row(r)[i];
+    std::vector<uint64_t> out(Gm.words(), 0);
+    for (uint32_t c = 0; c < Gm.cols(); ++c)
+        if ((acc[c >> 6] >> (c & 63)) & 1u) {
+            uint32_t o = gs.column_perm[c];
+            out[o >> 6] |= uint64_t{1} << (o & 63);
+        }
+    return out;
+}
+
+// w (original column order) lies in the code: permuted into the stored
+// column order it does not raise the rank of Gamma_0 (same row space).
+bool in_code(const GammaSet& gs, const std::vector<uint64_t>& w) {
+    const BitMatrix& G0 = gs.gammas[0];
+    BitMatrix S(G0.rows() + 1, G0.cols());
+    std::memcpy(S.data(), G0.data(), size_t(G0.rows()) * G0.words() * 8);
+    for (uint32_t c = 0; c < G0.cols(); ++c) {
+        uint32_t o = gs.column_perm[c];
+        if ((w[o >> 6] >> (o & 63)) & 1u) S.set(G0.rows(), c, true);
+    }
+    return rank_of(S) == G0.rows();
+}
+
+struct RoundLog {
+    uint32_t j, c;
+    RoundResult rr;
+};
+
+void upload(Engine& eng, const GammaSet& gs) {
+    const uint32_t m = gs.m(), k = gs.k(), W = gs.gammas[0].words();
+    std::vector<uint64_t> all(size_t(m) * k * W);
+    for (uint32_t j = 0; j < m; ++j)
+        std::memcpy(all.data() + size_t(j) * k * W, gs.gammas[j].data(), size_t(k) * W * 8);
+    eng.load(m, k, gs.n(), all.data(), gs.ranks.data());
+}
+
+// The level loop on the device over the Gamma set already loaded into eng
+// (run_bz_loop, engines.cpp:447-476, with the GPU RoundRunner), then the
+// witness. world > 1: every rank evaluates its contiguous task range of each
+// round and the per-round keys are min-reduced across ranks.
+void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uint32_t rank,
+                     uint32_t world, mdg_reduce_fn reduce, void* user, mdg_run& out) {
+    const uint32_t m = gs.m(), k = gs.k(), n = gs.n();
+    if (eng.m() != m || eng.k() != k || eng.n() != n)
+        throw std::invalid_argument("device holds a different Gamma set");
+    eng.set_kernel(cfg.kernel == MDG_KERNEL_RD ? Kernel::rd : Kernel::tab);
+    Engine::Counters c0 = eng.counters();
+    std::vector<RoundLog> log;
+    auto do_round = [&](uint32_t j, uint32_t g, uint32_t stop_at) {
+        RoundResult rr;
+        if (world <= 1) {
+            rr = eng.round(j, g, stop_at);
+        } else {
+            uint64_t T = eng.tasks(j, g);
+            uint64_t lo = T * rank / world, hi = T * (rank + 1) / world;
+            rr = eng.round(j, g, stop_at, lo, hi);
+            uint64_t key = rr.key;
+            int rc = reduce(user, &key, 1);
+            if (rc != 0) throw std::runtime_error("mdg: cross-rank reduction failed");
+            rr.key = key;
+            rr.w = key == ~0ull ? UINT32_MAX : uint32_t(key >> 40);
+        }
+        return rr;
+    };
+    RoundRunner runner = [&](uint32_t j, uint32_t g, RoundStats& rs) -> uint32_t {
+        RoundResult rr = do_round(j, g, rs.stop_at);
+        rs.combinations = rr.combinations;
+        rs.evaluated = rr.evaluated;
+        rs.additions = rr.evaluated; // one row XOR per evaluated codeword
+        rs.device_ms = rr.ms;
+        log.push_back({j, g, rr});
+        return rr.w;
+    };
+    Bounds bounds;
+    bounds.lower = 1;
+    bounds.upper = singleton_upper(n, k);
+    eng.timer_start();
+    out.er = run_bz_loop(gs, bounds, runner, cfg.level_cap);
+    out.loop_s = eng.timer_stop_ms() * 1e-3;
+    const uint32_t d = out.er.d;
+
+    if (cfg.want_witness) {
+        const RoundLog* src = nullptr;
+        if (out.er.witness_round >= 0) src = &log[size_t(out.er.witness_round)];
+        RoundLog extra;
+        if (!src) {
+            // U never came from a round (it is the Singleton bound, or a run
+            // with no rounds): search the levels for a codeword of weight U.
+            out.witness_from_trace = false;
+            for (uint32_t g = 1; g <= k && !src; ++g)
+                for (uint32_t j = 0; j < m && !src; ++j) {
+                    RoundResult rr = do_round(j, g, d);
+                    if (rr.w <= d) {
+                        extra = {j, g, rr};
+                        src = &extra;
+                    }
+                }
+        }
+        if (src) {
+            out.witness_idx = eng.witness(src->j, src->c, src->rr);
+            out.witness_gamma = int32_t(src->j);
+            out.witness_level = src->c;
+            out.witness = codeword(gs, src->j, out.witness_idx);
+            out.witness_ok = weight_of(out.witness) == d && in_code(gs, out.witness) && src->rr.w == d;
+        }
+    }
+    Engine::Counters c1 = eng.counters();
+    out.cnt.launches = c1.launches - c0.launches;
+    out.cnt.h2d = c1.h2d - c0.h2d;
+    out.cnt.d2h = c1.d2h - c0.d2h;
+    out.n = n;
+    out.k = k;
+    out.m = m;
+    out.k_last = gs.k_last;
+    out.perm = gs.column_perm;
+    out.gamma_hash.clear();
+    for (uint32_t j = 0; j < m; ++j) out.gamma_hash.push_back(hash_rows(gs.gammas[j]));
+    out.level_cap = cfg.level_cap;
+    out.trials = cfg.trials;
+    out.seed = cfg.seed;
+    out.devices = world;
+    out.kernel = cfg.kernel == MDG_KERNEL_RD ? "rd" : "tab";
+}
+
+// min_weight on the device(s): row_basis -> Gamma search -> Singleton U ->
+// level loop -> witness (engines.cpp:617-648).
+std::unique_ptr<mdg_run> min_weight_device(Engine& eng, const BitMatrix& G, const mdg_config& cfg,
+                                           uint32_t rank, uint32_t world, mdg_reduce_fn reduce,
+                                           void* user) {
+    auto t0 = std::chrono::steady_clock::now();
+    auto run = std::make_unique<mdg_run>();
+    Engine::Counters c0 = eng.counters();
+    GammaSet gs = best_gamma_over_permutations(row_basis(G), cfg.trials, cfg.seed);
+    auto t1 = std::chrono::steady_clock::now();
+    run->gamma_s = std::chrono::duration<double>(t1 - t0).count();
+    upload(eng, gs);
+    run_device_loop(eng, gs, cfg, rank, world, reduce, user, *run);
+    Engine::Counters c1 = eng.counters();
+    run->cnt.launches = c1.launches - c0.launches;
+    run->cnt.h2d = c1.h2d - c0.h2d;
+    run->cnt.d2h = c1.d2h - c0.d2h;
+    run->wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return run;
+}
+
+std::string json_of(const mdg_run& r) {
+    std::ostringstream o;
+    const auto& st = r.er.stats;
+    o << "{\"d\":" << r.er.d << ",\"n\":" << r.n << ",\"k\":" << r.k << ",\"algorithm\":\""
+      << r.algorithm << "\",\"m\":" << r.m << ",\"k_last\":" << r.k_last
+      << ",\"g_final\":" << st.g_final << ",\"row_additions\":" << st.row_additions
+      << ",\"combinations\":" << st.combinations << ",\"wall_seconds\":" << r.wall
+      << ",\"seed\":" << r.seed << ",\"workers\":" << r.devices;
+    // new keys: witness, trace, level cap, devices, throughput
+    o << ",\"capped\":" << (r.er.capped ? "true" : "false") << ",\"level_cap\":" << r.level_cap
+      << ",\"devices\":" << r.devices << ",\"kernel\":\"" << r.kernel << "\""
+      << ",\"combinations_evaluated\":" << st.evaluated
+      << ",\"device_seconds\":" << st.device_ms * 1e-3 << ",\"loop_seconds\":" << r.loop_s
+      << ",\"gamma_seconds\":" << r.gamma_s << ",\"gpu_launches\":" << r.cnt.launches
+      << ",\"codewords_per_s\":" << (st.device_ms > 0 ? double(st.evaluated) / (st.device_ms * 1e-3) : 0.0);
+    o << ",\"witness\":";
+    if (r.witness.empty()) {
+        o << "null";
+    } else {
+        o << "\"";
+        for (uint32_t c = 0; c < r.n; ++c) o << (((r.witness[c >> 6] >> (c & 63)) & 1u) ? '1' : '0');
+        o << "\"";
+    }
+    o << ",\"witness_ok\":" << (r.witness_ok ? "true" : "false") << ",\"trace\":[";
+    for (size_t i = 0; i < st.rounds.size(); ++i) {
+        const auto& x = st.rounds[i];
+        o << (i ? "," : "") << "[" << x.c << "," << x.j << "," << x.w << "," << x.U_after << "]";
+    }
+    o << "],\"levels\":[";
+    for (size_t i = 0; i < st.levels.size(); ++i) {
+        const auto& x = st.levels[i];
+        o << (i ? "," : "") << "[" << x.c << "," << x.L_after << "," << x.U_after << "]";
+    }
+    o << "]}";
+    return o.str();
+}
+
+long copy_out(const std::string& s, char* buf, size_t cap) {
+    if (!buf || s.size() + 1 > cap) {
+        g_err = "buffer too small (need " + std::to_string(s.size() + 1) + " bytes)";
+        return -static_cast<long>(s.size() + 1);
+    }
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return static_cast<long>(s.size());
+}
+
+} // namespace
+
+std::string mdg_json_of(const mdg_run& r) { return json_of(r); }
+
+extern "C" {
+
+const char* mdg_last_error(void) { return g_err.c_str(); }
+const char* mdg_version(void) { return "mdg 0.1 (sm_100a)"; }
+
+int mdg_open(int device, mdg_ctx** out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null out");
+        auto c = std::make_unique<mdg_ctx>();
+        c->eng = std::make_unique<Engine>(device);
+        *out = c.release();
+    });
+}
+
+void mdg_close(mdg_ctx* ctx) { delete ctx; }
+
+int mdg_load_gammas(mdg_ctx* ctx, uint32_t m, uint32_t k, uint32_t n, const uint64_t* rows,
+                    const uint32_t* ranks) {
+    return guard([&] {
+        if (!ctx || !rows) throw std::invalid_argument("null argument");
+        ctx->eng->load(m, k, n, rows, ranks);
+    });
+}
+
+static void fill_out(const RoundResult& rr, mdg_round_out* out) {
+    out->min_weight = rr.w;
+    out->stopped_early = rr.stopped ? 1u : 0u;
+    out->argmin_key = rr.key;
+    out->combinations = rr.combinations;
+    out->evaluated = rr.evaluated;
+    out->task_lo = rr.task_lo;
+    out->task_hi = rr.task_hi;
+    out->device_ms = rr.ms;
+}
+
+static RoundResult to_rr(const mdg_round_out* out) {
+    RoundResult rr;
+    rr.w = out->min_weight;
+    rr.key = out->argmin_key;
+    rr.combinations = out->combinations;
+    rr.evaluated = out->evaluated;
+    return rr;
+}
+
+int mdg_round(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t stop_at, mdg_round_out* out) {
+    return guard([&] {
+        if (!ctx || !out) throw std::invalid_argument("null argument");
+        fill_out(ctx->eng->round(j, c, stop_at), out);
+    });
+}
+
+int mdg_round_tasks(mdg_ctx* ctx, uint32_t j, uint32_t c, uint64_t* n_tasks) {
+    return guard([&] {
+        if (!ctx || !n_tasks) throw std::invalid_argument("null argument");
+        *n_tasks = ctx->eng->tasks(j, c);
+    });
+}
+
+int mdg_round_range(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t stop_at, uint64_t task_lo,
+                    uint64_t task_hi, mdg_round_out* out) {
+    return guard([&] {
+        if (!ctx || !out) throw std::invalid_argument("null argument");
+        if (task_lo > task_hi) throw std::invalid_argument("task range reversed");
+        fill_out(ctx->eng->round(j, c, stop_at, task_lo, task_hi), out);
+    });
+}
+
+int mdg_round_hist(mdg_ctx* ctx, uint32_t j, uint32_t c, uint64_t* hist, mdg_round_out* out) {
+    return guard([&] {
+        if (!ctx || !hist || !out) throw std::invalid_argument("null argument");
+        fill_out(ctx->eng->round_hist(j, c, hist), out);
+    });
+}
+
+int mdg_round_witness(mdg_ctx* ctx, uint32_t j, uint32_t c, const mdg_round_out* out, uint32_t* idx) {
+    return guard([&] {
+        if (!ctx || !out || !idx) throw std::invalid_argument("null argument");
+        auto v = ctx->eng->witness(j, c, to_rr(out));
+        std::memcpy(idx, v.data(), v.size() * 4);
+    });
+}
+
+int mdg_set_kernel(mdg_ctx* ctx, int kernel) {
+    return guard([&] {
+        if (!ctx) throw std::invalid_argument("null argument");
+        if (kernel != MDG_KERNEL_TAB && kernel != MDG_KERNEL_RD)
+            throw std::invalid_argument("unknown kernel");
+        ctx->eng->set_kernel(kernel == MDG_KERNEL_RD ? Kernel::rd : Kernel::tab);
+    });
+}
+
+// ------------------------------------------------------------- gamma sets
+int mdg_gset_build(const uint64_t* G, uint32_t k, uint32_t n, uint32_t trials, uint64_t seed,
+                   mdg_gset** out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null out");
+        auto g = std::make_unique<mdg_gset>();
+        g->gs = best_gamma_over_permutations(row_basis(from_rows(G, k, n)), trials, seed);
+        *out = g.release();
+    });
+}
+
+int mdg_gset_compute(const uint64_t* G, uint32_t k, uint32_t n, mdg_gset** out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null out");
+        auto g = std::make_unique<mdg_gset>();
+        g->gs = compute_gamma_matrices(from_rows(G, k, n));
+        *out = g.release();
+    });
+}
+
+void mdg_gset_free(mdg_gset* gs) { delete gs; }
+
+int mdg_gset_info(const mdg_gset* g, uint32_t* m, uint32_t* k, uint32_t* n, uint32_t* k_last) {
+    return guard([&] {
+        if (!g) throw std::invalid_argument("null gset");
+        if (m) *m = g->gs.m();
+        if (k) *k = g->gs.k();
+        if (n) *n = g->gs.n();
+        if (k_last) *k_last = g->gs.k_last;
+    });
+}
+
+int mdg_gset_gamma(const mdg_gset* g, uint32_t j, uint64_t* rows) {
+    return guard([&] {
+        if (!g || !rows) throw std::invalid_argument("null argument");
+        if (j >= g->gs.m()) throw std::invalid_argument("gamma index out of range");
+        const BitMatrix& M = g->gs.gammas[j];
+        std::memcpy(rows, M.data(), size_t(M.rows()) * M.words() * 8);
+    });
+}
+
+int mdg_gset_ranks(const mdg_gset* g, uint32_t* ranks) {
+    return guard([&] {
+        if (!g || !ranks) throw std::invalid_argument("null argument");
+        std::memcpy(ranks, g->gs.ranks.data(), g->gs.ranks.size() * 4);
+    });
+}
+
+int mdg_gset_perm(const mdg_gset* g, uint32_t* perm) {
+    return guard([&] {
+        if (!g || !perm) throw std::invalid_argument("null argument");
+        std::memcpy(perm, g->gs.column_perm.data(), g->gs.column_perm.size() * 4);
+    });
+}
+
+uint64_t mdg_gset_hash(const mdg_gset* g, uint32_t j) {
+    if (!g || j >= g->gs.m()) return 0;
+    return hash_rows(g->gs.gammas[j]);
+}
+
+int mdg_load_gset(mdg_ctx* ctx, const mdg_gset* g) {
+    return guard([&] {
+        if (!ctx || !g) throw std::invalid_argument("null argument");
+        const GammaSet& gs = g->gs;
+        uint32_t W = gs.gammas[0].words();
+        std::vector<uint64_t> all(size_t(gs.m()) * gs.k() * W);
+        for (uint32_t j = 0; j < gs.m(); ++j)
+            std::memcpy(all.data() + size_t(j) * gs.k() * W, gs.gammas[j].data(), size_t(gs.k()) * W * 8);
+        ctx->eng->load(gs.m(), gs.k(), gs.n(), all.data(), gs.ranks.data());
+    });
+}
+
+uint32_t mdg_lower_bound(uint32_t m, uint32_t g, uint32_t k, uint32_t k_last) {
+    return lower_bound(m, g, k, k_last);
+}
+
+uint32_t mdg_singleton_upper(uint32_t n, uint32_t k) {
+    if (k < 1 || n < k) {
+        g_err = "singleton_upper: need n >= k >= 1";
+        return 0;
+    }
+    return singleton_upper(n, k);
+}
+
+// ---------------------------------------------------------------- loops
+int mdg_bz_loop_cb(const mdg_gset* g, uint32_t lower, uint32_t upper, uint32_t level_cap,
+                   mdg_round_fn fn, void* user, mdg_run** out) {
+    return guard([&] {
+        if (!g || !fn || !out) throw std::invalid_argument("null argument");
+        auto t0 = std::chrono::steady_clock::now();
+        auto run = std::make_unique<mdg_run>();
+        RoundRunner runner = [&](uint32_t j, uint32_t c, RoundStats& rs) -> uint32_t {
+            uint32_t w = UINT32_MAX;
+            int rc = fn(user, j, c, rs.stop_at, &w);
+            if (rc != 0) throw std::runtime_error("round callback failed with status " + std::to_string(rc));
+            rs.combinations = binomial(g->gs.k(), c);
+            return w;
+        };
+        Bounds b;
+        b.lower = lower;
+        b.upper = upper;
+        run->er = run_bz_loop(g->gs, b, runner, level_cap);
+        run->n = g->gs.n();
+        run->k = g->gs.k();
+        run->m = g->gs.m();
+        run->k_last = g->gs.k_last;
+        run->perm = g->gs.column_perm;
+        run->level_cap = level_cap;
+        run->algorithm = "callback";
+        run->kernel = "callback";
+        for (uint32_t j = 0; j < run->m; ++j) run->gamma_hash.push_back(hash_rows(g->gs.gammas[j]));
+        run->wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *out = run.release();
+    });
+}
+
+void mdg_config_default(mdg_config* cfg) {
+    if (!cfg) return;
+    cfg->trials = 10;
+    cfg->seed = 0;
+    cfg->level_cap = 0;
+    cfg->kernel = MDG_KERNEL_TAB;
+    cfg->want_witness = 1;
+}
+
+int mdg_min_weight(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n, const mdg_config* cfg,
+                   mdg_run** out) {
+    return mdg_min_weight_dist(ctx, G, k, n, cfg, 0, 1, nullptr, nullptr, out);
+}
+
+int mdg_min_weight_dist(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n,
+                        const mdg_config* cfg, uint32_t rank, uint32_t world,
+                        mdg_reduce_fn reduce_min, void* user, mdg_run** out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null out");
+        if (world < 1 || rank >= world) throw std::invalid_argument("bad rank / world");
+        if (world > 1 && !reduce_min) throw std::invalid_argument("multi-rank run needs a reducer");
+        mdg_config c;
+        mdg_config_default(&c);
+        if (cfg) c = *cfg;
+        if (c.trials < 1) throw std::invalid_argument("best_gamma_over_permutations: trials must be >= 1");
+        std::unique_ptr<mdg_ctx> own;
+        if (!ctx) {
+            own = std::make_unique<mdg_ctx>();
+            own->eng = std::make_unique<Engine>(0);
+            ctx = own.get();
+        }
+        BitMatrix M = from_rows(G, k, n);
+        *out = min_weight_device(*ctx->eng, M, c, rank, world, reduce_min, user).release();
+    });
+}
+
+int mdg_bz_loop_device(mdg_ctx* ctx, const mdg_gset* g, const mdg_config* cfg, mdg_run** out) {
+    return mdg_bz_loop_device_dist(ctx, g, cfg, 0, 1, nullptr, nullptr, out);
+}
+
+int mdg_bz_loop_device_dist(mdg_ctx* ctx, const mdg_gset* g, const mdg_config* cfg, uint32_t rank,
+                            uint32_t world, mdg_reduce_fn reduce_min, void* user, mdg_run** out) {
+    return guard([&] {
+        if (!ctx || !g || !out) throw std::invalid_argument("null argument");
+        if (world < 1 || rank >= world) throw std::invalid_argument("bad rank / world");
+        if (world > 1 && !reduce_min) throw std::invalid_argument("multi-rank run needs a reducer");
+        mdg_config c;
+        mdg_config_default(&c);
+        if (cfg) c = *cfg;
+        auto t0 = std::chrono::steady_clock::now();
+        auto run = std::make_unique<mdg_run>();
+        run_device_loop(*ctx->eng, g->gs, c, rank, world, reduce_min, user, *run);
+        run->wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *out = run.release();
+    });
+}
+
+int mdg_timer_start(mdg_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) throw std::invalid_argument("null ctx");
+        ctx->eng->timer_start();
+    });
+}
+
+int mdg_timer_stop(mdg_ctx* ctx, double* ms) {
+    return guard([&] {
+        if (!ctx || !ms) throw std::invalid_argument("null argument");
+        *ms = ctx->eng->timer_stop_ms();
+    });
+}
+
+int mdg_ctx_counters(mdg_ctx* ctx, uint64_t* launches, uint64_t* h2d, uint64_t* d2h) {
+    return guard([&] {
+        if (!ctx) throw std::invalid_argument("null ctx");
+        Engine::Counters c = ctx->eng->counters();
+        if (launches) *launches = c.launches;
+        if (h2d) *h2d = c.h2d;
+        if (d2h) *d2h = c.d2h;
+    });
+}
+
+int mdg_device_info(mdg_ctx* ctx, int* sms, int* device) {
+    return guard([&] {
+        if (!ctx) throw std::invalid_argument("null ctx");
+        if (sms) *sms = ctx->eng->sm_count();
+        if (device) *device = ctx->eng->device();
+    });
+}
+
+int mdg_nccl_unique_id(uint8_t id[128]) {
+    return guard([&] { Engine::nccl_unique_id(id); });
+}
+
+int mdg_nccl_init(mdg_ctx* ctx, const uint8_t id[128], uint32_t rank, uint32_t world) {
+    return guard([&] {
+        if (!ctx) throw std::invalid_argument("null ctx");
+        ctx->eng->nccl_init(id, rank, world);
+    });
+}
+
+int mdg_nccl_reduce_min(void* ctx, uint64_t* keys, uint32_t count) {
+    return guard([&] {
+        if (!ctx) throw std::invalid_argument("null ctx");
+        static_cast<mdg_ctx*>(ctx)->eng->nccl_reduce_min(keys, count);
+    });
+}
+
+// ----------------------------------------------------------- run results
+int mdg_run_info_get(const mdg_run* r, mdg_run_info* info) {
+    return guard([&] {
+        if (!r || !info) throw std::invalid_argument("null argument");
+        std::memset(info, 0, sizeof *info);
+        const auto& st = r->er.stats;
+        info->d = r->er.d;
+        info->capped = r->er.capped ? 1 : 0;
+        info->n = r->n;
+        info->k = r->k;
+        info->m = r->m;
+        info->k_last = r->k_last;
+        info->g_final = st.g_final;
+        info->n_rounds = uint32_t(st.rounds.size());
+        info->n_levels = uint32_t(st.levels.size());
+        info->witness_ok = r->witness_ok ? 1 : 0;
+        info->combinations = st.combinations;
+        info->evaluated = st.evaluated;
+        info->row_additions = st.row_additions;
+        info->wall_seconds = r->wall;
+        info->device_seconds = st.device_ms * 1e-3;
+        info->gamma_seconds = r->gamma_s;
+        info->loop_seconds = r->loop_s;
+        info->launches = r->cnt.launches;
+        info->h2d_bytes = r->cnt.h2d;
+        info->d2h_bytes = r->cnt.d2h;
+    });
+}
+
+int mdg_run_rounds(const mdg_run* r, mdg_round_rec* out) {
+    return guard([&] {
+        if (!r || !out) throw std::invalid_argument("null argument");
+        for (size_t i = 0; i < r->er.stats.rounds.size(); ++i) {
+            const auto& x = r->er.stats.rounds[i];
+            out[i] = {x.c, x.j, x.w, x.U_after};
+        }
+    });
+}
+
+int mdg_run_levels(const mdg_run* r, mdg_level_rec* out) {
+    return guard([&] {
+        if (!r || !out) throw std::invalid_argument("null argument");
+        for (size_t i = 0; i < r->er.stats.levels.size(); ++i) {
+            const auto& x = r->er.stats.levels[i];
+            out[i] = {x.c, x.L_after, x.U_after, 0};
+        }
+    });
+}
+
+int mdg_run_witness(const mdg_run* r, uint64_t* row) {
+    return guard([&] {
+        if (!r || !row) throw std::invalid_argument("null argument");
+        if (r->witness.empty()) throw std::invalid_argument("run has no witness");
+        std::memcpy(row, r->witness.data(), r->witness.size() * 8);
+    });
+}
+
+int mdg_run_perm(const mdg_run* r, uint32_t* perm) {
+    return guard([&] {
+        if (!r || !perm) throw std::invalid_argument("null argument");
+        std::memcpy(perm, r->perm.data(), r->perm.size() * 4);
+    });
+}
+
+uint64_t mdg_run_gamma_hash(const mdg_run* r, uint32_t j) {
+    if (!r || j >= r->gamma_hash.size()) return 0;
+    return r->gamma_hash[j];
+}
+
+long mdg_run_json(const mdg_run* r, char* buf, size_t cap) {
+    if (!r) {
+        g_err = "null run";
+        return MDG_EINVAL;
+    }
+    return copy_out(json_of(*r), buf, cap);
+}
+
+void mdg_run_free(mdg_run* r) { delete r; }
+
+// -------------------------------------------------------------- misc I/O
+int mdg_parse_matrix(const char* text, uint32_t* k, uint32_t* n, uint64_t* rows_out) {
+    return guard([&] {
+        if (!text) throw std::invalid_argument("null text");
+        BitMatrix M = parse_matrix(text);
+        if (k) *k = M.rows();
+        if (n) *n = M.cols();
+        if (rows_out) std::memcpy(rows_out, M.data(), size_t(M.rows()) * M.words() * 8);
+    });
+}
+
+long mdg_serialize_matrix(const uint64_t* rows, uint32_t k, uint32_t n, char* buf, size_t cap) {
+    std::string s;
+    int rc = guard([&] { s = serialize_matrix(from_rows(rows, k, n)); });
+    if (rc) return rc;
+    return copy_out(s, buf, cap);
+}
+
+int mdg_gen_matrix(uint32_t n, uint32_t k, uint64_t seed, int identity, uint64_t* rows) {
+    return guard([&] {
+        if (!rows) throw std::invalid_argument("null out");
+        BitMatrix M = gen_matrix(n, k, seed, identity != 0);
+        std::memcpy(rows, M.data(), size_t(k) * M.words() * 8);
+    });
+}
+
+uint32_t mdg_rank(const uint64_t* rows, uint32_t k, uint32_t n) {
+    uint32_t r = 0;
+    guard([&] { r = rank_of(from_rows(rows, k, n)); });
+    return r;
+}
+
+uint64_t mdg_hash_rows(const uint64_t* rows, uint32_t k, uint32_t n) {
+    uint64_t h = 0;
+    guard([&] { h = hash_rows(from_rows(rows, k, n)); });
+    return h;
+}
+
+int mdg_binomial(uint32_t p, uint32_t q, uint64_t* out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null out");
+        *out = binomial(p, q);
+    });
+}
+
+int mdg_rd_unrank(uint32_t c, uint64_t rank, uint32_t* idx) {
+    return guard([&] {
+        if (!idx || c < 1) throw std::invalid_argument("bad argument");
+        rd_unrank(c, rank, idx);
+    });
+}
+
+uint64_t mdg_rd_rank(uint32_t c, const uint32_t* idx) {
+    uint64_t r = 0;
+    guard([&] { r = rd_rank(c, idx); });
+    return r;
+}
+
+} // extern "C"

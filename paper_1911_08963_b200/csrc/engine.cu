@@ -1,0 +1,1089 @@
+// Device side of the B200 Brouwer–Zimmermann round: one (c, Gamma_j) round =
+// the minimum Hamming weight over all C(k, c) XOR-sums of c rows of Gamma_j
+// (reference: round_* in proj/src/engines.cpp:175-443; level loop :447-476).
+//
+// Data layout in HBM / shared memory:
+//   * Gamma_j is stored "compacted": its identity block (columns
+//     [j*k, j*k + rank_j), rows [0, rank_j), gamma.cpp:44-71) is dropped, so a
+//     row is NW = ceil((n - rank_j)/32) u32 words, and the weight of a sum
+//     over row set S is |S ∩ [0, rank_j)| + popcount of the compacted sum.
+//     For full-rank blocks that count is the constant c.
+//   * suffix table (per Gamma, per suffix size s, built once and reused by
+//     every level): all s-subsets Q of [0,k) in reverse-colex order, XOR-sum
+//     (+ identity count) per entry, YS words per entry — the reference's
+//     "saved additions" table (engines.cpp:96-151) turned into a GPU operand.
+//
+// Kernels (all integer; no tensor cores):
+//   tab_round<NW,HID>  persistent grid over tiles (prefix chunk x suffix chunk);
+//                      prefix sums built in smem per tile, each lane holds R
+//                      suffix sums in registers, one XOR + POPC per word per
+//                      codeword; warp __reduce_min_sync; global 64-bit
+//                      atomicMin of (weight << 40 | tile); every tile polls the
+//                      global bound for early exit.
+//   tab_find           re-evaluates the winning tile to name the witness.
+//   tab_hist           same walk, per-warp shared-memory weight histograms.
+//   rd_round / rd_find revolving-door walk of contiguous rank ranges (the
+//                      north_star formulation; cross-check engine).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <sstream>
+
+#include "engine.hpp"
+
+namespace mdg {
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess)                                                                  \
+            throw CudaError(std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #x);      \
+    } while (0)
+
+namespace {
+
+constexpr int kWarps = 8;           // warps per block (tab kernels)
+constexpr int kThreads = kWarps * 32;
+constexpr int kTX = 256;            // prefixes per tile (= threads that build them)
+constexpr uint32_t kBT = kMaxC + 1; // binomial table row stride
+constexpr int kKeyShift = 40;
+
+__host__ __device__ constexpr int r_for(int nw) { return nw <= 4 ? 8 : (nw <= 8 ? 4 : 2); }
+__host__ __device__ constexpr int stride_for(int words) {
+    return words <= 2 ? 2 : ((words + 3) / 4) * 4;
+}
+
+// -------------------------------------------------------------- helpers
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint64_t BT(const uint64_t* __restrict__ T, uint32_t x, uint32_t t) {
+    return __ldg(T + size_t(x) * kBT + t);
+}
+
+// largest x in [i-1, hi-1] with C(x, i) <= r (colex unrank step)
+__device__ __forceinline__ uint32_t colex_top(const uint64_t* __restrict__ T, uint64_t r,
+                                              uint32_t i, uint32_t hi) {
+    uint32_t lo = i - 1, h = hi - 1;
+    while (lo < h) {
+        uint32_t mid = (lo + h + 1) >> 1;
+        if (BT(T, mid, i) <= r) lo = mid; else h = mid - 1;
+    }
+    return lo;
+}
+
+template <int NW>
+__device__ __forceinline__ void load_row(const uint32_t* __restrict__ rows, uint32_t r,
+                                         uint32_t (&v)[NW]) {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) v[w] = __ldg(rows + size_t(r) * NW + w);
+}
+
+template <int NW>
+__device__ __forceinline__ void xor_row(const uint32_t* __restrict__ rows, uint32_t r,
+                                        uint32_t (&v)[NW]) {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) v[w] ^= __ldg(rows + size_t(r) * NW + w);
+}
+
+// vector load of S consecutive u32 (S = 2 or a multiple of 4), 8/16-byte aligned
+template <int S>
+__device__ __forceinline__ void vload(const uint32_t* p, uint32_t (&v)[S]) {
+    if constexpr (S == 2) {
+        uint2 t = *reinterpret_cast<const uint2*>(p);
+        v[0] = t.x; v[1] = t.y;
+    } else {
+#pragma unroll
+        for (int i = 0; i < S / 4; ++i) {
+            uint4 t = *reinterpret_cast<const uint4*>(p + 4 * i);
+            v[4 * i] = t.x; v[4 * i + 1] = t.y; v[4 * i + 2] = t.z; v[4 * i + 3] = t.w;
+        }
+    }
+}
+template <int S>
+__device__ __forceinline__ void vload_global(const uint32_t* __restrict__ p, uint32_t (&v)[S]) {
+    if constexpr (S == 2) {
+        uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
+        v[0] = t.x; v[1] = t.y;
+    } else {
+#pragma unroll
+        for (int i = 0; i < S / 4; ++i) {
+            uint4 t = __ldg(reinterpret_cast<const uint4*>(p + 4 * i));
+            v[4 * i] = t.x; v[4 * i + 1] = t.y; v[4 * i + 2] = t.z; v[4 * i + 3] = t.w;
+        }
+    }
+}
+
+// ------------------------------------------------------ suffix table build
+// entry y: Q' = colex_unrank(y, s) ⊆ [0,k), Q = {k-1-q'}; XOR of rows(Q)
+// (+ |Q ∩ [0, id_rows)| in word NW when HID).
+template <int NW, bool HID>
+__global__ void ytab_build(const uint32_t* __restrict__ rows, const uint64_t* __restrict__ T,
+                           uint32_t k, uint32_t s, uint32_t id_rows, uint64_t count,
+                           uint32_t* __restrict__ out) {
+    constexpr int YS = stride_for(NW + (HID ? 1 : 0));
+    uint64_t y = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (y >= count) return;
+    uint32_t acc[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) acc[w] = 0;
+    uint32_t id = 0;
+    uint64_t r = y;
+    uint32_t hi = k;
+    for (uint32_t i = s; i >= 1; --i) {
+        uint32_t x = colex_top(T, r, i, hi);
+        r -= BT(T, x, i);
+        hi = x;
+        uint32_t q = k - 1 - x;
+        xor_row<NW>(rows, q, acc);
+        id += q < id_rows;
+    }
+    uint32_t* o = out + y * YS;
+#pragma unroll
+    for (int w = 0; w < YS; ++w) o[w] = w < NW ? acc[w] : (HID && w == NW ? id : 0u);
+}
+
+struct TabArgs {
+    const uint32_t* rows;
+    const uint32_t* ytab;
+    const uint64_t* binom;
+    const uint64_t* prefix;
+    uint32_t k, p, s, emin, npiv, id_rows, add_const, stop_at;
+    uint64_t tile_lo, tile_hi;
+    unsigned long long* best_key;
+    unsigned long long* evaluated;
+    unsigned long long* find_out;  // tab_find only
+    uint32_t find_target;          // tab_find only
+    uint32_t nbins;                // tab_hist only
+    unsigned long long* hist;      // tab_hist only
+};
+
+struct TileInfo {
+    uint32_t e, nx, nyv, stop;
+    uint64_t x0, y0;
+};
+
+// decode tile -> (pivot, prefix chunk, suffix chunk); thread 0 only
+template <int YC>
+__device__ __forceinline__ void decode_tile(const TabArgs& a, uint64_t tile, TileInfo& ti) {
+    uint32_t lo = 0, hi = a.npiv - 1; // largest i with prefix[i] <= tile
+    while (lo < hi) {
+        uint32_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(a.prefix + mid) <= tile) lo = mid; else hi = mid - 1;
+    }
+    uint32_t e = a.emin + lo;
+    uint64_t local = tile - __ldg(a.prefix + lo);
+    uint64_t NY = BT(a.binom, a.k - 1 - e, a.s);
+    uint64_t nty = (NY + YC - 1) / YC;
+    uint64_t tx = local / nty, ty = local - tx * nty;
+    uint64_t NX = BT(a.binom, e, a.p - 1);
+    ti.e = e;
+    ti.x0 = tx * kTX;
+    ti.nx = uint32_t(umin64(uint64_t(kTX), NX - ti.x0));
+    ti.y0 = ty * YC;
+    ti.nyv = uint32_t(umin64(uint64_t(YC), NY - ti.y0));
+}
+
+// prefix sum for pivot e, colex rank x among (p-1)-subsets of [0, e)
+template <int NW, bool HID>
+__device__ __forceinline__ void build_prefix(const TabArgs& a, uint32_t e, uint64_t x,
+                                             uint32_t* dst) {
+    constexpr int XS = stride_for(NW + (HID ? 1 : 0));
+    uint32_t acc[NW];
+    load_row<NW>(a.rows, e, acc);
+    uint32_t id = e < a.id_rows;
+    uint64_t r = x;
+    uint32_t hi = e;
+    for (uint32_t i = a.p - 1; i >= 1; --i) {
+        uint32_t q = colex_top(a.binom, r, i, hi);
+        r -= BT(a.binom, q, i);
+        hi = q;
+        xor_row<NW>(a.rows, q, acc);
+        id += q < a.id_rows;
+    }
+#pragma unroll
+    for (int w = 0; w < XS; ++w) dst[w] = w < NW ? acc[w] : (HID && w == NW ? id : 0u);
+}
+
+template <int NW, bool HID>
+__device__ __forceinline__ void load_suffixes(const TabArgs& a, const TileInfo& ti,
+                                              uint32_t (&Y)[r_for(NW)][NW],
+                                              uint32_t (&idY)[r_for(NW)],
+                                              bool (&valid)[r_for(NW)]) {
+    constexpr int R = r_for(NW);
+    constexpr int YS = stride_for(NW + (HID ? 1 : 0));
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        uint32_t yl = r * kThreads + warp * 32 + lane;
+        valid[r] = yl < ti.nyv;
+        uint64_t y = ti.y0 + (valid[r] ? yl : 0u); // invalid lanes duplicate entry y0
+        uint32_t v[YS];
+        vload_global<YS>(a.ytab + y * YS, v);
+#pragma unroll
+        for (int w = 0; w < NW; ++w) Y[r][w] = v[w];
+        idY[r] = HID ? v[NW] : 0u;
+    }
+}
+
+template <int NW, bool HID>
+__global__ void __launch_bounds__(kThreads) tab_round(TabArgs a) {
+    constexpr int R = r_for(NW);
+    constexpr int YC = R * kThreads;
+    constexpr int XS = stride_for(NW + (HID ? 1 : 0));
+    __shared__ __align__(16) uint32_t xs[kTX * XS];
+    __shared__ TileInfo ti;
+    const uint32_t lane = threadIdx.x & 31;
+    unsigned long long seen = ~0ull; // lane 0's view of the global best key
+    unsigned long long done_local = 0;
+
+    for (uint64_t tile = a.tile_lo + blockIdx.x; tile < a.tile_hi; tile += gridDim.x) {
+        if (threadIdx.x == 0) {
+            unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
+            ti.stop = (g >> kKeyShift) <= a.stop_at;
+            if (!ti.stop) {
+                decode_tile<YC>(a, tile, ti);
+                done_local += uint64_t(ti.nx) * ti.nyv;
+            }
+        }
+        __syncthreads();
+        if (ti.stop) break;
+        if (threadIdx.x < ti.nx) build_prefix<NW, HID>(a, ti.e, ti.x0 + threadIdx.x, xs + threadIdx.x * XS);
+        uint32_t Y[R][NW], idY[R];
+        bool valid[R];
+        load_suffixes<NW, HID>(a, ti, Y, idY, valid);
+        __syncthreads();
+
+        uint32_t best = 0xFFFFFFFFu;
+        const uint32_t nx = ti.nx;
+        for (uint32_t xi = 0; xi < nx; ++xi) {
+            uint32_t X[XS];
+            vload<XS>(xs + xi * XS, X);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int i = 0; i < NW; ++i) w += __popc(X[i] ^ Y[r][i]);
+                if (HID) w += X[NW] + idY[r];
+                best = min(best, w);
+            }
+        }
+        best += a.add_const;
+        best = __reduce_min_sync(0xFFFFFFFFu, best);
+        if (lane == 0) {
+            unsigned long long key = (static_cast<unsigned long long>(best) << kKeyShift) | tile;
+            if (key < seen) {
+                unsigned long long old = atomicMin(a.best_key, key);
+                seen = old < key ? old : key;
+            }
+        }
+        __syncthreads(); // xs / ti reused by the next tile
+    }
+    if (threadIdx.x == 0 && done_local) atomicAdd(a.evaluated, done_local);
+}
+
+// witness: the smallest (x_local, y_local) of the tile whose weight == target
+template <int NW, bool HID>
+__global__ void __launch_bounds__(kThreads) tab_find(TabArgs a) {
+    constexpr int R = r_for(NW);
+    constexpr int YC = R * kThreads;
+    constexpr int XS = stride_for(NW + (HID ? 1 : 0));
+    __shared__ __align__(16) uint32_t xs[kTX * XS];
+    __shared__ TileInfo ti;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) decode_tile<YC>(a, a.tile_lo, ti);
+    __syncthreads();
+    if (threadIdx.x < ti.nx) build_prefix<NW, HID>(a, ti.e, ti.x0 + threadIdx.x, xs + threadIdx.x * XS);
+    uint32_t Y[R][NW], idY[R];
+    bool valid[R];
+    load_suffixes<NW, HID>(a, ti, Y, idY, valid);
+    __syncthreads();
+    unsigned long long cand = ~0ull;
+    for (uint32_t xi = 0; xi < ti.nx; ++xi) {
+        uint32_t X[XS];
+        vload<XS>(xs + xi * XS, X);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            uint32_t w = 0;
+#pragma unroll
+            for (int i = 0; i < NW; ++i) w += __popc(X[i] ^ Y[r][i]);
+            if (HID) w += X[NW] + idY[r];
+            w += a.add_const;
+            uint32_t yl = r * kThreads + warp * 32 + lane;
+            if (valid[r] && w == a.find_target) {
+                unsigned long long c = (static_cast<unsigned long long>(xi) << 32) | yl;
+                cand = c < cand ? c : cand;
+            }
+        }
+    }
+    if (cand != ~0ull) atomicMin(a.find_out, cand);
+}
+
+// full weight histogram (config 5): per-warp privatized bins in smem
+template <int NW, bool HID>
+__global__ void __launch_bounds__(kThreads) tab_hist(TabArgs a) {
+    constexpr int R = r_for(NW);
+    constexpr int YC = R * kThreads;
+    constexpr int XS = stride_for(NW + (HID ? 1 : 0));
+    extern __shared__ __align__(16) uint32_t dyn[];
+    uint32_t* xs = dyn;
+    uint32_t* bins = dyn + kTX * XS; // kWarps x nbins
+    __shared__ TileInfo ti;
+    const uint32_t warp = threadIdx.x >> 5;
+    for (uint32_t i = threadIdx.x; i < kWarps * a.nbins; i += kThreads) bins[i] = 0;
+    unsigned long long done_local = 0;
+    uint32_t* mybins = bins + warp * a.nbins;
+    for (uint64_t tile = a.tile_lo + blockIdx.x; tile < a.tile_hi; tile += gridDim.x) {
+        if (threadIdx.x == 0) {
+            decode_tile<YC>(a, tile, ti);
+            done_local += uint64_t(ti.nx) * ti.nyv;
+        }
+        __syncthreads();
+        if (threadIdx.x < ti.nx) build_prefix<NW, HID>(a, ti.e, ti.x0 + threadIdx.x, xs + threadIdx.x * XS);
+        uint32_t Y[R][NW], idY[R];
+        bool valid[R];
+        load_suffixes<NW, HID>(a, ti, Y, idY, valid);
+        __syncthreads();
+        for (uint32_t xi = 0; xi < ti.nx; ++xi) {
+            uint32_t X[XS];
+            vload<XS>(xs + xi * XS, X);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                uint32_t w = a.add_const;
+#pragma unroll
+                for (int i = 0; i < NW; ++i) w += __popc(X[i] ^ Y[r][i]);
+                if (HID) w += X[NW] + idY[r];
+                if (valid[r]) atomicAdd(mybins + w, 1u);
+            }
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < a.nbins; b += kThreads) {
+        unsigned long long s = 0;
+        for (int w = 0; w < kWarps; ++w) s += bins[w * a.nbins + b];
+        if (s) atomicAdd(a.hist + b, s);
+    }
+    if (threadIdx.x == 0 && done_local) atomicAdd(a.evaluated, done_local);
+}
+
+// ------------------------------------------------------- revolving door
+// Each thread walks RD_CHUNK consecutive ranks of the revolving-door order
+// (Knuth 7.2.1.3 Algorithm R; host.cpp rd_unrank) starting from its unranked
+// first combination. Gamma_j rows live in shared memory; one 3-input XOR per
+// word per step (row out ^ row in).
+constexpr uint32_t kRdChunk = 2048;
+constexpr int kRdThreads = 256;
+
+struct RdArgs {
+    const uint32_t* rows;
+    const uint64_t* binom;
+    uint32_t k, c, id_rows, add_const, stop_at;
+    uint64_t total;              // C(k, c)
+    uint64_t task_lo, task_hi;   // chunk range
+    unsigned long long* best_key;
+    unsigned long long* evaluated;
+    unsigned long long* find_out;
+    uint32_t find_target;
+};
+
+__device__ __forceinline__ void rd_unrank_dev(const uint64_t* __restrict__ T, uint32_t c,
+                                              uint64_t rank, uint32_t* idx) {
+    uint64_t r = rank;
+    for (uint32_t t = c; t >= 1; --t) {
+        // smallest x >= t-1 with C(x+1, t) > r  (binary search on x in [t-1, 1023])
+        uint32_t lo = t - 1, hi = kMaxK - 1;
+        while (lo < hi) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (BT(T, mid + 1, t) > r) hi = mid; else lo = mid + 1;
+        }
+        idx[t - 1] = lo;
+        r = BT(T, lo + 1, t) - 1 - r;
+    }
+}
+
+// Algorithm R successor on c_1 < ... < c_t (cc[0] = c_1), cc[t] = k sentinel.
+// Returns false at the end; sets out/in rows.
+__device__ __forceinline__ bool rd_next(uint32_t* cc, uint32_t t, uint32_t& out, uint32_t& in) {
+    if (t & 1) {
+        if (cc[0] + 1 < cc[1]) { out = cc[0]; in = cc[0] + 1; cc[0] += 1; return true; }
+    } else {
+        if (cc[0] > 0) { out = cc[0]; in = cc[0] - 1; cc[0] -= 1; return true; }
+    }
+    // j = 2..t: R4 when (j + t) odd, R5 when (j + t) even
+    for (uint32_t j = 2; j <= t; ++j) {
+        if ((j + t) & 1) { // R4: try to decrease c_j (c_j = c_{j-1} + 1)
+            if (cc[j - 1] >= j) {
+                out = cc[j - 1]; in = j - 2;
+                cc[j - 1] = cc[j - 2]; cc[j - 2] = j - 2;
+                return true;
+            }
+        } else {           // R5: try to increase c_j (c_{j-1} = j - 2)
+            if (cc[j - 1] + 1 < cc[j]) {
+                out = j - 2; in = cc[j - 1] + 1;
+                cc[j - 2] = cc[j - 1]; cc[j - 1] += 1;
+                return true;
+            }
+        }
+    }
+    return false;
+}
+
+template <int NW, bool FIND>
+__global__ void __launch_bounds__(kRdThreads) rd_round(RdArgs a) {
+    extern __shared__ __align__(16) uint32_t srows[]; // k x NW
+    for (uint32_t i = threadIdx.x; i < a.k * NW; i += blockDim.x) srows[i] = a.rows[i];
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    unsigned long long seen = ~0ull, done_local = 0;
+    uint32_t cc[kMaxC + 1];
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t chunk = a.task_lo + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;; chunk += stride) {
+        // warp-uniform loop exit: all lanes of a warp iterate together
+        bool active = chunk < a.task_hi;
+        if (!FIND) {
+            unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
+            if ((g >> kKeyShift) <= a.stop_at) active = false;
+        }
+        if (__all_sync(0xFFFFFFFFu, !active)) break;
+        uint32_t best = 0xFFFFFFFFu;
+        uint64_t best_rank = ~0ull;
+        if (active) {
+            uint64_t r0 = chunk * kRdChunk;
+            uint64_t r1 = umin64(r0 + kRdChunk, a.total);
+            rd_unrank_dev(a.binom, a.c, r0, cc);
+            cc[a.c] = a.k;
+            uint32_t cw[NW];
+#pragma unroll
+            for (int w = 0; w < NW; ++w) cw[w] = 0;
+            uint32_t id = 0;
+            for (uint32_t i = 0; i < a.c; ++i) {
+#pragma unroll
+                for (int w = 0; w < NW; ++w) cw[w] ^= srows[cc[i] * NW + w];
+                id += cc[i] < a.id_rows;
+            }
+            for (uint64_t rk = r0;;) {
+                uint32_t w = id + a.add_const;
+#pragma unroll
+                for (int i = 0; i < NW; ++i) w += __popc(cw[i]);
+                if (FIND) {
+                    if (w == a.find_target && rk < best_rank) best_rank = rk;
+                } else {
+                    best = min(best, w);
+                }
+                if (++rk >= r1) break;
+                uint32_t o, n;
+                rd_next(cc, a.c, o, n);
+#pragma unroll
+                for (int i = 0; i < NW; ++i) cw[i] ^= srows[o * NW + i] ^ srows[n * NW + i];
+                id += (n < a.id_rows) - (o < a.id_rows);
+            }
+            done_local += r1 - r0;
+        }
+        if (FIND) {
+            if (best_rank != ~0ull) atomicMin(a.find_out, best_rank);
+        } else {
+            uint32_t wmin = __reduce_min_sync(0xFFFFFFFFu, best);
+            // lowest chunk id among lanes achieving the warp min (deterministic key)
+            unsigned long long mykey = (best == wmin && active)
+                ? ((static_cast<unsigned long long>(wmin) << kKeyShift) | chunk) : ~0ull;
+            for (int off = 16; off; off >>= 1) {
+                unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, mykey, off);
+                mykey = o < mykey ? o : mykey;
+            }
+            if (lane == 0 && mykey < seen) {
+                unsigned long long old = atomicMin(a.best_key, mykey);
+                seen = old < mykey ? old : mykey;
+            }
+        }
+    }
+    if (!FIND && done_local) atomicAdd(a.evaluated, done_local);
+}
+
+// ------------------------------------------------------------ dispatch
+template <template <int, bool> class F, typename... Args>
+void dispatch_nw_hid(uint32_t nw, bool hid, Args&&... args) {
+#define MDG_CASE(N)                                                              \
+    case N:                                                                      \
+        if (hid) F<N, true>::run(args...); else F<N, false>::run(args...);       \
+        break;
+    switch (nw) {
+        MDG_CASE(1) MDG_CASE(2) MDG_CASE(3) MDG_CASE(4) MDG_CASE(5) MDG_CASE(6) MDG_CASE(7)
+        MDG_CASE(8) MDG_CASE(9) MDG_CASE(10) MDG_CASE(11) MDG_CASE(12) MDG_CASE(13)
+        MDG_CASE(14) MDG_CASE(15) MDG_CASE(16)
+        default: throw std::invalid_argument("row width beyond the device limit");
+    }
+#undef MDG_CASE
+}
+
+template <int NW, bool HID>
+struct YtabLaunch {
+    static void run(const uint32_t* rows, const uint64_t* T, uint32_t k, uint32_t s,
+                    uint32_t id_rows, uint64_t count, uint32_t* out, cudaStream_t st) {
+        uint64_t blocks = (count + 255) / 256;
+        ytab_build<NW, HID><<<dim3(uint32_t(blocks)), 256, 0, st>>>(rows, T, k, s, id_rows, count, out);
+    }
+};
+
+template <int NW, bool HID>
+struct TabLaunch {
+    // grid: number of tiles for mode 0/2 (clamped to the resident-block count)
+    static void run(const TabArgs& a, uint64_t grid, cudaStream_t st, int mode, size_t dyn, int sms) {
+        if (mode == 0) {
+            static int occ = 0;
+            if (!occ) {
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tab_round<NW, HID>, kThreads, 0);
+                if (occ < 1) occ = 1;
+            }
+            uint64_t g = std::max<uint64_t>(1, std::min<uint64_t>(grid, uint64_t(sms) * occ));
+            tab_round<NW, HID><<<uint32_t(g), kThreads, 0, st>>>(a);
+        }
+        else if (mode == 1) tab_find<NW, HID><<<1, kThreads, 0, st>>>(a);
+        else {
+            auto fn = tab_hist<NW, HID>;
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, dyn);
+            if (occ < 1) occ = 1;
+            uint64_t g = std::max<uint64_t>(1, std::min<uint64_t>(grid, uint64_t(sms) * occ));
+            fn<<<uint32_t(g), kThreads, dyn, st>>>(a);
+        }
+    }
+};
+
+template <int NW, bool FIND>
+struct RdLaunchT {
+    static void run(const RdArgs& a, int grid, cudaStream_t st) {
+        size_t smem = size_t(a.k) * NW * 4;
+        auto fn = rd_round<NW, FIND>;
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        fn<<<grid, kRdThreads, smem, st>>>(a);
+    }
+};
+template <int NW, bool FIND>
+struct RdLaunch : RdLaunchT<NW, FIND> {};
+
+} // namespace
+
+// ================================================================ host side
+uint32_t tab_yc(uint32_t nw32) { return uint32_t(r_for(int(nw32))) * kThreads; }
+uint32_t tab_tx() { return kTX; }
+
+static uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+static uint64_t plan_cost(uint32_t k, uint32_t c, uint32_t s, uint32_t TX, uint32_t YC,
+                          uint64_t* tiles_out) {
+    uint32_t p = c - s;
+    uint64_t cost = 0, tiles = 0;
+    for (uint32_t e = p - 1; e + s <= k - 1; ++e) {
+        uint64_t NX = binomial(e, p - 1), NY = binomial(k - 1 - e, s);
+        uint64_t ntx = ceil_div(NX, TX), nty = ceil_div(NY, YC);
+        tiles += ntx * nty;
+        cost += NX * nty * YC + ntx * nty * uint64_t(YC) * 24; // masked lanes + per-tile overhead
+    }
+    if (tiles_out) *tiles_out = tiles;
+    return cost;
+}
+
+TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32) {
+    TabPlan pl;
+    pl.k = k;
+    pl.c = c;
+    pl.TX = kTX;
+    pl.YC = tab_yc(nw32);
+    uint32_t best_s = 0;
+    if (c >= 2) {
+        uint64_t best_cost = ~uint64_t{0};
+        for (uint32_t s = 1; s <= c - 1; ++s) {
+            uint64_t entries = binomial(k, s);
+            if (entries > (uint64_t{1} << 22) && s > 1) break;
+            uint64_t cost = plan_cost(k, c, s, pl.TX, pl.YC, nullptr);
+            if (cost < best_cost) { best_cost = cost; best_s = s; }
+        }
+    }
+    pl.s = best_s;
+    pl.p = c - best_s;
+    pl.emin = pl.p - 1;
+    pl.emax = k - 1 - pl.s;
+    pl.prefix.assign(1, 0);
+    for (uint32_t e = pl.emin; e <= pl.emax; ++e) {
+        uint64_t NX = binomial(e, pl.p - 1), NY = binomial(k - 1 - e, pl.s);
+        pl.prefix.push_back(pl.prefix.back() + ceil_div(NX, pl.TX) * ceil_div(NY, pl.YC));
+    }
+    return pl;
+}
+
+// host colex unrank: t-subset of [0, hi) with colex rank r, ascending
+static void colex_unrank_host(uint64_t r, uint32_t t, uint32_t hi, uint32_t* out) {
+    for (uint32_t i = t; i >= 1; --i) {
+        uint32_t x = hi - 1;
+        while (binomial(x, i) > r) --x;
+        out[i - 1] = x;
+        r -= binomial(x, i);
+        hi = x;
+    }
+}
+
+void tab_decode(const TabPlan& pl, uint64_t tile, uint32_t x_local, uint32_t y_local, uint32_t* idx) {
+    uint32_t i = uint32_t(std::upper_bound(pl.prefix.begin(), pl.prefix.end(), tile) - pl.prefix.begin()) - 1;
+    uint32_t e = pl.emin + i;
+    uint64_t local = tile - pl.prefix[i];
+    uint64_t NY = binomial(pl.k - 1 - e, pl.s);
+    uint64_t nty = ceil_div(NY, pl.YC);
+    uint64_t tx = local / nty, ty = local % nty;
+    uint64_t x = tx * pl.TX + x_local, y = ty * pl.YC + y_local;
+    std::vector<uint32_t> out;
+    std::vector<uint32_t> tmp(pl.c + 1);
+    if (pl.p > 1) colex_unrank_host(x, pl.p - 1, e, tmp.data());
+    for (uint32_t q = 0; q + 1 < pl.p; ++q) out.push_back(tmp[q]);
+    out.push_back(e);
+    if (pl.s) {
+        colex_unrank_host(y, pl.s, pl.k, tmp.data());
+        for (uint32_t q = 0; q < pl.s; ++q) out.push_back(pl.k - 1 - tmp[q]);
+    }
+    std::sort(out.begin(), out.end());
+    std::copy(out.begin(), out.end(), idx);
+}
+
+// ------------------------------------------------------------ NCCL (dlopen)
+namespace {
+typedef struct { char internal[128]; } ncclUniqueId_t;
+typedef void* ncclComm_t;
+struct NcclApi {
+    void* h = nullptr;
+    int (*GetUniqueId)(ncclUniqueId_t*) = nullptr;
+    int (*CommInitRank)(ncclComm_t*, int, ncclUniqueId_t, int) = nullptr;
+    int (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    int (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(int) = nullptr;
+};
+NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* nm : names) {
+            api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+            if (api.h) break;
+        }
+        if (!api.h) return;
+        api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(api.h, "ncclGetUniqueId"));
+        api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(api.h, "ncclCommInitRank"));
+        api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(api.h, "ncclAllReduce"));
+        api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.h, "ncclCommDestroy"));
+        api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.h, "ncclGetErrorString"));
+    });
+    if (!api.h || !api.AllReduce) throw std::runtime_error("NCCL (libnccl.so.2) not available");
+    return api;
+}
+constexpr int kNcclUint64 = 5; // ncclUint64
+constexpr int kNcclMin = 3;    // ncclMin
+} // namespace
+
+// ------------------------------------------------------------ Engine impl
+struct GammaDev {
+    uint32_t* rows = nullptr;  // k x nw (compacted)
+    uint32_t nw = 0;
+    uint32_t id_rows = 0;      // identity rows [0, id_rows)
+    uint32_t n_compact = 0;
+    std::vector<uint32_t> host_rows; // compacted copy for witness checks
+};
+
+struct Engine::Impl {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, tev0 = nullptr, tev1 = nullptr;
+    Engine::Counters cnt;
+    uint64_t* binom = nullptr;
+    unsigned long long* scratch = nullptr;   // [0] best key, [1] evaluated, [2] find
+    unsigned long long* host_scratch = nullptr; // pinned
+    uint64_t* prefix_dev = nullptr;
+    uint64_t* prefix_host = nullptr;         // pinned
+    size_t prefix_cap = 0;
+    unsigned long long* hist_dev = nullptr;
+    size_t hist_cap = 0;
+    std::vector<GammaDev> gammas;
+    std::map<std::pair<uint32_t, uint32_t>, uint32_t*> ytabs; // (j, s) -> table
+    ncclComm_t comm = nullptr;
+    uint64_t* red_dev = nullptr;
+    size_t red_cap = 0;
+};
+
+static std::vector<uint64_t> make_binom_table() {
+    std::vector<uint64_t> T(size_t(kMaxK + 1) * kBT, 0);
+    for (uint32_t x = 0; x <= kMaxK; ++x) {
+        T[size_t(x) * kBT] = 1;
+        for (uint32_t t = 1; t <= kMaxC && t <= x; ++t) {
+            uint64_t a = T[size_t(x - 1) * kBT + t - 1], b = (t <= x - 1) ? T[size_t(x - 1) * kBT + t] : 0;
+            uint64_t s = a + b;
+            T[size_t(x) * kBT + t] = (s < a || a == ~0ull || b == ~0ull) ? ~0ull : s;
+        }
+    }
+    return T;
+}
+
+Engine::Engine(int device) : device_(device), impl_(new Impl) {
+    int count = 0;
+    CK(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw std::invalid_argument("mdg: no such CUDA device");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    sms_ = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&impl_->ev0));
+    CK(cudaEventCreate(&impl_->ev1));
+    CK(cudaEventCreate(&impl_->tev0));
+    CK(cudaEventCreate(&impl_->tev1));
+    auto T = make_binom_table();
+    CK(cudaMalloc(&impl_->binom, T.size() * 8));
+    CK(cudaMemcpy(impl_->binom, T.data(), T.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&impl_->scratch, 4 * 8));
+    CK(cudaHostAlloc(&impl_->host_scratch, 4 * 8, cudaHostAllocDefault));
+    impl_->prefix_cap = kMaxK + 2;
+    CK(cudaMalloc(&impl_->prefix_dev, impl_->prefix_cap * 8));
+    CK(cudaHostAlloc(&impl_->prefix_host, impl_->prefix_cap * 8, cudaHostAllocDefault));
+}
+
+Engine::~Engine() {
+    if (!impl_) return;
+    cudaSetDevice(device_);
+    if (impl_->stream) cudaStreamSynchronize(impl_->stream);
+    for (auto& g : impl_->gammas) cudaFree(g.rows);
+    for (auto& kv : impl_->ytabs) cudaFree(kv.second);
+    if (impl_->comm) {
+        try { nccl().CommDestroy(impl_->comm); } catch (...) {}
+    }
+    cudaFree(impl_->red_dev);
+    cudaFree(impl_->hist_dev);
+    cudaFree(impl_->binom);
+    cudaFree(impl_->scratch);
+    cudaFree(impl_->prefix_dev);
+    cudaFreeHost(impl_->host_scratch);
+    cudaFreeHost(impl_->prefix_host);
+    cudaEventDestroy(impl_->ev0);
+    cudaEventDestroy(impl_->ev1);
+    cudaEventDestroy(impl_->tev0);
+    cudaEventDestroy(impl_->tev1);
+    cudaStreamDestroy(impl_->stream);
+}
+
+void Engine::load(uint32_t m, uint32_t k, uint32_t n, const uint64_t* rows, const uint32_t* ranks) {
+    if (m < 1 || k < 1 || n < 1) throw std::invalid_argument("mdg_load: empty matrix set");
+    if (k > kMaxK) throw std::invalid_argument("mdg_load: k exceeds the device limit of 1024 rows");
+    CK(cudaSetDevice(device_));
+    CK(cudaStreamSynchronize(impl_->stream));
+    for (auto& g : impl_->gammas) cudaFree(g.rows);
+    for (auto& kv : impl_->ytabs) cudaFree(kv.second);
+    impl_->gammas.clear();
+    impl_->ytabs.clear();
+    const uint32_t W = (n + 63) / 64;
+    for (uint32_t j = 0; j < m; ++j) {
+        const uint64_t* G = rows + size_t(j) * k * W;
+        uint32_t rk = ranks ? ranks[j] : 0;
+        uint32_t off = j * k;
+        if (ranks) {
+            if (rk > k || off + rk > n) throw std::invalid_argument("mdg_load: rank out of range");
+            // the identity block the kernels elide must really be there (gamma.cpp:44-71)
+            for (uint32_t r = 0; r < k; ++r)
+                for (uint32_t t = 0; t < rk; ++t) {
+                    uint32_t col = off + t;
+                    bool bit = (G[size_t(r) * W + col / 64] >> (col % 64)) & 1u;
+                    if (bit != (r == t))
+                        throw std::invalid_argument("mdg_load: Gamma " + std::to_string(j) +
+                                                    " lacks its identity block");
+                }
+        }
+        GammaDev gd;
+        gd.id_rows = rk;
+        gd.n_compact = n - rk;
+        gd.nw = std::max<uint32_t>(1, (gd.n_compact + 31) / 32);
+        if (gd.nw > kMaxWords32)
+            throw std::invalid_argument("mdg_load: row width exceeds the device limit (n - rank <= 512)");
+        gd.host_rows.assign(size_t(k) * gd.nw, 0);
+        for (uint32_t r = 0; r < k; ++r) {
+            uint32_t o = 0;
+            for (uint32_t col = 0; col < n; ++col) {
+                if (ranks && col >= off && col < off + rk) continue;
+                if ((G[size_t(r) * W + col / 64] >> (col % 64)) & 1u)
+                    gd.host_rows[size_t(r) * gd.nw + o / 32] |= 1u << (o % 32);
+                ++o;
+            }
+        }
+        CK(cudaMalloc(&gd.rows, gd.host_rows.size() * 4));
+        CK(cudaMemcpyAsync(gd.rows, gd.host_rows.data(), gd.host_rows.size() * 4, cudaMemcpyHostToDevice,
+                           impl_->stream));
+        CK(cudaStreamSynchronize(impl_->stream));
+        impl_->cnt.h2d += gd.host_rows.size() * 4;
+        impl_->gammas.push_back(std::move(gd));
+    }
+    m_ = m;
+    k_ = k;
+    n_ = n;
+}
+
+void Engine::check_round(uint32_t j, uint32_t c) const {
+    if (j >= m_) throw std::invalid_argument("round: gamma index out of range");
+    if (c < 1 || c > k_) throw std::invalid_argument("round: need 1 <= g <= k");
+    if (c > kMaxC) throw std::invalid_argument("round: level beyond the device limit of 64");
+    binomial(k_, c); // throws std::overflow_error when C(k, c) exceeds 64 bits
+}
+
+static uint32_t* ensure_ytab(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t s) {
+    auto key = std::make_pair(j, s);
+    auto it = im.ytabs.find(key);
+    if (it != im.ytabs.end()) return it->second;
+    const GammaDev& g = im.gammas[j];
+    bool hid = g.id_rows > 0 && g.id_rows < k;
+    uint32_t YS = uint32_t(stride_for(int(g.nw) + (hid ? 1 : 0)));
+    uint64_t count = binomial(k, s);
+    uint32_t* t = nullptr;
+    CK(cudaMalloc(&t, size_t(count) * YS * 4));
+    dispatch_nw_hid<YtabLaunch>(g.nw, hid, g.rows, im.binom, k, s, g.id_rows, count, t, im.stream);
+    CK(cudaGetLastError());
+    im.cnt.launches += 1;
+    im.ytabs[key] = t;
+    return t;
+}
+
+uint64_t Engine::tasks(uint32_t j, uint32_t c) {
+    check_round(j, c);
+    if (kernel_ == Kernel::rd) return ceil_div(binomial(k_, c), kRdChunk);
+    return make_tab_plan(k_, c, impl_->gammas[j].nw).tiles();
+}
+
+RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t task_lo, uint64_t task_hi) {
+    check_round(j, c);
+    CK(cudaSetDevice(device_));
+    Impl& im = *impl_;
+    const GammaDev& g = im.gammas[j];
+    const bool hid = g.id_rows > 0 && g.id_rows < k_;
+    const uint32_t add_const = (g.id_rows == k_) ? c : 0;
+    RoundResult rr;
+    rr.combinations = binomial(k_, c);
+    CK(cudaMemsetAsync(im.scratch, 0xFF, 8, im.stream));
+    CK(cudaMemsetAsync(im.scratch + 1, 0, 8, im.stream));
+    if (kernel_ == Kernel::tab) {
+        TabPlan pl = make_tab_plan(k_, c, g.nw);
+        uint64_t lo = std::min(task_lo, pl.tiles()), hi = std::min(task_hi, pl.tiles());
+        rr.task_lo = lo;
+        rr.task_hi = hi;
+        uint32_t* yt = ensure_ytab(im, j, k_, pl.s);
+        std::copy(pl.prefix.begin(), pl.prefix.end(), im.prefix_host);
+        CK(cudaMemcpyAsync(im.prefix_dev, im.prefix_host, pl.prefix.size() * 8, cudaMemcpyHostToDevice, im.stream));
+        TabArgs a{};
+        a.rows = g.rows; a.ytab = yt; a.binom = im.binom; a.prefix = im.prefix_dev;
+        a.k = k_; a.p = pl.p; a.s = pl.s; a.emin = pl.emin; a.npiv = uint32_t(pl.prefix.size() - 1);
+        a.id_rows = g.id_rows; a.add_const = add_const; a.stop_at = stop_at;
+        a.tile_lo = lo; a.tile_hi = hi;
+        a.best_key = im.scratch; a.evaluated = im.scratch + 1;
+        CK(cudaEventRecord(im.ev0, im.stream));
+        if (hi > lo) {
+            dispatch_nw_hid<TabLaunch>(g.nw, hid, a, hi - lo, im.stream, 0, size_t(0), sms_);
+            CK(cudaGetLastError());
+            im.cnt.launches += 1;
+        }
+        im.cnt.h2d += pl.prefix.size() * 8;
+        CK(cudaEventRecord(im.ev1, im.stream));
+    } else {
+        uint64_t total = binomial(k_, c);
+        uint64_t chunks = ceil_div(total, kRdChunk);
+        uint64_t lo = std::min(task_lo, chunks), hi = std::min(task_hi, chunks);
+        rr.task_lo = lo;
+        rr.task_hi = hi;
+        RdArgs a{};
+        a.rows = g.rows; a.binom = im.binom; a.k = k_; a.c = c; a.id_rows = g.id_rows;
+        a.add_const = add_const; a.stop_at = stop_at; a.total = total;
+        a.task_lo = lo; a.task_hi = hi;
+        a.best_key = im.scratch; a.evaluated = im.scratch + 1;
+        CK(cudaEventRecord(im.ev0, im.stream));
+        if (hi > lo) {
+            uint64_t threads = hi - lo;
+            int grid = int(std::min<uint64_t>(ceil_div(threads, kRdThreads), uint64_t(sms_) * 8));
+            switch (g.nw) {
+#define RD_CASE(N) case N: RdLaunch<N, false>::run(a, grid, im.stream); break;
+                RD_CASE(1) RD_CASE(2) RD_CASE(3) RD_CASE(4) RD_CASE(5) RD_CASE(6) RD_CASE(7) RD_CASE(8)
+                RD_CASE(9) RD_CASE(10) RD_CASE(11) RD_CASE(12) RD_CASE(13) RD_CASE(14) RD_CASE(15) RD_CASE(16)
+#undef RD_CASE
+                default: throw std::invalid_argument("row width beyond the device limit");
+            }
+            CK(cudaGetLastError());
+            im.cnt.launches += 1;
+        }
+        CK(cudaEventRecord(im.ev1, im.stream));
+    }
+    CK(cudaMemcpyAsync(im.host_scratch, im.scratch, 16, cudaMemcpyDeviceToHost, im.stream));
+    im.cnt.d2h += 16;
+    CK(cudaStreamSynchronize(im.stream));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, im.ev0, im.ev1));
+    rr.ms = ms;
+    rr.key = im.host_scratch[0];
+    rr.evaluated = im.host_scratch[1];
+    rr.w = rr.key == ~0ull ? UINT32_MAX : uint32_t(rr.key >> kKeyShift);
+    rr.stopped = rr.w != UINT32_MAX && rr.w <= stop_at;
+    return rr;
+}
+
+RoundResult Engine::round_hist(uint32_t j, uint32_t c, uint64_t* hist) {
+    check_round(j, c);
+    CK(cudaSetDevice(device_));
+    Impl& im = *impl_;
+    const GammaDev& g = im.gammas[j];
+    const bool hid = g.id_rows > 0 && g.id_rows < k_;
+    const uint32_t add_const = (g.id_rows == k_) ? c : 0;
+    const uint32_t nbins = n_ + 1;
+    if (im.hist_cap < nbins) {
+        cudaFree(im.hist_dev);
+        CK(cudaMalloc(&im.hist_dev, nbins * 8));
+        im.hist_cap = nbins;
+    }
+    RoundResult rr;
+    rr.combinations = binomial(k_, c);
+    TabPlan pl = make_tab_plan(k_, c, g.nw);
+    uint32_t* yt = ensure_ytab(im, j, k_, pl.s);
+    std::copy(pl.prefix.begin(), pl.prefix.end(), im.prefix_host);
+    CK(cudaMemcpyAsync(im.prefix_dev, im.prefix_host, pl.prefix.size() * 8, cudaMemcpyHostToDevice, im.stream));
+    CK(cudaMemsetAsync(im.hist_dev, 0, nbins * 8, im.stream));
+    CK(cudaMemsetAsync(im.scratch + 1, 0, 8, im.stream));
+    TabArgs a{};
+    a.rows = g.rows; a.ytab = yt; a.binom = im.binom; a.prefix = im.prefix_dev;
+    a.k = k_; a.p = pl.p; a.s = pl.s; a.emin = pl.emin; a.npiv = uint32_t(pl.prefix.size() - 1);
+    a.id_rows = g.id_rows; a.add_const = add_const;
+    a.tile_lo = 0; a.tile_hi = pl.tiles();
+    a.evaluated = im.scratch + 1;
+    a.nbins = nbins;
+    a.hist = im.hist_dev;
+    int XS = stride_for(int(g.nw) + (hid ? 1 : 0));
+    size_t dyn = size_t(kTX) * XS * 4 + size_t(kWarps) * nbins * 4;
+    CK(cudaEventRecord(im.ev0, im.stream));
+    dispatch_nw_hid<TabLaunch>(g.nw, hid, a, pl.tiles(), im.stream, 2, dyn, sms_);
+    CK(cudaGetLastError());
+    im.cnt.launches += 1;
+    im.cnt.h2d += pl.prefix.size() * 8;
+    im.cnt.d2h += nbins * 8 + 8;
+    CK(cudaEventRecord(im.ev1, im.stream));
+    CK(cudaMemcpyAsync(hist, im.hist_dev, nbins * 8, cudaMemcpyDeviceToHost, im.stream));
+    CK(cudaMemcpyAsync(im.host_scratch + 1, im.scratch + 1, 8, cudaMemcpyDeviceToHost, im.stream));
+    CK(cudaStreamSynchronize(im.stream));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, im.ev0, im.ev1));
+    rr.ms = ms;
+    rr.evaluated = im.host_scratch[1];
+    rr.task_hi = pl.tiles();
+    for (uint32_t w = 0; w < nbins; ++w)
+        if (hist[w]) { rr.w = w; break; }
+    rr.key = rr.w == UINT32_MAX ? ~0ull : (uint64_t(rr.w) << kKeyShift);
+    return rr;
+}
+
+std::vector<uint32_t> Engine::witness(uint32_t j, uint32_t c, const RoundResult& rr) {
+    check_round(j, c);
+    if (rr.key == ~0ull) throw std::invalid_argument("witness: the round evaluated nothing");
+    CK(cudaSetDevice(device_));
+    Impl& im = *impl_;
+    const GammaDev& g = im.gammas[j];
+    const bool hid = g.id_rows > 0 && g.id_rows < k_;
+    const uint32_t add_const = (g.id_rows == k_) ? c : 0;
+    const uint64_t task = rr.key & ((uint64_t{1} << kKeyShift) - 1);
+    const uint32_t target = uint32_t(rr.key >> kKeyShift);
+    std::vector<uint32_t> idx(c);
+    CK(cudaMemsetAsync(im.scratch + 2, 0xFF, 8, im.stream));
+    if (kernel_ == Kernel::tab) {
+        TabPlan pl = make_tab_plan(k_, c, g.nw);
+        uint32_t* yt = ensure_ytab(im, j, k_, pl.s);
+        std::copy(pl.prefix.begin(), pl.prefix.end(), im.prefix_host);
+        CK(cudaMemcpyAsync(im.prefix_dev, im.prefix_host, pl.prefix.size() * 8, cudaMemcpyHostToDevice, im.stream));
+        TabArgs a{};
+        a.rows = g.rows; a.ytab = yt; a.binom = im.binom; a.prefix = im.prefix_dev;
+        a.k = k_; a.p = pl.p; a.s = pl.s; a.emin = pl.emin; a.npiv = uint32_t(pl.prefix.size() - 1);
+        a.id_rows = g.id_rows; a.add_const = add_const;
+        a.tile_lo = task; a.tile_hi = task + 1;
+        a.find_out = im.scratch + 2;
+        a.find_target = target;
+        dispatch_nw_hid<TabLaunch>(g.nw, hid, a, uint64_t(1), im.stream, 1, size_t(0), sms_);
+        CK(cudaGetLastError());
+        im.cnt.launches += 1;
+        im.cnt.d2h += 8;
+        CK(cudaMemcpyAsync(im.host_scratch + 2, im.scratch + 2, 8, cudaMemcpyDeviceToHost, im.stream));
+        CK(cudaStreamSynchronize(im.stream));
+        uint64_t f = im.host_scratch[2];
+        if (f == ~0ull) throw std::logic_error("witness: winning tile holds no codeword of the round minimum");
+        tab_decode(pl, task, uint32_t(f >> 32), uint32_t(f & 0xFFFFFFFFu), idx.data());
+    } else {
+        RdArgs a{};
+        a.rows = g.rows; a.binom = im.binom; a.k = k_; a.c = c; a.id_rows = g.id_rows;
+        a.add_const = add_const; a.total = binomial(k_, c);
+        a.task_lo = task; a.task_hi = task + 1;
+        a.find_out = im.scratch + 2;
+        a.find_target = target;
+        switch (g.nw) {
+#define RD_CASE(N) case N: RdLaunch<N, true>::run(a, 1, im.stream); break;
+            RD_CASE(1) RD_CASE(2) RD_CASE(3) RD_CASE(4) RD_CASE(5) RD_CASE(6) RD_CASE(7) RD_CASE(8)
+            RD_CASE(9) RD_CASE(10) RD_CASE(11) RD_CASE(12) RD_CASE(13) RD_CASE(14) RD_CASE(15) RD_CASE(16)
+#undef RD_CASE
+            default: throw std::invalid_argument("row width beyond the device limit");
+        }
+        CK(cudaGetLastError());
+        im.cnt.launches += 1;
+        im.cnt.d2h += 8;
+        CK(cudaMemcpyAsync(im.host_scratch + 2, im.scratch + 2, 8, cudaMemcpyDeviceToHost, im.stream));
+        CK(cudaStreamSynchronize(im.stream));
+        uint64_t f = im.host_scratch[2];
+        if (f == ~0ull) throw std::logic_error("witness: winning chunk holds no codeword of the round minimum");
+        rd_unrank(c, f, idx.data());
+    }
+    return idx;
+}
+
+Engine::Counters Engine::counters() const { return impl_->cnt; }
+void Engine::reset_counters() { impl_->cnt = Counters{}; }
+void Engine::timer_start() {
+    CK(cudaSetDevice(device_));
+    CK(cudaEventRecord(impl_->tev0, impl_->stream));
+}
+double Engine::timer_stop_ms() {
+    CK(cudaSetDevice(device_));
+    CK(cudaEventRecord(impl_->tev1, impl_->stream));
+    CK(cudaEventSynchronize(impl_->tev1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, impl_->tev0, impl_->tev1));
+    return ms;
+}
+
+void Engine::nccl_unique_id(uint8_t id[128]) {
+    ncclUniqueId_t u;
+    int rc = nccl().GetUniqueId(&u);
+    if (rc != 0) throw std::runtime_error("ncclGetUniqueId failed");
+    std::memcpy(id, u.internal, 128);
+}
+
+void Engine::nccl_init(const uint8_t id[128], uint32_t rank, uint32_t world) {
+    CK(cudaSetDevice(device_));
+    ncclUniqueId_t u;
+    std::memcpy(u.internal, id, 128);
+    int rc = nccl().CommInitRank(&impl_->comm, int(world), u, int(rank));
+    if (rc != 0) throw std::runtime_error(std::string("ncclCommInitRank: ") + nccl().GetErrorString(rc));
+}
+
+void Engine::nccl_reduce_min(uint64_t* keys, uint32_t count) {
+    if (!impl_->comm) throw std::logic_error("nccl_reduce_min: communicator not initialised");
+    CK(cudaSetDevice(device_));
+    Impl& im = *impl_;
+    if (im.red_cap < count) {
+        cudaFree(im.red_dev);
+        CK(cudaMalloc(&im.red_dev, size_t(count) * 8));
+        im.red_cap = count;
+    }
+    CK(cudaMemcpyAsync(im.red_dev, keys, size_t(count) * 8, cudaMemcpyHostToDevice, im.stream));
+    int rc = nccl().AllReduce(im.red_dev, im.red_dev, count, kNcclUint64, kNcclMin, im.comm, im.stream);
+    im.cnt.h2d += size_t(count) * 8;
+    im.cnt.d2h += size_t(count) * 8;
+    if (rc != 0) throw std::runtime_error(std::string("ncclAllReduce: ") + nccl().GetErrorString(rc));
+    CK(cudaMemcpyAsync(keys, im.red_dev, size_t(count) * 8, cudaMemcpyDeviceToHost, im.stream));
+    CK(cudaStreamSynchronize(im.stream));
+}
+
+} // namespace mdg

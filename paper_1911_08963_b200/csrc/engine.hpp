@@ -1,0 +1,102 @@
+// Device engine of the B200 Brouwer–Zimmermann round (host-facing C++).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "mdg.hpp"
+
+namespace mdg {
+
+class CudaError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+
+enum class Kernel : int { tab = 0, rd = 1 };
+
+// Limits of the device path (checked up front, std::invalid_argument).
+constexpr uint32_t kMaxK = 1024;        // rows of a Gamma
+constexpr uint32_t kMaxC = 64;          // level
+constexpr uint32_t kMaxWords32 = 16;    // 32-bit words of a compacted row (n' <= 512)
+
+struct RoundResult {
+    uint32_t w = UINT32_MAX;
+    bool stopped = false;
+    uint64_t key = ~uint64_t{0};
+    uint64_t combinations = 0;
+    uint64_t evaluated = 0;
+    uint64_t task_lo = 0, task_hi = 0;
+    double ms = 0;
+};
+
+// Pivot split of a level-c round (the "tab" kernel's enumeration): a sorted
+// c-subset S = P ∪ Q with |P| = p, |Q| = s, e = max(P) < min(Q). For pivot e
+// the prefixes are (p-1)-subsets of [0, e) plus e, NX(e) = C(e, p-1), and the
+// suffixes are s-subsets of (e, k), NY(e) = C(k-1-e, s) — a prefix of one
+// suffix table in reverse-colex order. Tiles are TX prefixes x YC suffixes.
+struct TabPlan {
+    uint32_t k = 0, c = 0, p = 0, s = 0, emin = 0, emax = 0;
+    uint32_t TX = 0, YC = 0;
+    std::vector<uint64_t> prefix; // tiles before pivot emin + i; size npiv + 1
+    uint64_t tiles() const { return prefix.empty() ? 0 : prefix.back(); }
+};
+
+class Engine {
+public:
+    explicit Engine(int device);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    // ranks == nullptr: raw matrices (no identity elision)
+    void load(uint32_t m, uint32_t k, uint32_t n, const uint64_t* rows, const uint32_t* ranks);
+    uint32_t m() const { return m_; }
+    uint32_t k() const { return k_; }
+    uint32_t n() const { return n_; }
+
+    void set_kernel(Kernel kern) { kernel_ = kern; }
+    Kernel kernel() const { return kernel_; }
+
+    uint64_t tasks(uint32_t j, uint32_t c);
+    RoundResult round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t task_lo = 0,
+                      uint64_t task_hi = UINT64_MAX);
+    RoundResult round_hist(uint32_t j, uint32_t c, uint64_t* hist);
+    std::vector<uint32_t> witness(uint32_t j, uint32_t c, const RoundResult& rr);
+
+    // NCCL (loaded at runtime) for the multi-GPU reduction
+    void nccl_init(const uint8_t id[128], uint32_t rank, uint32_t world);
+    void nccl_reduce_min(uint64_t* keys, uint32_t count);
+    static void nccl_unique_id(uint8_t id[128]);
+
+    int device() const { return device_; }
+    int sm_count() const { return sms_; }
+
+    // counters (kernel launches, host<->device bytes) and a CUDA-event timer
+    // on the engine's stream (host gaps between launches included)
+    struct Counters { uint64_t launches = 0, h2d = 0, d2h = 0; };
+    Counters counters() const;
+    void reset_counters();
+    void timer_start();
+    double timer_stop_ms();
+
+    struct Impl;
+
+private:
+    void check_round(uint32_t j, uint32_t c) const;
+    int device_ = 0, sms_ = 0;
+    uint32_t m_ = 0, k_ = 0, n_ = 0;
+    Kernel kernel_ = Kernel::tab;
+    std::unique_ptr<Impl> impl_;
+};
+
+TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32);
+uint32_t tab_yc(uint32_t nw32);
+uint32_t tab_tx();
+// reconstruct the combination of tile `tile`, local prefix x / suffix y
+void tab_decode(const TabPlan& plan, uint64_t tile, uint32_t x_local, uint32_t y_local,
+                uint32_t* idx);
+
+} // namespace mdg

@@ -1,0 +1,378 @@
+// Host side of the B200 Brouwer–Zimmermann engine: F2 matrices, the Gamma
+// systematization + permutation search, the bounds and the level loop.
+// Everything here must reproduce the reference bit for bit (Gamma matrices,
+// column_perm, per-round/per-level trace); tests/test_host.py pins it against
+// the golden vectors made from the compiled reference.
+#include <algorithm>
+#include <fstream>
+#include <limits>
+#include <random>
+#include <sstream>
+
+#include "mdg.hpp"
+
+namespace mdg {
+
+// ------------------------------------------------------------- BitMatrix
+void BitMatrix::swap_rows(uint32_t a, uint32_t b) {
+    if (a == b) return;
+    uint64_t* x = row(a);
+    uint64_t* y = row(b);
+    for (uint32_t i = 0; i < W_; ++i) std::swap(x[i], y[i]);
+}
+
+// f2core.cpp:9-16 (column swap; the bits move, nothing else)
+void BitMatrix::swap_cols(uint32_t a, uint32_t b) {
+    if (a == b) return;
+    const uint32_t wa = a >> 6, wb = b >> 6, sa = a & 63, sb = b & 63;
+    for (uint32_t r = 0; r < rows_; ++r) {
+        uint64_t* p = row(r);
+        uint64_t va = (p[wa] >> sa) & 1u, vb = (p[wb] >> sb) & 1u;
+        if (va != vb) {
+            p[wa] ^= uint64_t{1} << sa;
+            p[wb] ^= uint64_t{1} << sb;
+        }
+    }
+}
+
+uint32_t BitMatrix::row_weight(uint32_t r) const {
+    uint32_t w = 0;
+    const uint64_t* p = row(r);
+    for (uint32_t i = 0; i < W_; ++i) w += static_cast<uint32_t>(__builtin_popcountll(p[i]));
+    return w;
+}
+
+namespace {
+// f2core.cpp:63-75: pivot = first row at or below `rank` with a 1 in `col`
+uint32_t rref_in_place(BitMatrix& w) {
+    uint32_t rank = 0;
+    for (uint32_t col = 0; col < w.cols() && rank < w.rows(); ++col) {
+        uint32_t pivot = rank;
+        while (pivot < w.rows() && !w.get(pivot, col)) ++pivot;
+        if (pivot == w.rows()) continue;
+        w.swap_rows(rank, pivot);
+        for (uint32_t r = 0; r < w.rows(); ++r)
+            if (r != rank && w.get(r, col)) w.xor_row(r, rank);
+        ++rank;
+    }
+    return rank;
+}
+} // namespace
+
+uint32_t rank_of(const BitMatrix& m) {
+    BitMatrix w = m;
+    return rref_in_place(w);
+}
+
+BitMatrix rref_of(const BitMatrix& m) {
+    BitMatrix w = m;
+    uint32_t rank = rref_in_place(w);
+    BitMatrix out(rank, m.cols());
+    std::copy(w.data(), w.data() + size_t(rank) * w.words(), out.data());
+    return out;
+}
+
+BitMatrix row_basis(const BitMatrix& m) {
+    BitMatrix b = rref_of(m);
+    if (b.rows() == 0) throw std::invalid_argument("row_basis: zero matrix spans the zero code");
+    return b;
+}
+
+uint64_t hash_rows(const BitMatrix& m) {
+    uint64_t h = 1469598103934665603ull;
+    const uint64_t* p = m.data();
+    for (size_t i = 0, e = size_t(m.rows()) * m.words(); i < e; ++i)
+        for (int b = 0; b < 8; ++b) {
+            h ^= (p[i] >> (8 * b)) & 0xff;
+            h *= 1099511628211ull;
+        }
+    return h;
+}
+
+// ---------------------------------------------------------------- Gammas
+BitMatrix permute_columns(const BitMatrix& m, const std::vector<uint32_t>& perm) {
+    BitMatrix out(m.rows(), m.cols());
+    for (uint32_t j = 0; j < m.cols(); ++j)
+        for (uint32_t r = 0; r < m.rows(); ++r)
+            if (m.get(r, perm[j])) out.set(r, j, true);
+    return out;
+}
+
+// gamma.cpp:32-75 — progressive block diagonalization. Per block, the pivot is
+// the first workable column at or after the target and, in it, the first row
+// at or below the block rank; column swaps are mirrored into column_perm and
+// into every earlier snapshot.
+GammaSet compute_gamma_matrices(const BitMatrix& G) {
+    const uint32_t k = G.rows();
+    const uint32_t n = G.cols();
+    if (k == 0 || k > n) throw std::invalid_argument("compute_gamma_matrices: need 1 <= k <= n");
+    if (rank_of(G) != k)
+        throw std::invalid_argument("compute_gamma_matrices: rank-deficient generator matrix");
+    GammaSet gs;
+    gs.column_perm.resize(n);
+    for (uint32_t i = 0; i < n; ++i) gs.column_perm[i] = i;
+    BitMatrix w = G;
+    for (uint32_t offset = 0; offset < n; offset += k) {
+        uint32_t br = 0;
+        for (; br < k; ++br) {
+            const uint32_t target = offset + br;
+            if (target >= n) break;
+            uint32_t pc = n, pr = k;
+            for (uint32_t c = target; c < n && pc == n; ++c) {
+                const uint32_t wi = c >> 6;
+                const uint64_t bit = uint64_t{1} << (c & 63);
+                for (uint32_t r = br; r < k; ++r)
+                    if (w.row(r)[wi] & bit) { pc = c; pr = r; break; }
+            }
+            if (pc == n) break;
+            if (pc != target) {
+                w.swap_cols(target, pc);
+                std::swap(gs.column_perm[target], gs.column_perm[pc]);
+                for (auto& snap : gs.gammas) snap.swap_cols(target, pc);
+            }
+            if (pr != br) w.swap_rows(br, pr);
+            const uint32_t wi = target >> 6;
+            const uint64_t bit = uint64_t{1} << (target & 63);
+            for (uint32_t r = 0; r < k; ++r)
+                if (r != br && (w.row(r)[wi] & bit)) w.xor_row(r, br);
+        }
+        if (br == 0) break;
+        gs.gammas.push_back(w);
+        gs.ranks.push_back(br);
+        if (br < k) break;
+    }
+    gs.k_last = gs.ranks.back();
+    return gs;
+}
+
+// gamma.cpp:77-94 — identity plus `trials` Fisher–Yates shuffles
+// (util.hpp:28-33, j = next() % i), keeping the lexicographic max of
+// (m, k_last) with the earliest winner on ties.
+GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint64_t seed) {
+    if (trials < 1) throw std::invalid_argument("best_gamma_over_permutations: trials must be >= 1");
+    GammaSet best = compute_gamma_matrices(G);
+    SplitMix64 rng(seed);
+    const uint32_t n = G.cols();
+    for (uint32_t t = 0; t < trials; ++t) {
+        std::vector<uint32_t> perm(n);
+        for (uint32_t i = 0; i < n; ++i) perm[i] = i;
+        for (size_t i = perm.size(); i > 1; --i) {
+            size_t j = static_cast<size_t>(rng.next() % i);
+            std::swap(perm[i - 1], perm[j]);
+        }
+        GammaSet cand = compute_gamma_matrices(permute_columns(G, perm));
+        for (uint32_t j = 0; j < cand.column_perm.size(); ++j)
+            cand.column_perm[j] = perm[cand.column_perm[j]];
+        if (cand.m() > best.m() || (cand.m() == best.m() && cand.k_last > best.k_last))
+            best = std::move(cand);
+    }
+    return best;
+}
+
+// gamma.cpp:96-100
+uint32_t lower_bound(uint32_t m, uint32_t g, uint32_t k, uint32_t k_last) {
+    int64_t partial = static_cast<int64_t>(g) + 1 - static_cast<int64_t>(k) + k_last;
+    if (partial < 0) partial = 0;
+    return (m - 1) * (g + 1) + static_cast<uint32_t>(partial);
+}
+
+// gamma.cpp:102-106
+uint32_t singleton_upper(uint32_t n, uint32_t k) {
+    if (k < 1 || n < k) throw std::invalid_argument("singleton_upper: need n >= k >= 1");
+    return n - k + 1;
+}
+
+// ------------------------------------------------------------ level loop
+// engines.cpp:447-476, verbatim semantics: U from the bounds, L = max(1, lower);
+// for g = 1..k, for each Gamma: the fast path ends the run as soon as U <= L
+// (no L update for that level); otherwise run the round and U = min(U, w).
+// After a full level L = max(L, lower_bound(m, g, k, k_last)); stop at L >= U.
+// Added: the level cap (a round at level g > cap is never run; capped=true)
+// and the trace. rs.stop_at carries the current L to the runner: a round may
+// stop once it has found a weight <= L, because at that point U > L and
+// d >= L, so its minimum is exactly L.
+EngineResult run_bz_loop(const GammaSet& gs, Bounds bounds, const RoundRunner& round,
+                         uint32_t level_cap) {
+    const uint32_t k = gs.k();
+    const uint32_t m = gs.m();
+    uint32_t U = bounds.upper;
+    uint32_t L = bounds.lower < 1 ? 1 : bounds.lower;
+    EngineResult res;
+    bool done = U <= L;
+    for (uint32_t g = 1; !done && g <= k; ++g) {
+        if (level_cap && g > level_cap) {
+            res.capped = true;
+            break;
+        }
+        for (uint32_t j = 0; j < m; ++j) {
+            if (U <= L) {
+                done = true;
+                break;
+            }
+            RoundStats rs;
+            rs.g = g;
+            rs.gamma_index = j;
+            rs.stop_at = L;
+            uint32_t w = round(j, g, rs);
+            res.stats.row_additions += rs.additions;
+            res.stats.combinations += rs.combinations;
+            res.stats.evaluated += rs.evaluated;
+            res.stats.device_ms += rs.device_ms;
+            res.stats.per_g.push_back(rs);
+            res.stats.g_final = g;
+            if (w < U) {
+                U = w;
+                res.witness_round = static_cast<int32_t>(res.stats.rounds.size());
+            } else if (w == U && res.witness_round < 0) {
+                res.witness_round = static_cast<int32_t>(res.stats.rounds.size());
+            }
+            res.stats.rounds.push_back({g, j, w, U});
+        }
+        if (done) break;
+        uint32_t nl = lower_bound(m, g, k, gs.k_last);
+        if (nl > L) L = nl;
+        res.stats.levels.push_back({g, L, U});
+        if (L >= U) done = true;
+    }
+    res.d = U;
+    return res;
+}
+
+// ----------------------------------------------------------------- I/O
+ParseError::ParseError(uint32_t line_no, uint32_t column_no, const std::string& message)
+    : std::invalid_argument("line " + std::to_string(line_no) + ", column " +
+                            std::to_string(column_no) + ": " + message),
+      line(line_no),
+      column(column_no) {}
+
+namespace {
+bool blank_or_comment(const std::string& line) {
+    for (char ch : line) {
+        if (ch == ' ' || ch == '\t' || ch == '\r') continue;
+        return ch == '#';
+    }
+    return true;
+}
+std::string strip(const std::string& line) {
+    size_t b = line.find_first_not_of(" \t\r");
+    if (b == std::string::npos) return "";
+    size_t e = line.find_last_not_of(" \t\r");
+    return line.substr(b, e - b + 1);
+}
+} // namespace
+
+// io.cpp:33-73 — header "n k", then k rows of exactly n symbols from {0,1};
+// '#' comment and blank lines anywhere; errors carry line and column.
+BitMatrix parse_matrix(const std::string& text) {
+    std::istringstream in(text);
+    std::string line;
+    uint32_t line_no = 0;
+    uint64_t n = 0, k = 0;
+    bool have_header = false;
+    while (!have_header) {
+        if (!std::getline(in, line)) throw ParseError(line_no + 1, 1, "missing header line");
+        ++line_no;
+        if (blank_or_comment(line)) continue;
+        std::istringstream hs(strip(line));
+        if (!(hs >> n >> k)) throw ParseError(line_no, 1, "header must be two integers: n k");
+        std::string rest;
+        if (hs >> rest) throw ParseError(line_no, 1, "header must be exactly: n k");
+        if (n < 1 || k < 1) throw ParseError(line_no, 1, "n and k must be >= 1");
+        if (n > 1u << 20 || k > 1u << 20) throw ParseError(line_no, 1, "unreasonable dimensions");
+        have_header = true;
+    }
+    BitMatrix M(static_cast<uint32_t>(k), static_cast<uint32_t>(n));
+    uint32_t row = 0;
+    while (row < k) {
+        if (!std::getline(in, line))
+            throw ParseError(line_no + 1, 1,
+                             "expected " + std::to_string(k) + " rows, got " + std::to_string(row));
+        ++line_no;
+        if (blank_or_comment(line)) continue;
+        std::string data = strip(line);
+        if (data.size() != n)
+            throw ParseError(line_no, static_cast<uint32_t>(data.size()) + 1,
+                             "row must have exactly " + std::to_string(n) + " symbols");
+        for (uint32_t c = 0; c < n; ++c) {
+            if (data[c] == '1') M.set(row, c, true);
+            else if (data[c] != '0') throw ParseError(line_no, c + 1, "symbols must be 0 or 1");
+        }
+        ++row;
+    }
+    return M;
+}
+
+BitMatrix parse_matrix_file(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw std::invalid_argument("cannot open file: " + path);
+    std::stringstream ss;
+    ss << in.rdbuf();
+    return parse_matrix(ss.str());
+}
+
+// io.cpp:81-88
+std::string serialize_matrix(const BitMatrix& M) {
+    std::string out = std::to_string(M.cols()) + " " + std::to_string(M.rows()) + "\n";
+    out.reserve(out.size() + size_t(M.rows()) * (M.cols() + 1));
+    for (uint32_t r = 0; r < M.rows(); ++r) {
+        for (uint32_t c = 0; c < M.cols(); ++c) out += M.get(r, c) ? '1' : '0';
+        out += '\n';
+    }
+    return out;
+}
+
+// SURVEY.md §8d input convention (BASELINE.json configs): mt19937_64(seed),
+// one draw per bit, bit = draw & 1, row-major over A; G = (I_k | A).
+BitMatrix gen_matrix(uint32_t n, uint32_t k, uint64_t seed, bool identity) {
+    if (k < 1 || n < 1 || (identity && k > n)) throw std::invalid_argument("gen_matrix: bad shape");
+    std::mt19937_64 eng(seed);
+    BitMatrix G(k, n);
+    const uint32_t off = identity ? k : 0;
+    for (uint32_t r = 0; r < k; ++r) {
+        if (identity) G.set(r, r, true);
+        for (uint32_t c = off; c < n; ++c)
+            if (eng() & 1) G.set(r, c, true);
+    }
+    return G;
+}
+
+// ------------------------------------------------------------ binomials
+// enumeration.cpp:9-20: exact, throws std::overflow_error past 64 bits
+uint64_t binomial(uint32_t p, int64_t q) {
+    if (q < 0 || q > static_cast<int64_t>(p)) return 0;
+    uint64_t qq = static_cast<uint64_t>(q);
+    if (qq > p - qq) qq = p - qq;
+    unsigned __int128 c = 1;
+    for (uint64_t i = 1; i <= qq; ++i) {
+        c = c * (p - qq + i) / i;
+        if (c > std::numeric_limits<uint64_t>::max())
+            throw std::overflow_error("binomial: value exceeds 64 bits");
+    }
+    return static_cast<uint64_t>(c);
+}
+
+// Revolving-door order R(n,t) = R(n-1,t) ++ reverse(R(n-1,t-1)) (n-1 appended)
+// — Knuth TAOCP 7.2.1.3. No reference counterpart (its only Gray machinery is
+// the binary reflected code, enumeration.hpp:19-20). idx ascending.
+//   rank(c_1 < ... < c_t) = sum_i (-1)^(t-i) (C(c_i + 1, i) - 1)
+//   unrank: for t down to 1, c_t = min{x : C(x+1, t) > r}, r <- C(x+1,t) - 1 - r
+void rd_unrank(uint32_t c, uint64_t rank, uint32_t* idx) {
+    uint64_t r = rank;
+    for (uint32_t t = c; t >= 1; --t) {
+        uint32_t x = t - 1;
+        while (binomial(x + 1, t) <= r) ++x;
+        idx[t - 1] = x;
+        r = binomial(x + 1, t) - 1 - r;
+    }
+}
+
+uint64_t rd_rank(uint32_t c, const uint32_t* idx) {
+    int64_t s = 0;
+    for (uint32_t i = 1; i <= c; ++i) {
+        int64_t term = static_cast<int64_t>(binomial(idx[i - 1] + 1, i)) - 1;
+        s += ((c - i) % 2 == 0) ? term : -term;
+    }
+    return static_cast<uint64_t>(s);
+}
+
+} // namespace mdg

@@ -1,0 +1,152 @@
+// `mindist` command line for the GPU engine — the reference's `mindist
+// mindist <file> --algorithm ... --seed S --trials T` (cli.cpp:69-112,
+// 257-278) with `--algorithm gpu`, emitting the reference's JSON record
+// (cli.cpp:223-238) plus the new keys (witness, trace, levels, capped, ...).
+// Exit codes as the reference: 0 ok, 1 internal error, 2 invalid input or
+// config (cli.cpp:198-219).
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <iostream>
+#include <string>
+#include <vector>
+
+#include "mdg.h"
+#include "mdg.hpp"
+
+namespace {
+
+int usage() {
+    std::cerr << "usage:\n"
+                 "  mindist mindist FILE [--algorithm gpu] [--kernel tab|rd] [--trials T]\n"
+                 "                       [--seed S] [--level-cap C] [--device D] [--pretty]\n"
+                 "  mindist gen --n N --k K --seed S [--plain]\n";
+    return 2;
+}
+
+int exit_code(int rc) {
+    if (rc == MDG_OK) return 0;
+    std::cerr << (rc == MDG_EINVAL || rc == MDG_EOVERFLOW ? "error: " : "internal error: ")
+              << mdg_last_error() << "\n";
+    return (rc == MDG_EINVAL || rc == MDG_EOVERFLOW) ? 2 : 1;
+}
+
+bool parse_u64(const char* s, uint64_t& out) {
+    char* end = nullptr;
+    errno = 0;
+    unsigned long long v = std::strtoull(s, &end, 10);
+    if (errno || !end || *end || s[0] == '-') return false;
+    out = v;
+    return true;
+}
+
+} // namespace
+
+int main(int argc, char** argv) {
+    if (argc < 2) return usage();
+    std::string cmd = argv[1];
+    if (cmd == "gen") {
+        uint64_t n = 0, k = 0, seed = 0;
+        bool plain = false;
+        for (int i = 2; i < argc; ++i) {
+            std::string a = argv[i];
+            if (a == "--plain") { plain = true; continue; }
+            if (i + 1 >= argc) return usage();
+            uint64_t* dst = a == "--n" ? &n : a == "--k" ? &k : a == "--seed" ? &seed : nullptr;
+            if (!dst || !parse_u64(argv[++i], *dst)) return usage();
+        }
+        try {
+            mdg::BitMatrix M = mdg::gen_matrix(uint32_t(n), uint32_t(k), seed, !plain);
+            std::cout << "# mt19937_64 seed " << seed << (plain ? " (plain)" : " (I|A)") << "\n"
+                      << mdg::serialize_matrix(M);
+        } catch (const std::exception& e) {
+            std::cerr << "error: " << e.what() << "\n";
+            return 2;
+        }
+        return 0;
+    }
+    if (cmd != "mindist" || argc < 3) return usage();
+    std::string path = argv[2];
+    mdg_config cfg;
+    mdg_config_default(&cfg);
+    bool pretty = false;
+    int device = 0;
+    bool seed_given = false;
+    for (int i = 3; i < argc; ++i) {
+        std::string a = argv[i];
+        if (a == "--pretty") { pretty = true; continue; }
+        if (i + 1 >= argc) return usage();
+        std::string v = argv[++i];
+        uint64_t x = 0;
+        if (a == "--algorithm") {
+            if (v != "gpu") {
+                std::cerr << "error: unknown algorithm: " << v << " (this build provides 'gpu')\n";
+                return 2;
+            }
+        } else if (a == "--kernel") {
+            if (v == "tab") cfg.kernel = MDG_KERNEL_TAB;
+            else if (v == "rd") cfg.kernel = MDG_KERNEL_RD;
+            else { std::cerr << "error: unknown kernel: " << v << "\n"; return 2; }
+        } else if (a == "--trials" && parse_u64(v.c_str(), x)) {
+            cfg.trials = uint32_t(x);
+        } else if (a == "--seed" && parse_u64(v.c_str(), x)) {
+            cfg.seed = x;
+            seed_given = true;
+        } else if (a == "--level-cap" && parse_u64(v.c_str(), x)) {
+            cfg.level_cap = uint32_t(x);
+        } else if (a == "--device" && parse_u64(v.c_str(), x)) {
+            device = int(x);
+        } else {
+            std::cerr << "error: bad option " << a << " " << v << "\n";
+            return 2;
+        }
+    }
+    if (!seed_given) { // cli.cpp:46-53 draws and logs a seed
+        cfg.seed = (uint64_t(std::rand()) << 32) ^ uint64_t(std::rand()) ^ uint64_t(time(nullptr));
+        std::cerr << "seed: " << cfg.seed << "\n";
+    }
+    mdg::BitMatrix G;
+    try {
+        G = mdg::parse_matrix_file(path);
+    } catch (const std::invalid_argument& e) {
+        std::cerr << "error: " << e.what() << "\n";
+        return 2;
+    }
+    mdg_ctx* ctx = nullptr;
+    int rc = mdg_open(device, &ctx);
+    if (rc) return exit_code(rc);
+    mdg_run* run = nullptr;
+    rc = mdg_min_weight(ctx, G.data(), G.rows(), G.cols(), &cfg, &run);
+    if (rc) {
+        mdg_close(ctx);
+        return exit_code(rc);
+    }
+    std::vector<char> buf(1 << 20);
+    long len = mdg_run_json(run, buf.data(), buf.size());
+    if (len < 0) {
+        buf.resize(size_t(-len) + 16);
+        len = mdg_run_json(run, buf.data(), buf.size());
+    }
+    if (pretty) {
+        mdg_run_info info;
+        mdg_run_info_get(run, &info);
+        std::cout << "d:             " << info.d << (info.capped ? " (level cap: upper bound)" : "") << "\n"
+                  << "n:             " << info.n << "\n"
+                  << "k:             " << info.k << "\n"
+                  << "algorithm:     gpu\n"
+                  << "m:             " << info.m << "\n"
+                  << "k_last:        " << info.k_last << "\n"
+                  << "g_final:       " << info.g_final << "\n"
+                  << "row_additions: " << info.row_additions << "\n"
+                  << "combinations:  " << info.combinations << "\n"
+                  << "wall_seconds:  " << info.wall_seconds << "\n"
+                  << "seed:          " << cfg.seed << "\n"
+                  << "workers:       1\n"
+                  << "witness_ok:    " << (info.witness_ok ? "true" : "false") << "\n";
+    } else {
+        std::cout << buf.data() << "\n";
+    }
+    mdg_run_free(run);
+    mdg_close(ctx);
+    return 0;
+}

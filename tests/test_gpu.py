@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA round kernels and the GPU front door against the
+reference golden vectors and the C oracle (bit-exact: every result here is an
+integer). Run on a B200 with ``pytest -m gpu``. Everything goes through the
+C ABI (lib/libmdg.so)."""
+import threading
+from math import comb
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+KERNELS = [0, 1]  # tab, rd
+
+
+def popcount_rows(rows, idx):
+    acc = np.zeros(rows.shape[1], dtype=np.uint64)
+    for r in idx:
+        acc ^= rows[r]
+    return sum(bin(int(x)).count("1") for x in acc), acc
+
+
+# ------------------------------------------------------------------ rounds
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_round_minima_vs_reference(mdg, device, kernel):
+    device.set_kernel(kernel)
+    for case in load_golden("rounds"):
+        rows, n = mdg.parse_matrix(case["matrix"])
+        device.load_gammas(rows, n, ranks=None)
+        for lv in case["levels"]:
+            out = device.round(0, lv["c"])
+            assert out.min_weight == lv["min"], (case["n"], case["k"], lv, kernel)
+            assert out.combinations == lv["combinations"]
+            assert out.evaluated == lv["combinations"]
+            idx = device.round_witness(0, lv["c"], out)
+            assert len(set(idx)) == lv["c"]
+            assert popcount_rows(rows, idx)[0] == lv["min"]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_round_random_shapes_vs_oracle(mdg, device, kernel):
+    """Raw matrices of many widths (every NW template 1..16) and levels vs the oracle."""
+    rng = np.random.default_rng(7)
+    device.set_kernel(kernel)
+    for n in [5, 31, 32, 33, 64, 65, 97, 128, 160, 200, 256, 300, 384, 450, 512]:
+        k = int(rng.integers(6, 26))
+        W = (n + 63) // 64
+        rows = rng.integers(0, 2**63, size=(k, W), dtype=np.uint64)
+        if n % 64:
+            rows[:, -1] &= np.uint64((1 << (n % 64)) - 1)
+        device.load_gammas(rows, n, ranks=None)
+        for c in range(1, min(k, 5) + 1):
+            w, combos = port.round_min(rows, n, c)
+            out = device.round(0, c)
+            assert (out.min_weight, out.evaluated) == (w, combos), (n, k, c, kernel)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_identity_elision_rounds_vs_oracle(mdg, device, kernel):
+    """Gamma sets with full and partial identity blocks (compacted rows + identity count)
+    give the oracle's per-round minima on the uncompacted matrices."""
+    device.set_kernel(kernel)
+    for (n, k, seed) in [(80, 40, 1), (300, 200, 11), (50, 30, 4), (70, 20, 5), (45, 40, 6)]:
+        G = mdg.gen_matrix(n, k, seed, True)
+        gs = mdg.GammaSet.build(G, n, 3, seed)
+        device.load_gset(gs)
+        for j in range(gs.m):
+            g = gs.gamma(j)
+            for c in range(1, 4):
+                w, combos = port.round_min(g, n, c)
+                out = device.round(j, c)
+                assert (out.min_weight, out.evaluated) == (w, combos), (n, k, j, c, kernel)
+                idx = device.round_witness(j, c, out)
+                assert popcount_rows(g, idx)[0] == w
+
+
+def test_histogram_cfg5(mdg, device):
+    h = load_golden("cfg5_hist")
+    rows = mdg.gen_matrix(256, 100, 3, identity=False)
+    device.load_gammas(rows, 256, ranks=None)
+    for lv in h["levels"]:
+        out, hist = device.round_hist(0, lv["c"], 256)
+        assert hist.tolist() == lv["hist"], lv["c"]
+        assert out.min_weight == lv["min"]
+        assert out.evaluated == lv["count"] == comb(100, lv["c"])
+        full = device.round(0, lv["c"])
+        assert full.min_weight == lv["min"]
+
+
+def test_histogram_with_identity_vs_oracle(mdg, device):
+    G = mdg.gen_matrix(70, 20, 5, True)
+    gs = mdg.GammaSet.build(G, 70, 3, 5)
+    device.load_gset(gs)
+    for j in range(gs.m):
+        for c in (1, 2, 3, 4):
+            w, hist_ref = port.round_hist(gs.gamma(j), 70, c)
+            out, hist = device.round_hist(j, c, 70)
+            assert hist.tolist() == hist_ref.tolist() and out.min_weight == w
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_partition_covers_round(mdg, device, kernel):
+    """Task ranges (the multi-GPU split) partition the round exactly."""
+    device.set_kernel(kernel)
+    G = mdg.gen_matrix(128, 64, 1, True)
+    gs = mdg.GammaSet.build(G, 128, 10, 1)
+    device.load_gset(gs)
+    for c in (2, 3, 4):
+        full = device.round(0, c)
+        T = device.tasks(0, c)
+        for world in (2, 3, 8):
+            parts = [device.round_range(0, c, T * r // world, T * (r + 1) // world) for r in range(world)]
+            assert sum(p.evaluated for p in parts) == comb(64, c)
+            assert min(p.min_weight for p in parts) == full.min_weight
+            assert min(p.argmin_key for p in parts) == full.argmin_key
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_early_exit_is_exact(mdg, device, kernel):
+    """stop_at: the round stops once a weight <= stop_at exists; the returned minimum is
+    then <= stop_at and is a real codeword weight."""
+    device.set_kernel(kernel)
+    G = mdg.gen_matrix(128, 64, 1, True)
+    gs = mdg.GammaSet.build(G, 128, 10, 1)
+    device.load_gset(gs)
+    full = device.round(0, 5)
+    early = device.round(0, 5, stop_at=full.min_weight + 3)
+    assert early.min_weight <= full.min_weight + 3 and early.min_weight >= full.min_weight
+    assert early.stopped_early and early.evaluated < full.evaluated
+    idx = device.round_witness(0, 5, early)
+    g0 = gs.gamma(0)
+    assert popcount_rows(g0, idx)[0] == early.min_weight
+
+
+def test_kernels_agree_on_keys_weight(mdg, device):
+    G = mdg.gen_matrix(256, 32, 7, True)
+    gs = mdg.GammaSet.build(G, 256, 10, 7)
+    device.load_gset(gs)
+    for j in range(gs.m):
+        for c in (3, 5):
+            device.set_kernel(0)
+            a = device.round(j, c)
+            device.set_kernel(1)
+            b = device.round(j, c)
+            assert a.min_weight == b.min_weight and a.evaluated == b.evaluated
+    device.set_kernel(0)
+
+
+def test_round_argument_errors(mdg, device):
+    rows = mdg.gen_matrix(40, 10, 2, True)
+    device.load_gammas(rows, 40, ranks=None)
+    with pytest.raises(mdg.InvalidArgument):
+        device.round(0, 0)
+    with pytest.raises(mdg.InvalidArgument):
+        device.round(0, 11)
+    with pytest.raises(mdg.InvalidArgument):
+        device.round(1, 1)
+    out = device.round(0, 10)  # c = k: the single all-rows combination
+    assert out.evaluated == 1
+    w = popcount_rows(rows, range(10))[0]
+    assert out.min_weight == w
+    with pytest.raises(mdg.InvalidArgument):  # identity block missing at the claimed rank
+        device.load_gammas(np.ones((3, 1), dtype=np.uint64), 10, ranks=[3])
+
+
+# -------------------------------------------------------------- front door
+def _check_run(res, case, name):
+    assert res.rounds == case["rounds"], name
+    assert res.levels == case["levels"][: len(res.levels)] and len(res.levels) == len(case["levels"]), name
+    assert res.m == case["m"] and res.k_last == case["k_last"], name
+    assert res.g_final == case["g_final"], name
+    assert res.column_perm == case["column_perm"], name
+    assert res.gamma_hash == case["gamma_hash"], name
+    assert res.witness_ok, name
+    wt = sum(bin(int(x)).count("1") for x in res.witness)
+    assert wt == res.d, name
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("kind", ["kats", "seeded"])
+def test_min_weight_small_codes(mdg, device, kind, kernel):
+    for case in load_golden(kind):
+        rows, n = mdg.parse_matrix(case["matrix"])
+        res = mdg.min_weight(rows, n, case["trials"], case["seed"], kernel=kernel, device=device)
+        assert res.d == case["d"] == case["d_brute"], case["name"]
+        _check_run(res, case, case["name"])
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_s1", "cfg2_s2", "cfg2_s3", "cfg2_s4", "cfg2_s5",
+                                  "cfg2_s6", "cfg2_s7", "cfg2_s8", "cfg3", "cfg4"])
+def test_min_weight_configs(mdg, device, name):
+    case = next(c for c in load_golden("configs") if c["name"] == name)
+    g = case["gen"]
+    rows = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
+    res = mdg.min_weight(rows, g["n"], case["trials"], case["seed"], level_cap=case["level_cap"],
+                         device=device)
+    if case["capped"]:
+        assert res.capped and res.d == case["U_final"]
+    else:
+        assert not res.capped and res.d == case["d"]
+    _check_run(res, case, name)
+    # the witness lies in the code spanned by G (rank does not grow)
+    assert port.rank(np.vstack([rows, res.witness[None, :]]), g["n"]) == port.rank(rows, g["n"])
+
+
+def test_min_weight_cfg4_cap6(mdg, device):
+    import os
+    from conftest import GOLD
+    if not os.path.exists(os.path.join(GOLD, "configs_cap4_6.json")):
+        pytest.skip("cap-6 golden not generated")
+    case = next(c for c in load_golden("configs_cap4_6") if c["name"] == "cfg4")
+    g = case["gen"]
+    rows = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
+    res = mdg.min_weight(rows, g["n"], 10, g["seed"], level_cap=6, device=device)
+    assert res.capped and res.d == case["U_final"]
+    _check_run(res, case, "cfg4_cap6")
+
+
+def test_dist_two_ranks_threaded(mdg):
+    """The multi-rank front door (rank-range split + per-round min reduction) with two
+    ranks on one GPU as two host threads exchanging keys through a barrier (no kernel
+    ever waits on another); results equal the single-rank run."""
+    case = next(c for c in load_golden("configs") if c["name"] == "cfg2_s8")
+    g = case["gen"]
+    rows = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
+    world = 2
+    slots = [None] * world
+    bar = threading.Barrier(world)
+    results = [None] * world
+
+    def reducer_for(rank):
+        def red(keys):
+            slots[rank] = keys.copy()
+            bar.wait()
+            out = np.minimum.reduce([s for s in slots])
+            bar.wait()
+            return out
+        return red
+
+    def worker(rank):
+        dev = mdg.Device(0)
+        results[rank] = mdg.min_weight_dist(rows, g["n"], rank, world, reducer_for(rank),
+                                            trials=10, seed=g["seed"], device=dev)
+        dev.close()
+
+    ts = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for r in range(world):
+        res = results[r]
+        assert res.d == case["d"]
+        _check_run(res, case, f"rank{r}")
