@@ -202,6 +202,8 @@ int mdg_run_info_get(const mdg_run* r, mdg_run_info* info);
 int mdg_run_rounds(const mdg_run* r, mdg_round_rec* out);     /* n_rounds entries */
 int mdg_run_levels(const mdg_run* r, mdg_level_rec* out);     /* n_levels entries */
 int mdg_run_witness(const mdg_run* r, uint64_t* row);         /* W words, original columns */
+/* per executed round (n_rounds entries): codewords evaluated, kernel ms */
+int mdg_run_round_perf(const mdg_run* r, uint64_t* evaluated, double* device_ms);
 int mdg_run_perm(const mdg_run* r, uint32_t* perm);           /* column_perm (n) */
 uint64_t mdg_run_gamma_hash(const mdg_run* r, uint32_t j);
 /* The reference CLI's JSON record (cli.cpp:223-238) plus the new keys. */

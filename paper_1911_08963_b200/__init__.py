@@ -145,6 +145,7 @@ SYMBOLS = {
     "mdg_run_levels": (C.c_int, [C.c_void_p, C.POINTER(_LevelRec)]),
     "mdg_run_witness": (C.c_int, [C.c_void_p, u64p]),
     "mdg_run_perm": (C.c_int, [C.c_void_p, u32p]),
+    "mdg_run_round_perf": (C.c_int, [C.c_void_p, u64p, np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")]),
     "mdg_run_gamma_hash": (C.c_uint64, [C.c_void_p, C.c_uint32]),
     "mdg_run_json": (C.c_long, [C.c_void_p, C.c_char_p, C.c_size_t]),
     "mdg_run_free": (None, [C.c_void_p]),
@@ -475,6 +476,8 @@ class RunResult:
     h2d_bytes: int
     d2h_bytes: int
     rounds: list            # [c, j, w, U_after]
+    round_evaluated: list   # per executed round: codewords evaluated (this rank)
+    round_ms: list          # per executed round: kernel time (CUDA events)
     levels: list            # [c, L_after, U_after]
     column_perm: list
     gamma_hash: list
@@ -492,6 +495,9 @@ def _collect(h) -> RunResult:
     _check(L.mdg_run_levels(h, ll))
     perm = np.zeros(max(1, info.n), dtype=np.uint32)
     _check(L.mdg_run_perm(h, perm))
+    pe = np.zeros(max(1, info.n_rounds), dtype=np.uint64)
+    pm = np.zeros(max(1, info.n_rounds), dtype=np.float64)
+    _check(L.mdg_run_round_perf(h, pe, pm))
     wit = np.zeros(words(info.n), dtype=np.uint64)
     has_w = L.mdg_run_witness(h, wit) == 0
     cap = 1 << 16
@@ -509,6 +515,8 @@ def _collect(h) -> RunResult:
         gamma_seconds=info.gamma_seconds, loop_seconds=info.loop_seconds,
         launches=info.launches, h2d_bytes=info.h2d_bytes, d2h_bytes=info.d2h_bytes,
         rounds=[[r.c, r.j, r.w, r.U_after] for r in rr[: info.n_rounds]],
+        round_evaluated=[int(x) for x in pe[: info.n_rounds]],
+        round_ms=[float(x) for x in pm[: info.n_rounds]],
         levels=[[x.c, x.L_after, x.U_after] for x in ll[: info.n_levels]],
         column_perm=[int(x) for x in perm[: info.n]],
         gamma_hash=["%016x" % L.mdg_run_gamma_hash(h, j) for j in range(info.m)],

@@ -655,6 +655,17 @@ int mdg_run_witness(const mdg_run* r, uint64_t* row) {
     });
 }
 
+int mdg_run_round_perf(const mdg_run* r, uint64_t* evaluated, double* device_ms) {
+    return guard([&] {
+        if (!r) throw std::invalid_argument("null run");
+        const auto& pg = r->er.stats.per_g;
+        for (size_t i = 0; i < pg.size(); ++i) {
+            if (evaluated) evaluated[i] = pg[i].evaluated;
+            if (device_ms) device_ms[i] = pg[i].device_ms;
+        }
+    });
+}
+
 int mdg_run_perm(const mdg_run* r, uint32_t* perm) {
     return guard([&] {
         if (!r || !perm) throw std::invalid_argument("null argument");

@@ -52,7 +52,7 @@ constexpr int kTX = 256;            // prefixes per tile (= threads that build t
 constexpr uint32_t kBT = kMaxC + 1; // binomial table row stride
 constexpr int kKeyShift = 40;
 
-__host__ __device__ constexpr int r_for(int nw) { return nw <= 4 ? 8 : (nw <= 8 ? 4 : 2); }
+__host__ __device__ constexpr int r_for(int nw) { return nw <= 4 ? 8 : (nw <= 8 ? 4 : (nw <= 16 ? 2 : 1)); }
 __host__ __device__ constexpr int stride_for(int words) {
     return words <= 2 ? 2 : ((words + 3) / 4) * 4;
 }
@@ -150,10 +150,11 @@ struct TabArgs {
     const uint32_t* ytab;
     const uint64_t* binom;
     const uint64_t* prefix;
-    uint32_t k, p, s, emin, npiv, id_rows, add_const, stop_at;
+    uint32_t k, p, s, emin, npiv, id_rows, add_const, stop_at, tx;
     uint64_t tile_lo, tile_hi;
     unsigned long long* best_key;
     unsigned long long* evaluated;
+    unsigned long long* counter;   // dynamic tile scheduler (next tile - tile_lo)
     unsigned long long* find_out;  // tab_find only
     uint32_t find_target;          // tab_find only
     uint32_t nbins;                // tab_hist only
@@ -162,7 +163,7 @@ struct TabArgs {
 
 struct TileInfo {
     uint32_t e, nx, nyv, stop;
-    uint64_t x0, y0;
+    uint64_t x0, y0, tile;
 };
 
 // decode tile -> (pivot, prefix chunk, suffix chunk); thread 0 only
@@ -180,8 +181,9 @@ __device__ __forceinline__ void decode_tile(const TabArgs& a, uint64_t tile, Til
     uint64_t tx = local / nty, ty = local - tx * nty;
     uint64_t NX = BT(a.binom, e, a.p - 1);
     ti.e = e;
-    ti.x0 = tx * kTX;
-    ti.nx = uint32_t(umin64(uint64_t(kTX), NX - ti.x0));
+    ti.tile = tile;
+    ti.x0 = tx * a.tx;
+    ti.nx = uint32_t(umin64(uint64_t(a.tx), NX - ti.x0));
     ti.y0 = ty * YC;
     ti.nyv = uint32_t(umin64(uint64_t(YC), NY - ti.y0));
 }
@@ -239,17 +241,24 @@ __global__ void __launch_bounds__(kThreads) tab_round(TabArgs a) {
     unsigned long long seen = ~0ull; // lane 0's view of the global best key
     unsigned long long done_local = 0;
 
-    for (uint64_t tile = a.tile_lo + blockIdx.x; tile < a.tile_hi; tile += gridDim.x) {
+    for (;;) {
         if (threadIdx.x == 0) {
+            // early exit: the global bound already meets stop_at
             unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
-            ti.stop = (g >> kKeyShift) <= a.stop_at;
-            if (!ti.stop) {
-                decode_tile<YC>(a, tile, ti);
-                done_local += uint64_t(ti.nx) * ti.nyv;
+            uint32_t stop = (g >> kKeyShift) <= a.stop_at;
+            if (!stop) { // dynamic tile scheduler: uniform tiles, no static tail
+                uint64_t t = a.tile_lo + atomicAdd(a.counter, 1ull);
+                stop = t >= a.tile_hi;
+                if (!stop) {
+                    decode_tile<YC>(a, t, ti);
+                    done_local += uint64_t(ti.nx) * ti.nyv;
+                }
             }
+            ti.stop = stop;
         }
         __syncthreads();
         if (ti.stop) break;
+        const uint64_t tile = ti.tile;
         if (threadIdx.x < ti.nx) build_prefix<NW, HID>(a, ti.e, ti.x0 + threadIdx.x, xs + threadIdx.x * XS);
         uint32_t Y[R][NW], idY[R];
         bool valid[R];
@@ -329,18 +338,23 @@ __global__ void __launch_bounds__(kThreads) tab_hist(TabArgs a) {
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
     extern __shared__ __align__(16) uint32_t dyn[];
     uint32_t* xs = dyn;
-    uint32_t* bins = dyn + kTX * XS; // kWarps x nbins
+    uint32_t* bins = dyn + a.tx * XS; // kWarps x nbins
     __shared__ TileInfo ti;
     const uint32_t warp = threadIdx.x >> 5;
     for (uint32_t i = threadIdx.x; i < kWarps * a.nbins; i += kThreads) bins[i] = 0;
     unsigned long long done_local = 0;
     uint32_t* mybins = bins + warp * a.nbins;
-    for (uint64_t tile = a.tile_lo + blockIdx.x; tile < a.tile_hi; tile += gridDim.x) {
+    for (;;) {
         if (threadIdx.x == 0) {
-            decode_tile<YC>(a, tile, ti);
-            done_local += uint64_t(ti.nx) * ti.nyv;
+            uint64_t t = a.tile_lo + atomicAdd(a.counter, 1ull);
+            ti.stop = t >= a.tile_hi;
+            if (!ti.stop) {
+                decode_tile<YC>(a, t, ti);
+                done_local += uint64_t(ti.nx) * ti.nyv;
+            }
         }
         __syncthreads();
+        if (ti.stop) break;
         if (threadIdx.x < ti.nx) build_prefix<NW, HID>(a, ti.e, ti.x0 + threadIdx.x, xs + threadIdx.x * XS);
         uint32_t Y[R][NW], idY[R];
         bool valid[R];
@@ -374,7 +388,6 @@ __global__ void __launch_bounds__(kThreads) tab_hist(TabArgs a) {
 // (Knuth 7.2.1.3 Algorithm R; host.cpp rd_unrank) starting from its unranked
 // first combination. Gamma_j rows live in shared memory; one 3-input XOR per
 // word per step (row out ^ row in).
-constexpr uint32_t kRdChunk = 2048;
 constexpr int kRdThreads = 256;
 
 struct RdArgs {
@@ -382,6 +395,7 @@ struct RdArgs {
     const uint64_t* binom;
     uint32_t k, c, id_rows, add_const, stop_at;
     uint64_t total;              // C(k, c)
+    uint64_t chunk;              // ranks per task (rd_chunk)
     uint64_t task_lo, task_hi;   // chunk range
     unsigned long long* best_key;
     unsigned long long* evaluated;
@@ -451,8 +465,8 @@ __global__ void __launch_bounds__(kRdThreads) rd_round(RdArgs a) {
         uint32_t best = 0xFFFFFFFFu;
         uint64_t best_rank = ~0ull;
         if (active) {
-            uint64_t r0 = chunk * kRdChunk;
-            uint64_t r1 = umin64(r0 + kRdChunk, a.total);
+            uint64_t r0 = chunk * a.chunk;
+            uint64_t r1 = umin64(r0 + a.chunk, a.total);
             rd_unrank_dev(a.binom, a.c, r0, cc);
             cc[a.c] = a.k;
             uint32_t cw[NW];
@@ -511,8 +525,8 @@ void dispatch_nw_hid(uint32_t nw, bool hid, Args&&... args) {
         break;
     switch (nw) {
         MDG_CASE(1) MDG_CASE(2) MDG_CASE(3) MDG_CASE(4) MDG_CASE(5) MDG_CASE(6) MDG_CASE(7)
-        MDG_CASE(8) MDG_CASE(9) MDG_CASE(10) MDG_CASE(11) MDG_CASE(12) MDG_CASE(13)
-        MDG_CASE(14) MDG_CASE(15) MDG_CASE(16)
+        MDG_CASE(8) MDG_CASE(10) MDG_CASE(12) MDG_CASE(14) MDG_CASE(16) MDG_CASE(20)
+        MDG_CASE(24) MDG_CASE(28) MDG_CASE(32)
         default: throw std::invalid_argument("row width beyond the device limit");
     }
 #undef MDG_CASE
@@ -528,15 +542,20 @@ struct YtabLaunch {
 };
 
 template <int NW, bool HID>
+struct TabOcc {
+    static void run(int* occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, tab_round<NW, HID>, kThreads, 0);
+    }
+};
+
+template <int NW, bool HID>
 struct TabLaunch {
     // grid: number of tiles for mode 0/2 (clamped to the resident-block count)
     static void run(const TabArgs& a, uint64_t grid, cudaStream_t st, int mode, size_t dyn, int sms) {
         if (mode == 0) {
-            static int occ = 0;
-            if (!occ) {
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tab_round<NW, HID>, kThreads, 0);
-                if (occ < 1) occ = 1;
-            }
+            int occ = 0;
+            TabOcc<NW, HID>::run(&occ);
+            if (occ < 1) occ = 1;
             uint64_t g = std::max<uint64_t>(1, std::min<uint64_t>(grid, uint64_t(sms) * occ));
             tab_round<NW, HID><<<uint32_t(g), kThreads, 0, st>>>(a);
         }
@@ -552,6 +571,16 @@ struct TabLaunch {
         }
     }
 };
+
+__global__ void init_slots(unsigned long long* s, int n) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        s[4 * i + 0] = ~0ull; // best key
+        s[4 * i + 1] = 0;     // evaluated
+        s[4 * i + 2] = 0;     // tile counter
+        s[4 * i + 3] = ~0ull; // witness search result
+    }
+}
 
 template <int NW, bool FIND>
 struct RdLaunchT {
@@ -569,38 +598,76 @@ struct RdLaunch : RdLaunchT<NW, FIND> {};
 } // namespace
 
 // ================================================================ host side
+uint32_t template_width(uint32_t nw32) {
+    if (nw32 <= 8) return std::max<uint32_t>(nw32, 1);
+    if (nw32 <= 16) return (nw32 + 1) & ~1u;
+    if (nw32 <= 32) return (nw32 + 3) & ~3u;
+    throw std::invalid_argument("row width exceeds the device limit (n - rank <= 1024)");
+}
+
+uint64_t rd_chunk(uint64_t total) {
+    uint64_t chunk = 64;
+    while (chunk < 4096 && total / chunk > (uint64_t{1} << 20)) chunk *= 2;
+    return chunk;
+}
+
 uint32_t tab_yc(uint32_t nw32) { return uint32_t(r_for(int(nw32))) * kThreads; }
 uint32_t tab_tx() { return kTX; }
 
 static uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
+// saturating Pascal table C(x, t), x <= kMaxK, t <= kMaxC (host and device copies)
+static const std::vector<uint64_t>& binom_table() {
+    static const std::vector<uint64_t> T = [] {
+        std::vector<uint64_t> t(size_t(kMaxK + 1) * kBT, 0);
+        for (uint32_t x = 0; x <= kMaxK; ++x) {
+            t[size_t(x) * kBT] = 1;
+            for (uint32_t q = 1; q <= kMaxC && q <= x; ++q) {
+                uint64_t a = t[size_t(x - 1) * kBT + q - 1], b = t[size_t(x - 1) * kBT + q];
+                uint64_t sum = a + b;
+                t[size_t(x) * kBT + q] = (sum < a || a == ~0ull || b == ~0ull) ? ~0ull : sum;
+            }
+        }
+        return t;
+    }();
+    return T;
+}
+
+static inline uint64_t hb(uint32_t x, uint32_t t) {
+    if (t > x) return 0;
+    if (x <= kMaxK && t <= kMaxC) return binom_table()[size_t(x) * kBT + t];
+    return binomial(x, t);
+}
+
+// total cost in codeword-slots: masked suffix lanes + a per-tile overhead
 static uint64_t plan_cost(uint32_t k, uint32_t c, uint32_t s, uint32_t TX, uint32_t YC,
                           uint64_t* tiles_out) {
     uint32_t p = c - s;
     uint64_t cost = 0, tiles = 0;
     for (uint32_t e = p - 1; e + s <= k - 1; ++e) {
-        uint64_t NX = binomial(e, p - 1), NY = binomial(k - 1 - e, s);
+        uint64_t NX = hb(e, p - 1), NY = hb(k - 1 - e, s);
         uint64_t ntx = ceil_div(NX, TX), nty = ceil_div(NY, YC);
         tiles += ntx * nty;
-        cost += NX * nty * YC + ntx * nty * uint64_t(YC) * 24; // masked lanes + per-tile overhead
+        cost += NX * nty * YC + ntx * nty * uint64_t(YC) * 24;
     }
     if (tiles_out) *tiles_out = tiles;
     return cost;
 }
 
-TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32) {
+// Suffix size s minimizes the tile cost (suffix table <= 4M entries); the
+// prefix chunk TX is the largest of 256/128/64/32 that still yields >= 6
+// tiles per resident block, so the dynamic scheduler's tail stays short.
+TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_blocks) {
     TabPlan pl;
     pl.k = k;
     pl.c = c;
-    pl.TX = kTX;
     pl.YC = tab_yc(nw32);
     uint32_t best_s = 0;
     if (c >= 2) {
         uint64_t best_cost = ~uint64_t{0};
         for (uint32_t s = 1; s <= c - 1; ++s) {
-            uint64_t entries = binomial(k, s);
-            if (entries > (uint64_t{1} << 22) && s > 1) break;
-            uint64_t cost = plan_cost(k, c, s, pl.TX, pl.YC, nullptr);
+            if (hb(k, s) > (uint64_t{1} << 22) && s > 1) break;
+            uint64_t cost = plan_cost(k, c, s, kTX, pl.YC, nullptr);
             if (cost < best_cost) { best_cost = cost; best_s = s; }
         }
     }
@@ -608,9 +675,15 @@ TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32) {
     pl.p = c - best_s;
     pl.emin = pl.p - 1;
     pl.emax = k - 1 - pl.s;
+    pl.TX = 32;
+    for (uint32_t tx = kTX; tx >= 32; tx /= 2) {
+        uint64_t tiles = 0;
+        plan_cost(k, c, pl.s, tx, pl.YC, &tiles);
+        if (tiles >= uint64_t(resident_blocks) * 6 || tx == 32) { pl.TX = tx; break; }
+    }
     pl.prefix.assign(1, 0);
     for (uint32_t e = pl.emin; e <= pl.emax; ++e) {
-        uint64_t NX = binomial(e, pl.p - 1), NY = binomial(k - 1 - e, pl.s);
+        uint64_t NX = hb(e, pl.p - 1), NY = hb(k - 1 - e, pl.s);
         pl.prefix.push_back(pl.prefix.back() + ceil_div(NX, pl.TX) * ceil_div(NY, pl.YC));
     }
     return pl;
@@ -620,9 +693,9 @@ TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32) {
 static void colex_unrank_host(uint64_t r, uint32_t t, uint32_t hi, uint32_t* out) {
     for (uint32_t i = t; i >= 1; --i) {
         uint32_t x = hi - 1;
-        while (binomial(x, i) > r) --x;
+        while (hb(x, i) > r) --x;
         out[i - 1] = x;
-        r -= binomial(x, i);
+        r -= hb(x, i);
         hi = x;
     }
 }
@@ -631,7 +704,7 @@ void tab_decode(const TabPlan& pl, uint64_t tile, uint32_t x_local, uint32_t y_l
     uint32_t i = uint32_t(std::upper_bound(pl.prefix.begin(), pl.prefix.end(), tile) - pl.prefix.begin()) - 1;
     uint32_t e = pl.emin + i;
     uint64_t local = tile - pl.prefix[i];
-    uint64_t NY = binomial(pl.k - 1 - e, pl.s);
+    uint64_t NY = hb(pl.k - 1 - e, pl.s);
     uint64_t nty = ceil_div(NY, pl.YC);
     uint64_t tx = local / nty, ty = local % nty;
     uint64_t x = tx * pl.TX + x_local, y = ty * pl.YC + y_local;
@@ -685,44 +758,75 @@ constexpr int kNcclMin = 3;    // ncclMin
 
 // ------------------------------------------------------------ Engine impl
 struct GammaDev {
-    uint32_t* rows = nullptr;  // k x nw (compacted)
+    uint32_t* rows = nullptr;  // k x nw (compacted, zero-padded to the template width)
     uint32_t nw = 0;
     uint32_t id_rows = 0;      // identity rows [0, id_rows)
     uint32_t n_compact = 0;
-    std::vector<uint32_t> host_rows; // compacted copy for witness checks
+    bool hid = false;          // partial identity block: per-entry identity counts
 };
+
+struct PlanEntry {
+    TabPlan plan;
+    uint64_t* d_prefix = nullptr;
+};
+
+constexpr int kSlots = 4096; // per-round scratch slots {best key, evaluated, counter, find}
 
 struct Engine::Impl {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, tev0 = nullptr, tev1 = nullptr;
     Engine::Counters cnt;
     uint64_t* binom = nullptr;
-    unsigned long long* scratch = nullptr;   // [0] best key, [1] evaluated, [2] find
-    unsigned long long* host_scratch = nullptr; // pinned
-    uint64_t* prefix_dev = nullptr;
-    uint64_t* prefix_host = nullptr;         // pinned
-    size_t prefix_cap = 0;
+    unsigned long long* slots = nullptr;
+    unsigned long long* host_slot = nullptr; // pinned, 4 words
+    int next_slot = kSlots;                  // forces an init on first use
     unsigned long long* hist_dev = nullptr;
     size_t hist_cap = 0;
     std::vector<GammaDev> gammas;
     std::map<std::pair<uint32_t, uint32_t>, uint32_t*> ytabs; // (j, s) -> table
+    std::map<std::tuple<uint32_t, uint32_t, uint32_t, bool>, PlanEntry> plans; // (k, c, nw, hid)
+    std::map<std::pair<uint32_t, bool>, int> occ;                     // (nw, hid)
     ncclComm_t comm = nullptr;
     uint64_t* red_dev = nullptr;
     size_t red_cap = 0;
-};
 
-static std::vector<uint64_t> make_binom_table() {
-    std::vector<uint64_t> T(size_t(kMaxK + 1) * kBT, 0);
-    for (uint32_t x = 0; x <= kMaxK; ++x) {
-        T[size_t(x) * kBT] = 1;
-        for (uint32_t t = 1; t <= kMaxC && t <= x; ++t) {
-            uint64_t a = T[size_t(x - 1) * kBT + t - 1], b = (t <= x - 1) ? T[size_t(x - 1) * kBT + t] : 0;
-            uint64_t s = a + b;
-            T[size_t(x) * kBT + t] = (s < a || a == ~0ull || b == ~0ull) ? ~0ull : s;
+    unsigned long long* take_slot() {
+        if (next_slot >= kSlots) {
+            init_slots<<<(kSlots + 255) / 256, 256, 0, stream>>>(slots, kSlots);
+            CK(cudaGetLastError());
+            cnt.launches += 1;
+            next_slot = 0;
         }
+        return slots + 4 * size_t(next_slot++);
     }
-    return T;
-}
+    void read_slot(unsigned long long* slot) {
+        CK(cudaMemcpyAsync(host_slot, slot, 32, cudaMemcpyDeviceToHost, stream));
+        cnt.d2h += 32;
+    }
+    int resident(uint32_t nw, bool hid, int sms) {
+        auto key = std::make_pair(nw, hid);
+        auto it = occ.find(key);
+        if (it != occ.end()) return it->second * sms;
+        int o = 0;
+        dispatch_nw_hid<TabOcc>(nw, hid, &o);
+        if (o < 1) o = 1;
+        occ[key] = o;
+        return o * sms;
+    }
+    const PlanEntry& plan(uint32_t k, uint32_t c, const GammaDev& g, int sms) {
+        auto key = std::make_tuple(k, c, g.nw, g.hid);
+        auto it = plans.find(key);
+        if (it != plans.end()) return it->second;
+        PlanEntry pe;
+        pe.plan = make_tab_plan(k, c, g.nw, uint32_t(resident(g.nw, g.hid, sms)));
+        CK(cudaMalloc(&pe.d_prefix, pe.plan.prefix.size() * 8));
+        CK(cudaMemcpyAsync(pe.d_prefix, pe.plan.prefix.data(), pe.plan.prefix.size() * 8,
+                           cudaMemcpyHostToDevice, stream));
+        CK(cudaStreamSynchronize(stream));
+        cnt.h2d += pe.plan.prefix.size() * 8;
+        return plans.emplace(key, pe).first->second;
+    }
+};
 
 Engine::Engine(int device) : device_(device), impl_(new Impl) {
     int count = 0;
@@ -737,14 +841,11 @@ Engine::Engine(int device) : device_(device), impl_(new Impl) {
     CK(cudaEventCreate(&impl_->ev1));
     CK(cudaEventCreate(&impl_->tev0));
     CK(cudaEventCreate(&impl_->tev1));
-    auto T = make_binom_table();
+    const auto& T = binom_table();
     CK(cudaMalloc(&impl_->binom, T.size() * 8));
     CK(cudaMemcpy(impl_->binom, T.data(), T.size() * 8, cudaMemcpyHostToDevice));
-    CK(cudaMalloc(&impl_->scratch, 4 * 8));
-    CK(cudaHostAlloc(&impl_->host_scratch, 4 * 8, cudaHostAllocDefault));
-    impl_->prefix_cap = kMaxK + 2;
-    CK(cudaMalloc(&impl_->prefix_dev, impl_->prefix_cap * 8));
-    CK(cudaHostAlloc(&impl_->prefix_host, impl_->prefix_cap * 8, cudaHostAllocDefault));
+    CK(cudaMalloc(&impl_->slots, size_t(kSlots) * 32));
+    CK(cudaHostAlloc(&impl_->host_slot, 32, cudaHostAllocDefault));
 }
 
 Engine::~Engine() {
@@ -753,16 +854,15 @@ Engine::~Engine() {
     if (impl_->stream) cudaStreamSynchronize(impl_->stream);
     for (auto& g : impl_->gammas) cudaFree(g.rows);
     for (auto& kv : impl_->ytabs) cudaFree(kv.second);
+    for (auto& kv : impl_->plans) cudaFree(kv.second.d_prefix);
     if (impl_->comm) {
         try { nccl().CommDestroy(impl_->comm); } catch (...) {}
     }
     cudaFree(impl_->red_dev);
     cudaFree(impl_->hist_dev);
     cudaFree(impl_->binom);
-    cudaFree(impl_->scratch);
-    cudaFree(impl_->prefix_dev);
-    cudaFreeHost(impl_->host_scratch);
-    cudaFreeHost(impl_->prefix_host);
+    cudaFree(impl_->slots);
+    cudaFreeHost(impl_->host_slot);
     cudaEventDestroy(impl_->ev0);
     cudaEventDestroy(impl_->ev1);
     cudaEventDestroy(impl_->tev0);
@@ -775,11 +875,9 @@ void Engine::load(uint32_t m, uint32_t k, uint32_t n, const uint64_t* rows, cons
     if (k > kMaxK) throw std::invalid_argument("mdg_load: k exceeds the device limit of 1024 rows");
     CK(cudaSetDevice(device_));
     CK(cudaStreamSynchronize(impl_->stream));
-    for (auto& g : impl_->gammas) cudaFree(g.rows);
-    for (auto& kv : impl_->ytabs) cudaFree(kv.second);
-    impl_->gammas.clear();
-    impl_->ytabs.clear();
     const uint32_t W = (n + 63) / 64;
+    std::vector<GammaDev> next;
+    std::vector<std::vector<uint32_t>> host(m);
     for (uint32_t j = 0; j < m; ++j) {
         const uint64_t* G = rows + size_t(j) * k * W;
         uint32_t rk = ranks ? ranks[j] : 0;
@@ -799,26 +897,33 @@ void Engine::load(uint32_t m, uint32_t k, uint32_t n, const uint64_t* rows, cons
         GammaDev gd;
         gd.id_rows = rk;
         gd.n_compact = n - rk;
-        gd.nw = std::max<uint32_t>(1, (gd.n_compact + 31) / 32);
-        if (gd.nw > kMaxWords32)
-            throw std::invalid_argument("mdg_load: row width exceeds the device limit (n - rank <= 512)");
-        gd.host_rows.assign(size_t(k) * gd.nw, 0);
+        gd.nw = template_width(std::max<uint32_t>(1, (gd.n_compact + 31) / 32)); // zero-padded
+        gd.hid = rk > 0 && rk < k;
+        auto& hr = host[j];
+        hr.assign(size_t(k) * gd.nw, 0);
         for (uint32_t r = 0; r < k; ++r) {
             uint32_t o = 0;
             for (uint32_t col = 0; col < n; ++col) {
                 if (ranks && col >= off && col < off + rk) continue;
                 if ((G[size_t(r) * W + col / 64] >> (col % 64)) & 1u)
-                    gd.host_rows[size_t(r) * gd.nw + o / 32] |= 1u << (o % 32);
+                    hr[size_t(r) * gd.nw + o / 32] |= 1u << (o % 32);
                 ++o;
             }
         }
-        CK(cudaMalloc(&gd.rows, gd.host_rows.size() * 4));
-        CK(cudaMemcpyAsync(gd.rows, gd.host_rows.data(), gd.host_rows.size() * 4, cudaMemcpyHostToDevice,
-                           impl_->stream));
-        CK(cudaStreamSynchronize(impl_->stream));
-        impl_->cnt.h2d += gd.host_rows.size() * 4;
-        impl_->gammas.push_back(std::move(gd));
+        next.push_back(gd);
     }
+    for (auto& g : impl_->gammas) cudaFree(g.rows);
+    for (auto& kv : impl_->ytabs) cudaFree(kv.second);
+    impl_->gammas.clear();
+    impl_->ytabs.clear();
+    for (uint32_t j = 0; j < m; ++j) {
+        CK(cudaMalloc(&next[j].rows, host[j].size() * 4));
+        CK(cudaMemcpyAsync(next[j].rows, host[j].data(), host[j].size() * 4, cudaMemcpyHostToDevice,
+                           impl_->stream));
+        impl_->cnt.h2d += host[j].size() * 4;
+    }
+    CK(cudaStreamSynchronize(impl_->stream));
+    impl_->gammas = std::move(next);
     m_ = m;
     k_ = k;
     n_ = n;
@@ -836,22 +941,31 @@ static uint32_t* ensure_ytab(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t 
     auto it = im.ytabs.find(key);
     if (it != im.ytabs.end()) return it->second;
     const GammaDev& g = im.gammas[j];
-    bool hid = g.id_rows > 0 && g.id_rows < k;
-    uint32_t YS = uint32_t(stride_for(int(g.nw) + (hid ? 1 : 0)));
-    uint64_t count = binomial(k, s);
+    uint32_t YS = uint32_t(stride_for(int(g.nw) + (g.hid ? 1 : 0)));
+    uint64_t count = hb(k, s);
     uint32_t* t = nullptr;
     CK(cudaMalloc(&t, size_t(count) * YS * 4));
-    dispatch_nw_hid<YtabLaunch>(g.nw, hid, g.rows, im.binom, k, s, g.id_rows, count, t, im.stream);
+    dispatch_nw_hid<YtabLaunch>(g.nw, g.hid, g.rows, im.binom, k, s, g.id_rows, count, t, im.stream);
     CK(cudaGetLastError());
     im.cnt.launches += 1;
     im.ytabs[key] = t;
     return t;
 }
 
+static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe, uint32_t* yt,
+                        uint32_t k, uint32_t c) {
+    TabArgs a{};
+    a.rows = g.rows; a.ytab = yt; a.binom = im.binom; a.prefix = pe.d_prefix;
+    a.k = k; a.p = pe.plan.p; a.s = pe.plan.s; a.emin = pe.plan.emin;
+    a.npiv = uint32_t(pe.plan.prefix.size() - 1);
+    a.id_rows = g.id_rows; a.add_const = (g.id_rows == k) ? c : 0; a.tx = pe.plan.TX;
+    return a;
+}
+
 uint64_t Engine::tasks(uint32_t j, uint32_t c) {
     check_round(j, c);
-    if (kernel_ == Kernel::rd) return ceil_div(binomial(k_, c), kRdChunk);
-    return make_tab_plan(k_, c, impl_->gammas[j].nw).tiles();
+    if (kernel_ == Kernel::rd) return ceil_div(binomial(k_, c), rd_chunk(binomial(k_, c)));
+    return impl_->plan(k_, c, impl_->gammas[j], sms_).plan.tiles();
 }
 
 RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t task_lo, uint64_t task_hi) {
@@ -859,45 +973,40 @@ RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t tas
     CK(cudaSetDevice(device_));
     Impl& im = *impl_;
     const GammaDev& g = im.gammas[j];
-    const bool hid = g.id_rows > 0 && g.id_rows < k_;
-    const uint32_t add_const = (g.id_rows == k_) ? c : 0;
     RoundResult rr;
     rr.combinations = binomial(k_, c);
-    CK(cudaMemsetAsync(im.scratch, 0xFF, 8, im.stream));
-    CK(cudaMemsetAsync(im.scratch + 1, 0, 8, im.stream));
     if (kernel_ == Kernel::tab) {
-        TabPlan pl = make_tab_plan(k_, c, g.nw);
-        uint64_t lo = std::min(task_lo, pl.tiles()), hi = std::min(task_hi, pl.tiles());
+        const PlanEntry& pe = im.plan(k_, c, g, sms_);
+        uint64_t lo = std::min(task_lo, pe.plan.tiles()), hi = std::min(task_hi, pe.plan.tiles());
         rr.task_lo = lo;
         rr.task_hi = hi;
-        uint32_t* yt = ensure_ytab(im, j, k_, pl.s);
-        std::copy(pl.prefix.begin(), pl.prefix.end(), im.prefix_host);
-        CK(cudaMemcpyAsync(im.prefix_dev, im.prefix_host, pl.prefix.size() * 8, cudaMemcpyHostToDevice, im.stream));
-        TabArgs a{};
-        a.rows = g.rows; a.ytab = yt; a.binom = im.binom; a.prefix = im.prefix_dev;
-        a.k = k_; a.p = pl.p; a.s = pl.s; a.emin = pl.emin; a.npiv = uint32_t(pl.prefix.size() - 1);
-        a.id_rows = g.id_rows; a.add_const = add_const; a.stop_at = stop_at;
+        uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
+        unsigned long long* slot = im.take_slot();
+        TabArgs a = tab_args(im, g, pe, yt, k_, c);
+        a.stop_at = stop_at;
         a.tile_lo = lo; a.tile_hi = hi;
-        a.best_key = im.scratch; a.evaluated = im.scratch + 1;
+        a.best_key = slot; a.evaluated = slot + 1; a.counter = slot + 2;
         CK(cudaEventRecord(im.ev0, im.stream));
         if (hi > lo) {
-            dispatch_nw_hid<TabLaunch>(g.nw, hid, a, hi - lo, im.stream, 0, size_t(0), sms_);
+            dispatch_nw_hid<TabLaunch>(g.nw, g.hid, a, hi - lo, im.stream, 0, size_t(0), sms_);
             CK(cudaGetLastError());
             im.cnt.launches += 1;
         }
-        im.cnt.h2d += pl.prefix.size() * 8;
         CK(cudaEventRecord(im.ev1, im.stream));
+        im.read_slot(slot);
     } else {
         uint64_t total = binomial(k_, c);
-        uint64_t chunks = ceil_div(total, kRdChunk);
+        uint64_t chunks = ceil_div(total, rd_chunk(total));
         uint64_t lo = std::min(task_lo, chunks), hi = std::min(task_hi, chunks);
         rr.task_lo = lo;
         rr.task_hi = hi;
+        unsigned long long* slot = im.take_slot();
         RdArgs a{};
         a.rows = g.rows; a.binom = im.binom; a.k = k_; a.c = c; a.id_rows = g.id_rows;
-        a.add_const = add_const; a.stop_at = stop_at; a.total = total;
+        a.add_const = 0; // rd counts identity rows itself
+        a.stop_at = stop_at; a.total = total; a.chunk = rd_chunk(total);
         a.task_lo = lo; a.task_hi = hi;
-        a.best_key = im.scratch; a.evaluated = im.scratch + 1;
+        a.best_key = slot; a.evaluated = slot + 1;
         CK(cudaEventRecord(im.ev0, im.stream));
         if (hi > lo) {
             uint64_t threads = hi - lo;
@@ -905,7 +1014,7 @@ RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t tas
             switch (g.nw) {
 #define RD_CASE(N) case N: RdLaunch<N, false>::run(a, grid, im.stream); break;
                 RD_CASE(1) RD_CASE(2) RD_CASE(3) RD_CASE(4) RD_CASE(5) RD_CASE(6) RD_CASE(7) RD_CASE(8)
-                RD_CASE(9) RD_CASE(10) RD_CASE(11) RD_CASE(12) RD_CASE(13) RD_CASE(14) RD_CASE(15) RD_CASE(16)
+                RD_CASE(10) RD_CASE(12) RD_CASE(14) RD_CASE(16) RD_CASE(20) RD_CASE(24) RD_CASE(28) RD_CASE(32)
 #undef RD_CASE
                 default: throw std::invalid_argument("row width beyond the device limit");
             }
@@ -913,15 +1022,14 @@ RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t tas
             im.cnt.launches += 1;
         }
         CK(cudaEventRecord(im.ev1, im.stream));
+        im.read_slot(slot);
     }
-    CK(cudaMemcpyAsync(im.host_scratch, im.scratch, 16, cudaMemcpyDeviceToHost, im.stream));
-    im.cnt.d2h += 16;
     CK(cudaStreamSynchronize(im.stream));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, im.ev0, im.ev1));
     rr.ms = ms;
-    rr.key = im.host_scratch[0];
-    rr.evaluated = im.host_scratch[1];
+    rr.key = im.host_slot[0];
+    rr.evaluated = im.host_slot[1];
     rr.w = rr.key == ~0ull ? UINT32_MAX : uint32_t(rr.key >> kKeyShift);
     rr.stopped = rr.w != UINT32_MAX && rr.w <= stop_at;
     return rr;
@@ -932,8 +1040,6 @@ RoundResult Engine::round_hist(uint32_t j, uint32_t c, uint64_t* hist) {
     CK(cudaSetDevice(device_));
     Impl& im = *impl_;
     const GammaDev& g = im.gammas[j];
-    const bool hid = g.id_rows > 0 && g.id_rows < k_;
-    const uint32_t add_const = (g.id_rows == k_) ? c : 0;
     const uint32_t nbins = n_ + 1;
     if (im.hist_cap < nbins) {
         cudaFree(im.hist_dev);
@@ -942,37 +1048,31 @@ RoundResult Engine::round_hist(uint32_t j, uint32_t c, uint64_t* hist) {
     }
     RoundResult rr;
     rr.combinations = binomial(k_, c);
-    TabPlan pl = make_tab_plan(k_, c, g.nw);
-    uint32_t* yt = ensure_ytab(im, j, k_, pl.s);
-    std::copy(pl.prefix.begin(), pl.prefix.end(), im.prefix_host);
-    CK(cudaMemcpyAsync(im.prefix_dev, im.prefix_host, pl.prefix.size() * 8, cudaMemcpyHostToDevice, im.stream));
+    const PlanEntry& pe = im.plan(k_, c, g, sms_);
+    uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
+    unsigned long long* slot = im.take_slot();
     CK(cudaMemsetAsync(im.hist_dev, 0, nbins * 8, im.stream));
-    CK(cudaMemsetAsync(im.scratch + 1, 0, 8, im.stream));
-    TabArgs a{};
-    a.rows = g.rows; a.ytab = yt; a.binom = im.binom; a.prefix = im.prefix_dev;
-    a.k = k_; a.p = pl.p; a.s = pl.s; a.emin = pl.emin; a.npiv = uint32_t(pl.prefix.size() - 1);
-    a.id_rows = g.id_rows; a.add_const = add_const;
-    a.tile_lo = 0; a.tile_hi = pl.tiles();
-    a.evaluated = im.scratch + 1;
+    TabArgs a = tab_args(im, g, pe, yt, k_, c);
+    a.tile_lo = 0; a.tile_hi = pe.plan.tiles();
+    a.evaluated = slot + 1; a.counter = slot + 2;
     a.nbins = nbins;
     a.hist = im.hist_dev;
-    int XS = stride_for(int(g.nw) + (hid ? 1 : 0));
-    size_t dyn = size_t(kTX) * XS * 4 + size_t(kWarps) * nbins * 4;
+    int XS = stride_for(int(g.nw) + (g.hid ? 1 : 0));
+    size_t dyn = size_t(pe.plan.TX) * XS * 4 + size_t(kWarps) * nbins * 4;
     CK(cudaEventRecord(im.ev0, im.stream));
-    dispatch_nw_hid<TabLaunch>(g.nw, hid, a, pl.tiles(), im.stream, 2, dyn, sms_);
+    dispatch_nw_hid<TabLaunch>(g.nw, g.hid, a, pe.plan.tiles(), im.stream, 2, dyn, sms_);
     CK(cudaGetLastError());
     im.cnt.launches += 1;
-    im.cnt.h2d += pl.prefix.size() * 8;
-    im.cnt.d2h += nbins * 8 + 8;
     CK(cudaEventRecord(im.ev1, im.stream));
     CK(cudaMemcpyAsync(hist, im.hist_dev, nbins * 8, cudaMemcpyDeviceToHost, im.stream));
-    CK(cudaMemcpyAsync(im.host_scratch + 1, im.scratch + 1, 8, cudaMemcpyDeviceToHost, im.stream));
+    im.cnt.d2h += nbins * 8;
+    im.read_slot(slot);
     CK(cudaStreamSynchronize(im.stream));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, im.ev0, im.ev1));
     rr.ms = ms;
-    rr.evaluated = im.host_scratch[1];
-    rr.task_hi = pl.tiles();
+    rr.evaluated = im.host_slot[1];
+    rr.task_hi = pe.plan.tiles();
     for (uint32_t w = 0; w < nbins; ++w)
         if (hist[w]) { rr.w = w; break; }
     rr.key = rr.w == UINT32_MAX ? ~0ull : (uint64_t(rr.w) << kKeyShift);
@@ -985,53 +1085,45 @@ std::vector<uint32_t> Engine::witness(uint32_t j, uint32_t c, const RoundResult&
     CK(cudaSetDevice(device_));
     Impl& im = *impl_;
     const GammaDev& g = im.gammas[j];
-    const bool hid = g.id_rows > 0 && g.id_rows < k_;
-    const uint32_t add_const = (g.id_rows == k_) ? c : 0;
     const uint64_t task = rr.key & ((uint64_t{1} << kKeyShift) - 1);
     const uint32_t target = uint32_t(rr.key >> kKeyShift);
     std::vector<uint32_t> idx(c);
-    CK(cudaMemsetAsync(im.scratch + 2, 0xFF, 8, im.stream));
+    unsigned long long* slot = im.take_slot();
     if (kernel_ == Kernel::tab) {
-        TabPlan pl = make_tab_plan(k_, c, g.nw);
-        uint32_t* yt = ensure_ytab(im, j, k_, pl.s);
-        std::copy(pl.prefix.begin(), pl.prefix.end(), im.prefix_host);
-        CK(cudaMemcpyAsync(im.prefix_dev, im.prefix_host, pl.prefix.size() * 8, cudaMemcpyHostToDevice, im.stream));
-        TabArgs a{};
-        a.rows = g.rows; a.ytab = yt; a.binom = im.binom; a.prefix = im.prefix_dev;
-        a.k = k_; a.p = pl.p; a.s = pl.s; a.emin = pl.emin; a.npiv = uint32_t(pl.prefix.size() - 1);
-        a.id_rows = g.id_rows; a.add_const = add_const;
+        const PlanEntry& pe = im.plan(k_, c, g, sms_);
+        if (task >= pe.plan.tiles()) throw std::invalid_argument("witness: key names no task of this round");
+        uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
+        TabArgs a = tab_args(im, g, pe, yt, k_, c);
         a.tile_lo = task; a.tile_hi = task + 1;
-        a.find_out = im.scratch + 2;
+        a.find_out = slot + 3;
         a.find_target = target;
-        dispatch_nw_hid<TabLaunch>(g.nw, hid, a, uint64_t(1), im.stream, 1, size_t(0), sms_);
+        dispatch_nw_hid<TabLaunch>(g.nw, g.hid, a, uint64_t(1), im.stream, 1, size_t(0), sms_);
         CK(cudaGetLastError());
         im.cnt.launches += 1;
-        im.cnt.d2h += 8;
-        CK(cudaMemcpyAsync(im.host_scratch + 2, im.scratch + 2, 8, cudaMemcpyDeviceToHost, im.stream));
+        im.read_slot(slot);
         CK(cudaStreamSynchronize(im.stream));
-        uint64_t f = im.host_scratch[2];
+        uint64_t f = im.host_slot[3];
         if (f == ~0ull) throw std::logic_error("witness: winning tile holds no codeword of the round minimum");
-        tab_decode(pl, task, uint32_t(f >> 32), uint32_t(f & 0xFFFFFFFFu), idx.data());
+        tab_decode(pe.plan, task, uint32_t(f >> 32), uint32_t(f & 0xFFFFFFFFu), idx.data());
     } else {
         RdArgs a{};
         a.rows = g.rows; a.binom = im.binom; a.k = k_; a.c = c; a.id_rows = g.id_rows;
-        a.add_const = add_const; a.total = binomial(k_, c);
+        a.add_const = 0; a.total = binomial(k_, c); a.chunk = rd_chunk(a.total);
         a.task_lo = task; a.task_hi = task + 1;
-        a.find_out = im.scratch + 2;
+        a.find_out = slot + 3;
         a.find_target = target;
         switch (g.nw) {
 #define RD_CASE(N) case N: RdLaunch<N, true>::run(a, 1, im.stream); break;
             RD_CASE(1) RD_CASE(2) RD_CASE(3) RD_CASE(4) RD_CASE(5) RD_CASE(6) RD_CASE(7) RD_CASE(8)
-            RD_CASE(9) RD_CASE(10) RD_CASE(11) RD_CASE(12) RD_CASE(13) RD_CASE(14) RD_CASE(15) RD_CASE(16)
+            RD_CASE(10) RD_CASE(12) RD_CASE(14) RD_CASE(16) RD_CASE(20) RD_CASE(24) RD_CASE(28) RD_CASE(32)
 #undef RD_CASE
             default: throw std::invalid_argument("row width beyond the device limit");
         }
         CK(cudaGetLastError());
         im.cnt.launches += 1;
-        im.cnt.d2h += 8;
-        CK(cudaMemcpyAsync(im.host_scratch + 2, im.scratch + 2, 8, cudaMemcpyDeviceToHost, im.stream));
+        im.read_slot(slot);
         CK(cudaStreamSynchronize(im.stream));
-        uint64_t f = im.host_scratch[2];
+        uint64_t f = im.host_slot[3];
         if (f == ~0ull) throw std::logic_error("witness: winning chunk holds no codeword of the round minimum");
         rd_unrank(c, f, idx.data());
     }

@@ -20,7 +20,7 @@ enum class Kernel : int { tab = 0, rd = 1 };
 // Limits of the device path (checked up front, std::invalid_argument).
 constexpr uint32_t kMaxK = 1024;        // rows of a Gamma
 constexpr uint32_t kMaxC = 64;          // level
-constexpr uint32_t kMaxWords32 = 16;    // 32-bit words of a compacted row (n' <= 512)
+constexpr uint32_t kMaxWords32 = 32;    // 32-bit words of a compacted row (n' <= 1024)
 
 struct RoundResult {
     uint32_t w = UINT32_MAX;
@@ -92,9 +92,12 @@ private:
     std::unique_ptr<Impl> impl_;
 };
 
-TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32);
+TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_blocks);
 uint32_t tab_yc(uint32_t nw32);
 uint32_t tab_tx();
+// kernel template width for a row of nw32 words (rows are zero-padded up to it)
+uint32_t template_width(uint32_t nw32);
+uint64_t rd_chunk(uint64_t total);
 // reconstruct the combination of tile `tile`, local prefix x / suffix y
 void tab_decode(const TabPlan& plan, uint64_t tile, uint32_t x_local, uint32_t y_local,
                 uint32_t* idx);

@@ -45,7 +45,7 @@ def test_round_random_shapes_vs_oracle(mdg, device, kernel):
     """Raw matrices of many widths (every NW template 1..16) and levels vs the oracle."""
     rng = np.random.default_rng(7)
     device.set_kernel(kernel)
-    for n in [5, 31, 32, 33, 64, 65, 97, 128, 160, 200, 256, 300, 384, 450, 512]:
+    for n in [5, 31, 32, 33, 64, 65, 97, 128, 160, 200, 256, 300, 384, 450, 512, 520, 700, 900, 1024]:
         k = int(rng.integers(6, 26))
         W = (n + 63) // 64
         rows = rng.integers(0, 2**63, size=(k, W), dtype=np.uint64)
@@ -126,11 +126,12 @@ def test_early_exit_is_exact(mdg, device, kernel):
     G = mdg.gen_matrix(128, 64, 1, True)
     gs = mdg.GammaSet.build(G, 128, 10, 1)
     device.load_gset(gs)
-    full = device.round(0, 5)
-    early = device.round(0, 5, stop_at=full.min_weight + 3)
+    c = 7  # large enough that not every task starts before the bound fires
+    full = device.round(0, c)
+    early = device.round(0, c, stop_at=full.min_weight + 3)
     assert early.min_weight <= full.min_weight + 3 and early.min_weight >= full.min_weight
     assert early.stopped_early and early.evaluated < full.evaluated
-    idx = device.round_witness(0, 5, early)
+    idx = device.round_witness(0, c, early)
     g0 = gs.gamma(0)
     assert popcount_rows(g0, idx)[0] == early.min_weight
 
