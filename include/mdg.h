@@ -65,6 +65,8 @@ int mdg_load_gammas(mdg_ctx* ctx, uint32_t m, uint32_t k, uint32_t n, const uint
 typedef struct {
     uint32_t min_weight;      /* UINT32_MAX when nothing was evaluated */
     uint32_t stopped_early;   /* 1 when the early-exit bound fired */
+    uint32_t bounded;         /* 1: no codeword below the cutoff; min_weight == cutoff is a bound */
+    uint32_t reserved;
     uint64_t argmin_key;      /* opaque (weight << 40 | task); input of mdg_round_witness */
     uint64_t combinations;    /* C(k,c): the reference's RoundStats.combinations */
     uint64_t evaluated;       /* codewords actually evaluated on this device */
@@ -85,6 +87,14 @@ int mdg_round(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t stop_at, mdg_round_
 int mdg_round_tasks(mdg_ctx* ctx, uint32_t j, uint32_t c, uint64_t* n_tasks);
 int mdg_round_range(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t stop_at, uint64_t task_lo,
                     uint64_t task_hi, mdg_round_out* out);
+
+/* Bound-pruned round: only weights < cutoff matter (pass the level loop's U).
+ * Returns min(true minimum, cutoff); bounded = 1 when no codeword lies below
+ * the cutoff. run_bz_loop's U = min(U, w) — hence d and every (L, U) — is the
+ * same as with the exact round, while the kernel skips the rest of a codeword's
+ * weight as soon as a partial weight exceeds the bound. cutoff 0 = exact. */
+int mdg_round_bounded(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t stop_at, uint32_t cutoff,
+                      uint64_t task_lo, uint64_t task_hi, mdg_round_out* out);
 
 /* Full weight histogram of round (j, c) (no early exit): hist[0..n] (config 5;
  * no reference counterpart). Returns the min in out. */
@@ -123,7 +133,7 @@ uint32_t mdg_lower_bound(uint32_t m, uint32_t g, uint32_t k, uint32_t k_last);
 uint32_t mdg_singleton_upper(uint32_t n, uint32_t k);
 
 /* -------------------------------------------------------------- the loop */
-typedef struct { uint32_t c, j, w, U_after; } mdg_round_rec;
+typedef struct { uint32_t c, j, w, U_after, bounded; } mdg_round_rec;
 typedef struct { uint32_t c, L_after, U_after, pad; } mdg_level_rec;
 
 /* RoundRunner as a C callback (engines.hpp:151): return 0 and set *w, or a
@@ -150,6 +160,9 @@ typedef struct {
     uint32_t level_cap;   /* 0 = run to termination */
     int kernel;           /* MDG_KERNEL_TAB | MDG_KERNEL_RD */
     int want_witness;     /* 1 = reconstruct and verify a minimum-weight codeword */
+    int exact_rounds;     /* 1 = every round's exact minimum (per-round trace parity with the
+                             reference's rounds); 0 = rounds bounded by U (same d and (L, U)
+                             trace, faster) */
 } mdg_config;
 void mdg_config_default(mdg_config* cfg);
 int mdg_min_weight(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n, const mdg_config* cfg,

@@ -106,13 +106,15 @@ struct RoundStats {
     uint32_t g = 0;
     uint32_t gamma_index = 0;
     uint32_t stop_at = 0;          // set by the loop: current L (early-exit hint)
+    uint32_t upper = 0;            // set by the loop: current U (bound for pruned rounds)
+    bool bounded = false;          // set by the runner: w is only a lower bound (>= U)
     uint64_t additions = 0;
     uint64_t combinations = 0;     // C(k, g): the reference's counter
     uint64_t evaluated = 0;        // codewords the device actually evaluated
     double device_ms = 0;
 };
 
-struct RoundRec { uint32_t c, j, w, U_after; };
+struct RoundRec { uint32_t c, j, w, U_after, bounded; };
 struct LevelRec { uint32_t c, L_after, U_after; };
 
 struct WorkStats {

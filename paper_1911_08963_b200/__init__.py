@@ -59,14 +59,14 @@ u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 
 class _RoundOut(C.Structure):
     _fields_ = [("min_weight", C.c_uint32), ("stopped_early", C.c_uint32),
-                ("argmin_key", C.c_uint64), ("combinations", C.c_uint64),
+                ("bounded", C.c_uint32), ("reserved", C.c_uint32), ("argmin_key", C.c_uint64), ("combinations", C.c_uint64),
                 ("evaluated", C.c_uint64), ("task_lo", C.c_uint64), ("task_hi", C.c_uint64),
                 ("device_ms", C.c_double)]
 
 
 class _Config(C.Structure):
     _fields_ = [("trials", C.c_uint32), ("seed", C.c_uint64), ("level_cap", C.c_uint32),
-                ("kernel", C.c_int), ("want_witness", C.c_int)]
+                ("kernel", C.c_int), ("want_witness", C.c_int), ("exact_rounds", C.c_int)]
 
 
 class _RunInfo(C.Structure):
@@ -80,7 +80,8 @@ class _RunInfo(C.Structure):
 
 
 class _RoundRec(C.Structure):
-    _fields_ = [("c", C.c_uint32), ("j", C.c_uint32), ("w", C.c_uint32), ("U_after", C.c_uint32)]
+    _fields_ = [("c", C.c_uint32), ("j", C.c_uint32), ("w", C.c_uint32), ("U_after", C.c_uint32),
+                ("bounded", C.c_uint32)]
 
 
 class _LevelRec(C.Structure):
@@ -105,6 +106,8 @@ SYMBOLS = {
     "mdg_round_tasks": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64)]),
     "mdg_round_range": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                   C.c_uint64, C.POINTER(_RoundOut)]),
+    "mdg_round_bounded": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                    C.c_uint64, C.c_uint64, C.POINTER(_RoundOut)]),
     "mdg_round_hist": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, u64p, C.POINTER(_RoundOut)]),
     "mdg_round_witness": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(_RoundOut), u32p]),
     "mdg_set_kernel": (C.c_int, [C.c_void_p, C.c_int]),
@@ -327,6 +330,7 @@ class GammaSet:
 class RoundOut:
     min_weight: int
     stopped_early: bool
+    bounded: bool
     argmin_key: int
     combinations: int
     evaluated: int
@@ -339,7 +343,7 @@ class RoundOut:
 def _round_out(o: _RoundOut) -> RoundOut:
     raw = _RoundOut()
     C.pointer(raw)[0] = o
-    return RoundOut(int(o.min_weight), bool(o.stopped_early), int(o.argmin_key),
+    return RoundOut(int(o.min_weight), bool(o.stopped_early), bool(o.bounded), int(o.argmin_key),
                     int(o.combinations), int(o.evaluated), int(o.task_lo), int(o.task_hi),
                     float(o.device_ms), raw)
 
@@ -398,6 +402,13 @@ class Device:
         _check(lib().mdg_round_range(self._h, j, c, stop_at, task_lo, task_hi, C.byref(o)))
         return _round_out(o)
 
+    def round_bounded(self, j: int, c: int, cutoff: int, stop_at: int = 0, task_lo: int = 0,
+                      task_hi: int = (1 << 64) - 1) -> RoundOut:
+        """Round bounded by `cutoff` (only weights < cutoff matter): min(true min, cutoff)."""
+        o = _RoundOut()
+        _check(lib().mdg_round_bounded(self._h, j, c, stop_at, cutoff, task_lo, task_hi, C.byref(o)))
+        return _round_out(o)
+
     def round_hist(self, j: int, c: int, n: int) -> tuple[RoundOut, np.ndarray]:
         hist = np.zeros(n + 1, dtype=np.uint64)
         o = _RoundOut()
@@ -430,10 +441,10 @@ class Device:
 
     def bz_loop(self, gs: "GammaSet", level_cap: int = 0, kernel: int = KERNEL_TAB,
                 witness: bool = True, rank: int = 0, world: int = 1,
-                reduce_min: Callable | str | None = None) -> "RunResult":
+                reduce_min: Callable | str | None = None, exact_rounds: bool = False) -> "RunResult":
         """run_bz_loop on the device over the Gamma set loaded with load_gset (no search,
         no upload): the device-resident level loop (+ witness)."""
-        cfg = _config(0, 0, level_cap, kernel, witness)
+        cfg = _config(0, 0, level_cap, kernel, witness, exact_rounds)
         h = C.c_void_p()
         if world == 1:
             _check(lib().mdg_bz_loop_device(self._h, gs._h, C.byref(cfg), C.byref(h)))
@@ -476,6 +487,7 @@ class RunResult:
     h2d_bytes: int
     d2h_bytes: int
     rounds: list            # [c, j, w, U_after]
+    round_bounded: list     # per executed round: 1 when w is only the bound U (pruned round)
     round_evaluated: list   # per executed round: codewords evaluated (this rank)
     round_ms: list          # per executed round: kernel time (CUDA events)
     levels: list            # [c, L_after, U_after]
@@ -515,6 +527,7 @@ def _collect(h) -> RunResult:
         gamma_seconds=info.gamma_seconds, loop_seconds=info.loop_seconds,
         launches=info.launches, h2d_bytes=info.h2d_bytes, d2h_bytes=info.d2h_bytes,
         rounds=[[r.c, r.j, r.w, r.U_after] for r in rr[: info.n_rounds]],
+        round_bounded=[int(r.bounded) for r in rr[: info.n_rounds]],
         round_evaluated=[int(x) for x in pe[: info.n_rounds]],
         round_ms=[float(x) for x in pm[: info.n_rounds]],
         levels=[[x.c, x.L_after, x.U_after] for x in ll[: info.n_levels]],
@@ -527,21 +540,24 @@ def _collect(h) -> RunResult:
     return res
 
 
-def _config(trials, seed, level_cap, kernel, witness) -> _Config:
+def _config(trials, seed, level_cap, kernel, witness, exact_rounds=False) -> _Config:
     cfg = _Config()
     lib().mdg_config_default(C.byref(cfg))
     cfg.trials, cfg.seed, cfg.level_cap = trials, seed, level_cap
     cfg.kernel, cfg.want_witness = kernel, 1 if witness else 0
+    cfg.exact_rounds = 1 if exact_rounds else 0
     return cfg
 
 
 def min_weight(G: np.ndarray, n: int, trials: int = 10, seed: int = 0, level_cap: int = 0,
                kernel: int = KERNEL_TAB, witness: bool = True,
-               device: Optional[Device] = None) -> RunResult:
-    """md::min_weight (engines.cpp:617-648) with the GPU engine, plus trace and witness."""
+               device: Optional[Device] = None, exact_rounds: bool = False) -> RunResult:
+    """md::min_weight (engines.cpp:617-648) with the GPU engine, plus trace and witness.
+    exact_rounds=True computes every round's exact minimum (per-round trace parity);
+    the default bounds rounds by U (identical d and (L, U) trace)."""
     G = _rows(G)
     h = C.c_void_p()
-    cfg = _config(trials, seed, level_cap, kernel, witness)
+    cfg = _config(trials, seed, level_cap, kernel, witness, exact_rounds)
     _check(lib().mdg_min_weight(device.handle if device else None, G, G.shape[0], n,
                                 C.byref(cfg), C.byref(h)))
     return _collect(h)
@@ -551,13 +567,13 @@ def min_weight_dist(G: np.ndarray, n: int, rank: int, world: int,
                     reduce_min: Callable[[np.ndarray], np.ndarray] | str = "nccl",
                     trials: int = 10, seed: int = 0, level_cap: int = 0,
                     kernel: int = KERNEL_TAB, witness: bool = True,
-                    device: Optional[Device] = None) -> RunResult:
+                    device: Optional[Device] = None, exact_rounds: bool = False) -> RunResult:
     """Multi-GPU min_weight: each rank evaluates a contiguous task range of every round;
     the per-round key is combined by NCCL allreduce(min) (reduce_min='nccl', device must have
     called nccl_init) or by a Python callable (numpy uint64 array -> elementwise global min)."""
     G = _rows(G)
     h = C.c_void_p()
-    cfg = _config(trials, seed, level_cap, kernel, witness)
+    cfg = _config(trials, seed, level_cap, kernel, witness, exact_rounds)
     fn, user, keep = _reducer(reduce_min, device)
     _check(lib().mdg_min_weight_dist(device.handle if device else None, G, G.shape[0], n,
                                      C.byref(cfg), rank, world, fn, user, C.byref(h)))

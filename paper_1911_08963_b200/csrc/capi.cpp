@@ -35,6 +35,7 @@ struct mdg_run {
     uint32_t witness_level = 0;
     bool witness_ok = false;
     bool witness_from_trace = true;
+    bool exact_rounds = false;
     double wall = 0, gamma_s = 0, loop_s = 0;
     Engine::Counters cnt;
 };
@@ -137,24 +138,31 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
     eng.set_kernel(cfg.kernel == MDG_KERNEL_RD ? Kernel::rd : Kernel::tab);
     Engine::Counters c0 = eng.counters();
     std::vector<RoundLog> log;
-    auto do_round = [&](uint32_t j, uint32_t g, uint32_t stop_at) {
+    auto do_round = [&](uint32_t j, uint32_t g, uint32_t stop_at, uint32_t cutoff) {
         RoundResult rr;
         if (world <= 1) {
-            rr = eng.round(j, g, stop_at);
+            rr = eng.round(j, g, stop_at, 0, UINT64_MAX, cutoff);
         } else {
             uint64_t T = eng.tasks(j, g);
             uint64_t lo = T * rank / world, hi = T * (rank + 1) / world;
-            rr = eng.round(j, g, stop_at, lo, hi);
+            rr = eng.round(j, g, stop_at, lo, hi, cutoff);
             uint64_t key = rr.key;
             int rc = reduce(user, &key, 1);
             if (rc != 0) throw std::runtime_error("mdg: cross-rank reduction failed");
             rr.key = key;
+            rr.bounded = false;
             rr.w = key == ~0ull ? UINT32_MAX : uint32_t(key >> 40);
+            if (cutoff && (key == ~0ull || rr.w >= cutoff)) {
+                rr.w = cutoff;
+                rr.key = ~0ull;
+                rr.bounded = true;
+            }
         }
         return rr;
     };
     RoundRunner runner = [&](uint32_t j, uint32_t g, RoundStats& rs) -> uint32_t {
-        RoundResult rr = do_round(j, g, rs.stop_at);
+        RoundResult rr = do_round(j, g, rs.stop_at, cfg.exact_rounds ? 0u : rs.upper);
+        rs.bounded = rr.bounded;
         rs.combinations = rr.combinations;
         rs.evaluated = rr.evaluated;
         rs.additions = rr.evaluated; // one row XOR per evaluated codeword
@@ -180,8 +188,8 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
             out.witness_from_trace = false;
             for (uint32_t g = 1; g <= k && !src; ++g)
                 for (uint32_t j = 0; j < m && !src; ++j) {
-                    RoundResult rr = do_round(j, g, d);
-                    if (rr.w <= d) {
+                    RoundResult rr = do_round(j, g, d, d + 1);
+                    if (!rr.bounded && rr.w <= d) {
                         extra = {j, g, rr};
                         src = &extra;
                     }
@@ -211,6 +219,7 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
     out.seed = cfg.seed;
     out.devices = world;
     out.kernel = cfg.kernel == MDG_KERNEL_RD ? "rd" : "tab";
+    out.exact_rounds = cfg.exact_rounds != 0;
 }
 
 // min_weight on the device(s): row_basis -> Gamma search -> Singleton U ->
@@ -244,6 +253,7 @@ std::string json_of(const mdg_run& r) {
       << ",\"seed\":" << r.seed << ",\"workers\":" << r.devices;
     // new keys: witness, trace, level cap, devices, throughput
     o << ",\"capped\":" << (r.er.capped ? "true" : "false") << ",\"level_cap\":" << r.level_cap
+      << ",\"exact_rounds\":" << (r.exact_rounds ? "true" : "false")
       << ",\"devices\":" << r.devices << ",\"kernel\":\"" << r.kernel << "\""
       << ",\"combinations_evaluated\":" << st.evaluated
       << ",\"device_seconds\":" << st.device_ms * 1e-3 << ",\"loop_seconds\":" << r.loop_s
@@ -260,7 +270,8 @@ std::string json_of(const mdg_run& r) {
     o << ",\"witness_ok\":" << (r.witness_ok ? "true" : "false") << ",\"trace\":[";
     for (size_t i = 0; i < st.rounds.size(); ++i) {
         const auto& x = st.rounds[i];
-        o << (i ? "," : "") << "[" << x.c << "," << x.j << "," << x.w << "," << x.U_after << "]";
+        o << (i ? "," : "") << "[" << x.c << "," << x.j << "," << x.w << "," << x.U_after << ","
+          << x.bounded << "]";
     }
     o << "],\"levels\":[";
     for (size_t i = 0; i < st.levels.size(); ++i) {
@@ -311,6 +322,8 @@ int mdg_load_gammas(mdg_ctx* ctx, uint32_t m, uint32_t k, uint32_t n, const uint
 static void fill_out(const RoundResult& rr, mdg_round_out* out) {
     out->min_weight = rr.w;
     out->stopped_early = rr.stopped ? 1u : 0u;
+    out->bounded = rr.bounded ? 1u : 0u;
+    out->reserved = 0;
     out->argmin_key = rr.key;
     out->combinations = rr.combinations;
     out->evaluated = rr.evaluated;
@@ -348,6 +361,15 @@ int mdg_round_range(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t stop_at, uint
         if (!ctx || !out) throw std::invalid_argument("null argument");
         if (task_lo > task_hi) throw std::invalid_argument("task range reversed");
         fill_out(ctx->eng->round(j, c, stop_at, task_lo, task_hi), out);
+    });
+}
+
+int mdg_round_bounded(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t stop_at, uint32_t cutoff,
+                      uint64_t task_lo, uint64_t task_hi, mdg_round_out* out) {
+    return guard([&] {
+        if (!ctx || !out) throw std::invalid_argument("null argument");
+        if (task_lo > task_hi) throw std::invalid_argument("task range reversed");
+        fill_out(ctx->eng->round(j, c, stop_at, task_lo, task_hi, cutoff), out);
     });
 }
 
@@ -498,6 +520,7 @@ void mdg_config_default(mdg_config* cfg) {
     cfg->level_cap = 0;
     cfg->kernel = MDG_KERNEL_TAB;
     cfg->want_witness = 1;
+    cfg->exact_rounds = 0;
 }
 
 int mdg_min_weight(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n, const mdg_config* cfg,
@@ -632,7 +655,7 @@ int mdg_run_rounds(const mdg_run* r, mdg_round_rec* out) {
         if (!r || !out) throw std::invalid_argument("null argument");
         for (size_t i = 0; i < r->er.stats.rounds.size(); ++i) {
             const auto& x = r->er.stats.rounds[i];
-            out[i] = {x.c, x.j, x.w, x.U_after};
+            out[i] = {x.c, x.j, x.w, x.U_after, x.bounded};
         }
     });
 }

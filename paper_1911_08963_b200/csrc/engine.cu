@@ -116,6 +116,53 @@ __device__ __forceinline__ void vload_global(const uint32_t* __restrict__ p, uin
     }
 }
 
+// Sum of the popcounts of N words with a carry-save adder chain (Harley–Seal):
+// each CSA folds two more words into the running "ones" word with 2 LOP3
+// (0x96 sum, 0xE8 majority) and emits one carry word of weight 2, reduced
+// the same way. POPC count per codeword drops from N to 2 (N=3), 3 (N=4..5,7),
+// 4 (N=6,8), 5 (N=16) — the XU pipe (16 POPC/clk/SM) is the binding unit,
+// LOP3 runs 4x faster on the ALU pipe.
+template <int N>
+__device__ __forceinline__ uint32_t popsum(const uint32_t (&v)[N]) {
+    if constexpr (N == 0) {
+        return 0u;
+    } else if constexpr (N == 1) {
+        return __popc(v[0]);
+    } else if constexpr (N == 2) {
+        return __popc(v[0]) + __popc(v[1]);
+    } else {
+        constexpr int M = (N - 1) / 2;
+        uint32_t carries[M];
+        uint32_t ones = v[0];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const uint32_t b = v[1 + 2 * i], c = v[2 + 2 * i];
+            const uint32_t t = ones ^ b ^ c;
+            carries[i] = (ones & b) | (ones & c) | (b & c);
+            ones = t;
+        }
+        uint32_t w = __popc(ones);
+        if constexpr ((N - 1) % 2 == 1) w += __popc(v[N - 1]);
+        return w + 2u * popsum<M>(carries);
+    }
+}
+
+// weight of X ^ Y over words [B, E)
+template <int B, int E, int S, int NW>
+__device__ __forceinline__ uint32_t xor_weight(const uint32_t (&X)[S], const uint32_t (&Y)[NW]) {
+    if constexpr (E <= B) {
+        return 0u;
+    } else {
+        uint32_t a[E - B];
+#pragma unroll
+        for (int i = 0; i < E - B; ++i) a[i] = X[B + i] ^ Y[B + i];
+        return popsum<E - B>(a);
+    }
+}
+
+// words of the pruning stage-1 partial weight
+__host__ __device__ constexpr int prune_words(int nw) { return nw <= 1 ? 1 : (nw + 1) / 2; }
+
 // ------------------------------------------------------ suffix table build
 // entry y: Q' = colex_unrank(y, s) ⊆ [0,k), Q = {k-1-q'}; XOR of rows(Q)
 // (+ |Q ∩ [0, id_rows)| in word NW when HID).
@@ -151,6 +198,7 @@ struct TabArgs {
     const uint64_t* binom;
     const uint64_t* prefix;
     uint32_t k, p, s, emin, npiv, id_rows, add_const, stop_at, tx;
+    uint32_t cutoff;               // only weights < cutoff matter (0 = exact round)
     uint64_t tile_lo, tile_hi;
     unsigned long long* best_key;
     unsigned long long* evaluated;
@@ -164,6 +212,7 @@ struct TabArgs {
 struct TileInfo {
     uint32_t e, nx, nyv, stop;
     uint64_t x0, y0, tile;
+    int32_t T;                     // pruning bound on the compacted weight (inclusive)
 };
 
 // decode tile -> (pivot, prefix chunk, suffix chunk); thread 0 only
@@ -235,6 +284,9 @@ __global__ void __launch_bounds__(kThreads) tab_round(TabArgs a) {
     constexpr int R = r_for(NW);
     constexpr int YC = R * kThreads;
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
+    constexpr int P = prune_words(NW);
+    // prune only when the bound sits well below the mean partial weight (16 per word)
+    constexpr int kPruneLimit = 16 * P - 2;
     __shared__ __align__(16) uint32_t xs[kTX * XS];
     __shared__ TileInfo ti;
     const uint32_t lane = threadIdx.x & 31;
@@ -245,13 +297,19 @@ __global__ void __launch_bounds__(kThreads) tab_round(TabArgs a) {
         if (threadIdx.x == 0) {
             // early exit: the global bound already meets stop_at
             unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
-            uint32_t stop = (g >> kKeyShift) <= a.stop_at;
+            uint32_t gw = uint32_t(g >> kKeyShift);
+            uint32_t stop = gw <= a.stop_at;
             if (!stop) { // dynamic tile scheduler: uniform tiles, no static tail
                 uint64_t t = a.tile_lo + atomicAdd(a.counter, 1ull);
                 stop = t >= a.tile_hi;
                 if (!stop) {
                     decode_tile<YC>(a, t, ti);
                     done_local += uint64_t(ti.nx) * ti.nyv;
+                    // weights that still matter: <= min(cutoff - 1, best found so far)
+                    int64_t lim = a.cutoff ? int64_t(a.cutoff) - 1 : int64_t(0x7FFFFFFF);
+                    if (int64_t(gw) < lim) lim = gw;
+                    lim -= a.add_const;
+                    ti.T = lim < -1 ? -1 : (lim > 0x7FFFFFFF ? 0x7FFFFFFF : int32_t(lim));
                 }
             }
             ti.stop = stop;
@@ -267,21 +325,56 @@ __global__ void __launch_bounds__(kThreads) tab_round(TabArgs a) {
 
         uint32_t best = 0xFFFFFFFFu;
         const uint32_t nx = ti.nx;
-        for (uint32_t xi = 0; xi < nx; ++xi) {
-            uint32_t X[XS];
-            vload<XS>(xs + xi * XS, X);
+        int32_t T = ti.T;
+        if (T < 0) {
+            // every codeword of this round is >= cutoff: nothing below the bound
+        } else if (T < kPruneLimit) {
+            // bound-pruned walk: a partial weight over the first P words is a lower
+            // bound; the rest is computed only when some lane can still go <= T.
+            // Stage 1 for all R suffixes, then stage 2 per group of G suffixes only
+            // when some lane of the warp has a partial weight <= T there (a real,
+            // warp-uniform branch: a per-codeword vote gets if-converted and the
+            // predicated POPCs still occupy the XU pipe).
+            constexpr int G = R >= 4 ? 4 : R;
+            for (uint32_t xi = 0; xi < nx; ++xi) {
+                uint32_t X[XS];
+                vload<XS>(xs + xi * XS, X);
+                uint32_t part[R];
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                uint32_t w = 0;
+                for (int r = 0; r < R; ++r) {
+                    part[r] = xor_weight<0, P, XS, NW>(X, Y[r]);
+                    if (HID) part[r] += X[NW] + idY[r];
+                }
 #pragma unroll
-                for (int i = 0; i < NW; ++i) w += __popc(X[i] ^ Y[r][i]);
-                if (HID) w += X[NW] + idY[r];
-                best = min(best, w);
+                for (int g0 = 0; g0 < R; g0 += G) {
+                    uint32_t gmin = part[g0];
+#pragma unroll
+                    for (int r = 1; r < G; ++r) gmin = min(gmin, part[g0 + r]);
+                    if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= T)) {
+#pragma unroll
+                        for (int r = 0; r < G; ++r) {
+                            const uint32_t w = part[g0 + r] + xor_weight<P, NW, XS, NW>(X, Y[g0 + r]);
+                            best = min(best, w);
+                        }
+                        T = min(T, int32_t(best));
+                    }
+                }
+            }
+        } else {
+            for (uint32_t xi = 0; xi < nx; ++xi) {
+                uint32_t X[XS];
+                vload<XS>(xs + xi * XS, X);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    uint32_t w = xor_weight<0, NW, XS, NW>(X, Y[r]);
+                    if (HID) w += X[NW] + idY[r];
+                    best = min(best, w);
+                }
             }
         }
-        best += a.add_const;
+        if (best != 0xFFFFFFFFu) best += a.add_const;
         best = __reduce_min_sync(0xFFFFFFFFu, best);
-        if (lane == 0) {
+        if (lane == 0 && best != 0xFFFFFFFFu && (a.cutoff == 0 || best < a.cutoff)) {
             unsigned long long key = (static_cast<unsigned long long>(best) << kKeyShift) | tile;
             if (key < seen) {
                 unsigned long long old = atomicMin(a.best_key, key);
@@ -315,9 +408,7 @@ __global__ void __launch_bounds__(kThreads) tab_find(TabArgs a) {
         vload<XS>(xs + xi * XS, X);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            uint32_t w = 0;
-#pragma unroll
-            for (int i = 0; i < NW; ++i) w += __popc(X[i] ^ Y[r][i]);
+            uint32_t w = xor_weight<0, NW, XS, NW>(X, Y[r]);
             if (HID) w += X[NW] + idY[r];
             w += a.add_const;
             uint32_t yl = r * kThreads + warp * 32 + lane;
@@ -365,9 +456,7 @@ __global__ void __launch_bounds__(kThreads) tab_hist(TabArgs a) {
             vload<XS>(xs + xi * XS, X);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                uint32_t w = a.add_const;
-#pragma unroll
-                for (int i = 0; i < NW; ++i) w += __popc(X[i] ^ Y[r][i]);
+                uint32_t w = a.add_const + xor_weight<0, NW, XS, NW>(X, Y[r]);
                 if (HID) w += X[NW] + idY[r];
                 if (valid[r]) atomicAdd(mybins + w, 1u);
             }
@@ -968,7 +1057,8 @@ uint64_t Engine::tasks(uint32_t j, uint32_t c) {
     return impl_->plan(k_, c, impl_->gammas[j], sms_).plan.tiles();
 }
 
-RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t task_lo, uint64_t task_hi) {
+RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t task_lo, uint64_t task_hi,
+                          uint32_t cutoff) {
     check_round(j, c);
     CK(cudaSetDevice(device_));
     Impl& im = *impl_;
@@ -984,6 +1074,7 @@ RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t tas
         unsigned long long* slot = im.take_slot();
         TabArgs a = tab_args(im, g, pe, yt, k_, c);
         a.stop_at = stop_at;
+        a.cutoff = cutoff;
         a.tile_lo = lo; a.tile_hi = hi;
         a.best_key = slot; a.evaluated = slot + 1; a.counter = slot + 2;
         CK(cudaEventRecord(im.ev0, im.stream));
@@ -1031,7 +1122,12 @@ RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t tas
     rr.key = im.host_slot[0];
     rr.evaluated = im.host_slot[1];
     rr.w = rr.key == ~0ull ? UINT32_MAX : uint32_t(rr.key >> kKeyShift);
-    rr.stopped = rr.w != UINT32_MAX && rr.w <= stop_at;
+    if (cutoff && rr.w >= cutoff) { // rd reports full minima; tab never reports >= cutoff
+        rr.w = cutoff;
+        rr.key = ~0ull;
+        rr.bounded = true;
+    }
+    rr.stopped = !rr.bounded && rr.w != UINT32_MAX && rr.w <= stop_at;
     return rr;
 }
 

@@ -25,6 +25,7 @@ constexpr uint32_t kMaxWords32 = 32;    // 32-bit words of a compacted row (n' <
 struct RoundResult {
     uint32_t w = UINT32_MAX;
     bool stopped = false;
+    bool bounded = false;  // nothing below the cutoff: w == cutoff is only a lower bound
     uint64_t key = ~uint64_t{0};
     uint64_t combinations = 0;
     uint64_t evaluated = 0;
@@ -61,8 +62,11 @@ public:
     Kernel kernel() const { return kernel_; }
 
     uint64_t tasks(uint32_t j, uint32_t c);
+    // cutoff: only weights < cutoff matter (0 = the exact round minimum). With a
+    // cutoff the result is min(true minimum, cutoff) and `bounded` is set when no
+    // codeword lies below it — what run_bz_loop's U = min(U, w) needs.
     RoundResult round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t task_lo = 0,
-                      uint64_t task_hi = UINT64_MAX);
+                      uint64_t task_hi = UINT64_MAX, uint32_t cutoff = 0);
     RoundResult round_hist(uint32_t j, uint32_t c, uint64_t* hist);
     std::vector<uint32_t> witness(uint32_t j, uint32_t c, const RoundResult& rr);
 

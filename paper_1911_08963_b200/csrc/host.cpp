@@ -190,7 +190,9 @@ uint32_t singleton_upper(uint32_t n, uint32_t k) {
 // Added: the level cap (a round at level g > cap is never run; capped=true)
 // and the trace. rs.stop_at carries the current L to the runner: a round may
 // stop once it has found a weight <= L, because at that point U > L and
-// d >= L, so its minimum is exactly L.
+// d >= L, so its minimum is exactly L. rs.upper carries
+// U: a runner may return min(w, U) and set rs.bounded when no codeword lies
+// below U — U = min(U, w) and hence d and every (L, U) are unchanged.
 EngineResult run_bz_loop(const GammaSet& gs, Bounds bounds, const RoundRunner& round,
                          uint32_t level_cap) {
     const uint32_t k = gs.k();
@@ -213,7 +215,10 @@ EngineResult run_bz_loop(const GammaSet& gs, Bounds bounds, const RoundRunner& r
             rs.g = g;
             rs.gamma_index = j;
             rs.stop_at = L;
+            rs.upper = U;
             uint32_t w = round(j, g, rs);
+            if (rs.bounded && w < U)
+                throw std::logic_error("run_bz_loop: a bounded round reported a weight below U");
             res.stats.row_additions += rs.additions;
             res.stats.combinations += rs.combinations;
             res.stats.evaluated += rs.evaluated;
@@ -223,10 +228,10 @@ EngineResult run_bz_loop(const GammaSet& gs, Bounds bounds, const RoundRunner& r
             if (w < U) {
                 U = w;
                 res.witness_round = static_cast<int32_t>(res.stats.rounds.size());
-            } else if (w == U && res.witness_round < 0) {
+            } else if (w == U && !rs.bounded && res.witness_round < 0) {
                 res.witness_round = static_cast<int32_t>(res.stats.rounds.size());
             }
-            res.stats.rounds.push_back({g, j, w, U});
+            res.stats.rounds.push_back({g, j, w, U, rs.bounded ? 1u : 0u});
         }
         if (done) break;
         uint32_t nl = lower_bound(m, g, k, gs.k_last);

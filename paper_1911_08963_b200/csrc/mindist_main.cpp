@@ -19,7 +19,8 @@ namespace {
 int usage() {
     std::cerr << "usage:\n"
                  "  mindist mindist FILE [--algorithm gpu] [--kernel tab|rd] [--trials T]\n"
-                 "                       [--seed S] [--level-cap C] [--device D] [--pretty]\n"
+                 "                       [--seed S] [--level-cap C] [--device D] [--exact-rounds]\n"
+                 "                       [--pretty]\n"
                  "  mindist gen --n N --k K --seed S [--plain]\n";
     return 2;
 }
@@ -75,6 +76,7 @@ int main(int argc, char** argv) {
     for (int i = 3; i < argc; ++i) {
         std::string a = argv[i];
         if (a == "--pretty") { pretty = true; continue; }
+        if (a == "--exact-rounds") { cfg.exact_rounds = 1; continue; }
         if (i + 1 >= argc) return usage();
         std::string v = argv[++i];
         uint64_t x = 0;

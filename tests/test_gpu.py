@@ -167,9 +167,44 @@ def test_round_argument_errors(mdg, device):
         device.load_gammas(np.ones((3, 1), dtype=np.uint64), 10, ranks=[3])
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_bounded_round_vs_oracle(mdg, device, kernel):
+    """Bound-pruned rounds return min(true minimum, cutoff), flag `bounded` exactly when no
+    codeword lies below the cutoff, and name a witness of the returned weight otherwise."""
+    device.set_kernel(kernel)
+    for (n, k, seed) in [(128, 64, 1), (300, 200, 11), (256, 32, 7), (70, 20, 5)]:
+        G = mdg.gen_matrix(n, k, seed, True)
+        gs = mdg.GammaSet.build(G, n, 10, seed)
+        device.load_gset(gs)
+        for j in range(gs.m):
+            g = gs.gamma(j)
+            for c in (2, 3, 4):
+                w, _ = port.round_min(g, n, c)
+                for cutoff in (w - 3, w, w + 1, w + 5, 1, n + 1):
+                    if cutoff < 1:
+                        continue
+                    out = device.round_bounded(j, c, cutoff)
+                    assert out.min_weight == min(w, cutoff), (n, k, j, c, cutoff, kernel)
+                    assert out.bounded == (w >= cutoff), (n, k, j, c, cutoff)
+                    if not out.bounded:
+                        idx = device.round_witness(j, c, out)
+                        assert popcount_rows(g, idx)[0] == w
+
+
 # -------------------------------------------------------------- front door
-def _check_run(res, case, name):
-    assert res.rounds == case["rounds"], name
+def _check_run(res, case, name, exact=True):
+    if exact:
+        assert res.rounds == case["rounds"], name
+        assert not any(res.round_bounded), name
+    else:
+        # bounded rounds: w = min(exact w, U before the round); identical U after each round
+        U = case["n"] - case["k"] + 1
+        exp = []
+        for c, j, w, Ua in case["rounds"]:
+            exp.append([c, j, min(w, U), Ua])
+            assert res.round_bounded[len(exp) - 1] == (1 if w >= U else 0), (name, c, j)
+            U = Ua
+        assert res.rounds == exp, name
     assert res.levels == case["levels"][: len(res.levels)] and len(res.levels) == len(case["levels"]), name
     assert res.m == case["m"] and res.k_last == case["k_last"], name
     assert res.g_final == case["g_final"], name
@@ -180,29 +215,32 @@ def _check_run(res, case, name):
     assert wt == res.d, name
 
 
+@pytest.mark.parametrize("exact", [True, False])
 @pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("kind", ["kats", "seeded"])
-def test_min_weight_small_codes(mdg, device, kind, kernel):
+def test_min_weight_small_codes(mdg, device, kind, kernel, exact):
     for case in load_golden(kind):
         rows, n = mdg.parse_matrix(case["matrix"])
-        res = mdg.min_weight(rows, n, case["trials"], case["seed"], kernel=kernel, device=device)
+        res = mdg.min_weight(rows, n, case["trials"], case["seed"], kernel=kernel, device=device,
+                             exact_rounds=exact)
         assert res.d == case["d"] == case["d_brute"], case["name"]
-        _check_run(res, case, case["name"])
+        _check_run(res, case, case["name"], exact)
 
 
+@pytest.mark.parametrize("exact", [True, False])
 @pytest.mark.parametrize("name", ["cfg1", "cfg2_s1", "cfg2_s2", "cfg2_s3", "cfg2_s4", "cfg2_s5",
                                   "cfg2_s6", "cfg2_s7", "cfg2_s8", "cfg3", "cfg4"])
-def test_min_weight_configs(mdg, device, name):
+def test_min_weight_configs(mdg, device, name, exact):
     case = next(c for c in load_golden("configs") if c["name"] == name)
     g = case["gen"]
     rows = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
     res = mdg.min_weight(rows, g["n"], case["trials"], case["seed"], level_cap=case["level_cap"],
-                         device=device)
+                         device=device, exact_rounds=exact)
     if case["capped"]:
         assert res.capped and res.d == case["U_final"]
     else:
         assert not res.capped and res.d == case["d"]
-    _check_run(res, case, name)
+    _check_run(res, case, name, exact)
     # the witness lies in the code spanned by G (rank does not grow)
     assert port.rank(np.vstack([rows, res.witness[None, :]]), g["n"]) == port.rank(rows, g["n"])
 
@@ -217,7 +255,7 @@ def test_min_weight_cfg4_cap6(mdg, device):
     rows = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
     res = mdg.min_weight(rows, g["n"], 10, g["seed"], level_cap=6, device=device)
     assert res.capped and res.d == case["U_final"]
-    _check_run(res, case, "cfg4_cap6")
+    _check_run(res, case, "cfg4_cap6", exact=False)
 
 
 def test_dist_two_ranks_threaded(mdg):
@@ -255,4 +293,4 @@ def test_dist_two_ranks_threaded(mdg):
     for r in range(world):
         res = results[r]
         assert res.d == case["d"]
-        _check_run(res, case, f"rank{r}")
+        _check_run(res, case, f"rank{r}", exact=False)

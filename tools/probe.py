@@ -6,7 +6,7 @@ sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(_
 import paper_1911_08963_b200 as mdg  # noqa: E402
 
 
-def probe(n, k, seed, levels, kernel=0, reps=3):
+def probe(n, k, seed, levels, kernel=0, reps=3, cutoff=0):
     G = mdg.gen_matrix(n, k, seed, True)
     gs = mdg.GammaSet.build(G, n, 10, seed)
     dev = mdg.Device(0)
@@ -17,10 +17,10 @@ def probe(n, k, seed, levels, kernel=0, reps=3):
         for j in range(gs.m):
             best = None
             for _ in range(reps):
-                o = dev.round(j, c)
+                o = dev.round_bounded(j, c, cutoff) if cutoff else dev.round(j, c)
                 best = o if best is None or o.device_ms < best.device_ms else best
             cw = best.evaluated / (best.device_ms * 1e-3)
-            print(f"[{n},{k}] kernel={'tab' if kernel == 0 else 'rd'} c={c} j={j} w={best.min_weight} "
+            print(f"[{n},{k}] kernel={'tab' if kernel == 0 else 'rd'} cut={cutoff} c={c} j={j} w={best.min_weight} "
                   f"cw={best.evaluated} ms={best.device_ms:.3f} cw/s={cw:.3e} "
                   f"cw/clk/SM@1.965={cw / (sms * 1.965e9):.2f}", flush=True)
     dev.close()
@@ -28,6 +28,10 @@ def probe(n, k, seed, levels, kernel=0, reps=3):
 
 if __name__ == "__main__":
     probe(128, 64, 1, [5, 6, 7])
+    probe(128, 64, 1, [6, 7], cutoff=15)
+    probe(128, 64, 1, [6, 7], cutoff=17)
+    probe(300, 200, 11, [5], reps=1, cutoff=26)
+    probe(256, 32, 7, [9], cutoff=76)
     probe(128, 64, 1, [5, 6], kernel=1, reps=1)
     probe(256, 32, 7, [7, 9])
     probe(300, 200, 11, [4, 5, 6], reps=1)
