@@ -173,8 +173,52 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
     Bounds bounds;
     bounds.lower = 1;
     bounds.upper = singleton_upper(n, k);
+    const bool nccl_reduce = world > 1 && reduce == &mdg_nccl_reduce_min;
     eng.timer_start();
-    out.er = run_bz_loop(gs, bounds, runner, cfg.level_cap);
+    if (eng.kernel() == Kernel::tab && (world == 1 || nccl_reduce)) {
+        // device-chained level loop: same semantics as run_bz_loop, no host sync per round
+        Engine::ChainResult cr = eng.chain_loop(bounds.upper, bounds.lower, cfg.level_cap,
+                                                cfg.exact_rounds != 0, gs.k_last, rank, world);
+        EngineResult& er = out.er;
+        uint32_t U = bounds.upper;
+        for (const auto& r : cr.rounds) {
+            RoundStats rs;
+            rs.g = r.c;
+            rs.gamma_index = r.j;
+            rs.bounded = r.bounded != 0;
+            rs.combinations = binomial(k, r.c);
+            rs.evaluated = r.evaluated;
+            rs.additions = r.evaluated;
+            rs.device_ms = r.ms;
+            er.stats.row_additions += rs.additions;
+            er.stats.combinations += rs.combinations;
+            er.stats.evaluated += rs.evaluated;
+            er.stats.device_ms += rs.device_ms;
+            er.stats.per_g.push_back(rs);
+            er.stats.g_final = r.c;
+            if (r.w < U) {
+                U = r.w;
+                er.witness_round = int32_t(er.stats.rounds.size());
+            } else if (r.w == U && !rs.bounded && er.witness_round < 0) {
+                er.witness_round = int32_t(er.stats.rounds.size());
+            }
+            if (U != r.U_after) throw std::logic_error("chain_loop: device U disagrees with the trace");
+            er.stats.rounds.push_back({r.c, r.j, r.w, r.U_after, r.bounded});
+            if (r.level_end) er.stats.levels.push_back({r.c, r.L_after, r.U_after});
+            RoundResult rr;
+            rr.w = r.w;
+            rr.key = r.key;
+            rr.bounded = r.bounded != 0;
+            rr.evaluated = r.evaluated;
+            rr.combinations = rs.combinations;
+            rr.ms = r.ms;
+            log.push_back({r.j, r.c, rr});
+        }
+        er.d = cr.U;
+        er.capped = cr.capped;
+    } else {
+        out.er = run_bz_loop(gs, bounds, runner, cfg.level_cap);
+    }
     out.loop_s = eng.timer_stop_ms() * 1e-3;
     const uint32_t d = out.er.d;
 

@@ -192,7 +192,20 @@ __global__ void ytab_build(const uint32_t* __restrict__ rows, const uint64_t* __
     for (int w = 0; w < YS; ++w) o[w] = w < NW ? acc[w] : (HID && w == NW ? id : 0u);
 }
 
+// Device-side state of the level loop (run_bz_loop, engines.cpp:447-476) when
+// rounds are chained on the stream: round kernels read U / L / done at start,
+// a one-thread finalize kernel applies U = min(U, w), the per-level L update,
+// the fast path (U <= L) and termination (L >= U) exactly as the host loop.
+struct ChainState {
+    uint32_t U, L, done, exact;
+};
+struct ChainRec {
+    uint32_t c, j, w, U_after, bounded, ran, L_after, level_end;
+    unsigned long long key, evaluated;
+};
+
 struct TabArgs {
+    const ChainState* st;          // non-null: cutoff / stop_at / skip from the chain state
     const uint32_t* rows;
     const uint32_t* ytab;
     const uint64_t* binom;
@@ -292,13 +305,20 @@ __global__ void __launch_bounds__(kThreads) tab_round(TabArgs a) {
     const uint32_t lane = threadIdx.x & 31;
     unsigned long long seen = ~0ull; // lane 0's view of the global best key
     unsigned long long done_local = 0;
+    uint32_t cutoff = a.cutoff, stop_at = a.stop_at;
+    if (a.st) { // chained round: the loop state decides (same values in every block)
+        const ChainState cs = *a.st;
+        if (cs.done || cs.U <= cs.L) return;
+        cutoff = cs.exact ? 0u : cs.U;
+        stop_at = cs.L;
+    }
 
     for (;;) {
         if (threadIdx.x == 0) {
             // early exit: the global bound already meets stop_at
             unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
             uint32_t gw = uint32_t(g >> kKeyShift);
-            uint32_t stop = gw <= a.stop_at;
+            uint32_t stop = gw <= stop_at;
             if (!stop) { // dynamic tile scheduler: uniform tiles, no static tail
                 uint64_t t = a.tile_lo + atomicAdd(a.counter, 1ull);
                 stop = t >= a.tile_hi;
@@ -306,7 +326,7 @@ __global__ void __launch_bounds__(kThreads) tab_round(TabArgs a) {
                     decode_tile<YC>(a, t, ti);
                     done_local += uint64_t(ti.nx) * ti.nyv;
                     // weights that still matter: <= min(cutoff - 1, best found so far)
-                    int64_t lim = a.cutoff ? int64_t(a.cutoff) - 1 : int64_t(0x7FFFFFFF);
+                    int64_t lim = cutoff ? int64_t(cutoff) - 1 : int64_t(0x7FFFFFFF);
                     if (int64_t(gw) < lim) lim = gw;
                     lim -= a.add_const;
                     ti.T = lim < -1 ? -1 : (lim > 0x7FFFFFFF ? 0x7FFFFFFF : int32_t(lim));
@@ -374,7 +394,7 @@ __global__ void __launch_bounds__(kThreads) tab_round(TabArgs a) {
         }
         if (best != 0xFFFFFFFFu) best += a.add_const;
         best = __reduce_min_sync(0xFFFFFFFFu, best);
-        if (lane == 0 && best != 0xFFFFFFFFu && (a.cutoff == 0 || best < a.cutoff)) {
+        if (lane == 0 && best != 0xFFFFFFFFu && (cutoff == 0 || best < cutoff)) {
             unsigned long long key = (static_cast<unsigned long long>(best) << kKeyShift) | tile;
             if (key < seen) {
                 unsigned long long old = atomicMin(a.best_key, key);
@@ -384,6 +404,42 @@ __global__ void __launch_bounds__(kThreads) tab_round(TabArgs a) {
         __syncthreads(); // xs / ti reused by the next tile
     }
     if (threadIdx.x == 0 && done_local) atomicAdd(a.evaluated, done_local);
+}
+
+// One thread: close a chained round (engines.cpp:456-472 semantics).
+__global__ void chain_finalize(ChainState* st, const unsigned long long* slot, ChainRec* rec,
+                               uint32_t c, uint32_t j, uint32_t last_of_level, uint32_t lb) {
+    if (threadIdx.x != 0) return;
+    ChainRec r{};
+    r.c = c;
+    r.j = j;
+    if (st->done || st->U <= st->L) { // fast path: the round is not run, the loop ends
+        st->done = 1;
+        r.ran = 0;
+        *rec = r;
+        return;
+    }
+    const uint32_t cutoff = st->exact ? 0u : st->U;
+    unsigned long long key = slot[0];
+    uint32_t w = key == ~0ull ? 0xFFFFFFFFu : uint32_t(key >> kKeyShift);
+    if (cutoff && (key == ~0ull || w >= cutoff)) {
+        w = cutoff;
+        key = ~0ull;
+        r.bounded = 1;
+    }
+    r.ran = 1;
+    r.w = w;
+    r.key = key;
+    r.evaluated = slot[1];
+    if (w < st->U) st->U = w;
+    r.U_after = st->U;
+    if (last_of_level) {
+        if (lb > st->L) st->L = lb;
+        r.L_after = st->L;
+        r.level_end = 1;
+        if (st->L >= st->U) st->done = 1;
+    }
+    *rec = r;
 }
 
 // witness: the smallest (x_local, y_local) of the tile whose weight == target
@@ -878,6 +934,19 @@ struct Engine::Impl {
     ncclComm_t comm = nullptr;
     uint64_t* red_dev = nullptr;
     size_t red_cap = 0;
+    ChainState* d_state = nullptr;
+    ChainState* h_state = nullptr;   // pinned
+    ChainRec* d_recs = nullptr;
+    size_t recs_cap = 0;
+    std::vector<cudaEvent_t> evpool;
+    cudaEvent_t event(size_t i) {
+        while (evpool.size() <= i) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            evpool.push_back(e);
+        }
+        return evpool[i];
+    }
 
     unsigned long long* take_slot() {
         if (next_slot >= kSlots) {
@@ -935,6 +1004,8 @@ Engine::Engine(int device) : device_(device), impl_(new Impl) {
     CK(cudaMemcpy(impl_->binom, T.data(), T.size() * 8, cudaMemcpyHostToDevice));
     CK(cudaMalloc(&impl_->slots, size_t(kSlots) * 32));
     CK(cudaHostAlloc(&impl_->host_slot, 32, cudaHostAllocDefault));
+    CK(cudaMalloc(&impl_->d_state, sizeof(ChainState)));
+    CK(cudaHostAlloc(&impl_->h_state, sizeof(ChainState), cudaHostAllocDefault));
 }
 
 Engine::~Engine() {
@@ -948,6 +1019,10 @@ Engine::~Engine() {
         try { nccl().CommDestroy(impl_->comm); } catch (...) {}
     }
     cudaFree(impl_->red_dev);
+    cudaFree(impl_->d_state);
+    cudaFree(impl_->d_recs);
+    cudaFreeHost(impl_->h_state);
+    for (auto e : impl_->evpool) cudaEventDestroy(e);
     cudaFree(impl_->hist_dev);
     cudaFree(impl_->binom);
     cudaFree(impl_->slots);
@@ -1224,6 +1299,103 @@ std::vector<uint32_t> Engine::witness(uint32_t j, uint32_t c, const RoundResult&
         rd_unrank(c, f, idx.data());
     }
     return idx;
+}
+
+Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_cap, bool exact,
+                                       uint32_t k_last, uint32_t rank, uint32_t world) {
+    if (kernel_ != Kernel::tab) throw std::logic_error("chain_loop: tab kernel only");
+    if (world > 1 && !impl_->comm) throw std::logic_error("chain_loop: NCCL communicator not initialised");
+    CK(cudaSetDevice(device_));
+    Impl& im = *impl_;
+    // host work per check: ~2e8 codewords (~0.1 ms of device time) between looks at `done`
+    constexpr double kCheckWork = 2e8;
+    ChainState init{U0, L0 < 1 ? 1u : L0, 0u, exact ? 1u : 0u};
+    init.done = init.U <= init.L ? 1u : 0u;
+    *im.h_state = init;
+    CK(cudaMemcpyAsync(im.d_state, im.h_state, sizeof(ChainState), cudaMemcpyHostToDevice, im.stream));
+    im.cnt.h2d += sizeof(ChainState);
+    const size_t max_rounds = size_t(k_) * m_;
+    if (im.recs_cap < max_rounds) {
+        cudaFree(im.d_recs);
+        CK(cudaMalloc(&im.d_recs, max_rounds * sizeof(ChainRec)));
+        im.recs_cap = max_rounds;
+    }
+    ChainResult res;
+    size_t nrec = 0;
+    double pending = 0;
+    uint32_t g = 1;
+    bool done = init.done != 0;
+    while (!done && g <= k_) {
+        if (level_cap && g > level_cap) break;
+        bool too_big = g > kMaxC;
+        if (!too_big) {
+            try { binomial(k_, g); } catch (const std::overflow_error&) { too_big = true; }
+        }
+        if (too_big) { // the host loop would raise here only if it gets here
+            CK(cudaMemcpyAsync(im.h_state, im.d_state, sizeof(ChainState), cudaMemcpyDeviceToHost, im.stream));
+            CK(cudaStreamSynchronize(im.stream));
+            if (im.h_state->done) { done = true; break; }
+            check_round(0, g); // throws the reference's error for this level
+        }
+        const uint32_t lb = lower_bound(m_, g, k_, k_last);
+        for (uint32_t j = 0; j < m_; ++j) {
+            const GammaDev& gd = im.gammas[j];
+            const PlanEntry& pe = im.plan(k_, g, gd, sms_);
+            uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
+            unsigned long long* slot = im.take_slot();
+            TabArgs a = tab_args(im, gd, pe, yt, k_, g);
+            const uint64_t T = pe.plan.tiles();
+            a.st = im.d_state;
+            a.tile_lo = world > 1 ? T * rank / world : 0;
+            a.tile_hi = world > 1 ? T * (rank + 1) / world : T;
+            a.best_key = slot; a.evaluated = slot + 1; a.counter = slot + 2;
+            CK(cudaEventRecord(im.event(2 * nrec), im.stream));
+            if (a.tile_hi > a.tile_lo) {
+                dispatch_nw_hid<TabLaunch>(gd.nw, gd.hid, a, a.tile_hi - a.tile_lo, im.stream, 0, size_t(0), sms_);
+                CK(cudaGetLastError());
+                im.cnt.launches += 1;
+            }
+            CK(cudaEventRecord(im.event(2 * nrec + 1), im.stream));
+            if (world > 1) {
+                int rc = nccl().AllReduce(slot, slot, 1, kNcclUint64, kNcclMin, im.comm, im.stream);
+                if (rc != 0) throw std::runtime_error(std::string("ncclAllReduce: ") + nccl().GetErrorString(rc));
+            }
+            chain_finalize<<<1, 32, 0, im.stream>>>(im.d_state, slot, im.d_recs + nrec, g, j,
+                                                    j + 1 == m_ ? 1u : 0u, lb);
+            CK(cudaGetLastError());
+            im.cnt.launches += 1;
+            ++nrec;
+            pending += double(binomial(k_, g)) / world;
+        }
+        ++g;
+        if (pending >= kCheckWork || g > k_ || (level_cap && g > level_cap)) {
+            CK(cudaMemcpyAsync(im.h_state, im.d_state, sizeof(ChainState), cudaMemcpyDeviceToHost, im.stream));
+            CK(cudaStreamSynchronize(im.stream));
+            im.cnt.d2h += sizeof(ChainState);
+            done = im.h_state->done != 0;
+            pending = 0;
+        }
+    }
+    CK(cudaMemcpyAsync(im.h_state, im.d_state, sizeof(ChainState), cudaMemcpyDeviceToHost, im.stream));
+    std::vector<ChainRec> recs(nrec);
+    if (nrec)
+        CK(cudaMemcpyAsync(recs.data(), im.d_recs, nrec * sizeof(ChainRec), cudaMemcpyDeviceToHost, im.stream));
+    CK(cudaStreamSynchronize(im.stream));
+    im.cnt.d2h += sizeof(ChainState) + nrec * sizeof(ChainRec);
+    res.U = im.h_state->U;
+    res.L = im.h_state->L;
+    res.done = im.h_state->done != 0;
+    // run_bz_loop: capped when the loop reaches level cap + 1 (<= k) without being done
+    res.capped = !res.done && level_cap && level_cap < k_ && g > level_cap;
+    for (size_t i = 0; i < nrec; ++i) {
+        const ChainRec& r = recs[i];
+        if (!r.ran) continue;
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, im.event(2 * i), im.event(2 * i + 1)));
+        res.rounds.push_back({r.c, r.j, r.w, r.U_after, r.bounded, r.L_after, r.level_end, r.key,
+                              r.evaluated, double(ms)});
+    }
+    return res;
 }
 
 Engine::Counters Engine::counters() const { return impl_->cnt; }

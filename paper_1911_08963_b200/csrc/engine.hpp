@@ -68,6 +68,24 @@ public:
     RoundResult round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t task_lo = 0,
                       uint64_t task_hi = UINT64_MAX, uint32_t cutoff = 0);
     RoundResult round_hist(uint32_t j, uint32_t c, uint64_t* hist);
+
+    // The whole level loop with rounds chained on the stream ("tab" kernel):
+    // a device-side state carries U / L / done, a finalize kernel per round
+    // applies run_bz_loop's updates, and the host only synchronizes after
+    // enough enqueued work (or at the end) to look at `done`. world > 1 adds an
+    // in-stream NCCL allreduce(min) of every round's key (nccl_init first).
+    struct ChainRound {
+        uint32_t c, j, w, U_after, bounded, L_after, level_end;
+        uint64_t key, evaluated;
+        double ms;
+    };
+    struct ChainResult {
+        uint32_t U = 0, L = 0;
+        bool done = false, capped = false;
+        std::vector<ChainRound> rounds; // executed rounds, in loop order
+    };
+    ChainResult chain_loop(uint32_t U0, uint32_t L0, uint32_t level_cap, bool exact,
+                           uint32_t k_last, uint32_t rank = 0, uint32_t world = 1);
     std::vector<uint32_t> witness(uint32_t j, uint32_t c, const RoundResult& rr);
 
     // NCCL (loaded at runtime) for the multi-GPU reduction
