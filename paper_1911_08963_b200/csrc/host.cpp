@@ -4,14 +4,103 @@
 // column_perm, per-round/per-level trace); tests/test_host.py pins it against
 // the golden vectors made from the compiled reference.
 #include <algorithm>
+#include <cstdlib>
+#include <atomic>
+#include <exception>
+#include <thread>
 #include <fstream>
 #include <limits>
 #include <random>
 #include <sstream>
 
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+
 #include "mdg.hpp"
 
 namespace mdg {
+
+namespace {
+// Small persistent host thread pool for independent candidate systematizations
+// (thread creation would cost as much as the work). MDG_HOST_THREADS caps it.
+class HostPool {
+public:
+    static HostPool& get() {
+        static HostPool pool;
+        return pool;
+    }
+    unsigned size() const { return unsigned(workers_.size()) + 1; }
+    // runs fn(i) for i in [0, n) on the pool and the calling thread; rethrows the first error
+    void run(uint32_t n, const std::function<void(uint32_t)>& fn) {
+        std::unique_lock<std::mutex> lk(m_);
+        job_ = &fn;
+        n_ = n;
+        next_.store(0);
+        pending_ = unsigned(workers_.size());
+        err_ = nullptr;
+        ++gen_;
+        cv_.notify_all();
+        lk.unlock();
+        drain();
+        lk.lock();
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+        job_ = nullptr;
+        if (err_) std::rethrow_exception(err_);
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+
+private:
+    HostPool() {
+        unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        if (const char* e = std::getenv("MDG_HOST_THREADS")) hw = unsigned(std::max(1, std::atoi(e)));
+        hw = std::min(hw, 16u);
+        for (unsigned i = 1; i < hw; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    void drain() {
+        for (uint32_t i; (i = next_.fetch_add(1)) < n_;) {
+            try {
+                (*job_)(i);
+            } catch (...) {
+                std::lock_guard<std::mutex> lk(m_);
+                if (!err_) err_ = std::current_exception();
+            }
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+            }
+            drain();
+            std::lock_guard<std::mutex> lk(m_);
+            if (--pending_ == 0) done_cv_.notify_all();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex m_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(uint32_t)>* job_ = nullptr;
+    uint32_t n_ = 0;
+    std::atomic<uint32_t> next_{0};
+    unsigned pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+    std::exception_ptr err_;
+};
+} // namespace
 
 // ------------------------------------------------------------- BitMatrix
 void BitMatrix::swap_rows(uint32_t a, uint32_t b) {
@@ -90,11 +179,15 @@ uint64_t hash_rows(const BitMatrix& m) {
 }
 
 // ---------------------------------------------------------------- Gammas
+// gamma.cpp:16-22 — output column j = input column perm[j]
 BitMatrix permute_columns(const BitMatrix& m, const std::vector<uint32_t>& perm) {
     BitMatrix out(m.rows(), m.cols());
-    for (uint32_t j = 0; j < m.cols(); ++j)
-        for (uint32_t r = 0; r < m.rows(); ++r)
-            if (m.get(r, perm[j])) out.set(r, j, true);
+    for (uint32_t r = 0; r < m.rows(); ++r) {
+        const uint64_t* src = m.row(r);
+        uint64_t* dst = out.row(r);
+        for (uint32_t j = 0; j < m.cols(); ++j)
+            dst[j >> 6] |= ((src[perm[j] >> 6] >> (perm[j] & 63)) & 1u) << (j & 63);
+    }
     return out;
 }
 
@@ -102,12 +195,9 @@ BitMatrix permute_columns(const BitMatrix& m, const std::vector<uint32_t>& perm)
 // the first workable column at or after the target and, in it, the first row
 // at or below the block rank; column swaps are mirrored into column_perm and
 // into every earlier snapshot.
-GammaSet compute_gamma_matrices(const BitMatrix& G) {
+static GammaSet gamma_blocks(const BitMatrix& G) {
     const uint32_t k = G.rows();
     const uint32_t n = G.cols();
-    if (k == 0 || k > n) throw std::invalid_argument("compute_gamma_matrices: need 1 <= k <= n");
-    if (rank_of(G) != k)
-        throw std::invalid_argument("compute_gamma_matrices: rank-deficient generator matrix");
     GammaSet gs;
     gs.column_perm.resize(n);
     for (uint32_t i = 0; i < n; ++i) gs.column_perm[i] = i;
@@ -145,27 +235,49 @@ GammaSet compute_gamma_matrices(const BitMatrix& G) {
     return gs;
 }
 
+GammaSet compute_gamma_matrices(const BitMatrix& G) {
+    const uint32_t k = G.rows();
+    const uint32_t n = G.cols();
+    if (k == 0 || k > n) throw std::invalid_argument("compute_gamma_matrices: need 1 <= k <= n");
+    if (rank_of(G) != k)
+        throw std::invalid_argument("compute_gamma_matrices: rank-deficient generator matrix");
+    return gamma_blocks(G);
+}
+
 // gamma.cpp:77-94 — identity plus `trials` Fisher–Yates shuffles
 // (util.hpp:28-33, j = next() % i), keeping the lexicographic max of
-// (m, k_last) with the earliest winner on ties.
+// (m, k_last) with the earliest winner on ties. The permutations are drawn in
+// the reference's order; the candidates (independent of each other; a column
+// permutation keeps the rank, so the reference's per-candidate rank check is
+// the identity's) are systematized on host threads, then chosen in order.
 GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint64_t seed) {
     if (trials < 1) throw std::invalid_argument("best_gamma_over_permutations: trials must be >= 1");
     GammaSet best = compute_gamma_matrices(G);
     SplitMix64 rng(seed);
     const uint32_t n = G.cols();
+    std::vector<std::vector<uint32_t>> perms(trials);
     for (uint32_t t = 0; t < trials; ++t) {
-        std::vector<uint32_t> perm(n);
+        std::vector<uint32_t>& perm = perms[t];
+        perm.resize(n);
         for (uint32_t i = 0; i < n; ++i) perm[i] = i;
         for (size_t i = perm.size(); i > 1; --i) {
             size_t j = static_cast<size_t>(rng.next() % i);
             std::swap(perm[i - 1], perm[j]);
         }
-        GammaSet cand = compute_gamma_matrices(permute_columns(G, perm));
-        for (uint32_t j = 0; j < cand.column_perm.size(); ++j)
-            cand.column_perm[j] = perm[cand.column_perm[j]];
-        if (cand.m() > best.m() || (cand.m() == best.m() && cand.k_last > best.k_last))
-            best = std::move(cand);
     }
+    std::vector<GammaSet> cands(trials);
+    std::function<void(uint32_t)> work = [&](uint32_t t) {
+        cands[t] = gamma_blocks(permute_columns(G, perms[t]));
+        for (uint32_t j = 0; j < cands[t].column_perm.size(); ++j)
+            cands[t].column_perm[j] = perms[t][cands[t].column_perm[j]];
+    };
+    if (uint64_t(G.rows()) * n >= 4096 && trials >= 2 && HostPool::get().size() > 1)
+        HostPool::get().run(trials, work);
+    else
+        for (uint32_t t = 0; t < trials; ++t) work(t);
+    for (uint32_t t = 0; t < trials; ++t)
+        if (cands[t].m() > best.m() || (cands[t].m() == best.m() && cands[t].k_last > best.k_last))
+            best = std::move(cands[t]);
     return best;
 }
 
