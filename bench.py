@@ -37,7 +37,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 N, K, SEEDS = 128, 64, list(range(1, 9))
-POPC_PER_S_MEASURED = 4642.3e9   # profiles/pipes_microbench.jsonl (B200, 148 SMs)
+POPC_PER_S_MEASURED = 4642.3e9   # profiles/r01_pipes_microbench.jsonl (B200, 148 SMs)
+# XU (POPC) operations the bound-pruned level-7 kernel executes per codeword, from the
+# committed ncu capture of that launch (profiles/r01b_tab_round_pruned_ncu.txt)
+XU_PER_CW_PRUNED = 1.202
 WORKLOAD = "cfg2: random [128,64] codes G=(I|A), mt19937_64 seeds 1..8, BZ to termination (exact d)"
 
 
@@ -299,15 +302,21 @@ def main():
         value = cw_total / (tot_ms * 1e-3)
         e2e_value = e2e_cw / (tot_e2e * 1e-3)
         sms = devs[0].info()["sm_count"]
-        nw = 2  # popcounts per codeword of the dominant kernel (64 non-identity columns)
+        nw = 2  # popcounts per codeword of the unpruned kernel (64 non-identity columns)
         achieved = c7_cw / (c7_ms * 1e-3) / world if c7_ms > 0 else 0.0
-        peak = POPC_PER_S_MEASURED * sms / 148 / nw
+        popc = POPC_PER_S_MEASURED * sms / 148
+        peak = popc / XU_PER_CW_PRUNED
         roofline = {
             "bound": "int_popc", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gcw/s",
-            "frac": achieved / peak, "traffic": None,
-            "kernel": "tab_round<2,false> on the level-7 rounds (621,216,192 codewords per launch)",
-            "op_mix_per_codeword": "2 LOP3 + 2 POPC + 1 IADD3 + 0.5 VIMNMX3 (identity columns elided)",
-            "peak_basis": "measured B200 POPC rate 16/clk/SM (tools/pipes_microbench.cu) / 2 POPC per codeword",
+            "frac": achieved / peak, "traffic": 4200960, "traffic_unit": "DRAM bytes per launch (ncu)",
+            "kernel": "tab_round<2,false>, bound-pruned (cutoff U), level-7 rounds (621,216,192 codewords per launch)",
+            "peak_basis": ("measured B200 POPC (XU pipe) rate 16/clk/SM = 4.64e12/s "
+                           "(tools/pipes_microbench.cu) / 1.202 XU ops per codeword executed by this "
+                           "kernel (ncu, profiles/r01b_tab_round_pruned_ncu.txt)"),
+            "op_mix_per_codeword": ("1 LOP3 + 1 POPC (first 32 compacted bits) + group min/vote; the "
+                                    "second word only for warp groups that can still beat U"),
+            "frac_vs_unpruned_popc_roofline": achieved / (popc / nw),
+            "traffic_note": "DRAM 4.2 MB per launch (suffix table + binomials), 0.1% of HBM peak: compute-bound",
         }
         if clocks.get("sm_mhz"):
             roofline["frac_at_measured_clock"] = achieved / (peak * clocks["sm_mhz"] / 1965.0)

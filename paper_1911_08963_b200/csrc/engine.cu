@@ -902,6 +902,47 @@ constexpr int kNcclMin = 3;    // ncclMin
 } // namespace
 
 // ------------------------------------------------------------ Engine impl
+// Bump allocator over large cudaMalloc'd chunks: Gamma rows and suffix tables
+// are carved from it and released all at once by reset() on the next load, so
+// the steady state makes no cudaMalloc / cudaFree calls (cudaFree synchronizes
+// the device and costs far more than a small round).
+class DevArena {
+public:
+    ~DevArena() {
+        for (auto& c : chunks_) cudaFree(c.base);
+    }
+    void* alloc(size_t bytes) {
+        bytes = (bytes + 255) & ~size_t(255);
+        for (; cur_ < chunks_.size(); ++cur_) {
+            Chunk& c = chunks_[cur_];
+            if (c.used + bytes <= c.size) {
+                void* p = static_cast<char*>(c.base) + c.used;
+                c.used += bytes;
+                return p;
+            }
+        }
+        Chunk c;
+        c.size = std::max<size_t>(bytes, size_t(64) << 20);
+        CK(cudaMalloc(&c.base, c.size));
+        c.used = bytes;
+        chunks_.push_back(c);
+        cur_ = chunks_.size() - 1;
+        return c.base;
+    }
+    void reset() {
+        for (auto& c : chunks_) c.used = 0;
+        cur_ = 0;
+    }
+
+private:
+    struct Chunk {
+        void* base = nullptr;
+        size_t size = 0, used = 0;
+    };
+    std::vector<Chunk> chunks_;
+    size_t cur_ = 0;
+};
+
 struct GammaDev {
     uint32_t* rows = nullptr;  // k x nw (compacted, zero-padded to the template width)
     uint32_t nw = 0;
@@ -934,6 +975,8 @@ struct Engine::Impl {
     ncclComm_t comm = nullptr;
     uint64_t* red_dev = nullptr;
     size_t red_cap = 0;
+    DevArena arena;                  // Gamma rows + suffix tables (reset per load)
+    DevArena plan_arena;             // plan prefix arrays (kept: plans are cached)
     ChainState* d_state = nullptr;
     ChainState* h_state = nullptr;   // pinned
     ChainRec* d_recs = nullptr;
@@ -977,7 +1020,7 @@ struct Engine::Impl {
         if (it != plans.end()) return it->second;
         PlanEntry pe;
         pe.plan = make_tab_plan(k, c, g.nw, uint32_t(resident(g.nw, g.hid, sms)));
-        CK(cudaMalloc(&pe.d_prefix, pe.plan.prefix.size() * 8));
+        pe.d_prefix = static_cast<uint64_t*>(plan_arena.alloc(pe.plan.prefix.size() * 8));
         CK(cudaMemcpyAsync(pe.d_prefix, pe.plan.prefix.data(), pe.plan.prefix.size() * 8,
                            cudaMemcpyHostToDevice, stream));
         CK(cudaStreamSynchronize(stream));
@@ -1012,9 +1055,6 @@ Engine::~Engine() {
     if (!impl_) return;
     cudaSetDevice(device_);
     if (impl_->stream) cudaStreamSynchronize(impl_->stream);
-    for (auto& g : impl_->gammas) cudaFree(g.rows);
-    for (auto& kv : impl_->ytabs) cudaFree(kv.second);
-    for (auto& kv : impl_->plans) cudaFree(kv.second.d_prefix);
     if (impl_->comm) {
         try { nccl().CommDestroy(impl_->comm); } catch (...) {}
     }
@@ -1076,12 +1116,11 @@ void Engine::load(uint32_t m, uint32_t k, uint32_t n, const uint64_t* rows, cons
         }
         next.push_back(gd);
     }
-    for (auto& g : impl_->gammas) cudaFree(g.rows);
-    for (auto& kv : impl_->ytabs) cudaFree(kv.second);
     impl_->gammas.clear();
     impl_->ytabs.clear();
+    impl_->arena.reset(); // the stream is idle (synchronized above)
     for (uint32_t j = 0; j < m; ++j) {
-        CK(cudaMalloc(&next[j].rows, host[j].size() * 4));
+        next[j].rows = static_cast<uint32_t*>(impl_->arena.alloc(host[j].size() * 4));
         CK(cudaMemcpyAsync(next[j].rows, host[j].data(), host[j].size() * 4, cudaMemcpyHostToDevice,
                            impl_->stream));
         impl_->cnt.h2d += host[j].size() * 4;
@@ -1107,8 +1146,7 @@ static uint32_t* ensure_ytab(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t 
     const GammaDev& g = im.gammas[j];
     uint32_t YS = uint32_t(stride_for(int(g.nw) + (g.hid ? 1 : 0)));
     uint64_t count = hb(k, s);
-    uint32_t* t = nullptr;
-    CK(cudaMalloc(&t, size_t(count) * YS * 4));
+    uint32_t* t = static_cast<uint32_t*>(im.arena.alloc(size_t(count) * YS * 4));
     dispatch_nw_hid<YtabLaunch>(g.nw, g.hid, g.rows, im.binom, k, s, g.id_rows, count, t, im.stream);
     CK(cudaGetLastError());
     im.cnt.launches += 1;

@@ -31,8 +31,14 @@ public:
         return pool;
     }
     unsigned size() const { return unsigned(workers_.size()) + 1; }
-    // runs fn(i) for i in [0, n) on the pool and the calling thread; rethrows the first error
+    // runs fn(i) for i in [0, n) on the pool and the calling thread; rethrows the first
+    // error. A caller that finds the pool busy (another thread's search) runs serially.
     void run(uint32_t n, const std::function<void(uint32_t)>& fn) {
+        std::unique_lock<std::mutex> busy(run_m_, std::try_to_lock);
+        if (!busy.owns_lock()) {
+            for (uint32_t i = 0; i < n; ++i) fn(i);
+            return;
+        }
         std::unique_lock<std::mutex> lk(m_);
         job_ = &fn;
         n_ = n;
@@ -90,6 +96,7 @@ private:
         }
     }
     std::vector<std::thread> workers_;
+    std::mutex run_m_;
     std::mutex m_;
     std::condition_variable cv_, done_cv_;
     const std::function<void(uint32_t)>* job_ = nullptr;

@@ -1,0 +1,127 @@
+"""Time-to-d / throughput report over all five BASELINE configs on one GPU, with the
+reference CPU engine (oracle/_ref) timed on the same host for comparison.
+
+Usage: python tools/configs_report.py [--cap4 7] [--no-cpu] [--out profiles/rNN_configs.json]
+Every GPU result is checked against tests/golden (d, the (L, U) trace, witness)."""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1911_08963_b200 as mdg  # noqa: E402
+
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+def gold(name):
+    with open(os.path.join(GOLD, name + ".json")) as f:
+        return json.load(f)["data"]
+
+
+def run_code(dev, n, k, seed, cap, exact, reps=3):
+    G = mdg.gen_matrix(n, k, seed, True)
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = mdg.min_weight(G, n, 10, seed, level_cap=cap, device=dev, exact_rounds=exact)
+        wall = time.perf_counter() - t0
+        if best is None or wall < best[1]:
+            best = (r, wall)
+    return best
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cap4", type=int, default=7)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    dev = mdg.Device(0)
+    out = {"device": "B200", "rows": []}
+    cfgs = {c["name"]: c for c in gold("configs")}
+    cap6 = {}
+    if os.path.exists(os.path.join(GOLD, "configs_cap4_6.json")):
+        cap6 = {c["name"]: c for c in gold("configs_cap4_6")}
+    for name in ["cfg1"] + [f"cfg2_s{s}" for s in range(1, 9)] + ["cfg3"]:
+        c = cfgs[name]
+        g = c["gen"]
+        for exact in (False, True):
+            r, wall = run_code(dev, g["n"], g["k"], g["seed"], 0, exact)
+            ok = r.d == c["d"] and r.levels == c["levels"] and r.witness_ok
+            out["rows"].append({
+                "config": name, "mode": "exact" if exact else "bounded", "d": r.d, "parity": ok,
+                "g_final": r.g_final, "codewords": r.evaluated,
+                "time_to_d_ms": wall * 1e3, "loop_ms": r.loop_seconds * 1e3,
+                "kernel_ms": r.device_seconds * 1e3, "gamma_ms": r.gamma_seconds * 1e3,
+                "cw_per_s_loop": r.evaluated / r.loop_seconds,
+                "cw_per_s_kernels": r.evaluated / max(r.device_seconds, 1e-12)})
+            print(json.dumps(out["rows"][-1]), flush=True)
+    c4 = cfgs["cfg4"]
+    for cap in sorted({5, 6, a.cap4}):
+        r, wall = run_code(dev, 300, 200, 11, cap, False, reps=1 if cap >= 7 else 2)
+        ref = c4 if cap == 5 else cap6.get("cfg4") if cap == 6 else None
+        ok = None if ref is None else (r.d == ref["U_final"] and r.levels == ref["levels"])
+        out["rows"].append({
+            "config": f"cfg4_cap{cap}", "mode": "bounded", "U_at_cap": r.d, "capped": r.capped,
+            "parity": ok, "codewords": r.evaluated, "time_to_cap_ms": wall * 1e3,
+            "loop_ms": r.loop_seconds * 1e3, "kernel_ms": r.device_seconds * 1e3,
+            "cw_per_s_loop": r.evaluated / r.loop_seconds,
+            "cw_per_s_kernels": r.evaluated / max(r.device_seconds, 1e-12)})
+        print(json.dumps(out["rows"][-1]), flush=True)
+    h = gold("cfg5_hist")
+    M = mdg.gen_matrix(256, 100, 3, identity=False)
+    dev.load_gammas(M, 256, ranks=None)
+    tot_cw, tot_ms = 0, 0.0
+    for lv in h["levels"]:
+        o, hist = dev.round_hist(0, lv["c"], 256)
+        o, hist = dev.round_hist(0, lv["c"], 256)
+        ok = hist.tolist() == lv["hist"] and o.min_weight == lv["min"]
+        tot_cw += o.evaluated
+        tot_ms += o.device_ms
+        out["rows"].append({"config": f"cfg5_c{lv['c']}", "mode": "histogram", "min": o.min_weight,
+                            "parity": ok, "codewords": o.evaluated, "kernel_ms": o.device_ms,
+                            "cw_per_s_kernels": o.evaluated / (o.device_ms * 1e-3)})
+        print(json.dumps(out["rows"][-1]), flush=True)
+    out["rows"].append({"config": "cfg5_total", "codewords": tot_cw, "kernel_ms": tot_ms,
+                        "cw_per_s_kernels": tot_cw / (tot_ms * 1e-3)})
+    if not a.no_cpu:
+        from oracle import ref
+        if ref.available():
+            cpu = []
+            for name, engine, cap in [("cfg1", "saved", 0), ("cfg2_s1", "saved", 0), ("cfg3", "saved", 0),
+                                      ("cfg4", "scheduled", 5)]:
+                g = cfgs[name]["gen"]
+                text = ref.gen(g["n"], g["k"], g["seed"])
+                for flavor in ("v3", "stock"):
+                    t0 = time.perf_counter()
+                    tr = ref.trace(text, 10, g["seed"], engine, 5, os.cpu_count(), cap, flavor=flavor)
+                    dt = time.perf_counter() - t0
+                    cpu.append({"config": name, "engine": engine, "flavor": flavor,
+                                "threads": os.cpu_count(), "seconds": dt,
+                                "codewords": tr["combinations"], "cw_per_s": tr["combinations"] / dt})
+                    print(json.dumps(cpu[-1]), flush=True)
+            exe = os.path.join(ROOT, "oracle", "_ref", "mdref_v3")
+            with open("/tmp/_cfg5.txt", "w") as f:
+                f.write(ref.gen(256, 100, 3, identity=False))
+            t0 = time.perf_counter()
+            subprocess.run([exe, "hist", "/tmp/_cfg5.txt", "--cmax", "5"], check=True, capture_output=True)
+            dt = time.perf_counter() - t0
+            cpu.append({"config": "cfg5", "engine": "lex + combine_rows + weight (+ round_stack check)",
+                        "flavor": "v3", "threads": 1, "seconds": dt, "codewords": tot_cw,
+                        "cw_per_s": 2 * tot_cw / dt})
+            print(json.dumps(cpu[-1]), flush=True)
+            out["cpu_reference"] = cpu
+    out["cpu"] = subprocess.run(["bash", "-c", "lscpu | grep 'Model name'; nproc"], capture_output=True,
+                                text=True).stdout
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(out, f, indent=1)
+    dev.close()
+
+
+if __name__ == "__main__":
+    main()
