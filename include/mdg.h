@@ -182,6 +182,14 @@ int mdg_timer_stop(mdg_ctx* ctx, double* ms);
 int mdg_ctx_counters(mdg_ctx* ctx, uint64_t* launches, uint64_t* h2d_bytes, uint64_t* d2h_bytes);
 int mdg_device_info(mdg_ctx* ctx, int* sm_count, int* device);
 
+/* Brute force over all 2^k - 1 nonzero codewords of row_basis(G) (the
+ * reference's Algorithm::brute_gray, engines.cpp:480-558; min_weight's brute
+ * branch, engines.cpp:623-628): rejects k > brute_cap (BruteCapError,
+ * MDG_EINVAL; brute_cap in 1..63, EngineConfig::validate engines.cpp:90-91).
+ * Result: d and a witness; m = k_last = 0 and no trace, as the reference. */
+int mdg_brute_force(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n, uint32_t brute_cap,
+                    mdg_run** out);
+
 /* Multi-GPU (one process per GPU): every rank runs the same
  * host loop; each round's task range is split contiguously across ranks and
  * the per-round minimum key is combined with reduce_min (an NCCL

@@ -24,7 +24,7 @@ import numpy as np
 __all__ = [
     "MdgError", "InvalidArgument", "OverflowError_", "CudaFailure", "lib", "Device", "GammaSet",
     "RoundOut", "RunResult", "min_weight", "min_weight_dist", "run_bz_loop", "lower_bound",
-    "singleton_upper", "parse_matrix", "serialize_matrix", "gen_matrix", "binomial",
+    "singleton_upper", "brute_force", "parse_matrix", "serialize_matrix", "gen_matrix", "binomial",
     "rd_unrank", "rd_rank", "hash_rows", "rank_of", "words", "KERNEL_TAB", "KERNEL_RD",
 ]
 
@@ -140,6 +140,8 @@ SYMBOLS = {
     "mdg_timer_stop": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "mdg_ctx_counters": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_uint64)] * 3),
     "mdg_device_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "mdg_brute_force": (C.c_int, [C.c_void_p, u64p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                  C.POINTER(C.c_void_p)]),
     "mdg_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "mdg_nccl_init": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint32, C.c_uint32]),
     "mdg_nccl_reduce_min": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_uint32]),
@@ -578,6 +580,17 @@ def min_weight_dist(G: np.ndarray, n: int, rank: int, world: int,
     _check(lib().mdg_min_weight_dist(device.handle if device else None, G, G.shape[0], n,
                                      C.byref(cfg), rank, world, fn, user, C.byref(h)))
     del keep
+    return _collect(h)
+
+
+def brute_force(G: np.ndarray, n: int, brute_cap: int = 40,
+                device: Optional[Device] = None) -> RunResult:
+    """min_weight with Algorithm::brute_gray (engines.cpp:480-558, 623-628): all 2^k - 1
+    nonzero codewords of row_basis(G) on the GPU; d + witness, no trace (m = k_last = 0)."""
+    G = _rows(G)
+    h = C.c_void_p()
+    _check(lib().mdg_brute_force(device.handle if device else None, G, G.shape[0], n, brute_cap,
+                                 C.byref(h)))
     return _collect(h)
 
 

@@ -647,6 +647,60 @@ int mdg_device_info(mdg_ctx* ctx, int* sms, int* device) {
     });
 }
 
+int mdg_brute_force(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n, uint32_t brute_cap,
+                    mdg_run** out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null out");
+        if (brute_cap < 1 || brute_cap > 63)
+            throw std::invalid_argument("config: brute_cap must be in 1..63");
+        auto t0 = std::chrono::steady_clock::now();
+        std::unique_ptr<mdg_ctx> own;
+        if (!ctx) {
+            own = std::make_unique<mdg_ctx>();
+            own->eng = std::make_unique<Engine>(0);
+            ctx = own.get();
+        }
+        BitMatrix B = row_basis(from_rows(G, k, n));
+        if (B.rows() > brute_cap)
+            throw std::invalid_argument("brute force: k = " + std::to_string(B.rows()) + " exceeds cap " +
+                                        std::to_string(brute_cap) + "; use a Brouwer-Zimmermann engine");
+        Engine& eng = *ctx->eng;
+        Engine::Counters c0 = eng.counters();
+        Engine::BruteResult br = eng.brute_force(B.rows(), n, B.data());
+        auto run = std::make_unique<mdg_run>();
+        run->algorithm = "brute";
+        run->kernel = "span";
+        run->er.d = br.d;
+        const uint64_t total = (uint64_t{1} << B.rows()) - 1;
+        run->er.stats.combinations = total;
+        run->er.stats.row_additions = total; // serial Gray walk: one XOR per codeword
+        run->er.stats.evaluated = br.evaluated;
+        run->er.stats.device_ms = br.ms;
+        run->n = n;
+        run->k = B.rows();
+        run->m = 0;
+        run->k_last = 0;
+        std::vector<uint64_t> w(B.words(), 0);
+        for (uint32_t r : br.idx)
+            for (uint32_t i = 0; i < B.words(); ++i) w[i] ^= B.row(r)[i];
+        BitMatrix S(B.rows() + 1, n);
+        std::memcpy(S.data(), B.data(), size_t(B.rows()) * B.words() * 8);
+        std::memcpy(S.row(B.rows()), w.data(), B.words() * 8);
+        run->witness = w;
+        run->witness_idx = br.idx;
+        run->witness_ok = weight_of(w) == br.d && !br.idx.empty() && rank_of(S) == B.rows();
+        run->perm.resize(n);
+        for (uint32_t i = 0; i < n; ++i) run->perm[i] = i;
+        Engine::Counters c1 = eng.counters();
+        run->cnt.launches = c1.launches - c0.launches;
+        run->cnt.h2d = c1.h2d - c0.h2d;
+        run->cnt.d2h = c1.d2h - c0.d2h;
+        run->loop_s = br.ms * 1e-3;
+        run->wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *out = run.release();
+    });
+}
+
 int mdg_nccl_unique_id(uint8_t id[128]) {
     return guard([&] { Engine::nccl_unique_id(id); });
 }

@@ -201,8 +201,19 @@ struct ChainState {
 };
 struct ChainRec {
     uint32_t c, j, w, U_after, bounded, ran, L_after, level_end;
-    unsigned long long key, evaluated;
+    unsigned long long key, evaluated, t_ns; // t_ns: %globaltimer when the round closed
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// chain start time stamp (device clock), read back with the records
+__global__ void chain_stamp(unsigned long long* t) {
+    if (threadIdx.x == 0) *t = globaltimer_ns();
+}
 
 struct TabArgs {
     const ChainState* st;          // non-null: cutoff / stop_at / skip from the chain state
@@ -292,14 +303,74 @@ __device__ __forceinline__ void load_suffixes(const TabArgs& a, const TileInfo& 
     }
 }
 
+// Minimum of (compacted weight + identity count) over prefixes xs[x_begin, nx) x the
+// lane's R suffixes, considering only values <= T (T < 0: none; the caller maps
+// a cutoff / running best to T). Values above T may be reported as "none"
+// (0xFFFFFFFF) or exactly — never as anything smaller than the truth.
+template <int NW, bool HID>
+__device__ __forceinline__ uint32_t tile_min(const uint32_t* xs, uint32_t x_begin, uint32_t nx,
+                                             const uint32_t (&Y)[r_for(NW)][NW],
+                                             const uint32_t (&idY)[r_for(NW)], int32_t T) {
+    constexpr int R = r_for(NW);
+    constexpr int XS = stride_for(NW + (HID ? 1 : 0));
+    constexpr int P = prune_words(NW);
+    // prune only when the bound sits well below the mean partial weight (16 per word)
+    constexpr int kPruneLimit = 16 * P - 2;
+    uint32_t best = 0xFFFFFFFFu;
+    if (T < 0) {
+        // every codeword here is above the bound
+    } else if (T < kPruneLimit) {
+        // bound-pruned walk: a partial weight over the first P words is a lower
+        // bound; the rest is computed only when some lane can still go <= T.
+        // Stage 1 for all R suffixes, then stage 2 per group of G suffixes only
+        // when some lane of the warp has a partial weight <= T there (a real,
+        // warp-uniform branch: a per-codeword vote gets if-converted and the
+        // predicated POPCs still occupy the XU pipe).
+        constexpr int G = R >= 4 ? 4 : R;
+        for (uint32_t xi = x_begin; xi < nx; ++xi) {
+            uint32_t X[XS];
+            vload<XS>(xs + xi * XS, X);
+            uint32_t part[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                part[r] = xor_weight<0, P, XS, NW>(X, Y[r]);
+                if (HID) part[r] += X[NW] + idY[r];
+            }
+#pragma unroll
+            for (int g0 = 0; g0 < R; g0 += G) {
+                uint32_t gmin = part[g0];
+#pragma unroll
+                for (int r = 1; r < G; ++r) gmin = min(gmin, part[g0 + r]);
+                if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= T)) {
+#pragma unroll
+                    for (int r = 0; r < G; ++r) {
+                        const uint32_t w = part[g0 + r] + xor_weight<P, NW, XS, NW>(X, Y[g0 + r]);
+                        best = min(best, w);
+                    }
+                    T = min(T, int32_t(best));
+                }
+            }
+        }
+    } else {
+        for (uint32_t xi = x_begin; xi < nx; ++xi) {
+            uint32_t X[XS];
+            vload<XS>(xs + xi * XS, X);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                uint32_t w = xor_weight<0, NW, XS, NW>(X, Y[r]);
+                if (HID) w += X[NW] + idY[r];
+                best = min(best, w);
+            }
+        }
+    }
+    return best;
+}
+
 template <int NW, bool HID>
 __global__ void __launch_bounds__(kThreads) tab_round(TabArgs a) {
     constexpr int R = r_for(NW);
     constexpr int YC = R * kThreads;
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
-    constexpr int P = prune_words(NW);
-    // prune only when the bound sits well below the mean partial weight (16 per word)
-    constexpr int kPruneLimit = 16 * P - 2;
     __shared__ __align__(16) uint32_t xs[kTX * XS];
     __shared__ TileInfo ti;
     const uint32_t lane = threadIdx.x & 31;
@@ -343,55 +414,7 @@ __global__ void __launch_bounds__(kThreads) tab_round(TabArgs a) {
         load_suffixes<NW, HID>(a, ti, Y, idY, valid);
         __syncthreads();
 
-        uint32_t best = 0xFFFFFFFFu;
-        const uint32_t nx = ti.nx;
-        int32_t T = ti.T;
-        if (T < 0) {
-            // every codeword of this round is >= cutoff: nothing below the bound
-        } else if (T < kPruneLimit) {
-            // bound-pruned walk: a partial weight over the first P words is a lower
-            // bound; the rest is computed only when some lane can still go <= T.
-            // Stage 1 for all R suffixes, then stage 2 per group of G suffixes only
-            // when some lane of the warp has a partial weight <= T there (a real,
-            // warp-uniform branch: a per-codeword vote gets if-converted and the
-            // predicated POPCs still occupy the XU pipe).
-            constexpr int G = R >= 4 ? 4 : R;
-            for (uint32_t xi = 0; xi < nx; ++xi) {
-                uint32_t X[XS];
-                vload<XS>(xs + xi * XS, X);
-                uint32_t part[R];
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    part[r] = xor_weight<0, P, XS, NW>(X, Y[r]);
-                    if (HID) part[r] += X[NW] + idY[r];
-                }
-#pragma unroll
-                for (int g0 = 0; g0 < R; g0 += G) {
-                    uint32_t gmin = part[g0];
-#pragma unroll
-                    for (int r = 1; r < G; ++r) gmin = min(gmin, part[g0 + r]);
-                    if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= T)) {
-#pragma unroll
-                        for (int r = 0; r < G; ++r) {
-                            const uint32_t w = part[g0 + r] + xor_weight<P, NW, XS, NW>(X, Y[g0 + r]);
-                            best = min(best, w);
-                        }
-                        T = min(T, int32_t(best));
-                    }
-                }
-            }
-        } else {
-            for (uint32_t xi = 0; xi < nx; ++xi) {
-                uint32_t X[XS];
-                vload<XS>(xs + xi * XS, X);
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    uint32_t w = xor_weight<0, NW, XS, NW>(X, Y[r]);
-                    if (HID) w += X[NW] + idY[r];
-                    best = min(best, w);
-                }
-            }
-        }
+        uint32_t best = tile_min<NW, HID>(xs, 0, ti.nx, Y, idY, ti.T);
         if (best != 0xFFFFFFFFu) best += a.add_const;
         best = __reduce_min_sync(0xFFFFFFFFu, best);
         if (lane == 0 && best != 0xFFFFFFFFu && (cutoff == 0 || best < cutoff)) {
@@ -413,6 +436,7 @@ __global__ void chain_finalize(ChainState* st, const unsigned long long* slot, C
     ChainRec r{};
     r.c = c;
     r.j = j;
+    r.t_ns = globaltimer_ns();
     if (st->done || st->U <= st->L) { // fast path: the round is not run, the loop ends
         st->done = 1;
         r.ran = 0;
@@ -660,6 +684,175 @@ __global__ void __launch_bounds__(kRdThreads) rd_round(RdArgs a) {
     }
     if (!FIND && done_local) atomicAdd(a.evaluated, done_local);
 }
+
+
+// ------------------------------------------------------------ brute force
+// All 2^k - 1 nonzero codewords of a k-row basis (the reference's
+// brute_force_gray, engines.cpp:480-558, restated as a product of two spans):
+// rows split into A = [0, a) and B = [a, k); TA[i] = XOR of the A rows at the
+// set bits of gray(i) (2^a entries, binary reflected Gray order,
+// enumeration.hpp:19), TB likewise over B; codeword (x, y) = TA[x] ^ TB[y],
+// the pair (0, 0) excluded. Tiles are TX x-entries (smem) x YC y-entries
+// (registers), bound-pruned by the running minimum.
+template <int NW>
+__global__ void span_build(const uint32_t* __restrict__ rows, uint32_t first, uint64_t count,
+                           uint32_t* __restrict__ out) {
+    constexpr int S = stride_for(NW);
+    uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    uint64_t g = i ^ (i >> 1);
+    uint32_t acc[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) acc[w] = 0;
+    while (g) {
+        uint32_t b = uint32_t(__ffsll(static_cast<long long>(g)) - 1);
+        g &= g - 1;
+        xor_row<NW>(rows, first + b, acc);
+    }
+#pragma unroll
+    for (int w = 0; w < S; ++w) out[i * S + w] = w < NW ? acc[w] : 0u;
+}
+
+struct SpanArgs {
+    const uint32_t* ta;
+    const uint32_t* tb;
+    uint64_t na, nb, nty;
+    uint32_t tx;
+    uint64_t tile_lo, tile_hi;
+    unsigned long long* best_key;
+    unsigned long long* evaluated;
+    unsigned long long* counter;
+    unsigned long long* find_out;
+    uint32_t find_target;
+};
+
+template <int NW, bool FIND>
+__global__ void __launch_bounds__(kThreads) span_round(SpanArgs a) {
+    constexpr int R = r_for(NW);
+    constexpr int YC = R * kThreads;
+    constexpr int S = stride_for(NW);
+    __shared__ __align__(16) uint32_t xs[kTX * S];
+    __shared__ uint64_t s_x0, s_y0, s_tile;
+    __shared__ uint32_t s_nx, s_nyv, s_stop;
+    __shared__ int32_t s_T;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long seen = ~0ull, done_local = 0;
+    for (uint32_t it = 0;; ++it) {
+        if (threadIdx.x == 0) {
+            uint64_t t;
+            if (FIND) {
+                t = a.tile_lo;
+                s_stop = it > 0;
+            } else {
+                t = a.tile_lo + atomicAdd(a.counter, 1ull);
+                s_stop = t >= a.tile_hi;
+            }
+            if (!s_stop) {
+                uint64_t xt = t / a.nty, yt = t - xt * a.nty;
+                s_tile = t;
+                s_x0 = xt * a.tx;
+                s_nx = uint32_t(umin64(a.tx, a.na - s_x0));
+                s_y0 = yt * YC;
+                s_nyv = uint32_t(umin64(uint64_t(YC), a.nb - s_y0));
+                unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
+                uint32_t gw = uint32_t(g >> kKeyShift);
+                s_T = gw >= 0x7FFFFFFFu ? 0x7FFFFFFF : int32_t(gw);
+                done_local += uint64_t(s_nx) * s_nyv;
+            }
+        }
+        __syncthreads();
+        if (s_stop) break;
+        const uint32_t nx = s_nx, nyv = s_nyv;
+        const uint64_t x0 = s_x0, y0 = s_y0;
+        if (threadIdx.x < nx) {
+            uint32_t v[S];
+            vload_global<S>(a.ta + (x0 + threadIdx.x) * S, v);
+#pragma unroll
+            for (int w = 0; w < S; ++w) xs[threadIdx.x * S + w] = v[w];
+        }
+        uint32_t Y[R][NW], idY[R];
+        bool valid[R];
+        uint64_t yi[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            uint32_t yl = r * kThreads + warp * 32 + lane;
+            valid[r] = yl < nyv;
+            yi[r] = y0 + (valid[r] ? yl : 0u);
+            uint32_t v[S];
+            vload_global<S>(a.tb + yi[r] * S, v);
+#pragma unroll
+            for (int w = 0; w < NW; ++w) Y[r][w] = v[w];
+            idY[r] = 0;
+        }
+        __syncthreads();
+        if (FIND) {
+            unsigned long long cand = ~0ull;
+            for (uint32_t xi = 0; xi < nx; ++xi) {
+                uint32_t X[S];
+                vload<S>(xs + xi * S, X);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    uint32_t w = xor_weight<0, NW, S, NW>(X, Y[r]);
+                    bool zero_pair = x0 + xi == 0 && yi[r] == 0;
+                    if (valid[r] && !zero_pair && w == a.find_target) {
+                        unsigned long long c = (static_cast<unsigned long long>(xi) << 32) |
+                                               (r * kThreads + warp * 32 + lane);
+                        cand = c < cand ? c : cand;
+                    }
+                }
+            }
+            if (cand != ~0ull) atomicMin(a.find_out, cand);
+        } else {
+            uint32_t best = 0xFFFFFFFFu;
+            uint32_t xb = 0;
+            if (x0 == 0) { // row x = 0 is the zero vector: codewords from B alone, minus (0,0)
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    uint32_t w = 0;
+#pragma unroll
+                    for (int i = 0; i < NW; ++i) w += __popc(Y[r][i]);
+                    if (yi[r] != 0) best = min(best, w);
+                }
+                xb = 1;
+            }
+            // the bound must be warp-uniform: tile_min branches on it around warp votes
+            const uint32_t wbest = __reduce_min_sync(0xFFFFFFFFu, best);
+            const int32_t T = wbest == 0xFFFFFFFFu ? s_T : min(s_T, int32_t(wbest));
+            best = min(best, tile_min<NW, false>(xs, xb, nx, Y, idY, T));
+            best = __reduce_min_sync(0xFFFFFFFFu, best);
+            if (lane == 0 && best != 0xFFFFFFFFu) {
+                unsigned long long key = (static_cast<unsigned long long>(best) << kKeyShift) | s_tile;
+                if (key < seen) {
+                    unsigned long long old = atomicMin(a.best_key, key);
+                    seen = old < key ? old : key;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (!FIND && threadIdx.x == 0 && done_local) atomicAdd(a.evaluated, done_local);
+}
+
+template <int NW, bool HID>
+struct SpanLaunch { // HID unused: dispatch shape only
+    static void run(const uint32_t* rows, uint32_t a_rows, uint32_t b_rows, uint32_t* ta, uint32_t* tb,
+                    SpanArgs sa, int mode, cudaStream_t st, int sms) {
+        if (mode == 0) {
+            uint64_t na = uint64_t(1) << a_rows, nb = uint64_t(1) << b_rows;
+            span_build<NW><<<uint32_t((na + 255) / 256), 256, 0, st>>>(rows, 0, na, ta);
+            span_build<NW><<<uint32_t((nb + 255) / 256), 256, 0, st>>>(rows, a_rows, nb, tb);
+        } else if (mode == 1) {
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, span_round<NW, false>, kThreads, 0);
+            if (occ < 1) occ = 1;
+            uint64_t tiles = sa.tile_hi - sa.tile_lo;
+            uint64_t g = std::max<uint64_t>(1, std::min<uint64_t>(tiles, uint64_t(sms) * occ));
+            span_round<NW, false><<<uint32_t(g), kThreads, 0, st>>>(sa);
+        } else {
+            span_round<NW, true><<<1, kThreads, 0, st>>>(sa);
+        }
+    }
+};
 
 // ------------------------------------------------------------ dispatch
 template <template <int, bool> class F, typename... Args>
@@ -1361,6 +1554,10 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
     ChainResult res;
     size_t nrec = 0;
     double pending = 0;
+    unsigned long long* t0_slot = im.take_slot();
+    chain_stamp<<<1, 32, 0, im.stream>>>(t0_slot);
+    CK(cudaGetLastError());
+    im.cnt.launches += 1;
     uint32_t g = 1;
     bool done = init.done != 0;
     while (!done && g <= k_) {
@@ -1387,13 +1584,11 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
             a.tile_lo = world > 1 ? T * rank / world : 0;
             a.tile_hi = world > 1 ? T * (rank + 1) / world : T;
             a.best_key = slot; a.evaluated = slot + 1; a.counter = slot + 2;
-            CK(cudaEventRecord(im.event(2 * nrec), im.stream));
             if (a.tile_hi > a.tile_lo) {
                 dispatch_nw_hid<TabLaunch>(gd.nw, gd.hid, a, a.tile_hi - a.tile_lo, im.stream, 0, size_t(0), sms_);
                 CK(cudaGetLastError());
                 im.cnt.launches += 1;
             }
-            CK(cudaEventRecord(im.event(2 * nrec + 1), im.stream));
             if (world > 1) {
                 int rc = nccl().AllReduce(slot, slot, 1, kNcclUint64, kNcclMin, im.comm, im.stream);
                 if (rc != 0) throw std::runtime_error(std::string("ncclAllReduce: ") + nccl().GetErrorString(rc));
@@ -1418,22 +1613,91 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
     std::vector<ChainRec> recs(nrec);
     if (nrec)
         CK(cudaMemcpyAsync(recs.data(), im.d_recs, nrec * sizeof(ChainRec), cudaMemcpyDeviceToHost, im.stream));
+    unsigned long long t_start = 0;
+    CK(cudaMemcpyAsync(im.host_slot, t0_slot, 8, cudaMemcpyDeviceToHost, im.stream));
     CK(cudaStreamSynchronize(im.stream));
+    t_start = im.host_slot[0];
     im.cnt.d2h += sizeof(ChainState) + nrec * sizeof(ChainRec);
     res.U = im.h_state->U;
     res.L = im.h_state->L;
     res.done = im.h_state->done != 0;
     // run_bz_loop: capped when the loop reaches level cap + 1 (<= k) without being done
     res.capped = !res.done && level_cap && level_cap < k_ && g > level_cap;
+    // per-round device time: between consecutive round closes (device clock;
+    // includes the finalize launch, ~2 us)
+    unsigned long long prev = t_start;
     for (size_t i = 0; i < nrec; ++i) {
         const ChainRec& r = recs[i];
+        const double ms = r.t_ns > prev ? double(r.t_ns - prev) * 1e-6 : 0.0;
+        prev = r.t_ns;
         if (!r.ran) continue;
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, im.event(2 * i), im.event(2 * i + 1)));
         res.rounds.push_back({r.c, r.j, r.w, r.U_after, r.bounded, r.L_after, r.level_end, r.key,
-                              r.evaluated, double(ms)});
+                              r.evaluated, ms});
     }
     return res;
+}
+
+Engine::BruteResult Engine::brute_force(uint32_t k, uint32_t n, const uint64_t* rows) {
+    if (k < 1 || k > 62) throw std::invalid_argument("brute force: need 1 <= k <= 62");
+    load(1, k, n, rows, nullptr); // raw basis rows, no identity elision
+    CK(cudaSetDevice(device_));
+    Impl& im = *impl_;
+    const GammaDev& g = im.gammas[0];
+    const uint32_t a_rows = k / 2, b_rows = k - a_rows;
+    const uint64_t na = uint64_t(1) << a_rows, nb = uint64_t(1) << b_rows;
+    const uint32_t S = uint32_t(stride_for(int(g.nw)));
+    uint32_t* ta = static_cast<uint32_t*>(im.arena.alloc(size_t(na) * S * 4));
+    uint32_t* tb = static_cast<uint32_t*>(im.arena.alloc(size_t(nb) * S * 4));
+    SpanArgs sa{};
+    dispatch_nw_hid<SpanLaunch>(g.nw, false, g.rows, a_rows, b_rows, ta, tb, sa, 0, im.stream, sms_);
+    CK(cudaGetLastError());
+    im.cnt.launches += 2;
+    const uint32_t YC = tab_yc(g.nw);
+    const uint64_t nty = ceil_div(nb, YC);
+    uint32_t tx = kTX;
+    int resident = im.resident(g.nw, false, sms_);
+    while (tx > 32 && ceil_div(na, tx) * nty < uint64_t(resident) * 6) tx /= 2;
+    const uint64_t tiles = ceil_div(na, tx) * nty;
+    unsigned long long* slot = im.take_slot();
+    sa.ta = ta; sa.tb = tb; sa.na = na; sa.nb = nb; sa.nty = nty; sa.tx = tx;
+    sa.tile_lo = 0; sa.tile_hi = tiles;
+    sa.best_key = slot; sa.evaluated = slot + 1; sa.counter = slot + 2; sa.find_out = slot + 3;
+    CK(cudaEventRecord(im.ev0, im.stream));
+    dispatch_nw_hid<SpanLaunch>(g.nw, false, g.rows, a_rows, b_rows, ta, tb, sa, 1, im.stream, sms_);
+    CK(cudaGetLastError());
+    im.cnt.launches += 1;
+    CK(cudaEventRecord(im.ev1, im.stream));
+    im.read_slot(slot);
+    CK(cudaStreamSynchronize(im.stream));
+    BruteResult br;
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, im.ev0, im.ev1));
+    br.ms = ms;
+    br.evaluated = im.host_slot[1] - 1; // tiles count the excluded zero pair (0, 0)
+    const uint64_t key = im.host_slot[0];
+    if (key == ~0ull) throw std::logic_error("brute force: no nonzero codeword evaluated");
+    br.d = uint32_t(key >> kKeyShift);
+    // witness: smallest (x, y) of the winning tile with that weight
+    unsigned long long* fslot = im.take_slot();
+    sa.tile_lo = key & ((uint64_t{1} << kKeyShift) - 1);
+    sa.tile_hi = sa.tile_lo + 1;
+    sa.find_out = fslot + 3;
+    sa.find_target = br.d;
+    dispatch_nw_hid<SpanLaunch>(g.nw, false, g.rows, a_rows, b_rows, ta, tb, sa, 2, im.stream, sms_);
+    CK(cudaGetLastError());
+    im.cnt.launches += 1;
+    im.read_slot(fslot);
+    CK(cudaStreamSynchronize(im.stream));
+    const uint64_t f = im.host_slot[3];
+    if (f == ~0ull) throw std::logic_error("brute force: winning tile holds no codeword of weight d");
+    const uint64_t xt = sa.tile_lo / nty, yt = sa.tile_lo % nty;
+    const uint64_t x = xt * tx + (f >> 32), y = yt * YC + (f & 0xFFFFFFFFu);
+    const uint64_t gx = x ^ (x >> 1), gy = y ^ (y >> 1);
+    for (uint32_t b = 0; b < a_rows; ++b)
+        if ((gx >> b) & 1u) br.idx.push_back(b);
+    for (uint32_t b = 0; b < b_rows; ++b)
+        if ((gy >> b) & 1u) br.idx.push_back(a_rows + b);
+    return br;
 }
 
 Engine::Counters Engine::counters() const { return impl_->cnt; }

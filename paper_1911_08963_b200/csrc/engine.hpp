@@ -84,6 +84,16 @@ public:
         bool done = false, capped = false;
         std::vector<ChainRound> rounds; // executed rounds, in loop order
     };
+    // Gray-code brute force over all 2^k - 1 nonzero codewords of a k-row basis
+    // (brute_force_gray, engines.cpp:480-558): d and the rows of one weight-d codeword.
+    struct BruteResult {
+        uint32_t d = 0;
+        uint64_t evaluated = 0;
+        double ms = 0;
+        std::vector<uint32_t> idx;
+    };
+    BruteResult brute_force(uint32_t k, uint32_t n, const uint64_t* rows);
+
     ChainResult chain_loop(uint32_t U0, uint32_t L0, uint32_t level_cap, bool exact,
                            uint32_t k_last, uint32_t rank = 0, uint32_t world = 1);
     std::vector<uint32_t> witness(uint32_t j, uint32_t c, const RoundResult& rr);

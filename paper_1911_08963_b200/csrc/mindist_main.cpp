@@ -18,7 +18,7 @@ namespace {
 
 int usage() {
     std::cerr << "usage:\n"
-                 "  mindist mindist FILE [--algorithm gpu] [--kernel tab|rd] [--trials T]\n"
+                 "  mindist mindist FILE [--algorithm gpu|brute] [--kernel tab|rd] [--trials T]\n"
                  "                       [--seed S] [--level-cap C] [--device D] [--exact-rounds]\n"
                  "                       [--pretty]\n"
                  "  mindist gen --n N --k K --seed S [--plain]\n";
@@ -73,6 +73,7 @@ int main(int argc, char** argv) {
     bool pretty = false;
     int device = 0;
     bool seed_given = false;
+    bool brute = false;
     for (int i = 3; i < argc; ++i) {
         std::string a = argv[i];
         if (a == "--pretty") { pretty = true; continue; }
@@ -81,8 +82,10 @@ int main(int argc, char** argv) {
         std::string v = argv[++i];
         uint64_t x = 0;
         if (a == "--algorithm") {
-            if (v != "gpu") {
-                std::cerr << "error: unknown algorithm: " << v << " (this build provides 'gpu')\n";
+            if (v == "brute") {
+                brute = true;
+            } else if (v != "gpu") {
+                std::cerr << "error: unknown algorithm: " << v << " (this build provides gpu, brute)\n";
                 return 2;
             }
         } else if (a == "--kernel") {
@@ -118,7 +121,8 @@ int main(int argc, char** argv) {
     int rc = mdg_open(device, &ctx);
     if (rc) return exit_code(rc);
     mdg_run* run = nullptr;
-    rc = mdg_min_weight(ctx, G.data(), G.rows(), G.cols(), &cfg, &run);
+    rc = brute ? mdg_brute_force(ctx, G.data(), G.rows(), G.cols(), 40, &run)
+               : mdg_min_weight(ctx, G.data(), G.rows(), G.cols(), &cfg, &run);
     if (rc) {
         mdg_close(ctx);
         return exit_code(rc);
@@ -135,7 +139,7 @@ int main(int argc, char** argv) {
         std::cout << "d:             " << info.d << (info.capped ? " (level cap: upper bound)" : "") << "\n"
                   << "n:             " << info.n << "\n"
                   << "k:             " << info.k << "\n"
-                  << "algorithm:     gpu\n"
+                  << "algorithm:     " << (brute ? "brute" : "gpu") << "\n"
                   << "m:             " << info.m << "\n"
                   << "k_last:        " << info.k_last << "\n"
                   << "g_final:       " << info.g_final << "\n"

@@ -294,3 +294,26 @@ def test_dist_two_ranks_threaded(mdg):
         res = results[r]
         assert res.d == case["d"]
         _check_run(res, case, f"rank{r}", exact=False)
+
+
+# ------------------------------------------------------------ brute force
+@pytest.mark.parametrize("kind", ["kats", "seeded"])
+def test_brute_force_vs_reference(mdg, device, kind):
+    """GPU Gray-code brute force (brute_force_gray, engines.cpp:480-558) == the reference's
+    brute-force d on every known-answer and seeded code; the witness has weight d."""
+    for case in load_golden(kind):
+        rows, n = mdg.parse_matrix(case["matrix"])
+        res = mdg.brute_force(rows, n, device=device)
+        assert res.d == case["d_brute"], case["name"]
+        assert res.witness_ok and (res.m, res.k_last, res.g_final) == (0, 0, 0), case["name"]
+        assert res.combinations == (1 << case["k"]) - 1 == res.evaluated, case["name"]
+
+
+def test_brute_force_cfg1_k40(mdg, device):
+    """Config 1 by exhaustion: all 2^40 - 1 codewords, d = 9 (== the BZ result)."""
+    G = mdg.gen_matrix(80, 40, 1, True)
+    res = mdg.brute_force(G, 80, device=device)
+    assert res.d == 9 and res.witness_ok
+    assert res.evaluated == (1 << 40) - 1
+    with pytest.raises(mdg.InvalidArgument):
+        mdg.brute_force(G, 80, brute_cap=39, device=device)
