@@ -28,6 +28,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -160,8 +161,23 @@ __device__ __forceinline__ uint32_t xor_weight(const uint32_t (&X)[S], const uin
     }
 }
 
-// words of the pruning stage-1 partial weight
-__host__ __device__ constexpr int prune_words(int nw) { return nw <= 1 ? 1 : (nw + 1) / 2; }
+// OR of the NW words of X ^ Y: popc(fold) <= popc(X ^ Y) (every set bit of the
+// fold is a set bit of some word) — a one-POPC lower bound on the weight.
+// f | (x ^ y) as ONE 3-input LOP3 (LUT 0xF6): keeps the per-word XORs out of
+// registers (the compiler would otherwise share them with the exact stage).
+__device__ __forceinline__ uint32_t or_xor(uint32_t f, uint32_t x, uint32_t y) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xF6;" : "=r"(r) : "r"(f), "r"(x), "r"(y));
+    return r;
+}
+
+template <int S, int NW>
+__device__ __forceinline__ uint32_t xor_fold(const uint32_t (&X)[S], const uint32_t (&Y)[NW]) {
+    uint32_t f = X[0] ^ Y[0];
+#pragma unroll
+    for (int i = 1; i < NW; ++i) f = or_xor(f, X[i], Y[i]);
+    return f;
+}
 
 // ------------------------------------------------------ suffix table build
 // entry y: Q' = colex_unrank(y, s) ⊆ [0,k), Q = {k-1-q'}; XOR of rows(Q)
@@ -223,6 +239,7 @@ struct TabArgs {
     const uint64_t* prefix;
     uint32_t k, p, s, emin, npiv, id_rows, add_const, stop_at, tx;
     uint32_t cutoff;               // only weights < cutoff matter (0 = exact round)
+    int32_t fold_limit;            // prune while the bound T <= this (host: fold statistics)
     uint64_t tile_lo, tile_hi;
     unsigned long long* best_key;
     unsigned long long* evaluated;
@@ -307,44 +324,45 @@ __device__ __forceinline__ void load_suffixes(const TabArgs& a, const TileInfo& 
 // lane's R suffixes, considering only values <= T (T < 0: none; the caller maps
 // a cutoff / running best to T). Values above T may be reported as "none"
 // (0xFFFFFFFF) or exactly — never as anything smaller than the truth.
+// fold_limit: prune only while T <= fold_limit (the host's bound below which the
+// fold test rejects almost every codeword; above it pruning would cost more than
+// it saves). T must be warp-uniform on entry.
 template <int NW, bool HID>
 __device__ __forceinline__ uint32_t tile_min(const uint32_t* xs, uint32_t x_begin, uint32_t nx,
                                              const uint32_t (&Y)[r_for(NW)][NW],
-                                             const uint32_t (&idY)[r_for(NW)], int32_t T) {
+                                             const uint32_t (&idY)[r_for(NW)], int32_t T,
+                                             int32_t fold_limit) {
     constexpr int R = r_for(NW);
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
-    constexpr int P = prune_words(NW);
-    // prune only when the bound sits well below the mean partial weight (16 per word)
-    constexpr int kPruneLimit = 16 * P - 2;
     uint32_t best = 0xFFFFFFFFu;
     if (T < 0) {
         // every codeword here is above the bound
-    } else if (T < kPruneLimit) {
-        // bound-pruned walk: a partial weight over the first P words is a lower
-        // bound; the rest is computed only when some lane can still go <= T.
-        // Stage 1 for all R suffixes, then stage 2 per group of G suffixes only
-        // when some lane of the warp has a partial weight <= T there (a real,
-        // warp-uniform branch: a per-codeword vote gets if-converted and the
-        // predicated POPCs still occupy the XU pipe).
+    } else if (T <= fold_limit) {
+        // bound-pruned walk. Stage 1: popc of the OR-fold of all words, a lower
+        // bound on the weight, for all R suffixes. Stage 2 (exact weight) per group
+        // of G suffixes only when some lane of the warp can still be <= T there —
+        // a real warp-uniform branch: a per-codeword vote gets if-converted and the
+        // predicated POPCs still occupy the XU pipe.
         constexpr int G = R >= 4 ? 4 : R;
         for (uint32_t xi = x_begin; xi < nx; ++xi) {
             uint32_t X[XS];
             vload<XS>(xs + xi * XS, X);
-            uint32_t part[R];
+            uint32_t lb[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                part[r] = xor_weight<0, P, XS, NW>(X, Y[r]);
-                if (HID) part[r] += X[NW] + idY[r];
+                lb[r] = __popc(xor_fold<XS, NW>(X, Y[r]));
+                if (HID) lb[r] += X[NW] + idY[r];
             }
 #pragma unroll
             for (int g0 = 0; g0 < R; g0 += G) {
-                uint32_t gmin = part[g0];
+                uint32_t gmin = lb[g0];
 #pragma unroll
-                for (int r = 1; r < G; ++r) gmin = min(gmin, part[g0 + r]);
+                for (int r = 1; r < G; ++r) gmin = min(gmin, lb[g0 + r]);
                 if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= T)) {
 #pragma unroll
                     for (int r = 0; r < G; ++r) {
-                        const uint32_t w = part[g0 + r] + xor_weight<P, NW, XS, NW>(X, Y[g0 + r]);
+                        uint32_t w = xor_weight<0, NW, XS, NW>(X, Y[g0 + r]);
+                        if (HID) w += X[NW] + idY[g0 + r];
                         best = min(best, w);
                     }
                     T = min(T, int32_t(best));
@@ -367,7 +385,7 @@ __device__ __forceinline__ uint32_t tile_min(const uint32_t* xs, uint32_t x_begi
 }
 
 template <int NW, bool HID>
-__global__ void __launch_bounds__(kThreads) tab_round(TabArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) tab_round(TabArgs a) {
     constexpr int R = r_for(NW);
     constexpr int YC = R * kThreads;
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
@@ -414,7 +432,7 @@ __global__ void __launch_bounds__(kThreads) tab_round(TabArgs a) {
         load_suffixes<NW, HID>(a, ti, Y, idY, valid);
         __syncthreads();
 
-        uint32_t best = tile_min<NW, HID>(xs, 0, ti.nx, Y, idY, ti.T);
+        uint32_t best = tile_min<NW, HID>(xs, 0, ti.nx, Y, idY, ti.T, a.fold_limit);
         if (best != 0xFFFFFFFFu) best += a.add_const;
         best = __reduce_min_sync(0xFFFFFFFFu, best);
         if (lane == 0 && best != 0xFFFFFFFFu && (cutoff == 0 || best < cutoff)) {
@@ -714,6 +732,7 @@ __global__ void span_build(const uint32_t* __restrict__ rows, uint32_t first, ui
 }
 
 struct SpanArgs {
+    int32_t fold_limit;
     const uint32_t* ta;
     const uint32_t* tb;
     uint64_t na, nb, nty;
@@ -727,7 +746,7 @@ struct SpanArgs {
 };
 
 template <int NW, bool FIND>
-__global__ void __launch_bounds__(kThreads) span_round(SpanArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) span_round(SpanArgs a) {
     constexpr int R = r_for(NW);
     constexpr int YC = R * kThreads;
     constexpr int S = stride_for(NW);
@@ -818,7 +837,7 @@ __global__ void __launch_bounds__(kThreads) span_round(SpanArgs a) {
             // the bound must be warp-uniform: tile_min branches on it around warp votes
             const uint32_t wbest = __reduce_min_sync(0xFFFFFFFFu, best);
             const int32_t T = wbest == 0xFFFFFFFFu ? s_T : min(s_T, int32_t(wbest));
-            best = min(best, tile_min<NW, false>(xs, xb, nx, Y, idY, T));
+            best = min(best, tile_min<NW, false>(xs, xb, nx, Y, idY, T, a.fold_limit));
             best = __reduce_min_sync(0xFFFFFFFFu, best);
             if (lane == 0 && best != 0xFFFFFFFFu) {
                 unsigned long long key = (static_cast<unsigned long long>(best) << kKeyShift) | s_tile;
@@ -1136,7 +1155,25 @@ private:
     size_t cur_ = 0;
 };
 
+// Largest bound T for which the OR-fold filter is worth running: random rows
+// give popc(fold) ~ sum_p q_p, q_p = 1 - 2^-(words holding bit p); prune while
+// T <= mean - 4 sd (beyond that most warps would take the exact path anyway).
+static int32_t fold_limit_for(uint32_t bits) {
+    const uint32_t words = (bits + 31) / 32;
+    double mean = 0, var = 0;
+    for (uint32_t p = 0; p < 32; ++p) {
+        uint32_t cover = 0;
+        for (uint32_t w = 0; w < words; ++w)
+            if (w * 32 + p < bits) ++cover;
+        double q = 1.0 - std::ldexp(1.0, -int(cover));
+        mean += q;
+        var += q * (1.0 - q);
+    }
+    return int32_t(std::floor(mean - 4.0 * std::sqrt(var)));
+}
+
 struct GammaDev {
+    int32_t fold_limit = -1;   // see fold_limit_for
     uint32_t* rows = nullptr;  // k x nw (compacted, zero-padded to the template width)
     uint32_t nw = 0;
     uint32_t id_rows = 0;      // identity rows [0, id_rows)
@@ -1296,6 +1333,7 @@ void Engine::load(uint32_t m, uint32_t k, uint32_t n, const uint64_t* rows, cons
         gd.n_compact = n - rk;
         gd.nw = template_width(std::max<uint32_t>(1, (gd.n_compact + 31) / 32)); // zero-padded
         gd.hid = rk > 0 && rk < k;
+        gd.fold_limit = fold_limit_for(gd.n_compact);
         auto& hr = host[j];
         hr.assign(size_t(k) * gd.nw, 0);
         for (uint32_t r = 0; r < k; ++r) {
@@ -1354,6 +1392,7 @@ static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe
     a.k = k; a.p = pe.plan.p; a.s = pe.plan.s; a.emin = pe.plan.emin;
     a.npiv = uint32_t(pe.plan.prefix.size() - 1);
     a.id_rows = g.id_rows; a.add_const = (g.id_rows == k) ? c : 0; a.tx = pe.plan.TX;
+    a.fold_limit = g.fold_limit;
     return a;
 }
 
@@ -1660,6 +1699,7 @@ Engine::BruteResult Engine::brute_force(uint32_t k, uint32_t n, const uint64_t* 
     const uint64_t tiles = ceil_div(na, tx) * nty;
     unsigned long long* slot = im.take_slot();
     sa.ta = ta; sa.tb = tb; sa.na = na; sa.nb = nb; sa.nty = nty; sa.tx = tx;
+    sa.fold_limit = g.fold_limit;
     sa.tile_lo = 0; sa.tile_hi = tiles;
     sa.best_key = slot; sa.evaluated = slot + 1; sa.counter = slot + 2; sa.find_out = slot + 3;
     CK(cudaEventRecord(im.ev0, im.stream));
