@@ -39,8 +39,8 @@ sys.path.insert(0, ROOT)
 N, K, SEEDS = 128, 64, list(range(1, 9))
 POPC_PER_S_MEASURED = 4642.3e9   # profiles/r01_pipes_microbench.jsonl (B200, 148 SMs)
 # XU (POPC) operations the bound-pruned level-7 kernel executes per codeword, from the
-# committed ncu capture of that launch (profiles/r01b_tab_round_pruned_ncu.txt)
-XU_PER_CW_PRUNED = 1.202
+# committed ncu capture of that launch (profiles/r01c_tab_round_fold_ncu.txt)
+XU_PER_CW_PRUNED = 1.076
 WORKLOAD = "cfg2: random [128,64] codes G=(I|A), mt19937_64 seeds 1..8, BZ to termination (exact d)"
 
 
@@ -311,8 +311,8 @@ def main():
             "frac": achieved / peak, "traffic": 4200960, "traffic_unit": "DRAM bytes per launch (ncu)",
             "kernel": "tab_round<2,false>, bound-pruned (cutoff U), level-7 rounds (621,216,192 codewords per launch)",
             "peak_basis": ("measured B200 POPC (XU pipe) rate 16/clk/SM = 4.64e12/s "
-                           "(tools/pipes_microbench.cu) / 1.202 XU ops per codeword executed by this "
-                           "kernel (ncu, profiles/r01b_tab_round_pruned_ncu.txt)"),
+                           "(tools/pipes_microbench.cu) / 1.076 XU ops per codeword executed by this "
+                           "kernel (ncu, profiles/r01c_tab_round_fold_ncu.txt)"),
             "op_mix_per_codeword": ("1 LOP3 + 1 POPC (first 32 compacted bits) + group min/vote; the "
                                     "second word only for warp groups that can still beat U"),
             "frac_vs_unpruned_popc_roofline": achieved / (popc / nw),

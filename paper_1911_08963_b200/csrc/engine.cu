@@ -1012,7 +1012,7 @@ static uint64_t plan_cost(uint32_t k, uint32_t c, uint32_t s, uint32_t TX, uint3
 }
 
 // Suffix size s minimizes the tile cost (suffix table <= 4M entries); the
-// prefix chunk TX is the largest of 256/128/64/32 that still yields >= 6
+// prefix chunk TX is the largest of 256/128/64/32/16 that still yields >= 16
 // tiles per resident block, so the dynamic scheduler's tail stays short.
 TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_blocks) {
     TabPlan pl;
@@ -1032,11 +1032,11 @@ TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_b
     pl.p = c - best_s;
     pl.emin = pl.p - 1;
     pl.emax = k - 1 - pl.s;
-    pl.TX = 32;
-    for (uint32_t tx = kTX; tx >= 32; tx /= 2) {
+    pl.TX = 16;
+    for (uint32_t tx = kTX; tx >= 16; tx /= 2) {
         uint64_t tiles = 0;
         plan_cost(k, c, pl.s, tx, pl.YC, &tiles);
-        if (tiles >= uint64_t(resident_blocks) * 6 || tx == 32) { pl.TX = tx; break; }
+        if (tiles >= uint64_t(resident_blocks) * 16 || tx == 16) { pl.TX = tx; break; }
     }
     pl.prefix.assign(1, 0);
     for (uint32_t e = pl.emin; e <= pl.emax; ++e) {
@@ -1695,7 +1695,7 @@ Engine::BruteResult Engine::brute_force(uint32_t k, uint32_t n, const uint64_t* 
     const uint64_t nty = ceil_div(nb, YC);
     uint32_t tx = kTX;
     int resident = im.resident(g.nw, false, sms_);
-    while (tx > 32 && ceil_div(na, tx) * nty < uint64_t(resident) * 6) tx /= 2;
+    while (tx > 16 && ceil_div(na, tx) * nty < uint64_t(resident) * 16) tx /= 2;
     const uint64_t tiles = ceil_div(na, tx) * nty;
     unsigned long long* slot = im.take_slot();
     sa.ta = ta; sa.tb = tb; sa.na = na; sa.nb = nb; sa.nty = nty; sa.tx = tx;
