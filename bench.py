@@ -313,8 +313,9 @@ def main():
             "peak_basis": ("measured B200 POPC (XU pipe) rate 16/clk/SM = 4.64e12/s "
                            "(tools/pipes_microbench.cu) / 1.076 XU ops per codeword executed by this "
                            "kernel (ncu, profiles/r01c_tab_round_fold_ncu.txt)"),
-            "op_mix_per_codeword": ("1 LOP3 + 1 POPC (first 32 compacted bits) + group min/vote; the "
-                                    "second word only for warp groups that can still beat U"),
+            "op_mix_per_codeword": ("2 LOP3 (XOR, fused OR-fold) + 1 POPC of the fold (a lower bound on "
+                                    "the weight) + group min / warp vote; the exact weight only for warp "
+                                    "groups that can still beat the bound (1.08 POPC per codeword measured)"),
             "frac_vs_unpruned_popc_roofline": achieved / (popc / nw),
             "traffic_note": "DRAM 4.2 MB per launch (suffix table + binomials), 0.1% of HBM peak: compute-bound",
         }

@@ -24,7 +24,7 @@ import numpy as np
 __all__ = [
     "MdgError", "InvalidArgument", "OverflowError_", "CudaFailure", "lib", "Device", "GammaSet",
     "RoundOut", "RunResult", "min_weight", "min_weight_dist", "run_bz_loop", "lower_bound",
-    "singleton_upper", "brute_force", "parse_matrix", "serialize_matrix", "gen_matrix", "binomial",
+    "singleton_upper", "brute_force", "nccl_unique_id", "parse_matrix", "serialize_matrix", "gen_matrix", "binomial",
     "rd_unrank", "rd_rank", "hash_rows", "rank_of", "words", "KERNEL_TAB", "KERNEL_RD",
 ]
 

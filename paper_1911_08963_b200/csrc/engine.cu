@@ -1572,9 +1572,11 @@ std::vector<uint32_t> Engine::witness(uint32_t j, uint32_t c, const RoundResult&
 }
 
 Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_cap, bool exact,
-                                       uint32_t k_last, uint32_t rank, uint32_t world) {
+                                       uint32_t k_last, uint32_t rank, uint32_t world,
+                                       bool allreduce) {
     if (kernel_ != Kernel::tab) throw std::logic_error("chain_loop: tab kernel only");
-    if (world > 1 && !impl_->comm) throw std::logic_error("chain_loop: NCCL communicator not initialised");
+    allreduce = allreduce || world > 1;
+    if (allreduce && !impl_->comm) throw std::logic_error("chain_loop: NCCL communicator not initialised");
     CK(cudaSetDevice(device_));
     Impl& im = *impl_;
     // host work per check: ~2e8 codewords (~0.1 ms of device time) between looks at `done`
@@ -1628,7 +1630,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
                 CK(cudaGetLastError());
                 im.cnt.launches += 1;
             }
-            if (world > 1) {
+            if (allreduce) {
                 int rc = nccl().AllReduce(slot, slot, 1, kNcclUint64, kNcclMin, im.comm, im.stream);
                 if (rc != 0) throw std::runtime_error(std::string("ncclAllReduce: ") + nccl().GetErrorString(rc));
             }

@@ -95,7 +95,8 @@ public:
     BruteResult brute_force(uint32_t k, uint32_t n, const uint64_t* rows);
 
     ChainResult chain_loop(uint32_t U0, uint32_t L0, uint32_t level_cap, bool exact,
-                           uint32_t k_last, uint32_t rank = 0, uint32_t world = 1);
+                           uint32_t k_last, uint32_t rank = 0, uint32_t world = 1,
+                           bool allreduce = false);
     std::vector<uint32_t> witness(uint32_t j, uint32_t c, const RoundResult& rr);
 
     // NCCL (loaded at runtime) for the multi-GPU reduction

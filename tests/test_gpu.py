@@ -317,3 +317,16 @@ def test_brute_force_cfg1_k40(mdg, device):
     assert res.evaluated == (1 << 40) - 1
     with pytest.raises(mdg.InvalidArgument):
         mdg.brute_force(G, 80, brute_cap=39, device=device)
+
+
+def test_nccl_single_rank(mdg):
+    """The in-stream NCCL allreduce(min) path of the chained loop, with one rank."""
+    case = next(c for c in load_golden("configs") if c["name"] == "cfg2_s8")
+    g = case["gen"]
+    rows = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
+    dev = mdg.Device(0)
+    dev.nccl_init(mdg.nccl_unique_id(), 0, 1)
+    res = mdg.min_weight_dist(rows, g["n"], 0, 1, "nccl", trials=10, seed=g["seed"], device=dev)
+    assert res.d == case["d"]
+    _check_run(res, case, "nccl1", exact=False)
+    dev.close()
