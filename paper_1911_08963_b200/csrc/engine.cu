@@ -28,7 +28,9 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -182,10 +184,12 @@ __device__ __forceinline__ uint32_t xor_fold(const uint32_t (&X)[S], const uint3
 // ------------------------------------------------------ suffix table build
 // entry y: Q' = colex_unrank(y, s) ⊆ [0,k), Q = {k-1-q'}; XOR of rows(Q)
 // (+ |Q ∩ [0, id_rows)| in word NW when HID).
+// reverse = false builds the prefix table instead: Q = Q' itself (plain colex
+// order, so the (p-1)-subsets of [0, e) are its first C(e, p-1) entries).
 template <int NW, bool HID>
 __global__ void ytab_build(const uint32_t* __restrict__ rows, const uint64_t* __restrict__ T,
                            uint32_t k, uint32_t s, uint32_t id_rows, uint64_t count,
-                           uint32_t* __restrict__ out) {
+                           uint32_t* __restrict__ out, bool reverse) {
     constexpr int YS = stride_for(NW + (HID ? 1 : 0));
     uint64_t y = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (y >= count) return;
@@ -199,7 +203,7 @@ __global__ void ytab_build(const uint32_t* __restrict__ rows, const uint64_t* __
         uint32_t x = colex_top(T, r, i, hi);
         r -= BT(T, x, i);
         hi = x;
-        uint32_t q = k - 1 - x;
+        uint32_t q = reverse ? k - 1 - x : x;
         xor_row<NW>(rows, q, acc);
         id += q < id_rows;
     }
@@ -235,11 +239,12 @@ struct TabArgs {
     const ChainState* st;          // non-null: cutoff / stop_at / skip from the chain state
     const uint32_t* rows;
     const uint32_t* ytab;
+    const uint32_t* xtab;          // optional prefix table (colex (p-1)-subset sums)
     const uint64_t* binom;
     const uint64_t* prefix;
     uint32_t k, p, s, emin, npiv, id_rows, add_const, stop_at, tx;
     uint32_t cutoff;               // only weights < cutoff matter (0 = exact round)
-    int32_t fold_limit;            // prune while the bound T <= this (host: fold statistics)
+    int32_t fold_lim[3];           // G = 1, 2, 4 fold groups usable while T <= fold_lim (host)
     uint64_t tile_lo, tile_hi;
     unsigned long long* best_key;
     unsigned long long* evaluated;
@@ -254,6 +259,7 @@ struct TileInfo {
     uint32_t e, nx, nyv, stop;
     uint64_t x0, y0, tile;
     int32_t T;                     // pruning bound on the compacted weight (inclusive)
+    int32_t G;                     // stage-1 fold groups for T (0 = exact weights)
 };
 
 // decode tile -> (pivot, prefix chunk, suffix chunk); thread 0 only
@@ -286,6 +292,16 @@ __device__ __forceinline__ void build_prefix(const TabArgs& a, uint32_t e, uint6
     uint32_t acc[NW];
     load_row<NW>(a.rows, e, acc);
     uint32_t id = e < a.id_rows;
+    if (a.xtab) { // row e + entry x of the prefix table: no unranking
+        uint32_t v[XS];
+        vload_global<XS>(a.xtab + x * XS, v);
+#pragma unroll
+        for (int w = 0; w < NW; ++w) acc[w] ^= v[w];
+        if (HID) id += v[NW];
+#pragma unroll
+        for (int w = 0; w < XS; ++w) dst[w] = w < NW ? acc[w] : (HID && w == NW ? id : 0u);
+        return;
+    }
     uint64_t r = x;
     uint32_t hi = e;
     for (uint32_t i = a.p - 1; i >= 1; --i) {
@@ -320,68 +336,107 @@ __device__ __forceinline__ void load_suffixes(const TabArgs& a, const TileInfo& 
     }
 }
 
-// Minimum of (compacted weight + identity count) over prefixes xs[x_begin, nx) x the
-// lane's R suffixes, considering only values <= T (T < 0: none; the caller maps
-// a cutoff / running best to T). Values above T may be reported as "none"
-// (0xFFFFFFFF) or exactly — never as anything smaller than the truth.
-// fold_limit: prune only while T <= fold_limit (the host's bound below which the
-// fold test rejects almost every codeword; above it pruning would cost more than
-// it saves). T must be warp-uniform on entry.
-template <int NW, bool HID>
-__device__ __forceinline__ uint32_t tile_min(const uint32_t* xs, uint32_t x_begin, uint32_t nx,
-                                             const uint32_t (&Y)[r_for(NW)][NW],
-                                             const uint32_t (&idY)[r_for(NW)], int32_t T,
-                                             int32_t fold_limit) {
+// OR-folds of the words of X ^ Y in G contiguous groups: sum_g popc(fold_g) is a
+// lower bound on the weight (G POPCs); larger G = tighter bound for sparse codewords.
+template <int G, int S, int NW>
+__device__ __forceinline__ uint32_t fold_bound(const uint32_t (&X)[S], const uint32_t (&Y)[NW]) {
+    uint32_t lb = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int b = g * NW / G, e = (g + 1) * NW / G;
+        if (b < e) {
+            uint32_t f = X[b] ^ Y[b];
+#pragma unroll
+            for (int i = b + 1; i < e; ++i) f = or_xor(f, X[i], Y[i]);
+            lb += __popc(f);
+        }
+    }
+    return lb;
+}
+
+// The bound-pruned walk with G fold groups (see tile_min).
+template <int NW, bool HID, int G>
+__device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t x_begin, uint32_t nx,
+                                                    const uint32_t (&Y)[r_for(NW)][NW],
+                                                    const uint32_t (&idY)[r_for(NW)], int32_t T) {
     constexpr int R = r_for(NW);
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
+    constexpr int GR = R >= 4 ? 4 : R; // suffixes per warp vote
     uint32_t best = 0xFFFFFFFFu;
-    if (T < 0) {
-        // every codeword here is above the bound
-    } else if (T <= fold_limit) {
-        // bound-pruned walk. Stage 1: popc of the OR-fold of all words, a lower
-        // bound on the weight, for all R suffixes. Stage 2 (exact weight) per group
-        // of G suffixes only when some lane of the warp can still be <= T there —
-        // a real warp-uniform branch: a per-codeword vote gets if-converted and the
-        // predicated POPCs still occupy the XU pipe.
-        constexpr int G = R >= 4 ? 4 : R;
-        for (uint32_t xi = x_begin; xi < nx; ++xi) {
-            uint32_t X[XS];
-            vload<XS>(xs + xi * XS, X);
-            uint32_t lb[R];
+    for (uint32_t xi = x_begin; xi < nx; ++xi) {
+        uint32_t X[XS];
+        vload<XS>(xs + xi * XS, X);
+        uint32_t lb[R];
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                lb[r] = __popc(xor_fold<XS, NW>(X, Y[r]));
-                if (HID) lb[r] += X[NW] + idY[r];
-            }
-#pragma unroll
-            for (int g0 = 0; g0 < R; g0 += G) {
-                uint32_t gmin = lb[g0];
-#pragma unroll
-                for (int r = 1; r < G; ++r) gmin = min(gmin, lb[g0 + r]);
-                if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= T)) {
-#pragma unroll
-                    for (int r = 0; r < G; ++r) {
-                        uint32_t w = xor_weight<0, NW, XS, NW>(X, Y[g0 + r]);
-                        if (HID) w += X[NW] + idY[g0 + r];
-                        best = min(best, w);
-                    }
-                    T = min(T, int32_t(best));
-                }
-            }
+        for (int r = 0; r < R; ++r) {
+            lb[r] = fold_bound<G, XS, NW>(X, Y[r]);
+            if (HID) lb[r] += X[NW] + idY[r];
         }
-    } else {
-        for (uint32_t xi = x_begin; xi < nx; ++xi) {
-            uint32_t X[XS];
-            vload<XS>(xs + xi * XS, X);
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                uint32_t w = xor_weight<0, NW, XS, NW>(X, Y[r]);
-                if (HID) w += X[NW] + idY[r];
-                best = min(best, w);
+        for (int g0 = 0; g0 < R; g0 += GR) {
+            uint32_t gmin = lb[g0];
+#pragma unroll
+            for (int r = 1; r < GR; ++r) gmin = min(gmin, lb[g0 + r]);
+            if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= T)) {
+#pragma unroll
+                for (int r = 0; r < GR; ++r) {
+                    uint32_t w = xor_weight<0, NW, XS, NW>(X, Y[g0 + r]);
+                    if (HID) w += X[NW] + idY[g0 + r];
+                    best = min(best, w);
+                }
+                T = min(T, int32_t(best));
             }
         }
     }
     return best;
+}
+
+// Minimum of (compacted weight + identity count) over prefixes xs[x_begin, nx) x the
+// lane's R suffixes, considering only values <= T (T < 0: none). Values above T may be
+// reported as "none" (0xFFFFFFFF) or exactly — never as anything smaller than the
+// truth. G (warp-uniform): 0 = exact weights for every codeword; 1, 2, 4 = stage-1
+// lower bound from that many OR-fold groups, exact weight only for warp groups of 4
+// suffixes in which some lane can still reach T (a real warp-uniform branch: a
+// per-codeword vote gets if-converted and the predicated POPCs would still occupy the
+// XU pipe). T must be warp-uniform on entry.
+template <int NW, bool HID>
+__device__ __forceinline__ uint32_t tile_min(const uint32_t* xs, uint32_t x_begin, uint32_t nx,
+                                             const uint32_t (&Y)[r_for(NW)][NW],
+                                             const uint32_t (&idY)[r_for(NW)], int32_t T,
+                                             int G) {
+    constexpr int R = r_for(NW);
+    constexpr int XS = stride_for(NW + (HID ? 1 : 0));
+    if (T < 0) return 0xFFFFFFFFu; // every codeword here is above the bound
+    if (G == 1) return tile_min_pruned<NW, HID, 1>(xs, x_begin, nx, Y, idY, T);
+    if constexpr (NW >= 4) {
+        if (G == 2) return tile_min_pruned<NW, HID, 2>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (NW >= 8) {
+        if (G == 4) return tile_min_pruned<NW, HID, 4>(xs, x_begin, nx, Y, idY, T);
+    }
+    uint32_t best = 0xFFFFFFFFu;
+    for (uint32_t xi = x_begin; xi < nx; ++xi) {
+        uint32_t X[XS];
+        vload<XS>(xs + xi * XS, X);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            uint32_t w = xor_weight<0, NW, XS, NW>(X, Y[r]);
+            if (HID) w += X[NW] + idY[r];
+            best = min(best, w);
+        }
+    }
+    return best;
+}
+
+// fold groups for bound T: the smallest G whose stage-1 bound still rejects almost every
+// codeword at T (lim[] from the host's density estimate; -1 = unusable), else 0 (exact)
+__device__ __forceinline__ int pick_groups(int32_t T, const int32_t (&lim)[3]) {
+    if (T <= lim[0]) return 1;
+    if (T <= lim[1]) return 2;
+    if (T <= lim[2]) return 4;
+    return 0;
 }
 
 template <int NW, bool HID>
@@ -419,6 +474,7 @@ __global__ void __launch_bounds__(kThreads, 4) tab_round(TabArgs a) {
                     if (int64_t(gw) < lim) lim = gw;
                     lim -= a.add_const;
                     ti.T = lim < -1 ? -1 : (lim > 0x7FFFFFFF ? 0x7FFFFFFF : int32_t(lim));
+                    ti.G = pick_groups(ti.T, a.fold_lim);
                 }
             }
             ti.stop = stop;
@@ -432,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 4) tab_round(TabArgs a) {
         load_suffixes<NW, HID>(a, ti, Y, idY, valid);
         __syncthreads();
 
-        uint32_t best = tile_min<NW, HID>(xs, 0, ti.nx, Y, idY, ti.T, a.fold_limit);
+        uint32_t best = tile_min<NW, HID>(xs, 0, ti.nx, Y, idY, ti.T, ti.G);
         if (best != 0xFFFFFFFFu) best += a.add_const;
         best = __reduce_min_sync(0xFFFFFFFFu, best);
         if (lane == 0 && best != 0xFFFFFFFFu && (cutoff == 0 || best < cutoff)) {
@@ -732,7 +788,7 @@ __global__ void span_build(const uint32_t* __restrict__ rows, uint32_t first, ui
 }
 
 struct SpanArgs {
-    int32_t fold_limit;
+    int32_t fold_lim[3];
     const uint32_t* ta;
     const uint32_t* tb;
     uint64_t na, nb, nty;
@@ -837,7 +893,7 @@ __global__ void __launch_bounds__(kThreads, 4) span_round(SpanArgs a) {
             // the bound must be warp-uniform: tile_min branches on it around warp votes
             const uint32_t wbest = __reduce_min_sync(0xFFFFFFFFu, best);
             const int32_t T = wbest == 0xFFFFFFFFu ? s_T : min(s_T, int32_t(wbest));
-            best = min(best, tile_min<NW, false>(xs, xb, nx, Y, idY, T, a.fold_limit));
+            best = min(best, tile_min<NW, false>(xs, xb, nx, Y, idY, T, pick_groups(T, a.fold_lim)));
             best = __reduce_min_sync(0xFFFFFFFFu, best);
             if (lane == 0 && best != 0xFFFFFFFFu) {
                 unsigned long long key = (static_cast<unsigned long long>(best) << kKeyShift) | s_tile;
@@ -892,9 +948,10 @@ void dispatch_nw_hid(uint32_t nw, bool hid, Args&&... args) {
 template <int NW, bool HID>
 struct YtabLaunch {
     static void run(const uint32_t* rows, const uint64_t* T, uint32_t k, uint32_t s,
-                    uint32_t id_rows, uint64_t count, uint32_t* out, cudaStream_t st) {
+                    uint32_t id_rows, uint64_t count, uint32_t* out, bool reverse, cudaStream_t st) {
         uint64_t blocks = (count + 255) / 256;
-        ytab_build<NW, HID><<<dim3(uint32_t(blocks)), 256, 0, st>>>(rows, T, k, s, id_rows, count, out);
+        ytab_build<NW, HID><<<dim3(uint32_t(blocks)), 256, 0, st>>>(rows, T, k, s, id_rows, count, out,
+                                                                   reverse);
     }
 };
 
@@ -1032,11 +1089,20 @@ TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_b
     pl.p = c - best_s;
     pl.emin = pl.p - 1;
     pl.emax = k - 1 - pl.s;
-    pl.TX = 16;
-    for (uint32_t tx = kTX; tx >= 16; tx /= 2) {
+    // tuning knobs (defaults measured on B200): tiles per resident block, smallest chunk
+    static const uint32_t kTilesPerBlock = [] {
+        const char* e = std::getenv("MDG_TILES_PER_BLOCK");
+        return e ? uint32_t(std::max(1, std::atoi(e))) : 16u;
+    }();
+    static const uint32_t kMinTX = [] {
+        const char* e = std::getenv("MDG_MIN_TX");
+        return e ? uint32_t(std::max(1, std::min(256, std::atoi(e)))) : 16u;
+    }();
+    pl.TX = kMinTX;
+    for (uint32_t tx = kTX; tx >= kMinTX; tx /= 2) {
         uint64_t tiles = 0;
         plan_cost(k, c, pl.s, tx, pl.YC, &tiles);
-        if (tiles >= uint64_t(resident_blocks) * 16 || tx == 16) { pl.TX = tx; break; }
+        if (tiles >= uint64_t(resident_blocks) * kTilesPerBlock || tx <= kMinTX) { pl.TX = tx; break; }
     }
     pl.prefix.assign(1, 0);
     for (uint32_t e = pl.emin; e <= pl.emax; ++e) {
@@ -1155,25 +1221,43 @@ private:
     size_t cur_ = 0;
 };
 
-// Largest bound T for which the OR-fold filter is worth running: random rows
-// give popc(fold) ~ sum_p q_p, q_p = 1 - 2^-(words holding bit p); prune while
-// T <= mean - 4 sd (beyond that most warps would take the exact path anyway).
-static int32_t fold_limit_for(uint32_t bits) {
-    const uint32_t words = (bits + 31) / 32;
-    double mean = 0, var = 0;
-    for (uint32_t p = 0; p < 32; ++p) {
-        uint32_t cover = 0;
-        for (uint32_t w = 0; w < words; ++w)
-            if (w * 32 + p < bits) ++cover;
-        double q = 1.0 - std::ldexp(1.0, -int(cover));
-        mean += q;
-        var += q * (1.0 - q);
+// Stage-1 limits for G = 1, 2, 4 fold groups over the template's NW words: with
+// codeword bit density rho_c, a fold bit over m words is set with probability
+// 1 - (1 - rho_c)^m, so popc(folds) ~ mean E_G, variance V_G; pruning with G groups
+// is worth it while the bound T <= E_G - 4 sqrt(V_G) (then almost no codeword passes).
+// G must not exceed the word count it splits (G=2 needs NW >= 4, G=4 needs NW >= 8).
+static void fold_limits(uint32_t bits, uint32_t nw, double rho_c, int32_t (&lim)[3]) {
+    const int Gs[3] = {1, 2, 4};
+    for (int gi = 0; gi < 3; ++gi) {
+        const int G = Gs[gi];
+        if ((G == 2 && nw < 4) || (G == 4 && nw < 8)) { lim[gi] = -1; continue; }
+        double mean = 0, var = 0;
+        for (int g = 0; g < G; ++g) {
+            const uint32_t b = uint32_t(g) * nw / G, e = uint32_t(g + 1) * nw / G;
+            for (uint32_t p = 0; p < 32; ++p) {
+                uint32_t m = 0;
+                for (uint32_t w = b; w < e; ++w)
+                    if (w * 32 + p < bits) ++m;
+                const double q = 1.0 - std::pow(1.0 - rho_c, double(m));
+                mean += q;
+                var += q * (1.0 - q);
+            }
+        }
+        lim[gi] = int32_t(std::floor(mean - 4.0 * std::sqrt(var)));
     }
-    return int32_t(std::floor(mean - 4.0 * std::sqrt(var)));
+    // a larger G only helps if it raises the limit
+    if (lim[1] <= lim[0]) lim[1] = -1;
+    if (lim[2] <= std::max(lim[0], lim[1])) lim[2] = -1;
+}
+
+// density of an XOR of c rows of density rho (independent bits)
+static double level_density(double rho, uint32_t c) {
+    return 0.5 * (1.0 - std::pow(1.0 - 2.0 * rho, double(c)));
 }
 
 struct GammaDev {
-    int32_t fold_limit = -1;   // see fold_limit_for
+    double rho = 0.5;          // bit density of the compacted rows
+    std::vector<uint32_t> host_rows; // compacted rows on the host (stage-1 sampling)
     uint32_t* rows = nullptr;  // k x nw (compacted, zero-padded to the template width)
     uint32_t nw = 0;
     uint32_t id_rows = 0;      // identity rows [0, id_rows)
@@ -1199,9 +1283,10 @@ struct Engine::Impl {
     unsigned long long* hist_dev = nullptr;
     size_t hist_cap = 0;
     std::vector<GammaDev> gammas;
-    std::map<std::pair<uint32_t, uint32_t>, uint32_t*> ytabs; // (j, s) -> table
+    std::map<std::tuple<uint32_t, uint32_t, bool>, uint32_t*> tables; // (j, size, reverse) -> table
     std::map<std::tuple<uint32_t, uint32_t, uint32_t, bool>, PlanEntry> plans; // (k, c, nw, hid)
     std::map<std::pair<uint32_t, bool>, int> occ;                     // (nw, hid)
+    std::map<std::pair<uint32_t, uint32_t>, std::array<int32_t, 3>> fold_cache; // (j, c)
     ncclComm_t comm = nullptr;
     uint64_t* red_dev = nullptr;
     size_t red_cap = 0;
@@ -1333,7 +1418,6 @@ void Engine::load(uint32_t m, uint32_t k, uint32_t n, const uint64_t* rows, cons
         gd.n_compact = n - rk;
         gd.nw = template_width(std::max<uint32_t>(1, (gd.n_compact + 31) / 32)); // zero-padded
         gd.hid = rk > 0 && rk < k;
-        gd.fold_limit = fold_limit_for(gd.n_compact);
         auto& hr = host[j];
         hr.assign(size_t(k) * gd.nw, 0);
         for (uint32_t r = 0; r < k; ++r) {
@@ -1345,10 +1429,15 @@ void Engine::load(uint32_t m, uint32_t k, uint32_t n, const uint64_t* rows, cons
                 ++o;
             }
         }
+        uint64_t ones = 0;
+        for (uint32_t x : hr) ones += uint32_t(__builtin_popcount(x));
+        gd.rho = gd.n_compact ? double(ones) / (double(k) * gd.n_compact) : 0.5;
+        gd.host_rows = hr;
         next.push_back(gd);
     }
     impl_->gammas.clear();
-    impl_->ytabs.clear();
+    impl_->tables.clear();
+    impl_->fold_cache.clear();
     impl_->arena.reset(); // the stream is idle (synchronized above)
     for (uint32_t j = 0; j < m; ++j) {
         next[j].rows = static_cast<uint32_t*>(impl_->arena.alloc(host[j].size() * 4));
@@ -1370,19 +1459,89 @@ void Engine::check_round(uint32_t j, uint32_t c) const {
     binomial(k_, c); // throws std::overflow_error when C(k, c) exceeds 64 bits
 }
 
-static uint32_t* ensure_ytab(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t s) {
-    auto key = std::make_pair(j, s);
-    auto it = im.ytabs.find(key);
-    if (it != im.ytabs.end()) return it->second;
+static uint32_t* ensure_table(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t s, bool reverse) {
+    auto key = std::make_tuple(j, s, reverse);
+    auto it = im.tables.find(key);
+    if (it != im.tables.end()) return it->second;
     const GammaDev& g = im.gammas[j];
     uint32_t YS = uint32_t(stride_for(int(g.nw) + (g.hid ? 1 : 0)));
     uint64_t count = hb(k, s);
     uint32_t* t = static_cast<uint32_t*>(im.arena.alloc(size_t(count) * YS * 4));
-    dispatch_nw_hid<YtabLaunch>(g.nw, g.hid, g.rows, im.binom, k, s, g.id_rows, count, t, im.stream);
+    dispatch_nw_hid<YtabLaunch>(g.nw, g.hid, g.rows, im.binom, k, s, g.id_rows, count, t, reverse,
+                                im.stream);
     CK(cudaGetLastError());
     im.cnt.launches += 1;
-    im.ytabs[key] = t;
+    im.tables[key] = t;
     return t;
+}
+
+// suffix table (reverse colex s-subsets)
+static uint32_t* ensure_ytab(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t s) {
+    return ensure_table(im, j, k, s, true);
+}
+
+// prefix table (colex (p-1)-subsets) when it is small enough, else nullptr (unrank per tile)
+static const uint32_t* ensure_xtab(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t pm1) {
+    if (pm1 == 0 || hb(k, pm1) > (uint64_t{1} << 22)) return nullptr;
+    return ensure_table(im, j, k, pm1, false);
+}
+
+// Stage-1 limits measured on the round's own codewords: 128 uniform random
+// c-subsets of Gamma_j's compacted rows (SplitMix64 seeded by (j, c)), lower bounds
+// lb_G = sum of popc over G fold groups (+ identity count), lim_G = mean - 4 sd.
+// Sampling captures the column structure the density model misses (the partial
+// Gamma's rows are e_r plus subsets of the pivot columns: dense in half the columns).
+static void sampled_fold_limits(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t c,
+                                int32_t (&lim)[3]) {
+    auto key = std::make_pair(j, c);
+    auto it = im.fold_cache.find(key);
+    if (it != im.fold_cache.end()) {
+        std::copy(it->second.begin(), it->second.end(), lim);
+        return;
+    }
+    const GammaDev& g = im.gammas[j];
+    const uint32_t nw = g.nw;
+    const int Gs[3] = {1, 2, 4};
+    double sum[3] = {0, 0, 0}, sq[3] = {0, 0, 0};
+    constexpr int kSamples = 128;
+    SplitMix64 rng(0x9E3779B97F4A7C15ull ^ (uint64_t(j) << 32) ^ c);
+    std::vector<uint32_t> acc(nw), pick;
+    std::vector<uint8_t> used(k);
+    for (int t = 0; t < kSamples; ++t) {
+        std::fill(acc.begin(), acc.end(), 0u);
+        uint32_t id = 0;
+        pick.clear();
+        for (uint32_t i = 0; i < c; ++i) { // c distinct rows
+            uint32_t r;
+            do { r = uint32_t(rng.next() % k); } while (used[r]);
+            used[r] = 1;
+            pick.push_back(r);
+            id += r < g.id_rows;
+            for (uint32_t w = 0; w < nw; ++w) acc[w] ^= g.host_rows[size_t(r) * nw + w];
+        }
+        for (uint32_t r : pick) used[r] = 0;
+        for (int gi = 0; gi < 3; ++gi) {
+            const int G = Gs[gi];
+            uint32_t lb = g.hid ? id : 0;
+            for (int q = 0; q < G; ++q) {
+                uint32_t f = 0;
+                for (uint32_t w = uint32_t(q) * nw / G; w < uint32_t(q + 1) * nw / G; ++w) f |= acc[w];
+                lb += uint32_t(__builtin_popcount(f));
+            }
+            sum[gi] += lb;
+            sq[gi] += double(lb) * lb;
+        }
+    }
+    for (int gi = 0; gi < 3; ++gi) {
+        const int G = Gs[gi];
+        if ((G == 2 && nw < 4) || (G == 4 && nw < 8)) { lim[gi] = -1; continue; }
+        const double mean = sum[gi] / kSamples;
+        const double var = std::max(0.0, sq[gi] / kSamples - mean * mean);
+        lim[gi] = int32_t(std::floor(mean - 4.0 * std::sqrt(var) - 1.0));
+    }
+    if (lim[1] <= lim[0]) lim[1] = -1;
+    if (lim[2] <= std::max(lim[0], lim[1])) lim[2] = -1;
+    im.fold_cache[key] = {lim[0], lim[1], lim[2]};
 }
 
 static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe, uint32_t* yt,
@@ -1392,7 +1551,8 @@ static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe
     a.k = k; a.p = pe.plan.p; a.s = pe.plan.s; a.emin = pe.plan.emin;
     a.npiv = uint32_t(pe.plan.prefix.size() - 1);
     a.id_rows = g.id_rows; a.add_const = (g.id_rows == k) ? c : 0; a.tx = pe.plan.TX;
-    a.fold_limit = g.fold_limit;
+    sampled_fold_limits(im, uint32_t(&g - im.gammas.data()), k, c, a.fold_lim);
+    a.xtab = ensure_xtab(im, uint32_t(&g - im.gammas.data()), k, pe.plan.p - 1);
     return a;
 }
 
@@ -1701,7 +1861,7 @@ Engine::BruteResult Engine::brute_force(uint32_t k, uint32_t n, const uint64_t* 
     const uint64_t tiles = ceil_div(na, tx) * nty;
     unsigned long long* slot = im.take_slot();
     sa.ta = ta; sa.tb = tb; sa.na = na; sa.nb = nb; sa.nty = nty; sa.tx = tx;
-    sa.fold_limit = g.fold_limit;
+    fold_limits(g.n_compact, g.nw, level_density(g.rho, k / 2), sa.fold_lim);
     sa.tile_lo = 0; sa.tile_hi = tiles;
     sa.best_key = slot; sa.evaluated = slot + 1; sa.counter = slot + 2; sa.find_out = slot + 3;
     CK(cudaEventRecord(im.ev0, im.stream));
