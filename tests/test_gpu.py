@@ -330,3 +330,35 @@ def test_nccl_single_rank(mdg):
     assert res.d == case["d"]
     _check_run(res, case, "nccl1", exact=False)
     dev.close()
+
+
+def test_cli_json_record(mdg, tmp_path):
+    """`mindist mindist FILE --algorithm gpu|brute` prints the reference's JSON record
+    (cli.cpp:223-238) plus the new keys; exit code 0."""
+    import json
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "paper_1911_08963_b200", "bin", "mindist")
+    kats = {c["name"]: c for c in load_golden("kats")}
+    f = tmp_path / "golay.txt"
+    f.write_text(kats["golay_23_12"]["matrix"])
+    for alg in ("gpu", "brute"):
+        r = subprocess.run([exe, "mindist", str(f), "--algorithm", alg, "--seed", "1"],
+                           capture_output=True, text=True, timeout=120)
+        assert r.returncode == 0, r.stderr
+        rec = json.loads(r.stdout)
+        for key in ("d", "n", "k", "algorithm", "m", "k_last", "g_final", "row_additions",
+                    "combinations", "wall_seconds", "seed", "workers", "witness", "witness_ok"):
+            assert key in rec, key
+        assert rec["d"] == 7 and rec["n"] == 23 and rec["k"] == 12 and rec["witness_ok"]
+        assert rec["algorithm"] == alg
+        assert rec["witness"].count("1") == 7
+        if alg == "gpu":
+            case = kats["golay_23_12"]
+            assert rec["levels"] == case["levels"]
+            assert (rec["m"], rec["k_last"], rec["g_final"]) == (case["m"], case["k_last"],
+                                                                 case["g_final"])
+    r = subprocess.run([exe, "mindist", str(f), "--seed", "1", "--pretty", "--exact-rounds"],
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "d:             7" in r.stdout

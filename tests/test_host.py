@@ -189,3 +189,16 @@ def test_revolving_door_rank_unrank_exhaustive(mdg):
                 prev = s
             assert len(seen) == N
     assert mdg.rd_unrank(3, 0) == [0, 1, 2]
+
+
+def test_zero_and_degenerate_inputs(mdg):
+    """row_basis of the zero matrix throws (f2core.cpp:92-97) -> invalid argument, never a
+    device call; trials 0 is rejected like gamma.cpp:79-80."""
+    Z = np.zeros((3, 1), dtype=np.uint64)
+    with pytest.raises(mdg.InvalidArgument):
+        mdg.GammaSet.build(Z, 10, 10, 1)
+    G = mdg.gen_matrix(20, 5, 1, True)
+    with pytest.raises(mdg.InvalidArgument):
+        mdg.GammaSet.build(G, 20, 0, 1)
+    with pytest.raises(mdg.InvalidArgument):
+        mdg.GammaSet.compute(np.zeros((0, 1), dtype=np.uint64), 20)
