@@ -639,6 +639,7 @@ struct RdArgs {
     uint32_t k, c, id_rows, add_const, stop_at;
     uint64_t total;              // C(k, c)
     uint64_t chunk;              // ranks per task (rd_chunk)
+    uint32_t smem_binom;         // 1: the (k+1) x (c+1) binomials are staged in smem
     uint64_t task_lo, task_hi;   // chunk range
     unsigned long long* best_key;
     unsigned long long* evaluated;
@@ -646,18 +647,19 @@ struct RdArgs {
     uint32_t find_target;
 };
 
-__device__ __forceinline__ void rd_unrank_dev(const uint64_t* __restrict__ T, uint32_t c,
-                                              uint64_t rank, uint32_t* idx) {
+// T: binomial table with row stride `stride` (x-major), x <= k
+__device__ __forceinline__ void rd_unrank_dev(const uint64_t* T, uint32_t stride, uint32_t k,
+                                              uint32_t c, uint64_t rank, uint32_t* idx) {
     uint64_t r = rank;
     for (uint32_t t = c; t >= 1; --t) {
-        // smallest x >= t-1 with C(x+1, t) > r  (binary search on x in [t-1, 1023])
-        uint32_t lo = t - 1, hi = kMaxK - 1;
+        // smallest x >= t-1 with C(x+1, t) > r  (binary search on x in [t-1, k-1])
+        uint32_t lo = t - 1, hi = k - 1;
         while (lo < hi) {
             uint32_t mid = (lo + hi) >> 1;
-            if (BT(T, mid + 1, t) > r) hi = mid; else lo = mid + 1;
+            if (T[size_t(mid + 1) * stride + t] > r) hi = mid; else lo = mid + 1;
         }
         idx[t - 1] = lo;
-        r = BT(T, lo + 1, t) - 1 - r;
+        r = T[size_t(lo + 1) * stride + t] - 1 - r;
     }
 }
 
@@ -690,9 +692,20 @@ __device__ __forceinline__ bool rd_next(uint32_t* cc, uint32_t t, uint32_t& out,
 
 template <int NW, bool FIND>
 __global__ void __launch_bounds__(kRdThreads) rd_round(RdArgs a) {
-    extern __shared__ __align__(16) uint32_t srows[]; // k x NW
+    // smem: [binomials C(x, t), x <= k, t <= c (when a.smem_binom)] [k x NW rows]
+    //       [(k-1) x NW adjacent pairs]
+    extern __shared__ __align__(16) unsigned long long rd_smem[];
+    const uint32_t bstride = a.smem_binom ? a.c + 1 : kBT;
+    const size_t bwords = a.smem_binom ? size_t(a.k + 1) * bstride : 0;
+    uint64_t* sbin = reinterpret_cast<uint64_t*>(rd_smem);
+    uint32_t* srows = reinterpret_cast<uint32_t*>(rd_smem + bwords);
+    for (size_t i = threadIdx.x; i < bwords; i += blockDim.x)
+        sbin[i] = BT(a.binom, uint32_t(i / bstride), uint32_t(i % bstride));
     for (uint32_t i = threadIdx.x; i < a.k * NW; i += blockDim.x) srows[i] = a.rows[i];
+    for (uint32_t i = threadIdx.x; i + NW < a.k * NW; i += blockDim.x)
+        srows[a.k * NW + i] = a.rows[i] ^ a.rows[i + NW];
     __syncthreads();
+    const uint64_t* tbin = a.smem_binom ? sbin : a.binom;
     const uint32_t lane = threadIdx.x & 31;
     unsigned long long seen = ~0ull, done_local = 0;
     uint32_t cc[kMaxC + 1];
@@ -708,9 +721,9 @@ __global__ void __launch_bounds__(kRdThreads) rd_round(RdArgs a) {
         uint32_t best = 0xFFFFFFFFu;
         uint64_t best_rank = ~0ull;
         if (active) {
-            uint64_t r0 = chunk * a.chunk;
+            const uint64_t r0 = chunk * a.chunk;
             uint64_t r1 = umin64(r0 + a.chunk, a.total);
-            rd_unrank_dev(a.binom, a.c, r0, cc);
+            rd_unrank_dev(tbin, bstride, a.k, a.c, r0, cc);
             cc[a.c] = a.k;
             uint32_t cw[NW];
 #pragma unroll
@@ -721,20 +734,43 @@ __global__ void __launch_bounds__(kRdThreads) rd_round(RdArgs a) {
                 for (int w = 0; w < NW; ++w) cw[w] ^= srows[cc[i] * NW + w];
                 id += cc[i] < a.id_rows;
             }
+            // c_1 and c_2 live in registers: the easy step of Algorithm R (~90 % of
+            // steps) moves only c_1 to an adjacent row, one pair-table load (rows
+            // c, c+1 pre-XORed in smem); the other steps fall back to the array.
+            const bool odd = a.c & 1u;
+            uint32_t c0 = cc[0], c1 = cc[1];
+            const uint32_t* spair = srows + a.k * NW;
             for (uint64_t rk = r0;;) {
-                uint32_t w = id + a.add_const;
-#pragma unroll
-                for (int i = 0; i < NW; ++i) w += __popc(cw[i]);
+                uint32_t w = id + a.add_const + popsum<NW>(cw);
                 if (FIND) {
                     if (w == a.find_target && rk < best_rank) best_rank = rk;
                 } else {
                     best = min(best, w);
                 }
                 if (++rk >= r1) break;
+                if (!FIND && ((rk - r0) & 1023u) == 0) { // poll the bound inside long chunks
+                    unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
+                    if ((g >> kKeyShift) <= a.stop_at || (best <= a.stop_at)) {
+                        r1 = rk; // stop here; the codewords up to rk were evaluated
+                        break;
+                    }
+                }
                 uint32_t o, n;
-                rd_next(cc, a.c, o, n);
+                if (odd ? (c0 + 1 < c1) : (c0 > 0)) {
+                    o = c0;
+                    n = odd ? c0 + 1 : c0 - 1;
+                    const uint32_t lo = odd ? c0 : c0 - 1;
+                    c0 = n;
 #pragma unroll
-                for (int i = 0; i < NW; ++i) cw[i] ^= srows[o * NW + i] ^ srows[n * NW + i];
+                    for (int i = 0; i < NW; ++i) cw[i] ^= spair[lo * NW + i];
+                } else {
+                    cc[0] = c0;
+                    rd_next(cc, a.c, o, n);
+                    c0 = cc[0];
+                    c1 = cc[1];
+#pragma unroll
+                    for (int i = 0; i < NW; ++i) cw[i] ^= srows[o * NW + i] ^ srows[n * NW + i];
+                }
                 id += (n < a.id_rows) - (o < a.id_rows);
             }
             done_local += r1 - r0;
@@ -999,11 +1035,17 @@ __global__ void init_slots(unsigned long long* s, int n) {
 template <int NW, bool FIND>
 struct RdLaunchT {
     static void run(const RdArgs& a, int grid, cudaStream_t st) {
-        size_t smem = size_t(a.k) * NW * 4;
+        size_t bin = size_t(a.k + 1) * (a.c + 1) * 8;
+        size_t smem = size_t(2 * a.k) * NW * 4; // rows + adjacent pairs
+        if (smem > 227 * 1024)
+            throw std::invalid_argument("rd kernel: Gamma exceeds shared memory; use the tab kernel");
+        RdArgs b = a;
+        b.smem_binom = smem + bin <= 160 * 1024 ? 1u : 0u;
+        if (b.smem_binom) smem += bin;
         auto fn = rd_round<NW, FIND>;
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        fn<<<grid, kRdThreads, smem, st>>>(a);
+        fn<<<grid, kRdThreads, smem, st>>>(b);
     }
 };
 template <int NW, bool FIND>
@@ -1019,9 +1061,11 @@ uint32_t template_width(uint32_t nw32) {
     throw std::invalid_argument("row width exceeds the device limit (n - rank <= 1024)");
 }
 
+// ranks per revolving-door task: ~2^18 tasks (about 1.8 per resident thread),
+// 256..8192 steps each so the per-task unrank stays a small share
 uint64_t rd_chunk(uint64_t total) {
-    uint64_t chunk = 64;
-    while (chunk < 4096 && total / chunk > (uint64_t{1} << 20)) chunk *= 2;
+    uint64_t chunk = 256;
+    while (chunk < 8192 && total / chunk > (uint64_t{1} << 18)) chunk *= 2;
     return chunk;
 }
 
