@@ -230,6 +230,46 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 
+
+// Close a chained round (run_bz_loop's per-round step, engines.cpp:456-472): the fast
+// path (U <= L ends the loop, the round is not run), U = min(U, w) with the bounded-round
+// rule, and after the last Gamma of a level L = max(L, lower_bound) and L >= U -> done.
+__device__ __forceinline__ void finalize_round(ChainState* st, const unsigned long long* slot,
+                                               ChainRec* rec, uint32_t c, uint32_t j,
+                                               uint32_t last_of_level, uint32_t lb) {
+    ChainRec r{};
+    r.c = c;
+    r.j = j;
+    r.t_ns = globaltimer_ns();
+    if (st->done || st->U <= st->L) { // fast path: the round is not run, the loop ends
+        st->done = 1;
+        r.ran = 0;
+        *rec = r;
+        return;
+    }
+    const uint32_t cutoff = st->exact ? 0u : st->U;
+    unsigned long long key = *reinterpret_cast<volatile const unsigned long long*>(slot);
+    uint32_t w = key == ~0ull ? 0xFFFFFFFFu : uint32_t(key >> kKeyShift);
+    if (cutoff && (key == ~0ull || w >= cutoff)) {
+        w = cutoff;
+        key = ~0ull;
+        r.bounded = 1;
+    }
+    r.ran = 1;
+    r.w = w;
+    r.key = key;
+    r.evaluated = *reinterpret_cast<volatile const unsigned long long*>(slot + 1);
+    if (w < st->U) st->U = w;
+    r.U_after = st->U;
+    if (last_of_level) {
+        if (lb > st->L) st->L = lb;
+        r.L_after = st->L;
+        r.level_end = 1;
+        if (st->L >= st->U) st->done = 1;
+    }
+    *rec = r;
+}
+
 // chain start time stamp (device clock), read back with the records
 __global__ void chain_stamp(unsigned long long* t) {
     if (threadIdx.x == 0) *t = globaltimer_ns();
@@ -237,6 +277,10 @@ __global__ void chain_stamp(unsigned long long* t) {
 
 struct TabArgs {
     const ChainState* st;          // non-null: cutoff / stop_at / skip from the chain state
+    ChainState* fin_st;            // non-null: the last block closes the round (fused finalize)
+    ChainRec* fin_rec;
+    unsigned long long* blocks_done;
+    uint32_t fin_c, fin_j, fin_last, fin_lb;
     const uint32_t* rows;
     const uint32_t* ytab;
     const uint32_t* xtab;          // optional prefix table (colex (p-1)-subset sums)
@@ -450,14 +494,15 @@ __global__ void __launch_bounds__(kThreads, 4) tab_round(TabArgs a) {
     unsigned long long seen = ~0ull; // lane 0's view of the global best key
     unsigned long long done_local = 0;
     uint32_t cutoff = a.cutoff, stop_at = a.stop_at;
+    bool skip = false;
     if (a.st) { // chained round: the loop state decides (same values in every block)
         const ChainState cs = *a.st;
-        if (cs.done || cs.U <= cs.L) return;
+        skip = cs.done || cs.U <= cs.L;
         cutoff = cs.exact ? 0u : cs.U;
         stop_at = cs.L;
     }
 
-    for (;;) {
+    for (; !skip;) {
         if (threadIdx.x == 0) {
             // early exit: the global bound already meets stop_at
             unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
@@ -500,44 +545,22 @@ __global__ void __launch_bounds__(kThreads, 4) tab_round(TabArgs a) {
         }
         __syncthreads(); // xs / ti reused by the next tile
     }
-    if (threadIdx.x == 0 && done_local) atomicAdd(a.evaluated, done_local);
+    if (threadIdx.x == 0) {
+        if (done_local) atomicAdd(a.evaluated, done_local);
+        if (a.fin_rec) { // fused finalize: the last block to finish closes the round
+            __threadfence();
+            if (atomicAdd(a.blocks_done, 1ull) == gridDim.x - 1) {
+                __threadfence();
+                finalize_round(a.fin_st, a.best_key, a.fin_rec, a.fin_c, a.fin_j, a.fin_last, a.fin_lb);
+            }
+        }
+    }
 }
 
 // One thread: close a chained round (engines.cpp:456-472 semantics).
 __global__ void chain_finalize(ChainState* st, const unsigned long long* slot, ChainRec* rec,
                                uint32_t c, uint32_t j, uint32_t last_of_level, uint32_t lb) {
-    if (threadIdx.x != 0) return;
-    ChainRec r{};
-    r.c = c;
-    r.j = j;
-    r.t_ns = globaltimer_ns();
-    if (st->done || st->U <= st->L) { // fast path: the round is not run, the loop ends
-        st->done = 1;
-        r.ran = 0;
-        *rec = r;
-        return;
-    }
-    const uint32_t cutoff = st->exact ? 0u : st->U;
-    unsigned long long key = slot[0];
-    uint32_t w = key == ~0ull ? 0xFFFFFFFFu : uint32_t(key >> kKeyShift);
-    if (cutoff && (key == ~0ull || w >= cutoff)) {
-        w = cutoff;
-        key = ~0ull;
-        r.bounded = 1;
-    }
-    r.ran = 1;
-    r.w = w;
-    r.key = key;
-    r.evaluated = slot[1];
-    if (w < st->U) st->U = w;
-    r.U_after = st->U;
-    if (last_of_level) {
-        if (lb > st->L) st->L = lb;
-        r.L_after = st->L;
-        r.level_end = 1;
-        if (st->L >= st->U) st->done = 1;
-    }
-    *rec = r;
+    if (threadIdx.x == 0) finalize_round(st, slot, rec, c, j, last_of_level, lb);
 }
 
 // witness: the smallest (x_local, y_local) of the tile whose weight == target
@@ -1025,10 +1048,12 @@ struct TabLaunch {
 __global__ void init_slots(unsigned long long* s, int n) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
-        s[4 * i + 0] = ~0ull; // best key
-        s[4 * i + 1] = 0;     // evaluated
-        s[4 * i + 2] = 0;     // tile counter
-        s[4 * i + 3] = ~0ull; // witness search result
+        s[8 * i + 0] = ~0ull; // best key
+        s[8 * i + 1] = 0;     // evaluated
+        s[8 * i + 2] = 0;     // tile counter
+        s[8 * i + 3] = ~0ull; // witness search result
+        s[8 * i + 4] = 0;     // blocks done (fused finalize)
+        s[8 * i + 5] = s[8 * i + 6] = s[8 * i + 7] = 0;
     }
 }
 
@@ -1314,7 +1339,7 @@ struct PlanEntry {
     uint64_t* d_prefix = nullptr;
 };
 
-constexpr int kSlots = 4096; // per-round scratch slots {best key, evaluated, counter, find}
+constexpr int kSlots = 4096; // per-round scratch slots {best key, evaluated, counter, find, blocks done}
 
 struct Engine::Impl {
     cudaStream_t stream = nullptr;
@@ -1357,7 +1382,7 @@ struct Engine::Impl {
             cnt.launches += 1;
             next_slot = 0;
         }
-        return slots + 4 * size_t(next_slot++);
+        return slots + 8 * size_t(next_slot++);
     }
     void read_slot(unsigned long long* slot) {
         CK(cudaMemcpyAsync(host_slot, slot, 32, cudaMemcpyDeviceToHost, stream));
@@ -1404,7 +1429,7 @@ Engine::Engine(int device) : device_(device), impl_(new Impl) {
     const auto& T = binom_table();
     CK(cudaMalloc(&impl_->binom, T.size() * 8));
     CK(cudaMemcpy(impl_->binom, T.data(), T.size() * 8, cudaMemcpyHostToDevice));
-    CK(cudaMalloc(&impl_->slots, size_t(kSlots) * 32));
+    CK(cudaMalloc(&impl_->slots, size_t(kSlots) * 64));
     CK(cudaHostAlloc(&impl_->host_slot, 32, cudaHostAllocDefault));
     CK(cudaMalloc(&impl_->d_state, sizeof(ChainState)));
     CK(cudaHostAlloc(&impl_->h_state, sizeof(ChainState), cudaHostAllocDefault));
@@ -1829,6 +1854,16 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
             a.tile_lo = world > 1 ? T * rank / world : 0;
             a.tile_hi = world > 1 ? T * (rank + 1) / world : T;
             a.best_key = slot; a.evaluated = slot + 1; a.counter = slot + 2;
+            const bool fuse = !allreduce && a.tile_hi > a.tile_lo;
+            if (fuse) { // the round kernel's last block closes the round: one launch per round
+                a.fin_st = im.d_state;
+                a.fin_rec = im.d_recs + nrec;
+                a.blocks_done = slot + 4;
+                a.fin_c = g;
+                a.fin_j = j;
+                a.fin_last = j + 1 == m_ ? 1u : 0u;
+                a.fin_lb = lb;
+            }
             if (a.tile_hi > a.tile_lo) {
                 dispatch_nw_hid<TabLaunch>(gd.nw, gd.hid, a, a.tile_hi - a.tile_lo, im.stream, 0, size_t(0), sms_);
                 CK(cudaGetLastError());
@@ -1838,10 +1873,12 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
                 int rc = nccl().AllReduce(slot, slot, 1, kNcclUint64, kNcclMin, im.comm, im.stream);
                 if (rc != 0) throw std::runtime_error(std::string("ncclAllReduce: ") + nccl().GetErrorString(rc));
             }
-            chain_finalize<<<1, 32, 0, im.stream>>>(im.d_state, slot, im.d_recs + nrec, g, j,
-                                                    j + 1 == m_ ? 1u : 0u, lb);
-            CK(cudaGetLastError());
-            im.cnt.launches += 1;
+            if (!fuse) {
+                chain_finalize<<<1, 32, 0, im.stream>>>(im.d_state, slot, im.d_recs + nrec, g, j,
+                                                        j + 1 == m_ ? 1u : 0u, lb);
+                CK(cudaGetLastError());
+                im.cnt.launches += 1;
+            }
             ++nrec;
             pending += double(binomial(k_, g)) / world;
         }

@@ -278,7 +278,7 @@ GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint6
         for (uint32_t j = 0; j < cands[t].column_perm.size(); ++j)
             cands[t].column_perm[j] = perms[t][cands[t].column_perm[j]];
     };
-    if (uint64_t(G.rows()) * n >= 4096 && trials >= 2 && HostPool::get().size() > 1)
+    if (uint64_t(G.rows()) * n >= 1024 && trials >= 2 && HostPool::get().size() > 1)
         HostPool::get().run(trials, work);
     else
         for (uint32_t t = 0; t < trials; ++t) work(t);

@@ -362,3 +362,17 @@ def test_cli_json_record(mdg, tmp_path):
     r = subprocess.run([exe, "mindist", str(f), "--seed", "1", "--pretty", "--exact-rounds"],
                        capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "d:             7" in r.stdout
+
+
+def test_cfg4_cap7_engines_agree(mdg, device):
+    """Config 4 to level cap 7 (4.7e12 codewords; no reference golden — the reference
+    needs ~1 h on 16 cores): the tab engine (bound-pruned) and the revolving-door engine
+    (exact weights, independent enumeration order) give the same (L, U) trace."""
+    G = mdg.gen_matrix(300, 200, 11, True)
+    a = mdg.min_weight(G, 300, 10, 11, level_cap=7, kernel=mdg.KERNEL_TAB, device=device)
+    b = mdg.min_weight(G, 300, 10, 11, level_cap=7, kernel=mdg.KERNEL_RD, device=device)
+    assert a.capped and b.capped and a.d == b.d
+    assert a.levels == b.levels and a.rounds == b.rounds
+    assert a.witness_ok and b.witness_ok
+    cap6 = next(c for c in load_golden("configs_cap4_6") if c["name"] == "cfg4")
+    assert a.levels[:6] == cap6["levels"]
