@@ -29,7 +29,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libmdg.so")
+LIB_PATH = os.environ.get("MDG_LIB") or os.path.join(_HERE, "lib", "libmdg.so")  # MDG_LIB: A/B builds
 KERNEL_TAB, KERNEL_RD = 0, 1
 
 

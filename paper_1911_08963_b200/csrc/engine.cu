@@ -407,7 +407,10 @@ __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t
                                                     const uint32_t (&idY)[r_for(NW)], int32_t T) {
     constexpr int R = r_for(NW);
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
-    constexpr int GR = R >= 4 ? 4 : R; // suffixes per warp vote
+#ifndef MDG_VOTE_GROUP
+#define MDG_VOTE_GROUP 4
+#endif
+    constexpr int GR = R >= MDG_VOTE_GROUP ? MDG_VOTE_GROUP : R; // suffixes per warp vote
     uint32_t best = 0xFFFFFFFFu;
     for (uint32_t xi = x_begin; xi < nx; ++xi) {
         uint32_t X[XS];
@@ -483,8 +486,11 @@ __device__ __forceinline__ int pick_groups(int32_t T, const int32_t (&lim)[3]) {
     return 0;
 }
 
+#ifndef MDG_MINBLK_SMALL
+#define MDG_MINBLK_SMALL 5
+#endif
 template <int NW, bool HID>
-__global__ void __launch_bounds__(kThreads, 4) tab_round(TabArgs a) {
+__global__ void __launch_bounds__(kThreads, NW <= 2 ? MDG_MINBLK_SMALL : 4) tab_round(TabArgs a) {
     constexpr int R = r_for(NW);
     constexpr int YC = R * kThreads;
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
