@@ -67,7 +67,7 @@ class ClockSampler:
         try:
             self._proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self._proc = None
             return
@@ -165,7 +165,7 @@ def run_reference_arm(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mdg", choices=["mdg", "reference"])
     ap.add_argument("--kernel", default="tab", choices=["tab", "rd"])
@@ -241,11 +241,13 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # clocks sampled every 20 ms from the start of warm-up to the end of the e2e loop
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.05)
     for _ in range(args.warmup):
         device_step()
 
-    sampler = ClockSampler(local)
-    sampler.start()
     ms_steps, cw_total, launches_total, c7_cw, c7_ms = [], 0, 0, 0, 0.0
     for _ in range(args.steps):
         l2_flush()

@@ -328,6 +328,55 @@ __device__ __forceinline__ void decode_tile(const TabArgs& a, uint64_t tile, Til
     ti.nyv = uint32_t(umin64(uint64_t(YC), NY - ti.y0));
 }
 
+// decode_tile by a whole warp (all 32 lanes call it; lane 0 writes ti): the pivot search
+// reads 32 prefix entries per step instead of a dependent binary search, and the two
+// binomials load in parallel -- the short rounds of a level loop are latency-bound.
+template <int YC>
+__device__ __forceinline__ void decode_tile_warp(const TabArgs& a, uint64_t tile, TileInfo& ti) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t base = 0, lo = 0;
+    uint64_t pv = 0, pre = 0;
+    for (;;) {
+        const uint32_t i = base + lane;
+        const bool in = i < a.npiv;
+        pv = in ? __ldg(a.prefix + i) : ~0ull;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, in && pv <= tile);
+        if (m != 0xFFFFFFFFu || base + 32 >= a.npiv) {
+            if (m) { // monotone prefix sums: the set lanes are a prefix of the warp
+                lo = base + __popc(m) - 1;
+                pre = __shfl_sync(0xFFFFFFFFu, pv, __popc(m) - 1);
+            } else { // the pivot is the last entry of the previous chunk (base > 0)
+                lo = base - 1;
+                pre = __ldg(a.prefix + lo);
+            }
+            break;
+        }
+        base += 32;
+    }
+    const uint32_t e = a.emin + lo;
+    const uint64_t b = lane == 0 ? BT(a.binom, a.k - 1 - e, a.s) : lane == 1 ? BT(a.binom, e, a.p - 1) : 0;
+    const uint64_t NY = __shfl_sync(0xFFFFFFFFu, b, 0), NX = __shfl_sync(0xFFFFFFFFu, b, 1);
+    if (lane == 0) {
+        const uint64_t local = tile - pre;
+        const uint64_t nty = (NY + YC - 1) / YC;
+        const uint64_t tx = local / nty, ty = local - tx * nty;
+        ti.e = e;
+        ti.tile = tile;
+        ti.x0 = tx * a.tx;
+        ti.nx = uint32_t(umin64(uint64_t(a.tx), NX - ti.x0));
+        ti.y0 = ty * YC;
+        ti.nyv = uint32_t(umin64(uint64_t(YC), NY - ti.y0));
+    }
+}
+
+// Programmatic dependent launch (chained rounds): the prologue of round N+1 (tile decode,
+// prefix build, suffix loads -- immutable tables only) overlaps round N's tail; the
+// chain state is read after griddepcontrol.wait. No-ops without the launch attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // prefix sum for pivot e, colex rank x among (p-1)-subsets of [0, e)
 template <int NW, bool HID>
 __device__ __forceinline__ void build_prefix(const TabArgs& a, uint32_t e, uint64_t x,
@@ -500,44 +549,64 @@ __global__ void __launch_bounds__(kThreads, NW <= 2 ? MDG_MINBLK_SMALL : 4) tab_
     unsigned long long seen = ~0ull; // lane 0's view of the global best key
     unsigned long long done_local = 0;
     uint32_t cutoff = a.cutoff, stop_at = a.stop_at;
+    // First tile: static (blockIdx.x; the launch clamps the grid to the tile count), and
+    // its operands come from immutable tables only, so under PDL this prologue overlaps
+    // the previous round. Later tiles: dynamic scheduler (atomic counter).
+    if (threadIdx.x < 32) decode_tile_warp<YC>(a, a.tile_lo + blockIdx.x, ti);
+    __syncthreads();
+    if (threadIdx.x < ti.nx) build_prefix<NW, HID>(a, ti.e, ti.x0 + threadIdx.x, xs + threadIdx.x * XS);
+    uint32_t Y[R][NW], idY[R];
+    bool valid[R];
+    load_suffixes<NW, HID>(a, ti, Y, idY, valid);
     bool skip = false;
     if (a.st) { // chained round: the loop state decides (same values in every block)
+        griddep_wait();
         const ChainState cs = *a.st;
         skip = cs.done || cs.U <= cs.L;
         cutoff = cs.exact ? 0u : cs.U;
         stop_at = cs.L;
     }
+    griddep_launch_dependents();
+    const bool dynamic = a.tile_lo + gridDim.x < a.tile_hi;
+    uint32_t gw = 0xFFFFFFFFu; // thread 0: the global best weight at the last tile fetch
 
-    for (; !skip;) {
-        if (threadIdx.x == 0) {
-            // early exit: the global bound already meets stop_at
-            unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
-            uint32_t gw = uint32_t(g >> kKeyShift);
-            uint32_t stop = gw <= stop_at;
-            if (!stop) { // dynamic tile scheduler: uniform tiles, no static tail
-                uint64_t t = a.tile_lo + atomicAdd(a.counter, 1ull);
-                stop = t >= a.tile_hi;
-                if (!stop) {
-                    decode_tile<YC>(a, t, ti);
-                    done_local += uint64_t(ti.nx) * ti.nyv;
-                    // weights that still matter: <= min(cutoff - 1, best found so far)
-                    int64_t lim = cutoff ? int64_t(cutoff) - 1 : int64_t(0x7FFFFFFF);
-                    if (int64_t(gw) < lim) lim = gw;
-                    lim -= a.add_const;
-                    ti.T = lim < -1 ? -1 : (lim > 0x7FFFFFFF ? 0x7FFFFFFF : int32_t(lim));
-                    ti.G = pick_groups(ti.T, a.fold_lim);
+    for (bool first = true; !skip; first = false) {
+        if (!first) {
+            if (!dynamic) break;
+            if (threadIdx.x < 32) {
+                uint32_t stop = 0;
+                uint64_t t = 0;
+                if (lane == 0) {
+                    // early exit: the global bound already meets stop_at
+                    unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
+                    gw = uint32_t(g >> kKeyShift);
+                    stop = gw <= stop_at;
+                    if (!stop) { // dynamic tile scheduler: uniform tiles, no static tail
+                        t = a.tile_lo + gridDim.x + atomicAdd(a.counter, 1ull);
+                        stop = t >= a.tile_hi;
+                    }
                 }
+                stop = __shfl_sync(0xFFFFFFFFu, stop, 0);
+                t = __shfl_sync(0xFFFFFFFFu, t, 0);
+                if (!stop) decode_tile_warp<YC>(a, t, ti);
+                if (lane == 0) ti.stop = stop;
             }
-            ti.stop = stop;
+            __syncthreads();
+            if (ti.stop) break;
+            if (threadIdx.x < ti.nx) build_prefix<NW, HID>(a, ti.e, ti.x0 + threadIdx.x, xs + threadIdx.x * XS);
+            load_suffixes<NW, HID>(a, ti, Y, idY, valid);
+        }
+        if (threadIdx.x == 0) {
+            done_local += uint64_t(ti.nx) * ti.nyv;
+            // weights that still matter: <= min(cutoff - 1, best found so far)
+            int64_t lim = cutoff ? int64_t(cutoff) - 1 : int64_t(0x7FFFFFFF);
+            if (int64_t(gw) < lim) lim = gw;
+            lim -= a.add_const;
+            ti.T = lim < -1 ? -1 : (lim > 0x7FFFFFFF ? 0x7FFFFFFF : int32_t(lim));
+            ti.G = pick_groups(ti.T, a.fold_lim);
         }
         __syncthreads();
-        if (ti.stop) break;
         const uint64_t tile = ti.tile;
-        if (threadIdx.x < ti.nx) build_prefix<NW, HID>(a, ti.e, ti.x0 + threadIdx.x, xs + threadIdx.x * XS);
-        uint32_t Y[R][NW], idY[R];
-        bool valid[R];
-        load_suffixes<NW, HID>(a, ti, Y, idY, valid);
-        __syncthreads();
 
         uint32_t best = tile_min<NW, HID>(xs, 0, ti.nx, Y, idY, ti.T, ti.G);
         if (best != 0xFFFFFFFFu) best += a.add_const;
@@ -1023,7 +1092,9 @@ struct YtabLaunch {
 template <int NW, bool HID>
 struct TabOcc {
     static void run(int* occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, tab_round<NW, HID>, kThreads, 0);
+        static int cached = -1; // per instantiation; the kernel's resources never change
+        if (cached < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached, tab_round<NW, HID>, kThreads, 0);
+        *occ = cached;
     }
 };
 
@@ -1031,12 +1102,22 @@ template <int NW, bool HID>
 struct TabLaunch {
     // grid: number of tiles for mode 0/2 (clamped to the resident-block count)
     static void run(const TabArgs& a, uint64_t grid, cudaStream_t st, int mode, size_t dyn, int sms) {
-        if (mode == 0) {
+        if (mode == 0 || mode == 3) { // 3: programmatic dependent launch after a chained round
             int occ = 0;
             TabOcc<NW, HID>::run(&occ);
             if (occ < 1) occ = 1;
             uint64_t g = std::max<uint64_t>(1, std::min<uint64_t>(grid, uint64_t(sms) * occ));
-            tab_round<NW, HID><<<uint32_t(g), kThreads, 0, st>>>(a);
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(uint32_t(g));
+            cfg.blockDim = dim3(kThreads);
+            cfg.dynamicSmemBytes = 0;
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = mode == 3 ? 1 : 0;
+            cudaLaunchKernelEx(&cfg, tab_round<NW, HID>, a);
         }
         else if (mode == 1) tab_find<NW, HID><<<1, kThreads, 0, st>>>(a);
         else {
@@ -1427,6 +1508,7 @@ Engine::Engine(int device) : device_(device), impl_(new Impl) {
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device));
     sms_ = prop.multiProcessorCount;
+    if (const char* e = std::getenv("MDG_PDL")) pdl_ = std::atoi(e) != 0;
     CK(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&impl_->ev0));
     CK(cudaEventCreate(&impl_->ev1));
@@ -1836,6 +1918,8 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
     im.cnt.launches += 1;
     uint32_t g = 1;
     bool done = init.done != 0;
+    uint64_t after_round = ~0ull; // launch count right after the last round launch
+    bool synced = false;          // a host copy was enqueued since that launch
     while (!done && g <= k_) {
         if (level_cap && g > level_cap) break;
         bool too_big = g > kMaxC;
@@ -1845,6 +1929,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
         if (too_big) { // the host loop would raise here only if it gets here
             CK(cudaMemcpyAsync(im.h_state, im.d_state, sizeof(ChainState), cudaMemcpyDeviceToHost, im.stream));
             CK(cudaStreamSynchronize(im.stream));
+            synced = true;
             if (im.h_state->done) { done = true; break; }
             check_round(0, g); // throws the reference's error for this level
         }
@@ -1871,9 +1956,14 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
                 a.fin_lb = lb;
             }
             if (a.tile_hi > a.tile_lo) {
-                dispatch_nw_hid<TabLaunch>(gd.nw, gd.hid, a, a.tile_hi - a.tile_lo, im.stream, 0, size_t(0), sms_);
+                // PDL only when the previous stream operation is this chain's previous round
+                // kernel (a table build or slot reset in between must complete first)
+                const int mode = fuse && pdl_ && im.cnt.launches == after_round && !synced ? 3 : 0;
+                dispatch_nw_hid<TabLaunch>(gd.nw, gd.hid, a, a.tile_hi - a.tile_lo, im.stream, mode, size_t(0), sms_);
                 CK(cudaGetLastError());
                 im.cnt.launches += 1;
+                after_round = im.cnt.launches;
+                synced = false;
             }
             if (allreduce) {
                 int rc = nccl().AllReduce(slot, slot, 1, kNcclUint64, kNcclMin, im.comm, im.stream);
@@ -1893,6 +1983,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
             CK(cudaMemcpyAsync(im.h_state, im.d_state, sizeof(ChainState), cudaMemcpyDeviceToHost, im.stream));
             CK(cudaStreamSynchronize(im.stream));
             im.cnt.d2h += sizeof(ChainState);
+            synced = true;
             done = im.h_state->done != 0;
             pending = 0;
         }

@@ -376,3 +376,10 @@ def test_cfg4_cap7_engines_agree(mdg, device):
     assert a.witness_ok and b.witness_ok
     cap6 = next(c for c in load_golden("configs_cap4_6") if c["name"] == "cfg4")
     assert a.levels[:6] == cap6["levels"]
+
+
+@pytest.mark.gpu
+def test_graft_smoke():
+    """The driver's smoke() (config 1 in exact and bounded round modes + a config-5 histogram)."""
+    import __graft_entry__
+    __graft_entry__.smoke()
