@@ -506,10 +506,10 @@ __device__ __forceinline__ uint32_t tile_min(const uint32_t* xs, uint32_t x_begi
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
     if (T < 0) return 0xFFFFFFFFu; // every codeword here is above the bound
     if (G == 1) return tile_min_pruned<NW, HID, 1>(xs, x_begin, nx, Y, idY, T);
-    if constexpr (NW >= 4) {
+    if constexpr (NW >= 3) {
         if (G == 2) return tile_min_pruned<NW, HID, 2>(xs, x_begin, nx, Y, idY, T);
     }
-    if constexpr (NW >= 8) {
+    if constexpr (NW >= 5) {
         if (G == 4) return tile_min_pruned<NW, HID, 4>(xs, x_begin, nx, Y, idY, T);
     }
     uint32_t best = 0xFFFFFFFFu;
@@ -1381,12 +1381,12 @@ private:
 // codeword bit density rho_c, a fold bit over m words is set with probability
 // 1 - (1 - rho_c)^m, so popc(folds) ~ mean E_G, variance V_G; pruning with G groups
 // is worth it while the bound T <= E_G - 4 sqrt(V_G) (then almost no codeword passes).
-// G must not exceed the word count it splits (G=2 needs NW >= 4, G=4 needs NW >= 8).
+// G must leave some group with two or more words (G=2 needs NW >= 3, G=4 needs NW >= 5).
 static void fold_limits(uint32_t bits, uint32_t nw, double rho_c, int32_t (&lim)[3]) {
     const int Gs[3] = {1, 2, 4};
     for (int gi = 0; gi < 3; ++gi) {
         const int G = Gs[gi];
-        if ((G == 2 && nw < 4) || (G == 4 && nw < 8)) { lim[gi] = -1; continue; }
+        if ((G == 2 && nw < 3) || (G == 4 && nw < 5)) { lim[gi] = -1; continue; }
         double mean = 0, var = 0;
         for (int g = 0; g < G; ++g) {
             const uint32_t b = uint32_t(g) * nw / G, e = uint32_t(g + 1) * nw / G;
@@ -1691,7 +1691,7 @@ static void sampled_fold_limits(Engine::Impl& im, uint32_t j, uint32_t k, uint32
     }
     for (int gi = 0; gi < 3; ++gi) {
         const int G = Gs[gi];
-        if ((G == 2 && nw < 4) || (G == 4 && nw < 8)) { lim[gi] = -1; continue; }
+        if ((G == 2 && nw < 3) || (G == 4 && nw < 5)) { lim[gi] = -1; continue; }
         const double mean = sum[gi] / kSamples;
         const double var = std::max(0.0, sq[gi] / kSamples - mean * mean);
         lim[gi] = int32_t(std::floor(mean - 4.0 * std::sqrt(var) - 1.0));
