@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -286,6 +287,7 @@ struct TabArgs {
     const uint32_t* xtab;          // optional prefix table (colex (p-1)-subset sums)
     const uint64_t* binom;
     const uint64_t* prefix;
+    const uint8_t* tr;             // per pivot: 1 = transposed tiles (null: none)
     uint32_t k, p, s, emin, npiv, id_rows, add_const, stop_at, tx;
     uint32_t cutoff;               // only weights < cutoff matter (0 = exact round)
     int32_t fold_lim[3];           // G = 1, 2, 4 fold groups usable while T <= fold_lim (host)
@@ -299,8 +301,13 @@ struct TabArgs {
     unsigned long long* hist;      // tab_hist only
 };
 
+// A tile of pivot e is an (smem side) x (register side) block of codewords. Normal
+// orientation: smem side = prefixes (row e ^ (p-1)-subset sums), register side = suffixes
+// from the suffix table. Transposed (tr = 1, pivots whose suffix range is shorter than a
+// register tile): smem side = suffixes, register side = prefixes -- no masked lanes.
+// x0/nx: smem-side start/count (<= TX); y0/nyv: register-side start/count (<= YC).
 struct TileInfo {
-    uint32_t e, nx, nyv, stop;
+    uint32_t e, nx, nyv, stop, tr;
     uint64_t x0, y0, tile;
     int32_t T;                     // pruning bound on the compacted weight (inclusive)
     int32_t G;                     // stage-1 fold groups for T (0 = exact weights)
@@ -317,15 +324,18 @@ __device__ __forceinline__ void decode_tile(const TabArgs& a, uint64_t tile, Til
     uint32_t e = a.emin + lo;
     uint64_t local = tile - __ldg(a.prefix + lo);
     uint64_t NY = BT(a.binom, a.k - 1 - e, a.s);
-    uint64_t nty = (NY + YC - 1) / YC;
-    uint64_t tx = local / nty, ty = local - tx * nty;
     uint64_t NX = BT(a.binom, e, a.p - 1);
+    const uint32_t tr = a.tr ? __ldg(a.tr + lo) : 0u;
+    const uint64_t A = tr ? NY : NX, B = tr ? NX : NY; // smem side, register side
+    uint64_t ntb = (B + YC - 1) / YC;
+    uint64_t ta = local / ntb, tb = local - ta * ntb;
     ti.e = e;
+    ti.tr = tr;
     ti.tile = tile;
-    ti.x0 = tx * a.tx;
-    ti.nx = uint32_t(umin64(uint64_t(a.tx), NX - ti.x0));
-    ti.y0 = ty * YC;
-    ti.nyv = uint32_t(umin64(uint64_t(YC), NY - ti.y0));
+    ti.x0 = ta * a.tx;
+    ti.nx = uint32_t(umin64(uint64_t(a.tx), A - ti.x0));
+    ti.y0 = tb * YC;
+    ti.nyv = uint32_t(umin64(uint64_t(YC), B - ti.y0));
 }
 
 // decode_tile by a whole warp (all 32 lanes call it; lane 0 writes ti): the pivot search
@@ -354,18 +364,23 @@ __device__ __forceinline__ void decode_tile_warp(const TabArgs& a, uint64_t tile
         base += 32;
     }
     const uint32_t e = a.emin + lo;
-    const uint64_t b = lane == 0 ? BT(a.binom, a.k - 1 - e, a.s) : lane == 1 ? BT(a.binom, e, a.p - 1) : 0;
+    const uint64_t b = lane == 0 ? BT(a.binom, a.k - 1 - e, a.s)
+                     : lane == 1 ? BT(a.binom, e, a.p - 1)
+                     : lane == 2 ? uint64_t(a.tr ? __ldg(a.tr + lo) : 0u) : 0;
     const uint64_t NY = __shfl_sync(0xFFFFFFFFu, b, 0), NX = __shfl_sync(0xFFFFFFFFu, b, 1);
+    const uint32_t tr = uint32_t(__shfl_sync(0xFFFFFFFFu, b, 2));
     if (lane == 0) {
+        const uint64_t A = tr ? NY : NX, B = tr ? NX : NY; // smem side, register side
         const uint64_t local = tile - pre;
-        const uint64_t nty = (NY + YC - 1) / YC;
-        const uint64_t tx = local / nty, ty = local - tx * nty;
+        const uint64_t ntb = (B + YC - 1) / YC;
+        const uint64_t ta = local / ntb, tb = local - ta * ntb;
         ti.e = e;
+        ti.tr = tr;
         ti.tile = tile;
-        ti.x0 = tx * a.tx;
-        ti.nx = uint32_t(umin64(uint64_t(a.tx), NX - ti.x0));
-        ti.y0 = ty * YC;
-        ti.nyv = uint32_t(umin64(uint64_t(YC), NY - ti.y0));
+        ti.x0 = ta * a.tx;
+        ti.nx = uint32_t(umin64(uint64_t(a.tx), A - ti.x0));
+        ti.y0 = tb * YC;
+        ti.nyv = uint32_t(umin64(uint64_t(YC), B - ti.y0));
     }
 }
 
@@ -408,6 +423,23 @@ __device__ __forceinline__ void build_prefix(const TabArgs& a, uint32_t e, uint6
     for (int w = 0; w < XS; ++w) dst[w] = w < NW ? acc[w] : (HID && w == NW ? id : 0u);
 }
 
+// smem-side item t of the tile: a prefix (normal) or a suffix-table entry (transposed)
+template <int NW, bool HID>
+__device__ __forceinline__ void build_smem_item(const TabArgs& a, const TileInfo& ti, uint32_t t,
+                                                uint32_t* dst) {
+    constexpr int XS = stride_for(NW + (HID ? 1 : 0));
+    if (!ti.tr) {
+        build_prefix<NW, HID>(a, ti.e, ti.x0 + t, dst);
+        return;
+    }
+    uint32_t v[XS];
+    vload_global<XS>(a.ytab + (ti.x0 + t) * XS, v);
+#pragma unroll
+    for (int w = 0; w < XS; ++w) dst[w] = v[w];
+}
+
+// register side of the tile: R entries per thread (lane-interleaved); lanes past nyv
+// duplicate entry y0 and are flagged invalid
 template <int NW, bool HID>
 __device__ __forceinline__ void load_suffixes(const TabArgs& a, const TileInfo& ti,
                                               uint32_t (&Y)[r_for(NW)][NW],
@@ -416,6 +448,23 @@ __device__ __forceinline__ void load_suffixes(const TabArgs& a, const TileInfo& 
     constexpr int R = r_for(NW);
     constexpr int YS = stride_for(NW + (HID ? 1 : 0));
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (ti.tr) { // prefixes: row e ^ prefix-table entry (the plan only transposes with a table)
+        uint32_t row[NW];
+        load_row<NW>(a.rows, ti.e, row);
+        const uint32_t id_e = ti.e < a.id_rows;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            uint32_t yl = r * kThreads + warp * 32 + lane;
+            valid[r] = yl < ti.nyv;
+            uint64_t x = ti.y0 + (valid[r] ? yl : 0u);
+            uint32_t v[YS];
+            vload_global<YS>(a.xtab + x * YS, v);
+#pragma unroll
+            for (int w = 0; w < NW; ++w) Y[r][w] = row[w] ^ v[w];
+            idY[r] = HID ? id_e + v[NW] : 0u;
+        }
+        return;
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         uint32_t yl = r * kThreads + warp * 32 + lane;
@@ -554,7 +603,7 @@ __global__ void __launch_bounds__(kThreads, NW <= 2 ? MDG_MINBLK_SMALL : 4) tab_
     // the previous round. Later tiles: dynamic scheduler (atomic counter).
     if (threadIdx.x < 32) decode_tile_warp<YC>(a, a.tile_lo + blockIdx.x, ti);
     __syncthreads();
-    if (threadIdx.x < ti.nx) build_prefix<NW, HID>(a, ti.e, ti.x0 + threadIdx.x, xs + threadIdx.x * XS);
+    if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(a, ti, threadIdx.x, xs + threadIdx.x * XS);
     uint32_t Y[R][NW], idY[R];
     bool valid[R];
     load_suffixes<NW, HID>(a, ti, Y, idY, valid);
@@ -593,7 +642,7 @@ __global__ void __launch_bounds__(kThreads, NW <= 2 ? MDG_MINBLK_SMALL : 4) tab_
             }
             __syncthreads();
             if (ti.stop) break;
-            if (threadIdx.x < ti.nx) build_prefix<NW, HID>(a, ti.e, ti.x0 + threadIdx.x, xs + threadIdx.x * XS);
+            if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(a, ti, threadIdx.x, xs + threadIdx.x * XS);
             load_suffixes<NW, HID>(a, ti, Y, idY, valid);
         }
         if (threadIdx.x == 0) {
@@ -649,7 +698,7 @@ __global__ void __launch_bounds__(kThreads) tab_find(TabArgs a) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) decode_tile<YC>(a, a.tile_lo, ti);
     __syncthreads();
-    if (threadIdx.x < ti.nx) build_prefix<NW, HID>(a, ti.e, ti.x0 + threadIdx.x, xs + threadIdx.x * XS);
+    if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(a, ti, threadIdx.x, xs + threadIdx.x * XS);
     uint32_t Y[R][NW], idY[R];
     bool valid[R];
     load_suffixes<NW, HID>(a, ti, Y, idY, valid);
@@ -698,7 +747,7 @@ __global__ void __launch_bounds__(kThreads) tab_hist(TabArgs a) {
         }
         __syncthreads();
         if (ti.stop) break;
-        if (threadIdx.x < ti.nx) build_prefix<NW, HID>(a, ti.e, ti.x0 + threadIdx.x, xs + threadIdx.x * XS);
+        if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(a, ti, threadIdx.x, xs + threadIdx.x * XS);
         uint32_t Y[R][NW], idY[R];
         bool valid[R];
         load_suffixes<NW, HID>(a, ti, Y, idY, valid);
@@ -1209,23 +1258,55 @@ static inline uint64_t hb(uint32_t x, uint32_t t) {
     return binomial(x, t);
 }
 
-// total cost in codeword-slots: masked suffix lanes + a per-tile overhead
+// the prefix table ((p-1)-subset sums) exists when it is non-empty and <= 4M entries
+static bool xtab_ok(uint32_t k, uint32_t pm1) { return pm1 >= 1 && hb(k, pm1) <= (uint64_t{1} << 22); }
+
+// MDG_TRANSPOSE=0 disables transposed tiles (A/B switch)
+static bool transpose_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("MDG_TRANSPOSE");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    return on;
+}
+
+// Orientation of pivot e's tiles: transposed (suffixes in smem, prefixes in registers)
+// when that masks fewer register lanes; needs the prefix table.
+static bool pivot_transposed(uint64_t NX, uint64_t NY, uint32_t YC, bool can) {
+    if (!can) return false;
+    const uint64_t waste_n = NX * (ceil_div(NY, YC) * YC - NY);
+    const uint64_t waste_t = NY * (ceil_div(NX, YC) * YC - NX);
+    return waste_t < waste_n;
+}
+
+// per-tile overhead of the cost model, in prefix rows (MDG_TILE_OVERHEAD)
+static uint64_t tile_overhead() {
+    static const uint64_t v = [] {
+        const char* e = std::getenv("MDG_TILE_OVERHEAD");
+        return e ? uint64_t(std::max(0, std::atoi(e))) : uint64_t(4);
+    }();
+    return v;
+}
+
+// total cost in codeword-slots: masked register lanes + a per-tile overhead
 static uint64_t plan_cost(uint32_t k, uint32_t c, uint32_t s, uint32_t TX, uint32_t YC,
                           uint64_t* tiles_out) {
     uint32_t p = c - s;
+    const bool can = transpose_enabled() && xtab_ok(k, p - 1);
     uint64_t cost = 0, tiles = 0;
     for (uint32_t e = p - 1; e + s <= k - 1; ++e) {
         uint64_t NX = hb(e, p - 1), NY = hb(k - 1 - e, s);
+        if (pivot_transposed(NX, NY, YC, can)) std::swap(NX, NY);
         uint64_t ntx = ceil_div(NX, TX), nty = ceil_div(NY, YC);
         tiles += ntx * nty;
-        cost += NX * nty * YC + ntx * nty * uint64_t(YC) * 24;
+        cost += NX * nty * YC + ntx * nty * uint64_t(YC) * tile_overhead();
     }
     if (tiles_out) *tiles_out = tiles;
     return cost;
 }
 
 // Suffix size s minimizes the tile cost (suffix table <= 4M entries); the
-// prefix chunk TX is the largest of 256/128/64/32/16 that still yields >= 16
+// prefix chunk TX is the largest of 256/128/64/32/16 that still yields >= 4
 // tiles per resident block, so the dynamic scheduler's tail stays short.
 TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_blocks) {
     TabPlan pl;
@@ -1241,6 +1322,10 @@ TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_b
             if (cost < best_cost) { best_cost = cost; best_s = s; }
         }
     }
+    if (const char* e = std::getenv("MDG_FORCE_S")) { // development: fixed suffix size
+        const int fs = std::atoi(e);
+        if (fs >= 1 && uint32_t(fs) < c) best_s = uint32_t(fs);
+    }
     pl.s = best_s;
     pl.p = c - best_s;
     pl.emin = pl.p - 1;
@@ -1248,7 +1333,7 @@ TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_b
     // tuning knobs (defaults measured on B200): tiles per resident block, smallest chunk
     static const uint32_t kTilesPerBlock = [] {
         const char* e = std::getenv("MDG_TILES_PER_BLOCK");
-        return e ? uint32_t(std::max(1, std::atoi(e))) : 16u;
+        return e ? uint32_t(std::max(1, std::atoi(e))) : 8u;
     }();
     static const uint32_t kMinTX = [] {
         const char* e = std::getenv("MDG_MIN_TX");
@@ -1260,10 +1345,21 @@ TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_b
         plan_cost(k, c, pl.s, tx, pl.YC, &tiles);
         if (tiles >= uint64_t(resident_blocks) * kTilesPerBlock || tx <= kMinTX) { pl.TX = tx; break; }
     }
+    const bool can = transpose_enabled() && xtab_ok(k, pl.p - 1);
     pl.prefix.assign(1, 0);
+    pl.tr.clear();
     for (uint32_t e = pl.emin; e <= pl.emax; ++e) {
         uint64_t NX = hb(e, pl.p - 1), NY = hb(k - 1 - e, pl.s);
+        const bool tr = pivot_transposed(NX, NY, pl.YC, can);
+        pl.tr.push_back(tr ? 1 : 0);
+        if (tr) std::swap(NX, NY);
         pl.prefix.push_back(pl.prefix.back() + ceil_div(NX, pl.TX) * ceil_div(NY, pl.YC));
+    }
+    if (std::getenv("MDG_PLAN_DEBUG")) {
+        size_t ntr = 0;
+        for (uint8_t t : pl.tr) ntr += t;
+        std::fprintf(stderr, "[mdg plan] k=%u c=%u nw=%u s=%u TX=%u YC=%u tiles=%llu transposed_pivots=%zu/%zu\n",
+                     k, c, nw32, pl.s, pl.TX, pl.YC, (unsigned long long)pl.tiles(), ntr, pl.tr.size());
     }
     return pl;
 }
@@ -1283,10 +1379,12 @@ void tab_decode(const TabPlan& pl, uint64_t tile, uint32_t x_local, uint32_t y_l
     uint32_t i = uint32_t(std::upper_bound(pl.prefix.begin(), pl.prefix.end(), tile) - pl.prefix.begin()) - 1;
     uint32_t e = pl.emin + i;
     uint64_t local = tile - pl.prefix[i];
-    uint64_t NY = hb(pl.k - 1 - e, pl.s);
-    uint64_t nty = ceil_div(NY, pl.YC);
-    uint64_t tx = local / nty, ty = local % nty;
-    uint64_t x = tx * pl.TX + x_local, y = ty * pl.YC + y_local;
+    const bool tr = !pl.tr.empty() && pl.tr[i];
+    uint64_t B = tr ? hb(e, pl.p - 1) : hb(pl.k - 1 - e, pl.s); // register side
+    uint64_t ntb = ceil_div(B, pl.YC);
+    uint64_t ta = local / ntb, tb = local % ntb;
+    uint64_t sm = ta * pl.TX + x_local, rg = tb * pl.YC + y_local; // smem / register index
+    uint64_t x = tr ? rg : sm, y = tr ? sm : rg;                   // prefix / suffix index
     std::vector<uint32_t> out;
     std::vector<uint32_t> tmp(pl.c + 1);
     if (pl.p > 1) colex_unrank_host(x, pl.p - 1, e, tmp.data());
@@ -1424,6 +1522,7 @@ struct GammaDev {
 struct PlanEntry {
     TabPlan plan;
     uint64_t* d_prefix = nullptr;
+    uint8_t* d_tr = nullptr; // per-pivot orientation (null: all normal)
 };
 
 constexpr int kSlots = 4096; // per-round scratch slots {best key, evaluated, counter, find, blocks done}
@@ -1491,11 +1590,17 @@ struct Engine::Impl {
         if (it != plans.end()) return it->second;
         PlanEntry pe;
         pe.plan = make_tab_plan(k, c, g.nw, uint32_t(resident(g.nw, g.hid, sms)));
-        pe.d_prefix = static_cast<uint64_t*>(plan_arena.alloc(pe.plan.prefix.size() * 8));
-        CK(cudaMemcpyAsync(pe.d_prefix, pe.plan.prefix.data(), pe.plan.prefix.size() * 8,
-                           cudaMemcpyHostToDevice, stream));
+        const size_t pb = pe.plan.prefix.size() * 8, tb = pe.plan.tr.size();
+        pe.d_prefix = static_cast<uint64_t*>(plan_arena.alloc(pb + tb));
+        CK(cudaMemcpyAsync(pe.d_prefix, pe.plan.prefix.data(), pb, cudaMemcpyHostToDevice, stream));
+        bool any_tr = false;
+        for (uint8_t t : pe.plan.tr) any_tr = any_tr || t;
+        if (any_tr) {
+            pe.d_tr = reinterpret_cast<uint8_t*>(pe.d_prefix) + pb;
+            CK(cudaMemcpyAsync(pe.d_tr, pe.plan.tr.data(), tb, cudaMemcpyHostToDevice, stream));
+        }
         CK(cudaStreamSynchronize(stream));
-        cnt.h2d += pe.plan.prefix.size() * 8;
+        cnt.h2d += pb + (any_tr ? tb : 0);
         return plans.emplace(key, pe).first->second;
     }
 };
@@ -1704,7 +1809,7 @@ static void sampled_fold_limits(Engine::Impl& im, uint32_t j, uint32_t k, uint32
 static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe, uint32_t* yt,
                         uint32_t k, uint32_t c) {
     TabArgs a{};
-    a.rows = g.rows; a.ytab = yt; a.binom = im.binom; a.prefix = pe.d_prefix;
+    a.rows = g.rows; a.ytab = yt; a.binom = im.binom; a.prefix = pe.d_prefix; a.tr = pe.d_tr;
     a.k = k; a.p = pe.plan.p; a.s = pe.plan.s; a.emin = pe.plan.emin;
     a.npiv = uint32_t(pe.plan.prefix.size() - 1);
     a.id_rows = g.id_rows; a.add_const = (g.id_rows == k) ? c : 0; a.tx = pe.plan.TX;

@@ -42,6 +42,7 @@ struct TabPlan {
     uint32_t k = 0, c = 0, p = 0, s = 0, emin = 0, emax = 0;
     uint32_t TX = 0, YC = 0;
     std::vector<uint64_t> prefix; // tiles before pivot emin + i; size npiv + 1
+    std::vector<uint8_t> tr;      // per pivot: 1 = transposed tiles (suffixes in smem)
     uint64_t tiles() const { return prefix.empty() ? 0 : prefix.back(); }
 };
 
