@@ -1306,7 +1306,7 @@ static uint64_t plan_cost(uint32_t k, uint32_t c, uint32_t s, uint32_t TX, uint3
 }
 
 // Suffix size s minimizes the tile cost (suffix table <= 4M entries); the
-// prefix chunk TX is the largest of 256/128/64/32/16 that still yields >= 4
+// prefix chunk TX is the largest of 256/128/64/32/16 that still yields >= 8
 // tiles per resident block, so the dynamic scheduler's tail stays short.
 TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_blocks) {
     TabPlan pl;
