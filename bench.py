@@ -5,14 +5,16 @@ codes, G = (I_64 | A), A from mt19937_64 seeds 1..8; one
 step = the full Brouwer–Zimmermann run to termination (exact d) of all eight
 codes. Metric: codewords evaluated per second (BASELINE.json `metric`).
 
-* value  — device-resident: the level loop over Gamma sets already in HBM
-           (mdg_bz_loop_device), timed with CUDA events on the engine stream
-           around each whole loop (host gaps between rounds included); summed
-           codewords / summed time, max over ranks for the time.
-* e2e    — the public front door mdg_min_weight from host matrices: row basis +
+* value  — device-resident: the level loops over Gamma sets already in HBM
+           (mdg_bz_loop_device, one context per code, --streams codes in flight
+           on one GPU), CUDA events around each whole step (host gaps
+           included); codewords / time, max over ranks for the time.
+* e2e    — the public front door from host matrices (mdg_min_weight_batch on
+           one GPU, mdg_min_weight_dist per code across ranks): row basis +
            Gamma search on the host, H2D of the Gammas, the device loop, D2H of
            every round result and the witness; CUDA-event timed the same way.
-* roofline — the dominant kernel (tab_round on the c = 7 rounds): achieved
+* roofline — the dominant kernel (tab_round on the c = 7 rounds, measured in a
+           separate pass with one loop at a time): achieved
            codewords/s vs the POPC issue-rate roofline measured on B200
            (profiles/pipes_microbench.jsonl: 4642 Gpopc/s = 16 POPC/clk/SM).
 * cpu_baseline — the reference's own engine (oracle/_ref, unmodified sources)
@@ -170,6 +172,9 @@ def main():
     ap.add_argument("--impl", default="mdg", choices=["mdg", "reference"])
     ap.add_argument("--kernel", default="tab", choices=["tab", "rd"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=4,
+                    help="codes in flight at once on one GPU (value: threads over resident "
+                         "contexts; e2e: mdg_min_weight_batch)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "mdg":
         args.warmup = 3
@@ -211,24 +216,44 @@ def main():
     for d, gs in zip(devs, gsets):
         d.load_gset(gs)
 
+    from concurrent.futures import ThreadPoolExecutor
+    pool = ThreadPoolExecutor(max_workers=max(1, args.streams))
+
+    def one_loop(i):
+        d, gs = devs[i], gsets[i]
+        if world > 1:
+            r = d.bz_loop(gs, kernel=kernel, rank=rank, world=world, reduce_min="nccl")
+        else:
+            r = d.bz_loop(gs, kernel=kernel)
+        if r.d != expect_d[i] or not r.witness_ok:
+            raise SystemExit(f"parity failure on seed {SEEDS[i]}: d={r.d} expected {expect_d[i]}")
+        return r
+
     def device_step():
-        tot_ms, tot_cw, launches = 0.0, 0, 0
+        """All eight level loops over the resident Gamma sets: with --streams > 1 (single
+        GPU) up to that many codes run at once, each context on its own stream (ctypes
+        releases the GIL); CUDA events on the torch stream bracket the whole step."""
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        if world > 1 or args.streams <= 1:
+            runs = [one_loop(i) for i in range(len(devs))]
+        else:
+            runs = list(pool.map(one_loop, range(len(devs))))
+        ev1.record()
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1), sum(r.evaluated for r in runs), sum(r.launches for r in runs)
+
+    def kernel_pass():
+        """The dominant kernel alone (roofline): level-7 rounds of each code, loops run one
+        after another so every launch has the GPU to itself."""
         c7_cw, c7_ms = 0, 0.0
-        for i, (d, gs) in enumerate(zip(devs, gsets)):
-            if world > 1:
-                r = d.bz_loop(gs, kernel=kernel, rank=rank, world=world, reduce_min="nccl")
-            else:
-                r = d.bz_loop(gs, kernel=kernel)
-            if r.d != expect_d[i] or not r.witness_ok:
-                raise SystemExit(f"parity failure on seed {SEEDS[i]}: d={r.d} expected {expect_d[i]}")
-            tot_ms += r.loop_seconds * 1e3
-            tot_cw += r.evaluated
-            launches += r.launches
+        for i in range(len(devs)):
+            r = one_loop(i)
             for (c, j, w, U), ev, ms in zip(r.rounds, r.round_evaluated, r.round_ms):
                 if c == 7:
                     c7_cw += ev
                     c7_ms += ms
-        return tot_ms, tot_cw, launches, c7_cw, c7_ms
+        return c7_cw, c7_ms
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=f"cuda:{local}")
 
@@ -248,44 +273,50 @@ def main():
     for _ in range(args.warmup):
         device_step()
 
-    ms_steps, cw_total, launches_total, c7_cw, c7_ms = [], 0, 0, 0, 0.0
+    ms_steps, cw_total, launches_total = [], 0, 0
     for _ in range(args.steps):
         l2_flush()
         barrier()
-        ms, cw, ln, a, b = device_step()
+        ms, cw, ln = device_step()
         barrier()
         ms_steps.append(ms)
         cw_total += cw
         launches_total += ln
+    c7_cw, c7_ms = 0, 0.0
+    for _ in range(max(1, min(args.steps, 3))):
+        l2_flush()
+        barrier()
+        a, b = kernel_pass()
         c7_cw += a
         c7_ms += b
 
-    # e2e through the public front door from host buffers (pinned copies of G)
+    # e2e through the public front door from host buffers (pinned copies of G): the batch
+    # call (mdg_min_weight_batch, --streams codes in flight) on one GPU, mdg_min_weight_dist
+    # per code across ranks; CUDA events on the torch stream bracket each step
     e2e_ms, e2e_cw, h2d, d2h = [], 0, 0, 0
     Gpin = [torch.from_numpy(G).pin_memory().numpy() for G in Gs]
     for step in range(args.warmup + args.steps):
         l2_flush()
         barrier()
-        t_ms, t_cw = 0.0, 0
-        for i, G in enumerate(Gpin):
-            d = devs[i]
-            d.timer_start()
-            if world > 1:
-                r = mdg.min_weight_dist(G, N, rank, world, "nccl", trials=10, seed=SEEDS[i],
-                                        kernel=kernel, device=d)
-            else:
-                r = mdg.min_weight(G, N, trials=10, seed=SEEDS[i], kernel=kernel, device=d)
-            t_ms += d.timer_stop()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        if world > 1:
+            runs = [mdg.min_weight_dist(G, N, rank, world, "nccl", trials=10, seed=SEEDS[i],
+                                        kernel=kernel, device=devs[i]) for i, G in enumerate(Gpin)]
+        else:
+            runs = mdg.min_weight_batch(Gpin, N, trials=10, seed=SEEDS, kernel=kernel,
+                                        device=devs[0], streams=args.streams)
+        ev1.record()
+        torch.cuda.synchronize()
+        for i, r in enumerate(runs):
             if r.d != expect_d[i] or not r.witness_ok:
                 raise SystemExit(f"e2e parity failure on seed {SEEDS[i]}")
-            t_cw += r.evaluated
-            if step >= args.warmup:
-                h2d += r.h2d_bytes
-                d2h += r.d2h_bytes
         barrier()
         if step >= args.warmup:
-            e2e_ms.append(t_ms)
-            e2e_cw += t_cw
+            e2e_ms.append(ev0.elapsed_time(ev1))
+            e2e_cw += sum(r.evaluated for r in runs)
+            h2d += sum(r.h2d_bytes for r in runs)
+            d2h += sum(r.d2h_bytes for r in runs)
     clocks = sampler.stop()
 
     # max over ranks of time, sum over ranks of codewords
@@ -348,15 +379,19 @@ def main():
             "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (mt19937_64 seeds 1..8, SURVEY.md §8d)",
             "config": {"workload": WORKLOAD, "kernel": args.kernel,
-                       "parallelism": f"rank-range split x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"rank-range split x{world}" if world > 1 else
+                                       f"single GPU, {min(args.streams, len(SEEDS))} codes in flight"),
                        "l2": "flushed between steps (256 MiB write); working set < 1 MiB",
                        "codewords_per_step": cw_total // args.steps,
-                       "time_to_d_ms_per_code": tot_ms / args.steps / len(SEEDS),
+                       "ms_per_code_amortized": tot_ms / args.steps / len(SEEDS),
                        "d": expect_d},
             "e2e": {"value": e2e_value, "unit": "cw/s", "h2d_bytes_per_step": h2d // args.steps,
                     "d2h_bytes_per_step": d2h // args.steps,
                     "ms_per_step": tot_e2e / args.steps,
-                    "path": "mdg_min_weight (C ABI) from pinned host matrices: Gamma search + H2D + loop + D2H"},
+                    "path": ("mdg_min_weight_dist per code (C ABI)" if world > 1 else
+                             "mdg_min_weight_batch (C ABI)") +
+                            " from pinned host matrices: row basis + Gamma search + H2D + level loop"
+                            " + witness + D2H"},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "clocks": clocks,

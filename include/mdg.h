@@ -168,6 +168,20 @@ void mdg_config_default(mdg_config* cfg);
 int mdg_min_weight(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n, const mdg_config* cfg,
                    mdg_run** out);
 
+/* Batch front door: mdg_min_weight for `count` codes (code i: k[i] rows of
+ * n[i] bits at G[i], the mdg_parse_matrix packing, configuration cfg[i]; cfg
+ * NULL = mdg_config_default for all) on ctx's device. Up to
+ * `streams` codes are in flight at once, each on its own engine and CUDA
+ * stream: one code's host Gamma search and upload overlap the others' device
+ * level loops, and their small rounds fill the SMs around the large ones.
+ * streams = 0 picks 4. out[i] receives code i's run (free each with
+ * mdg_run_free); every result equals mdg_min_weight's on that code. On error
+ * no run is returned. No reference counterpart (the reference takes one
+ * matrix per call); see INTEGRATION.md. */
+int mdg_min_weight_batch(mdg_ctx* ctx, uint32_t count, const uint64_t* const* G, const uint32_t* k,
+                         const uint32_t* n, const mdg_config* cfg, uint32_t streams,
+                         mdg_run** out);
+
 /* The level loop over the Gamma set already loaded into ctx (mdg_load_gset):
  * the device-resident variant of the front door (no Gamma search, no upload). */
 int mdg_bz_loop_device(mdg_ctx* ctx, const mdg_gset* gs, const mdg_config* cfg, mdg_run** out);

@@ -131,6 +131,8 @@ SYMBOLS = {
     "mdg_min_weight_dist": (C.c_int, [C.c_void_p, u64p, C.c_uint32, C.c_uint32,
                                       C.POINTER(_Config), C.c_uint32, C.c_uint32, C.c_void_p,
                                       C.c_void_p, C.POINTER(C.c_void_p)]),
+    "mdg_min_weight_batch": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.POINTER(C.c_uint64)), u32p, u32p,
+                                       C.POINTER(_Config), C.c_uint32, C.POINTER(C.c_void_p)]),
     "mdg_bz_loop_device": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(_Config),
                                      C.POINTER(C.c_void_p)]),
     "mdg_bz_loop_device_dist": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(_Config), C.c_uint32,
@@ -563,6 +565,34 @@ def min_weight(G: np.ndarray, n: int, trials: int = 10, seed: int = 0, level_cap
     _check(lib().mdg_min_weight(device.handle if device else None, G, G.shape[0], n,
                                 C.byref(cfg), C.byref(h)))
     return _collect(h)
+
+
+def min_weight_batch(Gs, n, trials: int = 10, seed=0, level_cap: int = 0,
+                     kernel: int = KERNEL_TAB, witness: bool = True, device: Optional[Device] = None,
+                     exact_rounds: bool = False, streams: int = 4) -> list:
+    """min_weight for many codes on one device (mdg_min_weight_batch): up to `streams` codes
+    in flight, each on its own engine/stream, so host Gamma searches overlap device loops.
+    Gs: sequence of packed row arrays; n and seed: one value for all codes or one per code.
+    Returns one RunResult per code, each equal to min_weight's."""
+    if device is None:
+        raise InvalidArgument("min_weight_batch needs a Device")
+    mats = [_rows(G) for G in Gs]
+    count = len(mats)
+    ns = list(n) if hasattr(n, "__len__") else [n] * count
+    if len(ns) != count:
+        raise InvalidArgument("one n per code")
+    P64 = C.POINTER(C.c_uint64)
+    ptrs = (P64 * max(1, count))(*[m.ctypes.data_as(P64) for m in mats])
+    ks = np.array([m.shape[0] for m in mats] or [0], dtype=np.uint32)
+    nn = np.array(ns or [0], dtype=np.uint32)
+    seeds = list(seed) if hasattr(seed, "__len__") else [seed] * count
+    if len(seeds) != count:
+        raise InvalidArgument("one seed per code")
+    cfgs = (_Config * max(1, count))(*[_config(trials, sd, level_cap, kernel, witness, exact_rounds)
+                                       for sd in seeds])
+    hs = (C.c_void_p * max(1, count))()
+    _check(lib().mdg_min_weight_batch(device.handle, count, ptrs, ks, nn, cfgs, streams, hs))
+    return [_collect(C.c_void_p(hs[i])) for i in range(count)]
 
 
 def min_weight_dist(G: np.ndarray, n: int, rank: int, world: int,

@@ -1,7 +1,13 @@
 // C ABI of the B200 Brouwer–Zimmermann engine (include/mdg.h) and the GPU
 // front door min_weight (reference: engines.cpp:617-648 + cli.cpp:69-112).
+#include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <thread>
 #include <memory>
 #include <sstream>
 #include <string>
@@ -15,6 +21,7 @@ using namespace mdg;
 
 struct mdg_ctx {
     std::unique_ptr<Engine> eng;
+    std::vector<std::unique_ptr<Engine>> extra; // mdg_min_weight_batch's further streams
 };
 
 struct mdg_gset {
@@ -224,6 +231,8 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
     out.loop_s = eng.timer_stop_ms() * 1e-3;
     const uint32_t d = out.er.d;
 
+    static const bool timing = std::getenv("MDG_TIMING") != nullptr;
+    auto tw0 = std::chrono::steady_clock::now();
     if (cfg.want_witness) {
         const RoundLog* src = nullptr;
         if (out.er.witness_round >= 0) src = &log[size_t(out.er.witness_round)];
@@ -246,7 +255,13 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
             out.witness_gamma = int32_t(src->j);
             out.witness_level = src->c;
             out.witness = codeword(gs, src->j, out.witness_idx);
+            auto tw1 = std::chrono::steady_clock::now();
             out.witness_ok = weight_of(out.witness) == d && in_code(gs, out.witness) && src->rr.w == d;
+            if (timing)
+                std::fprintf(stderr, "[mdg timing] witness search %.1f us (from trace: %d), check %.1f us\n",
+                             std::chrono::duration<double>(tw1 - tw0).count() * 1e6,
+                             int(out.witness_from_trace),
+                             std::chrono::duration<double>(std::chrono::steady_clock::now() - tw1).count() * 1e6);
         }
     }
     Engine::Counters c1 = eng.counters();
@@ -593,6 +608,48 @@ int mdg_min_weight_dist(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n,
         }
         BitMatrix M = from_rows(G, k, n);
         *out = min_weight_device(*ctx->eng, M, c, rank, world, reduce_min, user).release();
+    });
+}
+
+int mdg_min_weight_batch(mdg_ctx* ctx, uint32_t count, const uint64_t* const* G, const uint32_t* k,
+                         const uint32_t* n, const mdg_config* cfg, uint32_t streams,
+                         mdg_run** out) {
+    return guard([&] {
+        if (!ctx || !out || (count && (!G || !k || !n))) throw std::invalid_argument("null argument");
+        std::vector<mdg_config> cf(count);
+        for (uint32_t i = 0; i < count; ++i) {
+            if (!G[i]) throw std::invalid_argument("null matrix");
+            out[i] = nullptr;
+            mdg_config_default(&cf[i]);
+            if (cfg) cf[i] = cfg[i];
+            if (cf[i].trials < 1)
+                throw std::invalid_argument("best_gamma_over_permutations: trials must be >= 1");
+        }
+        const uint32_t S = std::max(1u, std::min(streams ? streams : 4u, std::max(count, 1u)));
+        const int dev = ctx->eng->device();
+        while (ctx->extra.size() + 1 < S) ctx->extra.push_back(std::make_unique<Engine>(dev));
+        std::vector<std::unique_ptr<mdg_run>> runs(count);
+        std::vector<std::exception_ptr> errs(S);
+        std::atomic<uint32_t> next{0};
+        auto worker = [&](uint32_t w) {
+            Engine& eng = w == 0 ? *ctx->eng : *ctx->extra[w - 1];
+            try {
+                for (uint32_t i; (i = next.fetch_add(1)) < count;) {
+                    BitMatrix M = from_rows(G[i], k[i], n[i]);
+                    runs[i] = min_weight_device(eng, M, cf[i], 0, 1, nullptr, nullptr);
+                }
+            } catch (...) {
+                errs[w] = std::current_exception();
+                next.store(count); // stop handing out codes
+            }
+        };
+        std::vector<std::thread> th;
+        for (uint32_t w = 1; w < S; ++w) th.emplace_back(worker, w);
+        worker(0);
+        for (auto& t : th) t.join();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+        for (uint32_t i = 0; i < count; ++i) out[i] = runs[i].release();
     });
 }
 

@@ -53,6 +53,7 @@ namespace {
 constexpr int kWarps = 8;           // warps per block (tab kernels)
 constexpr int kThreads = kWarps * 32;
 constexpr int kTX = 256;            // prefixes per tile (= threads that build them)
+constexpr int kFindX = 4;           // smem-side items per block of the witness search
 constexpr uint32_t kBT = kMaxC + 1; // binomial table row stride
 constexpr int kKeyShift = 40;
 
@@ -209,6 +210,51 @@ __global__ void ytab_build(const uint32_t* __restrict__ rows, const uint64_t* __
         id += q < id_rows;
     }
     uint32_t* o = out + y * YS;
+#pragma unroll
+    for (int w = 0; w < YS; ++w) o[w] = w < NW ? acc[w] : (HID && w == NW ? id : 0u);
+}
+
+// Several tables in one launch (the tables of the first levels of a chained loop: one
+// latency-bound launch instead of one per table and Gamma). Thread gi builds entry
+// gi - begin of the job whose range holds gi, exactly as ytab_build.
+constexpr int kMaxTableJobs = 48;
+struct TableJob {
+    const uint32_t* rows;
+    uint32_t* out;
+    uint64_t begin;
+    uint32_t s, id_rows, reverse, pad;
+};
+struct TableJobs {
+    uint32_t n, k;
+    uint64_t total;
+    TableJob job[kMaxTableJobs];
+};
+
+template <int NW, bool HID>
+__global__ void tables_build(const __grid_constant__ TableJobs J, const uint64_t* __restrict__ T) {
+    constexpr int YS = stride_for(NW + (HID ? 1 : 0));
+    const uint64_t gi = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (gi >= J.total) return;
+    uint32_t jb = 0;
+    for (uint32_t i = 1; i < J.n; ++i)
+        if (J.job[i].begin <= gi) jb = i;
+    const TableJob& jo = J.job[jb];
+    const uint64_t y = gi - jo.begin;
+    uint32_t acc[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) acc[w] = 0;
+    uint32_t id = 0;
+    uint64_t r = y;
+    uint32_t hi = J.k;
+    for (uint32_t i = jo.s; i >= 1; --i) {
+        uint32_t x = colex_top(T, r, i, hi);
+        r -= BT(T, x, i);
+        hi = x;
+        uint32_t q = jo.reverse ? J.k - 1 - x : x;
+        xor_row<NW>(jo.rows, q, acc);
+        id += q < jo.id_rows;
+    }
+    uint32_t* o = jo.out + y * YS;
 #pragma unroll
     for (int w = 0; w < YS; ++w) o[w] = w < NW ? acc[w] : (HID && w == NW ? id : 0u);
 }
@@ -690,23 +736,28 @@ __global__ void chain_finalize(ChainState* st, const unsigned long long* slot, C
 // witness: the smallest (x_local, y_local) of the tile whose weight == target
 template <int NW, bool HID>
 __global__ void __launch_bounds__(kThreads) tab_find(TabArgs a) {
+    // block b scans smem-side items [b * kFindX, (b + 1) * kFindX) of the tile (one block
+    // per slice: the whole tile in a few microseconds instead of one block's serial scan)
     constexpr int R = r_for(NW);
     constexpr int YC = R * kThreads;
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
-    __shared__ __align__(16) uint32_t xs[kTX * XS];
+    __shared__ __align__(16) uint32_t xs[kFindX * XS];
     __shared__ TileInfo ti;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) decode_tile<YC>(a, a.tile_lo, ti);
     __syncthreads();
-    if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(a, ti, threadIdx.x, xs + threadIdx.x * XS);
+    const uint32_t xb = blockIdx.x * kFindX;
+    if (xb >= ti.nx) return;
+    const uint32_t xe = min(ti.nx, xb + kFindX);
+    if (threadIdx.x < xe - xb) build_smem_item<NW, HID>(a, ti, xb + threadIdx.x, xs + threadIdx.x * XS);
     uint32_t Y[R][NW], idY[R];
     bool valid[R];
     load_suffixes<NW, HID>(a, ti, Y, idY, valid);
     __syncthreads();
     unsigned long long cand = ~0ull;
-    for (uint32_t xi = 0; xi < ti.nx; ++xi) {
+    for (uint32_t xi = xb; xi < xe; ++xi) {
         uint32_t X[XS];
-        vload<XS>(xs + xi * XS, X);
+        vload<XS>(xs + (xi - xb) * XS, X);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             uint32_t w = xor_weight<0, NW, XS, NW>(X, Y[r]);
@@ -1139,6 +1190,14 @@ struct YtabLaunch {
 };
 
 template <int NW, bool HID>
+struct TablesLaunch {
+    static void run(const TableJobs& J, const uint64_t* T, cudaStream_t st) {
+        uint64_t blocks = (J.total + 255) / 256;
+        tables_build<NW, HID><<<dim3(uint32_t(blocks)), 256, 0, st>>>(J, T);
+    }
+};
+
+template <int NW, bool HID>
 struct TabOcc {
     static void run(int* occ) {
         static int cached = -1; // per instantiation; the kernel's resources never change
@@ -1168,7 +1227,7 @@ struct TabLaunch {
             cfg.numAttrs = mode == 3 ? 1 : 0;
             cudaLaunchKernelEx(&cfg, tab_round<NW, HID>, a);
         }
-        else if (mode == 1) tab_find<NW, HID><<<1, kThreads, 0, st>>>(a);
+        else if (mode == 1) tab_find<NW, HID><<<(kTX + kFindX - 1) / kFindX, kThreads, 0, st>>>(a);
         else {
             auto fn = tab_hist<NW, HID>;
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
@@ -1737,6 +1796,54 @@ static uint32_t* ensure_table(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t
     return t;
 }
 
+// Build, in as few launches as possible, every suffix / prefix table the rounds of
+// levels [c_lo, c_hi] will ask for (ensure_ytab / ensure_xtab then find them cached).
+static void prebuild_tables(Engine::Impl& im, uint32_t m, uint32_t k, uint32_t c_lo, uint32_t c_hi,
+                            int sms) {
+    struct Need { uint32_t j, s; bool reverse; };
+    std::vector<Need> need;
+    auto want = [&](uint32_t j, uint32_t s, bool rev) {
+        if (s == 0 || im.tables.count(std::make_tuple(j, s, rev))) return;
+        for (const Need& q : need)
+            if (q.j == j && q.s == s && q.reverse == rev) return;
+        need.push_back({j, s, rev});
+    };
+    for (uint32_t c = c_lo; c <= c_hi; ++c)
+        for (uint32_t j = 0; j < m; ++j) {
+            const PlanEntry& pe = im.plan(k, c, im.gammas[j], sms);
+            want(j, pe.plan.s, true);
+            if (xtab_ok(k, pe.plan.p - 1)) want(j, pe.plan.p - 1, false);
+        }
+    // one launch per (row width, identity flag) group, <= kMaxTableJobs tables each
+    std::vector<bool> done(need.size(), false);
+    for (size_t a = 0; a < need.size(); ++a) {
+        if (done[a]) continue;
+        const GammaDev& ga = im.gammas[need[a].j];
+        TableJobs J{};
+        J.k = k;
+        for (size_t b = a; b < need.size() && J.n < uint32_t(kMaxTableJobs); ++b) {
+            const GammaDev& g = im.gammas[need[b].j];
+            if (done[b] || g.nw != ga.nw || g.hid != ga.hid) continue;
+            const uint32_t YS = uint32_t(stride_for(int(g.nw) + (g.hid ? 1 : 0)));
+            const uint64_t count = hb(k, need[b].s);
+            uint32_t* t = static_cast<uint32_t*>(im.arena.alloc(size_t(count) * YS * 4));
+            im.tables[std::make_tuple(need[b].j, need[b].s, need[b].reverse)] = t;
+            TableJob& jo = J.job[J.n++];
+            jo.rows = g.rows;
+            jo.out = t;
+            jo.begin = J.total;
+            jo.s = need[b].s;
+            jo.id_rows = g.id_rows;
+            jo.reverse = need[b].reverse ? 1u : 0u;
+            J.total += count;
+            done[b] = true;
+        }
+        dispatch_nw_hid<TablesLaunch>(ga.nw, ga.hid, J, im.binom, im.stream);
+        CK(cudaGetLastError());
+        im.cnt.launches += 1;
+    }
+}
+
 // suffix table (reverse colex s-subsets)
 static uint32_t* ensure_ytab(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t s) {
     return ensure_table(im, j, k, s, true);
@@ -2021,6 +2128,17 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
     chain_stamp<<<1, 32, 0, im.stream>>>(t0_slot);
     CK(cudaGetLastError());
     im.cnt.launches += 1;
+    {   // the tables of the cheap first levels in one launch (later levels build lazily:
+        // next to their rounds a table build is noise)
+        uint32_t c_hi = 0;
+        double work = 0;
+        for (uint32_t c = 1; c <= k_ && c <= kMaxC && (!level_cap || c <= level_cap); ++c) {
+            work += double(m_) * double(hb(k_, c));
+            if (work > 2e10) break;
+            c_hi = c;
+        }
+        if (c_hi >= 1 && !init.done) prebuild_tables(im, m_, k_, 1, c_hi, sms_);
+    }
     uint32_t g = 1;
     bool done = init.done != 0;
     uint64_t after_round = ~0ull; // launch count right after the last round launch

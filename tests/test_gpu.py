@@ -383,3 +383,24 @@ def test_graft_smoke():
     """The driver's smoke() (config 1 in exact and bounded round modes + a config-5 histogram)."""
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+@pytest.mark.parametrize("streams", [1, 3])
+def test_min_weight_batch_equals_single(mdg, device, streams):
+    """The batch front door (several codes in flight on their own streams) returns, code by
+    code, the golden result: d, per-round and per-level trace, Gamma set and a witness."""
+    cases = [c for c in load_golden("configs") if not c["capped"]]
+    mats, ns, seeds = [], [], []
+    for case in cases:
+        g = case["gen"]
+        mats.append(mdg.gen_matrix(g["n"], g["k"], g["seed"], True))
+        ns.append(g["n"])
+        seeds.append(case["seed"])
+    runs = mdg.min_weight_batch(mats, ns, trials=10, seed=seeds, device=device, streams=streams)
+    assert len(runs) == len(cases)
+    for res, case in zip(runs, cases):
+        assert not res.capped and res.d == case["d"], case["name"]
+        _check_run(res, case, case["name"], exact=False)
+    with pytest.raises(mdg.InvalidArgument):  # a zero matrix fails the whole batch
+        mdg.min_weight_batch([mats[0], np.zeros_like(mats[0])], 80, device=device, streams=2)
+    assert mdg.min_weight_batch([], 80, device=device) == []
