@@ -41,8 +41,9 @@ sys.path.insert(0, ROOT)
 N, K, SEEDS = 128, 64, list(range(1, 9))
 POPC_PER_S_MEASURED = 4642.3e9   # profiles/r01_pipes_microbench.jsonl (B200, 148 SMs)
 # XU (POPC) operations the bound-pruned level-7 kernel executes per codeword, from the
-# committed ncu capture of that launch (profiles/r01c_tab_round_fold_ncu.txt)
-XU_PER_CW_PRUNED = 1.076
+# committed ncu capture of that launch (profiles/r01e_tab_round_c7_ncu.txt)
+XU_PER_CW_PRUNED = 1.035
+DRAM_BYTES_PER_LAUNCH = 4225024  # same capture: dram__bytes_read.sum + dram__bytes_write.sum
 WORKLOAD = "cfg2: random [128,64] codes G=(I|A), mt19937_64 seeds 1..8, BZ to termination (exact d)"
 
 
@@ -289,6 +290,17 @@ def main():
         a, b = kernel_pass()
         c7_cw += a
         c7_ms += b
+    # BASELINE.md's roofline case: the config-2 level-7 round with early exit and bound
+    # pruning off (exact minimum of all C(64,7) codewords), seed 1, Gamma_0
+    ex_ms = []
+    if world == 1:
+        devs[0].set_pruning(False)
+        for _ in range(3):
+            l2_flush()
+            o = devs[0].round(0, 7)
+            ex_ms.append(o.device_ms)
+        ex_cw = o.evaluated
+        devs[0].set_pruning(True)
 
     # e2e through the public front door from host buffers (pinned copies of G): the batch
     # call (mdg_min_weight_batch, --streams codes in flight) on one GPU, mdg_min_weight_dist
@@ -341,15 +353,27 @@ def main():
         peak = popc / XU_PER_CW_PRUNED
         roofline = {
             "bound": "int_popc", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gcw/s",
-            "frac": achieved / peak, "traffic": 4200960, "traffic_unit": "DRAM bytes per launch (ncu)",
+            "frac": achieved / peak, "traffic": DRAM_BYTES_PER_LAUNCH, "traffic_unit": "DRAM bytes per launch (ncu)",
             "kernel": "tab_round<2,false>, bound-pruned (cutoff U), level-7 rounds (621,216,192 codewords per launch)",
             "peak_basis": ("measured B200 POPC (XU pipe) rate 16/clk/SM = 4.64e12/s "
-                           "(tools/pipes_microbench.cu) / 1.076 XU ops per codeword executed by this "
-                           "kernel (ncu, profiles/r01c_tab_round_fold_ncu.txt)"),
+                           "(tools/pipes_microbench.cu) / 1.035 XU ops per codeword executed by this "
+                           "kernel (ncu, profiles/r01e_tab_round_c7_ncu.txt)"),
             "op_mix_per_codeword": ("2 LOP3 (XOR, fused OR-fold) + 1 POPC of the fold (a lower bound on "
                                     "the weight) + group min / warp vote; the exact weight only for warp "
-                                    "groups that can still beat the bound (1.08 POPC per codeword measured)"),
+                                    "groups that can still beat the bound (1.035 POPC per codeword measured)"),
             "frac_vs_unpruned_popc_roofline": achieved / (popc / nw),
+            "unpruned_c7": ({
+                "what": "exact config-2 level-7 round with early exit and bound pruning off "
+                        "(every codeword's weight computed), seed 1, Gamma_0, best of 3 "
+                        "CUDA-event timings",
+                "achieved": ex_cw / (min(ex_ms) * 1e-3) / 1e9, "unit": "Gcw/s",
+                "peak_baseline_def": popc / 4 / 1e9,
+                "frac_baseline_def": ex_cw / (min(ex_ms) * 1e-3) / (popc / 4),
+                "baseline_def": "BASELINE.md: SMs x 16 POPC/clk x f / (2W), W = 2 u64 words per row",
+                "peak_elided": popc / nw / 1e9,
+                "frac_elided": ex_cw / (min(ex_ms) * 1e-3) / (popc / nw),
+                "elided_def": "identity block elided: 64 compacted bits = 2 POPC per codeword",
+            } if ex_ms else None),
             "traffic_note": "DRAM 4.2 MB per launch (suffix table + binomials), 0.1% of HBM peak: compute-bound",
         }
         if clocks.get("sm_mhz"):

@@ -107,6 +107,10 @@ int mdg_round_witness(mdg_ctx* ctx, uint32_t j, uint32_t c, const mdg_round_out*
 
 /* Kernel selection and launch geometry (0 = keep the current value). */
 int mdg_set_kernel(mdg_ctx* ctx, int kernel);
+/* Bound pruning of the tab kernel (on by default): off computes every
+ * codeword's exact weight (results are identical; for roofline measurements
+ * of the unpruned kernel). */
+int mdg_set_pruning(mdg_ctx* ctx, int on);
 
 /* ----------------------------------------------------------- host objects */
 typedef struct mdg_gset mdg_gset;   /* GammaSet (gamma.hpp:14-24) */

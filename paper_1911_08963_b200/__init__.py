@@ -111,6 +111,7 @@ SYMBOLS = {
     "mdg_round_hist": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, u64p, C.POINTER(_RoundOut)]),
     "mdg_round_witness": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(_RoundOut), u32p]),
     "mdg_set_kernel": (C.c_int, [C.c_void_p, C.c_int]),
+    "mdg_set_pruning": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_gset_build": (C.c_int, [u64p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                  C.POINTER(C.c_void_p)]),
     "mdg_gset_compute": (C.c_int, [u64p, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]),
@@ -390,6 +391,10 @@ class Device:
 
     def set_kernel(self, kernel: int):
         _check(lib().mdg_set_kernel(self._h, kernel))
+
+    def set_pruning(self, on: bool):
+        """Stage-1 bound pruning of the tab kernel (default on); off = every weight exact."""
+        _check(lib().mdg_set_pruning(self._h, 1 if on else 0))
 
     def round(self, j: int, c: int, stop_at: int = 0) -> RoundOut:
         o = _RoundOut()

@@ -458,6 +458,13 @@ int mdg_set_kernel(mdg_ctx* ctx, int kernel) {
     });
 }
 
+int mdg_set_pruning(mdg_ctx* ctx, int on) {
+    return guard([&] {
+        if (!ctx) throw std::invalid_argument("null argument");
+        ctx->eng->set_pruning(on != 0);
+    });
+}
+
 // ------------------------------------------------------------- gamma sets
 int mdg_gset_build(const uint64_t* G, uint32_t k, uint32_t n, uint32_t trials, uint64_t seed,
                    mdg_gset** out) {

@@ -1588,6 +1588,7 @@ constexpr int kSlots = 4096; // per-round scratch slots {best key, evaluated, co
 
 struct Engine::Impl {
     cudaStream_t stream = nullptr;
+    bool prune = true; // stage-1 bound pruning (mdg_set_pruning)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, tev0 = nullptr, tev1 = nullptr;
     Engine::Counters cnt;
     uint64_t* binom = nullptr;
@@ -1921,6 +1922,7 @@ static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe
     a.npiv = uint32_t(pe.plan.prefix.size() - 1);
     a.id_rows = g.id_rows; a.add_const = (g.id_rows == k) ? c : 0; a.tx = pe.plan.TX;
     sampled_fold_limits(im, uint32_t(&g - im.gammas.data()), k, c, a.fold_lim);
+    if (!im.prune) a.fold_lim[0] = a.fold_lim[1] = a.fold_lim[2] = -1; // exact weights only
     a.xtab = ensure_xtab(im, uint32_t(&g - im.gammas.data()), k, pe.plan.p - 1);
     return a;
 }
@@ -2304,6 +2306,7 @@ Engine::BruteResult Engine::brute_force(uint32_t k, uint32_t n, const uint64_t* 
 }
 
 Engine::Counters Engine::counters() const { return impl_->cnt; }
+void Engine::set_pruning(bool on) { impl_->prune = on; }
 void Engine::reset_counters() { impl_->cnt = Counters{}; }
 void Engine::timer_start() {
     CK(cudaSetDevice(device_));

@@ -60,6 +60,7 @@ public:
     uint32_t n() const { return n_; }
 
     void set_kernel(Kernel kern) { kernel_ = kern; }
+    void set_pruning(bool on);
     Kernel kernel() const { return kernel_; }
 
     uint64_t tasks(uint32_t j, uint32_t c);

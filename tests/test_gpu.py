@@ -404,3 +404,18 @@ def test_min_weight_batch_equals_single(mdg, device, streams):
     with pytest.raises(mdg.InvalidArgument):  # a zero matrix fails the whole batch
         mdg.min_weight_batch([mats[0], np.zeros_like(mats[0])], 80, device=device, streams=2)
     assert mdg.min_weight_batch([], 80, device=device) == []
+
+
+def test_pruning_off_same_minima(mdg, device):
+    """mdg_set_pruning(0) (every codeword's weight exact) returns the same round minima."""
+    for (n, k, seed) in [(128, 64, 1), (300, 200, 11), (256, 32, 7)]:
+        G = mdg.gen_matrix(n, k, seed, True)
+        gs = mdg.GammaSet.build(G, n, 10, seed)
+        device.load_gset(gs)
+        for j in range(gs.m):
+            for c in (2, 3, 4):
+                a = device.round(j, c)
+                device.set_pruning(False)
+                b = device.round(j, c)
+                device.set_pruning(True)
+                assert (a.min_weight, a.evaluated) == (b.min_weight, b.evaluated), (n, k, j, c)
