@@ -1799,13 +1799,14 @@ static uint32_t* ensure_table(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t
 
 // Build, in as few launches as possible, every suffix / prefix table the rounds of
 // levels [c_lo, c_hi] will ask for (ensure_ytab / ensure_xtab then find them cached).
-static void prebuild_tables(Engine::Impl& im, uint32_t m, uint32_t k, uint32_t c_lo, uint32_t c_hi,
-                            int sms) {
-    struct Need { uint32_t j, s; bool reverse; };
-    std::vector<Need> need;
+struct TableNeed { uint32_t j, s; bool reverse; };
+
+static std::vector<TableNeed> table_needs(Engine::Impl& im, uint32_t m, uint32_t k, uint32_t c_lo,
+                                          uint32_t c_hi, int sms) {
+    std::vector<TableNeed> need;
     auto want = [&](uint32_t j, uint32_t s, bool rev) {
         if (s == 0 || im.tables.count(std::make_tuple(j, s, rev))) return;
-        for (const Need& q : need)
+        for (const TableNeed& q : need)
             if (q.j == j && q.s == s && q.reverse == rev) return;
         need.push_back({j, s, rev});
     };
@@ -1815,6 +1816,21 @@ static void prebuild_tables(Engine::Impl& im, uint32_t m, uint32_t k, uint32_t c
             want(j, pe.plan.s, true);
             if (xtab_ok(k, pe.plan.p - 1)) want(j, pe.plan.p - 1, false);
         }
+    return need;
+}
+
+static uint64_t table_bytes(const Engine::Impl& im, uint32_t k, const std::vector<TableNeed>& need) {
+    uint64_t b = 0;
+    for (const TableNeed& q : need) {
+        const GammaDev& g = im.gammas[q.j];
+        b += hb(k, q.s) * uint64_t(stride_for(int(g.nw) + (g.hid ? 1 : 0))) * 4;
+    }
+    return b;
+}
+
+static void prebuild_tables(Engine::Impl& im, uint32_t m, uint32_t k, uint32_t c_lo, uint32_t c_hi,
+                            int sms) {
+    const std::vector<TableNeed> need = table_needs(im, m, k, c_lo, c_hi, sms);
     // one launch per (row width, identity flag) group, <= kMaxTableJobs tables each
     std::vector<bool> done(need.size(), false);
     for (size_t a = 0; a < need.size(); ++a) {
@@ -2130,16 +2146,20 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
     chain_stamp<<<1, 32, 0, im.stream>>>(t0_slot);
     CK(cudaGetLastError());
     im.cnt.launches += 1;
-    {   // the tables of the cheap first levels in one launch (later levels build lazily:
-        // next to their rounds a table build is noise)
-        uint32_t c_hi = 0;
+    // Tables: those of the first levels in one launch up front (while the levels add up to
+    // <= 2e10 codewords and their tables to <= 32 MB), then each later level's tables for
+    // all Gammas in one launch before its rounds.
+    uint32_t built_to = 0;
+    if (!init.done) {
         double work = 0;
         for (uint32_t c = 1; c <= k_ && c <= kMaxC && (!level_cap || c <= level_cap); ++c) {
             work += double(m_) * double(hb(k_, c));
-            if (work > 2e10) break;
-            c_hi = c;
+            if (c > 1 && (work > 2e10 ||
+                          table_bytes(im, k_, table_needs(im, m_, k_, 1, c, sms_)) > (uint64_t{32} << 20)))
+                break;
+            built_to = c;
         }
-        if (c_hi >= 1 && !init.done) prebuild_tables(im, m_, k_, 1, c_hi, sms_);
+        if (built_to >= 1) prebuild_tables(im, m_, k_, 1, built_to, sms_);
     }
     uint32_t g = 1;
     bool done = init.done != 0;
@@ -2159,6 +2179,10 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
             check_round(0, g); // throws the reference's error for this level
         }
         const uint32_t lb = lower_bound(m_, g, k_, k_last);
+        if (g > built_to) {
+            prebuild_tables(im, m_, k_, g, g, sms_);
+            built_to = g;
+        }
         for (uint32_t j = 0; j < m_; ++j) {
             const GammaDev& gd = im.gammas[j];
             const PlanEntry& pe = im.plan(k_, g, gd, sms_);
