@@ -120,6 +120,14 @@ typedef struct mdg_gset mdg_gset;   /* GammaSet (gamma.hpp:14-24) */
  * does (engines.cpp:619). */
 int mdg_gset_build(const uint64_t* G, uint32_t k, uint32_t n, uint32_t trials, uint64_t seed,
                    mdg_gset** out);
+/* The same search with the trials on the GPU: one warp per
+ * trial derives its column order (SplitMix64 skipped ahead to draw t*(n-1)) and
+ * the (m, k_last) of compute_gamma_matrices on it; the best trial's Gammas are
+ * rebuilt on the host. Identical result to mdg_gset_build for every (trials, seed);
+ * meant for trial counts far above the reference default of 10 (a larger k_last
+ * lifts L sooner). Needs k <= 512, n <= 4096. */
+int mdg_gset_build_gpu(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n, uint32_t trials,
+                       uint64_t seed, mdg_gset** out);
 /* compute_gamma_matrices on a full-rank G (gamma.cpp:32-75). */
 int mdg_gset_compute(const uint64_t* G, uint32_t k, uint32_t n, mdg_gset** out);
 void mdg_gset_free(mdg_gset* gs);
@@ -167,7 +175,12 @@ typedef struct {
     int exact_rounds;     /* 1 = every round's exact minimum (per-round trace parity with the
                              reference's rounds); 0 = rounds bounded by U (same d and (L, U)
                              trace, faster) */
+    int gamma_search;     /* MDG_GAMMA_HOST: the permutation trials on host threads;
+                             MDG_GAMMA_GPU: on the device (mdg_gset_build_gpu) -- the same
+                             Gamma set for the same trials and seed, faster for many trials */
 } mdg_config;
+#define MDG_GAMMA_HOST 0
+#define MDG_GAMMA_GPU 1
 void mdg_config_default(mdg_config* cfg);
 int mdg_min_weight(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n, const mdg_config* cfg,
                    mdg_run** out);

@@ -68,6 +68,7 @@ uint64_t hash_rows(const BitMatrix& m);  // FNV-1a 64 over the u64 words, little
 class SplitMix64 { // util.hpp:12-24
 public:
     explicit SplitMix64(uint64_t seed) : state_(seed) {}
+    void discard(uint64_t draws) { state_ += draws * 0x9E3779B97F4A7C15ull; } // skip ahead
     uint64_t next() {
         uint64_t z = (state_ += 0x9E3779B97F4A7C15ull);
         z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -97,6 +98,12 @@ struct Bounds {
 
 GammaSet compute_gamma_matrices(const BitMatrix& G);
 GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint64_t seed);
+// The column order of trial t of best_gamma_over_permutations(G, trials, seed) (n columns):
+// identity shuffled by Fisher-Yates with the generator advanced past the t earlier trials.
+std::vector<uint32_t> trial_permutation(uint32_t n, uint64_t seed, uint64_t t);
+// compute_gamma_matrices on G's columns in the order `perm`, column_perm composed with perm
+// (one candidate of the permutation search, gamma.cpp:85-91).
+GammaSet gamma_for_permutation(const BitMatrix& G, const std::vector<uint32_t>& perm);
 uint32_t lower_bound(uint32_t m, uint32_t g, uint32_t k, uint32_t k_last);
 uint32_t singleton_upper(uint32_t n, uint32_t k);
 BitMatrix permute_columns(const BitMatrix& m, const std::vector<uint32_t>& perm);

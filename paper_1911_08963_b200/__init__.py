@@ -66,7 +66,8 @@ class _RoundOut(C.Structure):
 
 class _Config(C.Structure):
     _fields_ = [("trials", C.c_uint32), ("seed", C.c_uint64), ("level_cap", C.c_uint32),
-                ("kernel", C.c_int), ("want_witness", C.c_int), ("exact_rounds", C.c_int)]
+                ("kernel", C.c_int), ("want_witness", C.c_int), ("exact_rounds", C.c_int),
+                ("gamma_search", C.c_int)]
 
 
 class _RunInfo(C.Structure):
@@ -114,6 +115,8 @@ SYMBOLS = {
     "mdg_set_pruning": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_gset_build": (C.c_int, [u64p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                  C.POINTER(C.c_void_p)]),
+    "mdg_gset_build_gpu": (C.c_int, [C.c_void_p, u64p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                     C.c_uint64, C.POINTER(C.c_void_p)]),
     "mdg_gset_compute": (C.c_int, [u64p, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]),
     "mdg_gset_free": (None, [C.c_void_p]),
     "mdg_gset_info": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_uint32)] * 4),
@@ -285,11 +288,17 @@ class GammaSet:
         self.m, self.k, self.n, self.k_last = int(m.value), int(k.value), int(n.value), int(kl.value)
 
     @classmethod
-    def build(cls, G: np.ndarray, n: int, trials: int = 10, seed: int = 0) -> "GammaSet":
-        """gamma.cpp:77-94 over row_basis(G) (f2core.cpp:92-97)."""
+    def build(cls, G: np.ndarray, n: int, trials: int = 10, seed: int = 0,
+              device: Optional["Device"] = None) -> "GammaSet":
+        """gamma.cpp:77-94 over row_basis(G) (f2core.cpp:92-97). With a device the trials
+        run on the GPU (mdg_gset_build_gpu): the same Gamma set, faster for many trials."""
         G = _rows(G)
         h = C.c_void_p()
-        _check(lib().mdg_gset_build(G, G.shape[0], n, trials, seed, C.byref(h)))
+        if device is None:
+            _check(lib().mdg_gset_build(G, G.shape[0], n, trials, seed, C.byref(h)))
+        else:
+            _check(lib().mdg_gset_build_gpu(device.handle, G, G.shape[0], n, trials, seed,
+                                            C.byref(h)))
         return cls(h.value)
 
     @classmethod
@@ -549,24 +558,29 @@ def _collect(h) -> RunResult:
     return res
 
 
-def _config(trials, seed, level_cap, kernel, witness, exact_rounds=False) -> _Config:
+def _config(trials, seed, level_cap, kernel, witness, exact_rounds=False,
+            gamma_search="host") -> _Config:
     cfg = _Config()
     lib().mdg_config_default(C.byref(cfg))
     cfg.trials, cfg.seed, cfg.level_cap = trials, seed, level_cap
     cfg.kernel, cfg.want_witness = kernel, 1 if witness else 0
     cfg.exact_rounds = 1 if exact_rounds else 0
+    if gamma_search not in ("host", "gpu"):
+        raise InvalidArgument("gamma_search must be 'host' or 'gpu'")
+    cfg.gamma_search = 1 if gamma_search == "gpu" else 0
     return cfg
 
 
 def min_weight(G: np.ndarray, n: int, trials: int = 10, seed: int = 0, level_cap: int = 0,
                kernel: int = KERNEL_TAB, witness: bool = True,
-               device: Optional[Device] = None, exact_rounds: bool = False) -> RunResult:
+               device: Optional[Device] = None, exact_rounds: bool = False,
+               gamma_search: str = "host") -> RunResult:
     """md::min_weight (engines.cpp:617-648) with the GPU engine, plus trace and witness.
     exact_rounds=True computes every round's exact minimum (per-round trace parity);
     the default bounds rounds by U (identical d and (L, U) trace)."""
     G = _rows(G)
     h = C.c_void_p()
-    cfg = _config(trials, seed, level_cap, kernel, witness, exact_rounds)
+    cfg = _config(trials, seed, level_cap, kernel, witness, exact_rounds, gamma_search)
     _check(lib().mdg_min_weight(device.handle if device else None, G, G.shape[0], n,
                                 C.byref(cfg), C.byref(h)))
     return _collect(h)

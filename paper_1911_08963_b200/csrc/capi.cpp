@@ -133,6 +133,25 @@ void upload(Engine& eng, const GammaSet& gs) {
     eng.load(m, k, gs.n(), all.data(), gs.ranks.data());
 }
 
+// best_gamma_over_permutations (gamma.cpp:77-94) with the trials on the GPU: the device
+// returns the best trial's (m, k_last) and index; the host keeps the identity unless that
+// is a strict improvement, exactly the reference's rule, and rebuilds the winner.
+GammaSet best_gamma_gpu(Engine& eng, const BitMatrix& B, uint32_t trials, uint64_t seed) {
+    if (trials < 1) throw std::invalid_argument("best_gamma_over_permutations: trials must be >= 1");
+    GammaSet best = compute_gamma_matrices(B);
+    const uint64_t key = eng.permutation_search(B.data(), B.rows(), B.cols(), trials, seed);
+    const uint32_t m = uint32_t(key >> 53), kl = uint32_t((key >> 42) & 0x7FF);
+    const uint64_t t = ((uint64_t{1} << 42) - 1) - (key & ((uint64_t{1} << 42) - 1));
+    if (m > best.m() || (m == best.m() && kl > best.k_last)) {
+        GammaSet cand = gamma_for_permutation(B, trial_permutation(B.cols(), seed, t));
+        if (cand.m() != m || cand.k_last != kl)
+            throw std::logic_error("gpu permutation search: trial " + std::to_string(t) +
+                                   " does not reproduce on the host");
+        return cand;
+    }
+    return best;
+}
+
 // The level loop on the device over the Gamma set already loaded into eng
 // (run_bz_loop, engines.cpp:447-476, with the GPU RoundRunner), then the
 // witness. world > 1: every rank evaluates its contiguous task range of each
@@ -291,7 +310,9 @@ std::unique_ptr<mdg_run> min_weight_device(Engine& eng, const BitMatrix& G, cons
     auto t0 = std::chrono::steady_clock::now();
     auto run = std::make_unique<mdg_run>();
     Engine::Counters c0 = eng.counters();
-    GammaSet gs = best_gamma_over_permutations(row_basis(G), cfg.trials, cfg.seed);
+    GammaSet gs = cfg.gamma_search == MDG_GAMMA_GPU
+                      ? best_gamma_gpu(eng, row_basis(G), cfg.trials, cfg.seed)
+                      : best_gamma_over_permutations(row_basis(G), cfg.trials, cfg.seed);
     auto t1 = std::chrono::steady_clock::now();
     run->gamma_s = std::chrono::duration<double>(t1 - t0).count();
     upload(eng, gs);
@@ -476,6 +497,16 @@ int mdg_gset_build(const uint64_t* G, uint32_t k, uint32_t n, uint32_t trials, u
     });
 }
 
+int mdg_gset_build_gpu(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n, uint32_t trials,
+                       uint64_t seed, mdg_gset** out) {
+    return guard([&] {
+        if (!ctx || !out || !G) throw std::invalid_argument("null argument");
+        auto g = std::make_unique<mdg_gset>();
+        g->gs = best_gamma_gpu(*ctx->eng, row_basis(from_rows(G, k, n)), trials, seed);
+        *out = g.release();
+    });
+}
+
 int mdg_gset_compute(const uint64_t* G, uint32_t k, uint32_t n, mdg_gset** out) {
     return guard([&] {
         if (!out) throw std::invalid_argument("null out");
@@ -589,6 +620,7 @@ void mdg_config_default(mdg_config* cfg) {
     cfg->kernel = MDG_KERNEL_TAB;
     cfg->want_witness = 1;
     cfg->exact_rounds = 0;
+    cfg->gamma_search = MDG_GAMMA_HOST;
 }
 
 int mdg_min_weight(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n, const mdg_config* cfg,

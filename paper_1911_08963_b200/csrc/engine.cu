@@ -2331,6 +2331,8 @@ Engine::BruteResult Engine::brute_force(uint32_t k, uint32_t n, const uint64_t* 
 
 Engine::Counters Engine::counters() const { return impl_->cnt; }
 void Engine::set_pruning(bool on) { impl_->prune = on; }
+struct CUstream_st* Engine::stream() const { return impl_->stream; }
+void Engine::count_launch() { impl_->cnt.launches += 1; }
 void Engine::reset_counters() { impl_->cnt = Counters{}; }
 void Engine::timer_start() {
     CK(cudaSetDevice(device_));

@@ -109,6 +109,14 @@ public:
     int device() const { return device_; }
     int sm_count() const { return sms_; }
 
+    // GPU permutation search (gsearch.cu): best (m, k_last, earliest trial) of `trials`
+    // SplitMix64 / Fisher-Yates column orders of the k x n matrix `rows` (row-major u64),
+    // packed as m << 53 | k_last << 42 | (2^42 - 1 - trial).
+    uint64_t permutation_search(const uint64_t* rows, uint32_t k, uint32_t n, uint32_t trials,
+                                uint64_t seed);
+    struct CUstream_st* stream() const; // the engine's CUDA stream
+    void count_launch();
+
     // counters (kernel launches, host<->device bytes) and a CUDA-event timer
     // on the engine's stream (host gaps between launches included)
     struct Counters { uint64_t launches = 0, h2d = 0, d2h = 0; };

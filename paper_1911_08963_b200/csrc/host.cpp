@@ -257,6 +257,24 @@ GammaSet compute_gamma_matrices(const BitMatrix& G) {
 // the reference's order; the candidates (independent of each other; a column
 // permutation keeps the rank, so the reference's per-candidate rank check is
 // the identity's) are systematized on host threads, then chosen in order.
+std::vector<uint32_t> trial_permutation(uint32_t n, uint64_t seed, uint64_t t) {
+    SplitMix64 rng(seed);
+    rng.discard(t * uint64_t(n ? n - 1 : 0));
+    std::vector<uint32_t> perm(n);
+    for (uint32_t i = 0; i < n; ++i) perm[i] = i;
+    for (size_t i = perm.size(); i > 1; --i) {
+        size_t j = static_cast<size_t>(rng.next() % i);
+        std::swap(perm[i - 1], perm[j]);
+    }
+    return perm;
+}
+
+GammaSet gamma_for_permutation(const BitMatrix& G, const std::vector<uint32_t>& perm) {
+    GammaSet g = gamma_blocks(permute_columns(G, perm));
+    for (uint32_t j = 0; j < g.column_perm.size(); ++j) g.column_perm[j] = perm[g.column_perm[j]];
+    return g;
+}
+
 GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint64_t seed) {
     if (trials < 1) throw std::invalid_argument("best_gamma_over_permutations: trials must be >= 1");
     GammaSet best = compute_gamma_matrices(G);

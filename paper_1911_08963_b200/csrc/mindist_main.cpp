@@ -20,7 +20,7 @@ int usage() {
     std::cerr << "usage:\n"
                  "  mindist mindist FILE [--algorithm gpu|brute] [--kernel tab|rd] [--trials T]\n"
                  "                       [--seed S] [--level-cap C] [--device D] [--exact-rounds]\n"
-                 "                       [--pretty]\n"
+                 "                       [--gamma-search host|gpu] [--pretty]\n"
                  "  mindist gen --n N --k K --seed S [--plain]\n";
     return 2;
 }
@@ -88,6 +88,10 @@ int main(int argc, char** argv) {
                 std::cerr << "error: unknown algorithm: " << v << " (this build provides gpu, brute)\n";
                 return 2;
             }
+        } else if (a == "--gamma-search") {
+            if (v == "host") cfg.gamma_search = MDG_GAMMA_HOST;
+            else if (v == "gpu") cfg.gamma_search = MDG_GAMMA_GPU;
+            else { std::cerr << "error: unknown gamma search: " << v << "\n"; return 2; }
         } else if (a == "--kernel") {
             if (v == "tab") cfg.kernel = MDG_KERNEL_TAB;
             else if (v == "rd") cfg.kernel = MDG_KERNEL_RD;

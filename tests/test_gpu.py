@@ -419,3 +419,58 @@ def test_pruning_off_same_minima(mdg, device):
                 b = device.round(j, c)
                 device.set_pruning(True)
                 assert (a.min_weight, a.evaluated) == (b.min_weight, b.evaluated), (n, k, j, c)
+
+
+def _sparse_code(rng, k, n, density):
+    """A random full-rank k x n matrix with sparse columns: column sets of size k are often
+    rank-deficient, so (m, k_last) depends on the column order."""
+    from oracle import port
+    while True:
+        dense = (rng.random((k, n)) < density).astype(np.uint64)
+        W = (n + 63) // 64
+        rows = np.zeros((k, W), dtype=np.uint64)
+        for c in range(n):
+            rows[:, c // 64] |= dense[:, c] << np.uint64(c % 64)
+        if port.rank(rows, n) == k:
+            return rows
+
+
+def test_gpu_permutation_search_equals_host(mdg, device):
+    """mdg_gset_build_gpu (one warp per trial) returns the host search's Gamma set bit for
+    bit: same (m, k_last), ranks, column_perm and Gammas for every trial count."""
+    rng = np.random.default_rng(5)
+    cases = []
+    for case in load_golden("kats") + load_golden("seeded")[:40]:
+        rows, n = mdg.parse_matrix(case["matrix"])
+        cases.append((rows, n))
+    for (k, n, dens) in [(12, 30, 0.15), (20, 50, 0.12), (30, 70, 0.08), (40, 90, 0.06),
+                         (64, 128, 0.5), (70, 150, 0.04), (100, 260, 0.03)]:
+        cases.append((_sparse_code(rng, k, n, dens), n))
+    cases.append((mdg.gen_matrix(300, 200, 11, True), 300))
+    varied = 0
+    for rows, n in cases:
+        try:
+            base = mdg.GammaSet.compute(rows, n)
+        except mdg.InvalidArgument:  # rank-deficient input: build() takes row_basis first
+            base = None
+        for trials in (1, 10, 257):
+            for seed in (0, 7):
+                h = mdg.GammaSet.build(rows, n, trials, seed)
+                g = mdg.GammaSet.build(rows, n, trials, seed, device=device)
+                assert (g.m, g.k_last, g.ranks) == (h.m, h.k_last, h.ranks), (n, trials, seed)
+                assert g.column_perm == h.column_perm, (n, trials, seed)
+                assert [g.hash(j) for j in range(g.m)] == [h.hash(j) for j in range(h.m)]
+                if base is not None and (h.m, h.k_last) != (base.m, base.k_last):
+                    varied += 1
+    assert varied > 0  # some cases really depend on the permutation
+
+
+def test_min_weight_gpu_gamma_search(mdg, device):
+    for name in ("cfg1", "cfg2_s3"):
+        case = next(c for c in load_golden("configs") if c["name"] == name)
+        g = case["gen"]
+        rows = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
+        res = mdg.min_weight(rows, g["n"], case["trials"], case["seed"], device=device,
+                             gamma_search="gpu")
+        assert res.d == case["d"]
+        _check_run(res, case, name, exact=False)
