@@ -672,14 +672,13 @@ __global__ void __launch_bounds__(kThreads, NW <= 2 ? MDG_MINBLK_SMALL : 4) tab_
                 uint32_t stop = 0;
                 uint64_t t = 0;
                 if (lane == 0) {
-                    // early exit: the global bound already meets stop_at
+                    // the next tile (dynamic scheduler: uniform tiles, no static tail) and the
+                    // global best, fetched together; early exit once the best meets stop_at
+                    // -- a tile claimed then is simply not evaluated
+                    t = a.tile_lo + gridDim.x + atomicAdd(a.counter, 1ull);
                     unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
                     gw = uint32_t(g >> kKeyShift);
-                    stop = gw <= stop_at;
-                    if (!stop) { // dynamic tile scheduler: uniform tiles, no static tail
-                        t = a.tile_lo + gridDim.x + atomicAdd(a.counter, 1ull);
-                        stop = t >= a.tile_hi;
-                    }
+                    stop = gw <= stop_at || t >= a.tile_hi;
                 }
                 stop = __shfl_sync(0xFFFFFFFFu, stop, 0);
                 t = __shfl_sync(0xFFFFFFFFu, t, 0);
