@@ -15,6 +15,7 @@ importing this package raises if ``libmdg.so`` is missing.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 import os
 from dataclasses import dataclass, field
 from typing import Callable, Optional
@@ -484,78 +485,102 @@ def nccl_unique_id() -> bytes:
 
 
 # ------------------------------------------------------------------ runs
-@dataclass
 class RunResult:
-    d: int
-    capped: bool
-    n: int
-    k: int
-    m: int
-    k_last: int
-    g_final: int
-    witness_ok: bool
-    combinations: int
-    evaluated: int
-    row_additions: int
-    wall_seconds: float
-    device_seconds: float
-    gamma_seconds: float
-    loop_seconds: float
-    launches: int
-    h2d_bytes: int
-    d2h_bytes: int
-    rounds: list            # [c, j, w, U_after]
-    round_bounded: list     # per executed round: 1 when w is only the bound U (pruned round)
-    round_evaluated: list   # per executed round: codewords evaluated (this rank)
-    round_ms: list          # per executed round: kernel time (CUDA events)
-    levels: list            # [c, L_after, U_after]
-    column_perm: list
-    gamma_hash: list
-    witness: Optional[np.ndarray]
-    json: str
+    """One min_weight / bz_loop / brute-force run. Scalars come with the result; the per-round
+    and per-level traces, column_perm, Gamma hashes, witness and JSON record are read from
+    the C run object on first use (it is freed with this object)."""
+
+    _SCALARS = ("d", "capped", "n", "k", "m", "k_last", "g_final", "witness_ok", "combinations",
+                "evaluated", "row_additions", "wall_seconds", "device_seconds", "gamma_seconds",
+                "loop_seconds", "launches", "h2d_bytes", "d2h_bytes")
+
+    def __init__(self, h):
+        info = _RunInfo()
+        _check(lib().mdg_run_info_get(h, C.byref(info)))
+        self._h = h
+        self._info = info
+        self._fin = weakref.finalize(self, lib().mdg_run_free, h)
+        self._cache = {}
+        for f in self._SCALARS:
+            v = getattr(info, f)
+            setattr(self, f, bool(v) if f in ("capped", "witness_ok") else v)
+
+    def _rounds(self):
+        if "rounds" not in self._cache:
+            nr = self._info.n_rounds
+            rr = (_RoundRec * max(1, nr))()
+            _check(lib().mdg_run_rounds(self._h, rr))
+            pe = np.zeros(max(1, nr), dtype=np.uint64)
+            pm = np.zeros(max(1, nr), dtype=np.float64)
+            _check(lib().mdg_run_round_perf(self._h, pe, pm))
+            self._cache["rounds"] = ([[r.c, r.j, r.w, r.U_after] for r in rr[:nr]],
+                                     [int(r.bounded) for r in rr[:nr]],
+                                     [int(x) for x in pe[:nr]], [float(x) for x in pm[:nr]])
+        return self._cache["rounds"]
+
+    @property
+    def rounds(self) -> list:            # [c, j, w, U_after]
+        return self._rounds()[0]
+
+    @property
+    def round_bounded(self) -> list:     # per executed round: 1 when w is only the bound U
+        return self._rounds()[1]
+
+    @property
+    def round_evaluated(self) -> list:   # per executed round: codewords evaluated (this rank)
+        return self._rounds()[2]
+
+    @property
+    def round_ms(self) -> list:          # per executed round: kernel time
+        return self._rounds()[3]
+
+    @property
+    def levels(self) -> list:            # [c, L_after, U_after]
+        if "levels" not in self._cache:
+            nl = self._info.n_levels
+            ll = (_LevelRec * max(1, nl))()
+            _check(lib().mdg_run_levels(self._h, ll))
+            self._cache["levels"] = [[x.c, x.L_after, x.U_after] for x in ll[:nl]]
+        return self._cache["levels"]
+
+    @property
+    def column_perm(self) -> list:
+        if "perm" not in self._cache:
+            perm = np.zeros(max(1, self.n), dtype=np.uint32)
+            _check(lib().mdg_run_perm(self._h, perm))
+            self._cache["perm"] = [int(x) for x in perm[: self.n]]
+        return self._cache["perm"]
+
+    @property
+    def gamma_hash(self) -> list:
+        if "hash" not in self._cache:
+            self._cache["hash"] = ["%016x" % lib().mdg_run_gamma_hash(self._h, j) for j in range(self.m)]
+        return self._cache["hash"]
+
+    @property
+    def witness(self) -> Optional[np.ndarray]:
+        if "witness" not in self._cache:
+            wit = np.zeros(words(self.n), dtype=np.uint64)
+            self._cache["witness"] = wit if lib().mdg_run_witness(self._h, wit) == 0 else None
+        return self._cache["witness"]
+
+    @property
+    def json(self) -> str:
+        """The CLI's JSON record of this run (mdg_run_json)."""
+        if "json" not in self._cache:
+            cap = 1 << 12
+            while True:
+                buf = C.create_string_buffer(cap)
+                ln = lib().mdg_run_json(self._h, buf, cap)
+                if ln >= 0:
+                    break
+                cap = -ln + 16
+            self._cache["json"] = buf.value.decode()
+        return self._cache["json"]
 
 
 def _collect(h) -> RunResult:
-    L = lib()
-    info = _RunInfo()
-    _check(L.mdg_run_info_get(h, C.byref(info)))
-    rr = (_RoundRec * max(1, info.n_rounds))()
-    ll = (_LevelRec * max(1, info.n_levels))()
-    _check(L.mdg_run_rounds(h, rr))
-    _check(L.mdg_run_levels(h, ll))
-    perm = np.zeros(max(1, info.n), dtype=np.uint32)
-    _check(L.mdg_run_perm(h, perm))
-    pe = np.zeros(max(1, info.n_rounds), dtype=np.uint64)
-    pm = np.zeros(max(1, info.n_rounds), dtype=np.float64)
-    _check(L.mdg_run_round_perf(h, pe, pm))
-    wit = np.zeros(words(info.n), dtype=np.uint64)
-    has_w = L.mdg_run_witness(h, wit) == 0
-    cap = 1 << 16
-    while True:
-        buf = C.create_string_buffer(cap)
-        ln = L.mdg_run_json(h, buf, cap)
-        if ln >= 0:
-            break
-        cap = -ln + 16
-    res = RunResult(
-        d=info.d, capped=bool(info.capped), n=info.n, k=info.k, m=info.m, k_last=info.k_last,
-        g_final=info.g_final, witness_ok=bool(info.witness_ok), combinations=info.combinations,
-        evaluated=info.evaluated, row_additions=info.row_additions,
-        wall_seconds=info.wall_seconds, device_seconds=info.device_seconds,
-        gamma_seconds=info.gamma_seconds, loop_seconds=info.loop_seconds,
-        launches=info.launches, h2d_bytes=info.h2d_bytes, d2h_bytes=info.d2h_bytes,
-        rounds=[[r.c, r.j, r.w, r.U_after] for r in rr[: info.n_rounds]],
-        round_bounded=[int(r.bounded) for r in rr[: info.n_rounds]],
-        round_evaluated=[int(x) for x in pe[: info.n_rounds]],
-        round_ms=[float(x) for x in pm[: info.n_rounds]],
-        levels=[[x.c, x.L_after, x.U_after] for x in ll[: info.n_levels]],
-        column_perm=[int(x) for x in perm[: info.n]],
-        gamma_hash=["%016x" % L.mdg_run_gamma_hash(h, j) for j in range(info.m)],
-        witness=wit if has_w else None,
-        json=buf.value.decode(),
-    )
-    L.mdg_run_free(h)
-    return res
+    return RunResult(h)
 
 
 def _config(trials, seed, level_cap, kernel, witness, exact_rounds=False,

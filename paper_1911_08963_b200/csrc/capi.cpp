@@ -669,13 +669,24 @@ int mdg_min_weight_batch(mdg_ctx* ctx, uint32_t count, const uint64_t* const* G,
         while (ctx->extra.size() + 1 < S) ctx->extra.push_back(std::make_unique<Engine>(dev));
         std::vector<std::unique_ptr<mdg_run>> runs(count);
         std::vector<std::exception_ptr> errs(S);
+        static const bool timing = std::getenv("MDG_TIMING") != nullptr;
+        const auto t_batch = std::chrono::steady_clock::now();
         std::atomic<uint32_t> next{0};
         auto worker = [&](uint32_t w) {
             Engine& eng = w == 0 ? *ctx->eng : *ctx->extra[w - 1];
             try {
                 for (uint32_t i; (i = next.fetch_add(1)) < count;) {
+                    const auto ts = std::chrono::steady_clock::now();
                     BitMatrix M = from_rows(G[i], k[i], n[i]);
                     runs[i] = min_weight_device(eng, M, cf[i], 0, 1, nullptr, nullptr);
+                    if (timing) {
+                        auto us = [&](std::chrono::steady_clock::time_point x) {
+                            return std::chrono::duration<double>(x - t_batch).count() * 1e6;
+                        };
+                        const double end = us(std::chrono::steady_clock::now());
+                        std::fprintf(stderr, "[mdg batch] code %u worker %u start %.0f gamma %.0f loop %.0f end %.0f us\n",
+                                     i, w, us(ts), runs[i]->gamma_s * 1e6, runs[i]->loop_s * 1e6, end);
+                    }
                 }
             } catch (...) {
                 errs[w] = std::current_exception();

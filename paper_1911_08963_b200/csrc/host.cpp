@@ -15,6 +15,7 @@
 
 #include <condition_variable>
 #include <functional>
+#include <memory>
 #include <mutex>
 
 #include "mdg.hpp"
@@ -32,80 +33,91 @@ public:
     }
     unsigned size() const { return unsigned(workers_.size()) + 1; }
     // runs fn(i) for i in [0, n) on the pool and the calling thread; rethrows the first
-    // error. A caller that finds the pool busy (another thread's search) runs serially.
+    // error. Several callers (e.g. the batch front door's workers) may run jobs at once:
+    // idle pool threads take items from any open job.
     void run(uint32_t n, const std::function<void(uint32_t)>& fn) {
-        std::unique_lock<std::mutex> busy(run_m_, std::try_to_lock);
-        if (!busy.owns_lock()) {
-            for (uint32_t i = 0; i < n; ++i) fn(i);
-            return;
+        if (n == 0) return;
+        auto job = std::make_shared<Job>();
+        job->fn = &fn;
+        job->n = n;
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            jobs_.push_back(job);
         }
-        std::unique_lock<std::mutex> lk(m_);
-        job_ = &fn;
-        n_ = n;
-        next_.store(0);
-        pending_ = unsigned(workers_.size());
-        err_ = nullptr;
-        ++gen_;
         cv_.notify_all();
-        lk.unlock();
-        drain();
-        lk.lock();
-        done_cv_.wait(lk, [&] { return pending_ == 0; });
-        job_ = nullptr;
-        if (err_) std::rethrow_exception(err_);
+        job->drain();
+        {
+            std::unique_lock<std::mutex> lk(job->m);
+            job->cv.wait(lk, [&] { return job->done.load() == job->n; });
+        }
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            jobs_.erase(std::remove(jobs_.begin(), jobs_.end(), job), jobs_.end());
+        }
+        if (job->err) std::rethrow_exception(job->err);
     }
     ~HostPool() {
         {
             std::lock_guard<std::mutex> lk(m_);
             stop_ = true;
-            ++gen_;
         }
         cv_.notify_all();
         for (auto& t : workers_) t.join();
     }
 
 private:
+    struct Job {
+        const std::function<void(uint32_t)>* fn = nullptr;
+        uint32_t n = 0;
+        std::atomic<uint32_t> next{0}, done{0};
+        std::mutex m;
+        std::condition_variable cv;
+        std::exception_ptr err;
+        bool open() const { return next.load() < n; }
+        void drain() {
+            for (uint32_t i; (i = next.fetch_add(1)) < n;) {
+                try {
+                    (*fn)(i);
+                } catch (...) {
+                    std::lock_guard<std::mutex> lk(m);
+                    if (!err) err = std::current_exception();
+                }
+                if (done.fetch_add(1) + 1 == n) {
+                    std::lock_guard<std::mutex> lk(m);
+                    cv.notify_all();
+                }
+            }
+        }
+    };
     HostPool() {
         unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         if (const char* e = std::getenv("MDG_HOST_THREADS")) hw = unsigned(std::max(1, std::atoi(e)));
         hw = std::min(hw, 16u);
         for (unsigned i = 1; i < hw; ++i) workers_.emplace_back([this] { loop(); });
     }
-    void drain() {
-        for (uint32_t i; (i = next_.fetch_add(1)) < n_;) {
-            try {
-                (*job_)(i);
-            } catch (...) {
-                std::lock_guard<std::mutex> lk(m_);
-                if (!err_) err_ = std::current_exception();
-            }
-        }
-    }
     void loop() {
-        uint64_t seen = 0;
         for (;;) {
+            std::shared_ptr<Job> job;
             {
                 std::unique_lock<std::mutex> lk(m_);
-                cv_.wait(lk, [&] { return gen_ != seen; });
-                seen = gen_;
+                cv_.wait(lk, [&] {
+                    if (stop_) return true;
+                    for (const auto& j : jobs_)
+                        if (j->open()) return true;
+                    return false;
+                });
                 if (stop_) return;
+                for (const auto& j : jobs_)
+                    if (j->open()) { job = j; break; }
             }
-            drain();
-            std::lock_guard<std::mutex> lk(m_);
-            if (--pending_ == 0) done_cv_.notify_all();
+            if (job) job->drain();
         }
     }
     std::vector<std::thread> workers_;
-    std::mutex run_m_;
     std::mutex m_;
-    std::condition_variable cv_, done_cv_;
-    const std::function<void(uint32_t)>* job_ = nullptr;
-    uint32_t n_ = 0;
-    std::atomic<uint32_t> next_{0};
-    unsigned pending_ = 0;
-    uint64_t gen_ = 0;
+    std::condition_variable cv_;
+    std::vector<std::shared_ptr<Job>> jobs_;
     bool stop_ = false;
-    std::exception_ptr err_;
 };
 } // namespace
 
