@@ -7,10 +7,14 @@ codes. Metric: codewords evaluated per second (BASELINE.json `metric`).
 
 * value  — device-resident: the level loops over Gamma sets already in HBM
            (mdg_bz_loop_device, one context per code, --streams codes in flight
-           on one GPU), CUDA events around each whole step (host gaps
-           included); codewords / time, max over ranks for the time.
-* e2e    — the public front door from host matrices (mdg_min_weight_batch on
-           one GPU, mdg_min_weight_dist per code across ranks): row basis +
+           per GPU), CUDA events around each whole step (host gaps included);
+           codewords / time, max over ranks for the time. Under torchrun the
+           eight codes are sharded across ranks (rank r owns codes r, r+N, ...;
+           independent objects, no data-path collective); config.round_split
+           reports SURVEY.md §8e's split of one code's rounds across the ranks
+           (mdg_min_weight_dist, NCCL allreduce(min) per round) beside it.
+* e2e    — the public front door from host matrices (mdg_min_weight_batch over
+           the rank's codes): row basis +
            Gamma search on the host, H2D of the Gammas, the device loop, D2H of
            every round result and the witness; CUDA-event timed the same way.
 * roofline — the dominant kernel (tab_round on the c = 7 rounds, measured in a
@@ -204,40 +208,35 @@ def main():
         gold = {c["name"]: c for c in json.load(f)["data"]}
     expect_d = [gold[f"cfg2_s{s}"]["d"] for s in SEEDS]
 
-    # one context per code (Gamma set resident in HBM), plus the host matrices
-    Gs = [mdg.gen_matrix(N, K, s, True) for s in SEEDS]
-    gsets = [mdg.GammaSet.build(G, N, 10, s) for G, s in zip(Gs, SEEDS)]
-    devs = [mdg.Device(local) for _ in SEEDS]
-    if world > 1:
-        for d in devs:  # one communicator per context (its own stream)
-            u = mdg.nccl_unique_id() if rank == 0 else None
-            o = [u]
-            dist.broadcast_object_list(o, src=0)
-            d.nccl_init(o[0], rank, world)
+    # Codes are independent objects: rank r owns codes r, r + N, ... (no data-path
+    # collective; the 8-code step is fixed, so scaling is strong). One context per owned
+    # code with its Gamma set resident in HBM, plus the host matrices.
+    mine = [i for i in range(len(SEEDS)) if i % world == rank]
+    Gs = [mdg.gen_matrix(N, K, SEEDS[i], True) for i in mine]
+    gsets = [mdg.GammaSet.build(G, N, 10, SEEDS[i]) for G, i in zip(Gs, mine)]
+    devs = [mdg.Device(local) for _ in mine]
     for d, gs in zip(devs, gsets):
         d.load_gset(gs)
+    anchor = devs[0] if devs else mdg.Device(local)
 
     from concurrent.futures import ThreadPoolExecutor
     pool = ThreadPoolExecutor(max_workers=max(1, args.streams))
 
-    def one_loop(i):
-        d, gs = devs[i], gsets[i]
-        if world > 1:
-            r = d.bz_loop(gs, kernel=kernel, rank=rank, world=world, reduce_min="nccl")
-        else:
-            r = d.bz_loop(gs, kernel=kernel)
+    def one_loop(x):
+        d, gs, i = devs[x], gsets[x], mine[x]
+        r = d.bz_loop(gs, kernel=kernel)
         if r.d != expect_d[i] or not r.witness_ok:
             raise SystemExit(f"parity failure on seed {SEEDS[i]}: d={r.d} expected {expect_d[i]}")
         return r
 
     def device_step():
-        """All eight level loops over the resident Gamma sets: with --streams > 1 (single
-        GPU) up to that many codes run at once, each context on its own stream (ctypes
-        releases the GIL); CUDA events on the torch stream bracket the whole step."""
+        """This rank's level loops over the resident Gamma sets: with --streams > 1 up to that
+        many codes run at once, each context on its own stream (ctypes releases the GIL);
+        CUDA events on the torch stream bracket the whole step."""
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-        if world > 1 or args.streams <= 1:
-            runs = [one_loop(i) for i in range(len(devs))]
+        if args.streams <= 1:
+            runs = [one_loop(x) for x in range(len(devs))]
         else:
             runs = list(pool.map(one_loop, range(len(devs))))
         ev1.record()
@@ -248,8 +247,8 @@ def main():
         """The dominant kernel alone (roofline): level-7 rounds of each code, loops run one
         after another so every launch has the GPU to itself."""
         c7_cw, c7_ms = 0, 0.0
-        for i in range(len(devs)):
-            r = one_loop(i)
+        for x in range(len(devs)):
+            r = one_loop(x)
             for (c, j, w, U), ev, ms in zip(r.rounds, r.round_evaluated, r.round_ms):
                 if c == 7:
                     c7_cw += ev
@@ -293,7 +292,7 @@ def main():
     # BASELINE.md's roofline case: the config-2 level-7 round with early exit and bound
     # pruning off (exact minimum of all C(64,7) codewords), seed 1, Gamma_0
     ex_ms = []
-    if world == 1:
+    if rank == 0 and devs:
         devs[0].set_pruning(False)
         for _ in range(3):
             l2_flush()
@@ -302,9 +301,9 @@ def main():
         ex_cw = o.evaluated
         devs[0].set_pruning(True)
 
-    # e2e through the public front door from host buffers (pinned copies of G): the batch
-    # call (mdg_min_weight_batch, --streams codes in flight) on one GPU, mdg_min_weight_dist
-    # per code across ranks; CUDA events on the torch stream bracket each step
+    # e2e through the public front door from host buffers (pinned copies of G): this rank's
+    # codes through mdg_min_weight_batch (--streams codes in flight); CUDA events on the
+    # torch stream bracket each step, max over ranks
     e2e_ms, e2e_cw, h2d, d2h = [], 0, 0, 0
     Gpin = [torch.from_numpy(G).pin_memory().numpy() for G in Gs]
     for step in range(args.warmup + args.steps):
@@ -312,23 +311,53 @@ def main():
         barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-        if world > 1:
-            runs = [mdg.min_weight_dist(G, N, rank, world, "nccl", trials=10, seed=SEEDS[i],
-                                        kernel=kernel, device=devs[i]) for i, G in enumerate(Gpin)]
-        else:
-            runs = mdg.min_weight_batch(Gpin, N, trials=10, seed=SEEDS, kernel=kernel,
-                                        device=devs[0], streams=args.streams)
+        runs = mdg.min_weight_batch(Gpin, N, trials=10, seed=[SEEDS[i] for i in mine], kernel=kernel,
+                                    device=anchor, streams=args.streams)
         ev1.record()
         torch.cuda.synchronize()
-        for i, r in enumerate(runs):
-            if r.d != expect_d[i] or not r.witness_ok:
-                raise SystemExit(f"e2e parity failure on seed {SEEDS[i]}")
+        for x, r in enumerate(runs):
+            if r.d != expect_d[mine[x]] or not r.witness_ok:
+                raise SystemExit(f"e2e parity failure on seed {SEEDS[mine[x]]}")
         barrier()
         if step >= args.warmup:
             e2e_ms.append(ev0.elapsed_time(ev1))
             e2e_cw += sum(r.evaluated for r in runs)
             h2d += sum(r.h2d_bytes for r in runs)
             d2h += sum(r.d2h_bytes for r in runs)
+
+    # SURVEY.md §8e's split of ONE code: every round's tiles divided across the ranks and the
+    # per-round key combined by an in-stream NCCL allreduce(min) (mdg_min_weight_dist);
+    # reported beside the sharded throughput, not part of it
+    split = None
+    if world > 1:
+        try:
+            sd = mdg.Device(local)
+            u = [mdg.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(u, src=0)
+            sd.nccl_init(u[0], rank, world)
+            G1 = mdg.gen_matrix(N, K, SEEDS[0], True)
+            sms_ = []
+            for step in range(args.warmup + args.steps):
+                barrier()
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record()
+                r = mdg.min_weight_dist(G1, N, rank, world, "nccl", trials=10, seed=SEEDS[0],
+                                        kernel=kernel, device=sd)
+                ev1.record()
+                torch.cuda.synchronize()
+                if r.d != expect_d[0] or not r.witness_ok:
+                    raise RuntimeError("round-split parity failure")
+                if step >= args.warmup:
+                    sms_.append(ev0.elapsed_time(ev1))
+            t = torch.tensor([max(sms_)], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            split = {"what": "config-2 seed 1 through mdg_min_weight_dist: each round's tiles split "
+                             f"across {world} ranks, NCCL allreduce(min) of the round key in stream",
+                     "ms_per_code": float(t.item()), "codewords": int(r.combinations),
+                     "cw_per_s": r.combinations / (float(t.item()) * 1e-3)}
+            sd.close()
+        except Exception as e:  # reported, never fatal
+            split = {"error": str(e)[:200]}
     clocks = sampler.stop()
 
     # max over ranks of time, sum over ranks of codewords
@@ -403,8 +432,11 @@ def main():
             "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (mt19937_64 seeds 1..8, SURVEY.md §8d)",
             "config": {"workload": WORKLOAD, "kernel": args.kernel,
-                       "parallelism": (f"rank-range split x{world}" if world > 1 else
+                       "parallelism": (f"{world} ranks, codes sharded (rank r owns codes r, r+{world}, ...), "
+                                       f"{args.streams} in flight per GPU; no data-path collective"
+                                       if world > 1 else
                                        f"single GPU, {min(args.streams, len(SEEDS))} codes in flight"),
+                       "round_split": split,
                        "l2": "flushed between steps (256 MiB write); working set < 1 MiB",
                        "codewords_per_step": cw_total // args.steps,
                        "ms_per_code_amortized": tot_ms / args.steps / len(SEEDS),
@@ -412,8 +444,7 @@ def main():
             "e2e": {"value": e2e_value, "unit": "cw/s", "h2d_bytes_per_step": h2d // args.steps,
                     "d2h_bytes_per_step": d2h // args.steps,
                     "ms_per_step": tot_e2e / args.steps,
-                    "path": ("mdg_min_weight_dist per code (C ABI)" if world > 1 else
-                             "mdg_min_weight_batch (C ABI)") +
+                    "path": "mdg_min_weight_batch (C ABI)" +
                             " from pinned host matrices: row basis + Gamma search + H2D + level loop"
                             " + witness + D2H"},
             "roofline": roofline,
