@@ -178,6 +178,9 @@ typedef struct {
     int gamma_search;     /* MDG_GAMMA_HOST: the permutation trials on host threads;
                              MDG_GAMMA_GPU: on the device (mdg_gset_build_gpu) -- the same
                              Gamma set for the same trials and seed, faster for many trials */
+    uint64_t split_min;   /* multi-rank runs: rounds of >= split_min codewords are split across
+                             the ranks and their keys reduced; smaller rounds run whole on every
+                             rank (identical results, no exchange). 0 = 2e8; 1 = split all */
 } mdg_config;
 #define MDG_GAMMA_HOST 0
 #define MDG_GAMMA_GPU 1

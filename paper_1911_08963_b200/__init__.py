@@ -68,7 +68,7 @@ class _RoundOut(C.Structure):
 class _Config(C.Structure):
     _fields_ = [("trials", C.c_uint32), ("seed", C.c_uint64), ("level_cap", C.c_uint32),
                 ("kernel", C.c_int), ("want_witness", C.c_int), ("exact_rounds", C.c_int),
-                ("gamma_search", C.c_int)]
+                ("gamma_search", C.c_int), ("split_min", C.c_uint64)]
 
 
 class _RunInfo(C.Structure):
@@ -460,10 +460,13 @@ class Device:
 
     def bz_loop(self, gs: "GammaSet", level_cap: int = 0, kernel: int = KERNEL_TAB,
                 witness: bool = True, rank: int = 0, world: int = 1,
-                reduce_min: Callable | str | None = None, exact_rounds: bool = False) -> "RunResult":
+                reduce_min: Callable | str | None = None, exact_rounds: bool = False,
+                split_min: int = 0) -> "RunResult":
         """run_bz_loop on the device over the Gamma set loaded with load_gset (no search,
-        no upload): the device-resident level loop (+ witness)."""
+        no upload): the device-resident level loop (+ witness). world > 1: see
+        min_weight_dist (split_min)."""
         cfg = _config(0, 0, level_cap, kernel, witness, exact_rounds)
+        cfg.split_min = split_min
         h = C.c_void_p()
         if world == 1:
             _check(lib().mdg_bz_loop_device(self._h, gs._h, C.byref(cfg), C.byref(h)))
@@ -643,13 +646,17 @@ def min_weight_dist(G: np.ndarray, n: int, rank: int, world: int,
                     reduce_min: Callable[[np.ndarray], np.ndarray] | str = "nccl",
                     trials: int = 10, seed: int = 0, level_cap: int = 0,
                     kernel: int = KERNEL_TAB, witness: bool = True,
-                    device: Optional[Device] = None, exact_rounds: bool = False) -> RunResult:
-    """Multi-GPU min_weight: each rank evaluates a contiguous task range of every round;
-    the per-round key is combined by NCCL allreduce(min) (reduce_min='nccl', device must have
-    called nccl_init) or by a Python callable (numpy uint64 array -> elementwise global min)."""
+                    device: Optional[Device] = None, exact_rounds: bool = False,
+                    split_min: int = 0) -> RunResult:
+    """Multi-GPU min_weight: each rank evaluates a contiguous task range of every round of at
+    least split_min codewords (0 = 2e8, 1 = every round; smaller rounds run whole on every
+    rank); the per-round key is combined by NCCL allreduce(min) (reduce_min='nccl', device
+    must have called nccl_init) or by a Python callable (numpy uint64 array -> elementwise
+    global min)."""
     G = _rows(G)
     h = C.c_void_p()
     cfg = _config(trials, seed, level_cap, kernel, witness, exact_rounds)
+    cfg.split_min = split_min
     fn, user, keep = _reducer(reduce_min, device)
     _check(lib().mdg_min_weight_dist(device.handle if device else None, G, G.shape[0], n,
                                      C.byref(cfg), rank, world, fn, user, C.byref(h)))

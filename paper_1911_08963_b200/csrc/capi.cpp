@@ -164,9 +164,11 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
     eng.set_kernel(cfg.kernel == MDG_KERNEL_RD ? Kernel::rd : Kernel::tab);
     Engine::Counters c0 = eng.counters();
     std::vector<RoundLog> log;
+    const uint64_t split_min = cfg.split_min ? cfg.split_min : uint64_t(200000000);
     auto do_round = [&](uint32_t j, uint32_t g, uint32_t stop_at, uint32_t cutoff) {
         RoundResult rr;
-        if (world <= 1) {
+        // a round below split_min codewords runs whole on every rank: no exchange
+        if (world <= 1 || double(binomial(k, g)) < double(split_min)) {
             rr = eng.round(j, g, stop_at, 0, UINT64_MAX, cutoff);
         } else {
             uint64_t T = eng.tasks(j, g);
@@ -206,7 +208,7 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
         // with the NCCL reducer the per-round allreduce(min) is enqueued in-stream
         Engine::ChainResult cr = eng.chain_loop(bounds.upper, bounds.lower, cfg.level_cap,
                                                 cfg.exact_rounds != 0, gs.k_last, rank, world,
-                                                nccl_reduce);
+                                                nccl_reduce, split_min);
         EngineResult& er = out.er;
         uint32_t U = bounds.upper;
         for (const auto& r : cr.rounds) {
@@ -621,6 +623,7 @@ void mdg_config_default(mdg_config* cfg) {
     cfg->want_witness = 1;
     cfg->exact_rounds = 0;
     cfg->gamma_search = MDG_GAMMA_HOST;
+    cfg->split_min = 0;
 }
 
 int mdg_min_weight(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n, const mdg_config* cfg,

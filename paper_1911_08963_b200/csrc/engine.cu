@@ -2119,7 +2119,7 @@ std::vector<uint32_t> Engine::witness(uint32_t j, uint32_t c, const RoundResult&
 
 Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_cap, bool exact,
                                        uint32_t k_last, uint32_t rank, uint32_t world,
-                                       bool allreduce) {
+                                       bool allreduce, uint64_t split_min) {
     if (kernel_ != Kernel::tab) throw std::logic_error("chain_loop: tab kernel only");
     allreduce = allreduce || world > 1;
     if (allreduce && !impl_->comm) throw std::logic_error("chain_loop: NCCL communicator not initialised");
@@ -2189,11 +2189,14 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
             unsigned long long* slot = im.take_slot();
             TabArgs a = tab_args(im, gd, pe, yt, k_, g);
             const uint64_t T = pe.plan.tiles();
+            // a round below split_min codewords runs whole on every rank: the same result
+            // everywhere with no exchange (the split would cost more in reduction latency)
+            const bool split = allreduce && double(binomial(k_, g)) >= double(split_min);
             a.st = im.d_state;
-            a.tile_lo = world > 1 ? T * rank / world : 0;
-            a.tile_hi = world > 1 ? T * (rank + 1) / world : T;
+            a.tile_lo = split ? T * rank / world : 0;
+            a.tile_hi = split ? T * (rank + 1) / world : T;
             a.best_key = slot; a.evaluated = slot + 1; a.counter = slot + 2;
-            const bool fuse = !allreduce && a.tile_hi > a.tile_lo;
+            const bool fuse = !split && a.tile_hi > a.tile_lo;
             if (fuse) { // the round kernel's last block closes the round: one launch per round
                 a.fin_st = im.d_state;
                 a.fin_rec = im.d_recs + nrec;
@@ -2213,7 +2216,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
                 after_round = im.cnt.launches;
                 synced = false;
             }
-            if (allreduce) {
+            if (split) {
                 int rc = nccl().AllReduce(slot, slot, 1, kNcclUint64, kNcclMin, im.comm, im.stream);
                 if (rc != 0) throw std::runtime_error(std::string("ncclAllReduce: ") + nccl().GetErrorString(rc));
             }
@@ -2224,7 +2227,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
                 im.cnt.launches += 1;
             }
             ++nrec;
-            pending += double(binomial(k_, g)) / world;
+            pending += double(binomial(k_, g)) / (split ? world : 1);
         }
         ++g;
         if (pending >= kCheckWork || g > k_ || (level_cap && g > level_cap)) {

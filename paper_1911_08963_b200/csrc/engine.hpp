@@ -96,9 +96,11 @@ public:
     };
     BruteResult brute_force(uint32_t k, uint32_t n, const uint64_t* rows);
 
+    // split_min: with world > 1 only rounds of >= split_min codewords are divided across
+    // the ranks (and reduced); smaller rounds run whole on every rank.
     ChainResult chain_loop(uint32_t U0, uint32_t L0, uint32_t level_cap, bool exact,
                            uint32_t k_last, uint32_t rank = 0, uint32_t world = 1,
-                           bool allreduce = false);
+                           bool allreduce = false, uint64_t split_min = 1);
     std::vector<uint32_t> witness(uint32_t j, uint32_t c, const RoundResult& rr);
 
     // NCCL (loaded at runtime) for the multi-GPU reduction

@@ -279,21 +279,38 @@ def test_dist_two_ranks_threaded(mdg):
             return out
         return red
 
-    def worker(rank):
-        dev = mdg.Device(0)
-        results[rank] = mdg.min_weight_dist(rows, g["n"], rank, world, reducer_for(rank),
-                                            trials=10, seed=g["seed"], device=dev)
-        dev.close()
+    calls = [0] * world
 
-    ts = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
-    for t in ts:
-        t.start()
-    for t in ts:
-        t.join()
-    for r in range(world):
-        res = results[r]
-        assert res.d == case["d"]
-        _check_run(res, case, f"rank{r}", exact=False)
+    def counting(rank, red):
+        def f(keys):
+            calls[rank] += 1
+            return red(keys)
+        return f
+
+    for split_min in (1, 0, 10**6):  # every round split / default (none here) / from level 5
+        calls[:] = [0] * world
+
+        def worker(rank):
+            dev = mdg.Device(0)
+            results[rank] = mdg.min_weight_dist(rows, g["n"], rank, world,
+                                                counting(rank, reducer_for(rank)), trials=10,
+                                                seed=g["seed"], device=dev, split_min=split_min)
+            dev.close()
+
+        ts = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        for r in range(world):
+            res = results[r]
+            assert res.d == case["d"]
+            _check_run(res, case, f"rank{r}", exact=False)
+        split_rounds = sum(1 for c, j, w, U in case["rounds"] if comb(64, c) >= max(split_min, 1)) \
+            if split_min else 0
+        assert calls[0] == calls[1] >= split_rounds, (split_min, calls)
+        if split_min == 0:
+            assert calls == [0, 0]  # cfg2 seed 8 never reaches 2e8-codeword rounds
 
 
 # ------------------------------------------------------------ brute force
@@ -326,9 +343,11 @@ def test_nccl_single_rank(mdg):
     rows = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
     dev = mdg.Device(0)
     dev.nccl_init(mdg.nccl_unique_id(), 0, 1)
-    res = mdg.min_weight_dist(rows, g["n"], 0, 1, "nccl", trials=10, seed=g["seed"], device=dev)
-    assert res.d == case["d"]
-    _check_run(res, case, "nccl1", exact=False)
+    for split_min in (1, 0):  # every round through NCCL / the default (none at this size)
+        res = mdg.min_weight_dist(rows, g["n"], 0, 1, "nccl", trials=10, seed=g["seed"],
+                                  device=dev, split_min=split_min)
+        assert res.d == case["d"]
+        _check_run(res, case, "nccl1", exact=False)
     dev.close()
 
 
