@@ -383,7 +383,9 @@ def main():
         roofline = {
             "bound": "int_popc", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gcw/s",
             "frac": achieved / peak, "traffic": DRAM_BYTES_PER_LAUNCH, "traffic_unit": "DRAM bytes per launch (ncu)",
-            "kernel": "tab_round<2,false>, bound-pruned (cutoff U), level-7 rounds (621,216,192 codewords per launch)",
+            "kernel": ("tab_level<2,false>: both level-7 rounds of a code in one launch (2 x 621,216,192 "
+                       "codewords), bound-pruned (cutoff U); the per-round kernel tab_round<2,false> "
+                       "is the one profiled in profiles/r01e_tab_round_c7_ncu.txt (same inner loop)"),
             "peak_basis": ("measured B200 POPC (XU pipe) rate 16/clk/SM = 4.64e12/s "
                            "(tools/pipes_microbench.cu) / 1.035 XU ops per codeword executed by this "
                            "kernel (ncu, profiles/r01e_tab_round_c7_ncu.txt)"),

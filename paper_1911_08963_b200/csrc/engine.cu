@@ -726,6 +726,144 @@ __global__ void __launch_bounds__(kThreads, NW <= 2 ? MDG_MINBLK_SMALL : 4) tab_
     }
 }
 
+// ------------------------------------------------------- fused level
+// All m rounds of one level in one launch (chained loop, single rank, Gammas of one row
+// width): the tile space is the m rounds' tiles back to back (round-major), one shared
+// dynamic scheduler, one finalize (the last block closes the rounds in order, exactly as
+// run_bz_loop would). Round j prunes with min(U, best of rounds i < j) - 1 and its own best:
+// every round i < j has true minimum >= its best, so round j's result is exact whenever it
+// lies below U_before_j = min(U, w_0 .. w_{j-1}), and >= U_before_j otherwise -- the
+// sequential finalize then reproduces each bounded w_j and the (L, U) trace bit for bit.
+// A tile is skipped once some round i <= j has a best <= L (the reference would stop there:
+// that round's minimum is exactly L and the rounds after it hit the fast path).
+constexpr int kMaxFuse = 16;
+struct LevelRound {
+    const uint32_t* rows;
+    const uint32_t* ytab;
+    const uint32_t* xtab;
+    unsigned long long* slot; // {best key, evaluated, -, -, -}
+    ChainRec* rec;
+    int32_t fold_lim[3];
+    uint32_t id_rows, add_const;
+};
+struct LevelDesc {
+    uint32_t m;
+    uint64_t T; // tiles per round (one plan for all rounds)
+    LevelRound r[kMaxFuse];
+};
+
+template <int NW, bool HID>
+__global__ void __launch_bounds__(kThreads, NW <= 2 ? MDG_MINBLK_SMALL : 4)
+tab_level(TabArgs a, const __grid_constant__ LevelDesc L) {
+    constexpr int R = r_for(NW);
+    constexpr int YC = R * kThreads;
+    constexpr int XS = stride_for(NW + (HID ? 1 : 0));
+    __shared__ __align__(16) uint32_t xs[kTX * XS];
+    __shared__ TileInfo ti;
+    __shared__ TabArgs sa; // a with the current tile's round fields
+    __shared__ uint32_t cur_j, skip_tile;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t total = uint64_t(L.m) * L.T;
+    auto set_round = [&](uint32_t j) { // thread 0
+        const LevelRound& r = L.r[j];
+        sa.rows = r.rows;
+        sa.ytab = r.ytab;
+        sa.xtab = r.xtab;
+        sa.id_rows = r.id_rows;
+        sa.add_const = r.add_const;
+        sa.fold_lim[0] = r.fold_lim[0];
+        sa.fold_lim[1] = r.fold_lim[1];
+        sa.fold_lim[2] = r.fold_lim[2];
+        cur_j = j;
+    };
+    if (threadIdx.x == 0) {
+        sa = a;
+        set_round(uint32_t(uint64_t(blockIdx.x) / L.T));
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) decode_tile_warp<YC>(sa, uint64_t(blockIdx.x) % L.T, ti);
+    __syncthreads();
+    if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(sa, ti, threadIdx.x, xs + threadIdx.x * XS);
+    uint32_t Y[R][NW], idY[R];
+    bool valid[R];
+    load_suffixes<NW, HID>(sa, ti, Y, idY, valid);
+    griddep_wait();
+    const ChainState cs = *a.st;
+    const bool skip = cs.done || cs.U <= cs.L;
+    const uint32_t cutoff = cs.exact ? 0u : cs.U, stop_at = cs.L;
+    const bool exact = cs.exact != 0;
+    griddep_launch_dependents();
+    const bool dynamic = uint64_t(gridDim.x) < total;
+
+    for (bool first = true; !skip; first = false) {
+        if (!first) {
+            if (!dynamic) break;
+            if (threadIdx.x < 32) {
+                uint32_t stop = 0;
+                uint64_t t = 0;
+                if (lane == 0) {
+                    t = gridDim.x + atomicAdd(a.counter, 1ull);
+                    stop = t >= total;
+                    if (!stop && uint32_t(t / L.T) != cur_j) set_round(uint32_t(t / L.T));
+                }
+                stop = __shfl_sync(0xFFFFFFFFu, stop, 0);
+                t = __shfl_sync(0xFFFFFFFFu, t, 0);
+                __syncwarp();
+                if (!stop) decode_tile_warp<YC>(sa, t % L.T, ti);
+                if (lane == 0) ti.stop = stop;
+            }
+            __syncthreads();
+            if (ti.stop) break;
+        }
+        if (threadIdx.x == 0) {
+            // bests of rounds 0..j: own best (ties still evaluated) and, bounded, the earlier
+            // rounds' (strictly below them); skip once any is <= L
+            const uint32_t j = cur_j;
+            uint32_t own = uint32_t(*reinterpret_cast<volatile unsigned long long*>(L.r[j].slot) >> kKeyShift);
+            uint32_t prev = 0xFFFFFFFFu, lowest = own;
+            for (uint32_t i = 0; i < j; ++i) {
+                const uint32_t b = uint32_t(*reinterpret_cast<volatile unsigned long long*>(L.r[i].slot) >> kKeyShift);
+                prev = min(prev, b);
+            }
+            lowest = min(lowest, prev);
+            skip_tile = lowest <= stop_at;
+            int64_t lim = cutoff ? int64_t(cutoff) - 1 : int64_t(0x7FFFFFFF);
+            if (int64_t(own) < lim) lim = own;
+            if (!exact && prev != 0xFFFFFFFFu && int64_t(prev) - 1 < lim) lim = int64_t(prev) - 1;
+            lim -= sa.add_const;
+            ti.T = lim < -1 ? -1 : (lim > 0x7FFFFFFF ? 0x7FFFFFFF : int32_t(lim));
+            ti.G = pick_groups(ti.T, sa.fold_lim);
+            if (!skip_tile) atomicAdd(L.r[j].slot + 1, uint64_t(ti.nx) * ti.nyv);
+        }
+        __syncthreads();
+        if (!skip_tile) {
+            if (!first) {
+                if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(sa, ti, threadIdx.x, xs + threadIdx.x * XS);
+                load_suffixes<NW, HID>(sa, ti, Y, idY, valid);
+                __syncthreads();
+            }
+            const uint64_t tile = ti.tile;
+            const uint32_t add = sa.add_const;
+            unsigned long long* best_key = L.r[cur_j].slot;
+            uint32_t best = tile_min<NW, HID>(xs, 0, ti.nx, Y, idY, ti.T, ti.G);
+            if (best != 0xFFFFFFFFu) best += add;
+            best = __reduce_min_sync(0xFFFFFFFFu, best);
+            if (lane == 0 && best != 0xFFFFFFFFu && (cutoff == 0 || best < cutoff))
+                atomicMin(best_key, (static_cast<unsigned long long>(best) << kKeyShift) | tile);
+        }
+        __syncthreads(); // xs / ti / sa reused by the next tile
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(a.blocks_done, 1ull) == gridDim.x - 1) {
+            __threadfence();
+            for (uint32_t j = 0; j < L.m; ++j)
+                finalize_round(a.fin_st, L.r[j].slot, L.r[j].rec, a.fin_c, j, j + 1 == L.m ? 1u : 0u,
+                               a.fin_lb);
+        }
+    }
+}
+
 // One thread: close a chained round (engines.cpp:456-472 semantics).
 __global__ void chain_finalize(ChainState* st, const unsigned long long* slot, ChainRec* rec,
                                uint32_t c, uint32_t j, uint32_t last_of_level, uint32_t lb) {
@@ -1193,6 +1331,26 @@ struct TablesLaunch {
     static void run(const TableJobs& J, const uint64_t* T, cudaStream_t st) {
         uint64_t blocks = (J.total + 255) / 256;
         tables_build<NW, HID><<<dim3(uint32_t(blocks)), 256, 0, st>>>(J, T);
+    }
+};
+
+template <int NW, bool HID>
+struct LevelLaunch {
+    static void run(const TabArgs& a, const LevelDesc& L, uint64_t total, bool pdl, cudaStream_t st,
+                    int sms) {
+        static int occ = -1;
+        if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tab_level<NW, HID>, kThreads, 0);
+        const uint64_t g = std::max<uint64_t>(1, std::min<uint64_t>(total, uint64_t(sms) * std::max(occ, 1)));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(uint32_t(g));
+        cfg.blockDim = dim3(kThreads);
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = pdl ? 1 : 0;
+        cudaLaunchKernelEx(&cfg, tab_level<NW, HID>, a, L);
     }
 };
 
@@ -1673,6 +1831,7 @@ Engine::Engine(int device) : device_(device), impl_(new Impl) {
     CK(cudaGetDeviceProperties(&prop, device));
     sms_ = prop.multiProcessorCount;
     if (const char* e = std::getenv("MDG_PDL")) pdl_ = std::atoi(e) != 0;
+    if (const char* e = std::getenv("MDG_FUSE_MAX")) fuse_max_ = std::atof(e);
     CK(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&impl_->ev0));
     CK(cudaEventCreate(&impl_->ev1));
@@ -2182,7 +2341,53 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
             prebuild_tables(im, m_, k_, g, g, sms_);
             built_to = g;
         }
-        for (uint32_t j = 0; j < m_; ++j) {
+        // small levels of Gammas of one row width: all m rounds in one launch (tab_level)
+        bool fuse_level = !allreduce && m_ >= 2 && m_ <= uint32_t(kMaxFuse) && fuse_max_ > 0 &&
+                          double(m_) * double(binomial(k_, g)) <= fuse_max_;
+        for (uint32_t j = 1; fuse_level && j < m_; ++j)
+            fuse_level = im.gammas[j].nw == im.gammas[0].nw && im.gammas[j].hid == im.gammas[0].hid;
+        if (fuse_level) {
+            const GammaDev& g0 = im.gammas[0];
+            const PlanEntry& pe = im.plan(k_, g, g0, sms_);
+            LevelDesc L{};
+            L.m = m_;
+            L.T = pe.plan.tiles();
+            TabArgs a{};
+            for (uint32_t j = 0; j < m_; ++j) {
+                const GammaDev& gd = im.gammas[j];
+                uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
+                TabArgs aj = tab_args(im, gd, pe, yt, k_, g);
+                if (j == 0) a = aj;
+                LevelRound& r = L.r[j];
+                r.rows = aj.rows;
+                r.ytab = aj.ytab;
+                r.xtab = aj.xtab;
+                r.slot = im.take_slot();
+                r.rec = im.d_recs + nrec + j;
+                r.fold_lim[0] = aj.fold_lim[0];
+                r.fold_lim[1] = aj.fold_lim[1];
+                r.fold_lim[2] = aj.fold_lim[2];
+                r.id_rows = aj.id_rows;
+                r.add_const = aj.add_const;
+            }
+            unsigned long long* ls = im.take_slot(); // shared counter + blocks done
+            a.st = im.d_state;
+            a.counter = ls + 2;
+            a.blocks_done = ls + 4;
+            a.fin_st = im.d_state;
+            a.fin_c = g;
+            a.fin_lb = lb;
+            const bool pdl = pdl_ && im.cnt.launches == after_round && !synced;
+            const uint64_t total = uint64_t(m_) * L.T;
+            dispatch_nw_hid<LevelLaunch>(g0.nw, g0.hid, a, L, total, pdl, im.stream, sms_);
+            CK(cudaGetLastError());
+            im.cnt.launches += 1;
+            after_round = im.cnt.launches;
+            synced = false;
+            nrec += m_;
+            pending += double(m_) * double(binomial(k_, g));
+        }
+        for (uint32_t j = 0; j < m_ && !fuse_level; ++j) {
             const GammaDev& gd = im.gammas[j];
             const PlanEntry& pe = im.plan(k_, g, gd, sms_);
             uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);

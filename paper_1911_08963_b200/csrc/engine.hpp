@@ -133,6 +133,7 @@ private:
     void check_round(uint32_t j, uint32_t c) const;
     int device_ = 0, sms_ = 0;
     bool pdl_ = true; // programmatic dependent launch between chained rounds (MDG_PDL=0: off)
+    double fuse_max_ = 4e9; // chained levels up to this many codewords run as one launch (MDG_FUSE_MAX)
     uint32_t m_ = 0, k_ = 0, n_ = 0;
     Kernel kernel_ = Kernel::tab;
     std::unique_ptr<Impl> impl_;
