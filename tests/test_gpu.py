@@ -493,3 +493,31 @@ def test_min_weight_gpu_gamma_search(mdg, device):
                              gamma_search="gpu")
         assert res.d == case["d"]
         _check_run(res, case, name, exact=False)
+
+
+def test_fused_levels_equal_per_round_launches(mdg):
+    """Chained loops with fused levels (default) and with one launch per round
+    (MDG_FUSE_MAX=0) give identical traces, d and witness weights in both round modes."""
+    import os
+    fused = mdg.Device(0)
+    os.environ["MDG_FUSE_MAX"] = "0"
+    try:
+        single = mdg.Device(0)
+    finally:
+        del os.environ["MDG_FUSE_MAX"]
+    codes = []
+    for name in ("cfg1", "cfg2_s3", "cfg3"):
+        case = next(c for c in load_golden("configs") if c["name"] == name)
+        g = case["gen"]
+        codes.append((mdg.gen_matrix(g["n"], g["k"], g["seed"], True), g["n"], case["seed"]))
+    for case in load_golden("seeded")[:60]:
+        rows, n = mdg.parse_matrix(case["matrix"])
+        codes.append((rows, n, case["seed"]))
+    for rows, n, seed in codes:
+        for exact in (False, True):
+            a = mdg.min_weight(rows, n, 10, seed, device=fused, exact_rounds=exact)
+            b = mdg.min_weight(rows, n, 10, seed, device=single, exact_rounds=exact)
+            assert (a.d, a.rounds, a.levels, a.round_bounded) == (b.d, b.rounds, b.levels, b.round_bounded)
+            assert a.witness_ok and b.witness_ok
+    fused.close()
+    single.close()
