@@ -45,9 +45,10 @@ sys.path.insert(0, ROOT)
 N, K, SEEDS = 128, 64, list(range(1, 9))
 POPC_PER_S_MEASURED = 4642.3e9   # profiles/r01_pipes_microbench.jsonl (B200, 148 SMs)
 # XU (POPC) operations the bound-pruned level-7 kernel executes per codeword, from the
-# committed ncu capture of that launch (profiles/r01e_tab_round_c7_ncu.txt)
-XU_PER_CW_PRUNED = 1.035
-DRAM_BYTES_PER_LAUNCH = 4225024  # same capture: dram__bytes_read.sum + dram__bytes_write.sum
+# committed ncu capture of that launch (profiles/r01f_tab_level_c7_ncu.txt: the fused
+# level-7 launch, both rounds)
+XU_PER_CW_PRUNED = 1.037
+DRAM_BYTES_PER_LAUNCH = 8425728  # same capture: dram__bytes_read.sum + dram__bytes_write.sum
 WORKLOAD = "cfg2: random [128,64] codes G=(I|A), mt19937_64 seeds 1..8, BZ to termination (exact d)"
 
 
@@ -384,14 +385,14 @@ def main():
             "bound": "int_popc", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gcw/s",
             "frac": achieved / peak, "traffic": DRAM_BYTES_PER_LAUNCH, "traffic_unit": "DRAM bytes per launch (ncu)",
             "kernel": ("tab_level<2,false>: both level-7 rounds of a code in one launch (2 x 621,216,192 "
-                       "codewords), bound-pruned (cutoff U); the per-round kernel tab_round<2,false> "
-                       "is the one profiled in profiles/r01e_tab_round_c7_ncu.txt (same inner loop)"),
+                       "codewords), bound-pruned (cutoff U), profiled in "
+                       "profiles/r01f_tab_level_c7_ncu.txt"),
             "peak_basis": ("measured B200 POPC (XU pipe) rate 16/clk/SM = 4.64e12/s "
-                           "(tools/pipes_microbench.cu) / 1.035 XU ops per codeword executed by this "
-                           "kernel (ncu, profiles/r01e_tab_round_c7_ncu.txt)"),
+                           "(tools/pipes_microbench.cu) / 1.037 XU ops per codeword executed by this "
+                           "kernel (ncu, profiles/r01f_tab_level_c7_ncu.txt)"),
             "op_mix_per_codeword": ("2 LOP3 (XOR, fused OR-fold) + 1 POPC of the fold (a lower bound on "
                                     "the weight) + group min / warp vote; the exact weight only for warp "
-                                    "groups that can still beat the bound (1.035 POPC per codeword measured)"),
+                                    "groups that can still beat the bound (1.037 POPC per codeword measured)"),
             "frac_vs_unpruned_popc_roofline": achieved / (popc / nw),
             "unpruned_c7": ({
                 "what": "exact config-2 level-7 round with early exit and bound pruning off "
@@ -405,7 +406,7 @@ def main():
                 "frac_elided": ex_cw / (min(ex_ms) * 1e-3) / (popc / nw),
                 "elided_def": "identity block elided: 64 compacted bits = 2 POPC per codeword",
             } if ex_ms else None),
-            "traffic_note": "DRAM 4.2 MB per launch (suffix table + binomials), 0.1% of HBM peak: compute-bound",
+            "traffic_note": "DRAM 8.4 MB per launch (the tables, read once), 0.3% of HBM bandwidth: compute-bound",
         }
         if clocks.get("sm_mhz"):
             roofline["frac_at_measured_clock"] = achieved / (peak * clocks["sm_mhz"] / 1965.0)
