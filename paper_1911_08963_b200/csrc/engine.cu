@@ -54,6 +54,7 @@ constexpr int kWarps = 8;           // warps per block (tab kernels)
 constexpr int kThreads = kWarps * 32;
 constexpr int kTX = 256;            // prefixes per tile (= threads that build them)
 constexpr int kFindX = 4;           // smem-side items per block of the witness search
+constexpr int kFoldDrop = 16;       // fold-group flag: stage 1 leaves out the last word
 constexpr uint32_t kBT = kMaxC + 1; // binomial table row stride
 constexpr int kKeyShift = 40;
 
@@ -337,6 +338,7 @@ struct TabArgs {
     uint32_t k, p, s, emin, npiv, id_rows, add_const, stop_at, tx;
     uint32_t cutoff;               // only weights < cutoff matter (0 = exact round)
     int32_t fold_lim[3];           // G = 1, 2, 4 fold groups usable while T <= fold_lim (host)
+    int32_t fold_lim_d[3];         // the same with the last word left out (-1: not applicable)
     uint64_t tile_lo, tile_hi;
     unsigned long long* best_key;
     unsigned long long* evaluated;
@@ -526,14 +528,14 @@ __device__ __forceinline__ void load_suffixes(const TabArgs& a, const TileInfo& 
 
 // OR-folds of the words of X ^ Y in G contiguous groups: sum_g popc(fold_g) is a
 // lower bound on the weight (G POPCs); larger G = tighter bound for sparse codewords.
-template <int G, int S, int NW>
+// Only the first NWF words take part (NWF = NW, or NW - 1 when the last word holds a few
+// bits only: its fold would cost a LOP3 per codeword for almost no bound).
+template <int G, int S, int NW, int NWF = NW>
 __device__ __forceinline__ uint32_t fold_bound(const uint32_t (&X)[S], const uint32_t (&Y)[NW]) {
     uint32_t lb = 0;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-        constexpr int dummy = 0;
-        (void)dummy;
-        const int b = g * NW / G, e = (g + 1) * NW / G;
+        const int b = g * NWF / G, e = (g + 1) * NWF / G;
         if (b < e) {
             uint32_t f = X[b] ^ Y[b];
 #pragma unroll
@@ -544,8 +546,8 @@ __device__ __forceinline__ uint32_t fold_bound(const uint32_t (&X)[S], const uin
     return lb;
 }
 
-// The bound-pruned walk with G fold groups (see tile_min).
-template <int NW, bool HID, int G>
+// The bound-pruned walk with G fold groups over the first NWF words (see tile_min).
+template <int NW, bool HID, int G, int NWF = NW>
 __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t x_begin, uint32_t nx,
                                                     const uint32_t (&Y)[r_for(NW)][NW],
                                                     const uint32_t (&idY)[r_for(NW)], int32_t T) {
@@ -562,7 +564,7 @@ __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t
         uint32_t lb[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            lb[r] = fold_bound<G, XS, NW>(X, Y[r]);
+            lb[r] = fold_bound<G, XS, NW, NWF>(X, Y[r]);
             if (HID) lb[r] += X[NW] + idY[r];
         }
 #pragma unroll
@@ -600,6 +602,15 @@ __device__ __forceinline__ uint32_t tile_min(const uint32_t* xs, uint32_t x_begi
     constexpr int R = r_for(NW);
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
     if (T < 0) return 0xFFFFFFFFu; // every codeword here is above the bound
+    if constexpr (NW >= 2) { // G | kFoldDrop: stage 1 skips the (nearly empty) last word
+        if (G == (1 | kFoldDrop)) return tile_min_pruned<NW, HID, 1, NW - 1>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (NW >= 4) {
+        if (G == (2 | kFoldDrop)) return tile_min_pruned<NW, HID, 2, NW - 1>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (NW >= 6) {
+        if (G == (4 | kFoldDrop)) return tile_min_pruned<NW, HID, 4, NW - 1>(xs, x_begin, nx, Y, idY, T);
+    }
     if (G == 1) return tile_min_pruned<NW, HID, 1>(xs, x_begin, nx, Y, idY, T);
     if constexpr (NW >= 3) {
         if (G == 2) return tile_min_pruned<NW, HID, 2>(xs, x_begin, nx, Y, idY, T);
@@ -623,9 +634,20 @@ __device__ __forceinline__ uint32_t tile_min(const uint32_t* xs, uint32_t x_begi
 
 // fold groups for bound T: the smallest G whose stage-1 bound still rejects almost every
 // codeword at T (lim[] from the host's density estimate; -1 = unusable), else 0 (exact)
+// Cheapest first: fewer groups (POPCs) first, and at equal G the fold without the last
+// (nearly empty) word (limd, kFoldDrop: one LOP3 less per codeword).
 __device__ __forceinline__ int pick_groups(int32_t T, const int32_t (&lim)[3]) {
     if (T <= lim[0]) return 1;
     if (T <= lim[1]) return 2;
+    if (T <= lim[2]) return 4;
+    return 0;
+}
+__device__ __forceinline__ int pick_groups(int32_t T, const int32_t (&lim)[3], const int32_t (&limd)[3]) {
+    if (T <= limd[0]) return 1 | kFoldDrop;
+    if (T <= lim[0]) return 1;
+    if (T <= limd[1]) return 2 | kFoldDrop;
+    if (T <= lim[1]) return 2;
+    if (T <= limd[2]) return 4 | kFoldDrop;
     if (T <= lim[2]) return 4;
     return 0;
 }
@@ -697,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, NW <= 2 ? MDG_MINBLK_SMALL : 4) tab_
             if (int64_t(gw) < lim) lim = gw;
             lim -= a.add_const;
             ti.T = lim < -1 ? -1 : (lim > 0x7FFFFFFF ? 0x7FFFFFFF : int32_t(lim));
-            ti.G = pick_groups(ti.T, a.fold_lim);
+            ti.G = pick_groups(ti.T, a.fold_lim, a.fold_lim_d);
         }
         __syncthreads();
         const uint64_t tile = ti.tile;
@@ -743,7 +765,7 @@ struct LevelRound {
     const uint32_t* xtab;
     unsigned long long* slot; // {best key, evaluated, -, -, -}
     ChainRec* rec;
-    int32_t fold_lim[3];
+    int32_t fold_lim[3], fold_lim_d[3];
     uint32_t id_rows, add_const;
 };
 struct LevelDesc {
@@ -774,6 +796,9 @@ tab_level(TabArgs a, const __grid_constant__ LevelDesc L) {
         sa.fold_lim[0] = r.fold_lim[0];
         sa.fold_lim[1] = r.fold_lim[1];
         sa.fold_lim[2] = r.fold_lim[2];
+        sa.fold_lim_d[0] = r.fold_lim_d[0];
+        sa.fold_lim_d[1] = r.fold_lim_d[1];
+        sa.fold_lim_d[2] = r.fold_lim_d[2];
         cur_j = j;
     };
     if (threadIdx.x == 0) {
@@ -832,7 +857,7 @@ tab_level(TabArgs a, const __grid_constant__ LevelDesc L) {
             if (!exact && prev != 0xFFFFFFFFu && int64_t(prev) - 1 < lim) lim = int64_t(prev) - 1;
             lim -= sa.add_const;
             ti.T = lim < -1 ? -1 : (lim > 0x7FFFFFFF ? 0x7FFFFFFF : int32_t(lim));
-            ti.G = pick_groups(ti.T, sa.fold_lim);
+            ti.G = pick_groups(ti.T, sa.fold_lim, sa.fold_lim_d);
             if (!skip_tile) atomicAdd(L.r[j].slot + 1, uint64_t(ti.nx) * ti.nyv);
         }
         __syncthreads();
@@ -1758,7 +1783,7 @@ struct Engine::Impl {
     std::map<std::tuple<uint32_t, uint32_t, bool>, uint32_t*> tables; // (j, size, reverse) -> table
     std::map<std::tuple<uint32_t, uint32_t, uint32_t, bool>, PlanEntry> plans; // (k, c, nw, hid)
     std::map<std::pair<uint32_t, bool>, int> occ;                     // (nw, hid)
-    std::map<std::pair<uint32_t, uint32_t>, std::array<int32_t, 3>> fold_cache; // (j, c)
+    std::map<std::pair<uint32_t, uint32_t>, std::array<int32_t, 6>> fold_cache; // (j, c)
     ncclComm_t comm = nullptr;
     uint64_t* red_dev = nullptr;
     size_t red_cap = 0;
@@ -2030,23 +2055,40 @@ static const uint32_t* ensure_xtab(Engine::Impl& im, uint32_t j, uint32_t k, uin
     return ensure_table(im, j, k, pm1, false);
 }
 
+// Words of Gamma g's compacted rows that the stage-1 fold covers: all NW template words,
+// or NW - 1 when the last one holds fewer than 12 bits (template padding or a short tail):
+// folding it would cost a LOP3 per codeword for at most a few bits of bound.
+static uint32_t fold_words(const GammaDev& g) {
+    const uint32_t full = g.n_compact / 32, tail = g.n_compact % 32;
+    const uint32_t fw = full + (tail >= 12 ? 1u : 0u);
+    return (g.nw >= 2 && fw + 1 == g.nw) ? g.nw - 1 : g.nw;
+}
+
 // Stage-1 limits measured on the round's own codewords: 128 uniform random
 // c-subsets of Gamma_j's compacted rows (SplitMix64 seeded by (j, c)), lower bounds
 // lb_G = sum of popc over G fold groups (+ identity count), lim_G = mean - 4 sd.
 // Sampling captures the column structure the density model misses (the partial
 // Gamma's rows are e_r plus subsets of the pivot columns: dense in half the columns).
 static void sampled_fold_limits(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t c,
-                                int32_t (&lim)[3]) {
+                                int32_t (&lim)[3], int32_t (&limd)[3]) {
     auto key = std::make_pair(j, c);
     auto it = im.fold_cache.find(key);
     if (it != im.fold_cache.end()) {
-        std::copy(it->second.begin(), it->second.end(), lim);
+        std::copy(it->second.begin(), it->second.begin() + 3, lim);
+        std::copy(it->second.begin() + 3, it->second.end(), limd);
         return;
     }
     const GammaDev& g = im.gammas[j];
+    if (hb(k, c) < (uint64_t{1} << 20)) { // a small round: exact weights cost nothing, skip sampling
+        for (int q = 0; q < 3; ++q) lim[q] = limd[q] = -1;
+        im.fold_cache[key] = {-1, -1, -1, -1, -1, -1};
+        return;
+    }
     const uint32_t nw = g.nw;
+    const uint32_t fwd = fold_words(g); // < nw: the fold may leave the last word out
+    const uint32_t fws[2] = {nw, fwd};
     const int Gs[3] = {1, 2, 4};
-    double sum[3] = {0, 0, 0}, sq[3] = {0, 0, 0};
+    double sum[2][3] = {}, sq[2][3] = {};
     constexpr int kSamples = 128;
     SplitMix64 rng(0x9E3779B97F4A7C15ull ^ (uint64_t(j) << 32) ^ c);
     std::vector<uint32_t> acc(nw), pick;
@@ -2064,28 +2106,36 @@ static void sampled_fold_limits(Engine::Impl& im, uint32_t j, uint32_t k, uint32
             for (uint32_t w = 0; w < nw; ++w) acc[w] ^= g.host_rows[size_t(r) * nw + w];
         }
         for (uint32_t r : pick) used[r] = 0;
+        for (int v = 0; v < 2; ++v)
+            for (int gi = 0; gi < 3; ++gi) {
+                const int G = Gs[gi];
+                const uint32_t fw = fws[v];
+                uint32_t lb = g.hid ? id : 0;
+                for (int q = 0; q < G; ++q) {
+                    uint32_t f = 0;
+                    for (uint32_t w = uint32_t(q) * fw / G; w < uint32_t(q + 1) * fw / G; ++w) f |= acc[w];
+                    lb += uint32_t(__builtin_popcount(f));
+                }
+                sum[v][gi] += lb;
+                sq[v][gi] += double(lb) * lb;
+            }
+    }
+    int32_t out[2][3];
+    for (int v = 0; v < 2; ++v) {
+        const uint32_t fw = fws[v];
         for (int gi = 0; gi < 3; ++gi) {
             const int G = Gs[gi];
-            uint32_t lb = g.hid ? id : 0;
-            for (int q = 0; q < G; ++q) {
-                uint32_t f = 0;
-                for (uint32_t w = uint32_t(q) * nw / G; w < uint32_t(q + 1) * nw / G; ++w) f |= acc[w];
-                lb += uint32_t(__builtin_popcount(f));
-            }
-            sum[gi] += lb;
-            sq[gi] += double(lb) * lb;
+            if ((v == 1 && fw == nw) || (G == 2 && fw < 3) || (G == 4 && fw < 5)) { out[v][gi] = -1; continue; }
+            const double mean = sum[v][gi] / kSamples;
+            const double var = std::max(0.0, sq[v][gi] / kSamples - mean * mean);
+            out[v][gi] = int32_t(std::floor(mean - 4.0 * std::sqrt(var) - 1.0));
         }
+        if (out[v][1] <= out[v][0]) out[v][1] = -1;
+        if (out[v][2] <= std::max(out[v][0], out[v][1])) out[v][2] = -1;
     }
-    for (int gi = 0; gi < 3; ++gi) {
-        const int G = Gs[gi];
-        if ((G == 2 && nw < 3) || (G == 4 && nw < 5)) { lim[gi] = -1; continue; }
-        const double mean = sum[gi] / kSamples;
-        const double var = std::max(0.0, sq[gi] / kSamples - mean * mean);
-        lim[gi] = int32_t(std::floor(mean - 4.0 * std::sqrt(var) - 1.0));
-    }
-    if (lim[1] <= lim[0]) lim[1] = -1;
-    if (lim[2] <= std::max(lim[0], lim[1])) lim[2] = -1;
-    im.fold_cache[key] = {lim[0], lim[1], lim[2]};
+    std::copy(out[0], out[0] + 3, lim);
+    std::copy(out[1], out[1] + 3, limd);
+    im.fold_cache[key] = {lim[0], lim[1], lim[2], limd[0], limd[1], limd[2]};
 }
 
 static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe, uint32_t* yt,
@@ -2095,8 +2145,9 @@ static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe
     a.k = k; a.p = pe.plan.p; a.s = pe.plan.s; a.emin = pe.plan.emin;
     a.npiv = uint32_t(pe.plan.prefix.size() - 1);
     a.id_rows = g.id_rows; a.add_const = (g.id_rows == k) ? c : 0; a.tx = pe.plan.TX;
-    sampled_fold_limits(im, uint32_t(&g - im.gammas.data()), k, c, a.fold_lim);
-    if (!im.prune) a.fold_lim[0] = a.fold_lim[1] = a.fold_lim[2] = -1; // exact weights only
+    sampled_fold_limits(im, uint32_t(&g - im.gammas.data()), k, c, a.fold_lim, a.fold_lim_d);
+    if (!im.prune) // exact weights only
+        for (int q = 0; q < 3; ++q) a.fold_lim[q] = a.fold_lim_d[q] = -1;
     a.xtab = ensure_xtab(im, uint32_t(&g - im.gammas.data()), k, pe.plan.p - 1);
     return a;
 }
@@ -2367,6 +2418,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
                 r.fold_lim[0] = aj.fold_lim[0];
                 r.fold_lim[1] = aj.fold_lim[1];
                 r.fold_lim[2] = aj.fold_lim[2];
+                for (int q = 0; q < 3; ++q) r.fold_lim_d[q] = aj.fold_lim_d[q];
                 r.id_rows = aj.id_rows;
                 r.add_const = aj.add_const;
             }
