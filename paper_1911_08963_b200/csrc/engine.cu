@@ -531,8 +531,8 @@ __device__ __forceinline__ void load_suffixes(const TabArgs& a, const TileInfo& 
 // Only the first NWF words take part (NWF = NW, or NW - 1 when the last word holds a few
 // bits only: its fold would cost a LOP3 per codeword for almost no bound).
 template <int G, int S, int NW, int NWF = NW>
-__device__ __forceinline__ uint32_t fold_bound(const uint32_t (&X)[S], const uint32_t (&Y)[NW]) {
-    uint32_t lb = 0;
+__device__ __forceinline__ uint32_t fold_bound(const uint32_t (&X)[S], const uint32_t (&Y)[NW],
+                                               uint32_t lb = 0) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         const int b = g * NWF / G, e = (g + 1) * NWF / G;
@@ -561,18 +561,18 @@ __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t
     for (uint32_t xi = x_begin; xi < nx; ++xi) {
         uint32_t X[XS];
         vload<XS>(xs + xi * XS, X);
+        // partial identity block: the register item's count starts the popcount sum (one
+        // IADD3 with the fold POPCs) and the smem item's comes off the bound once per row
+        const int32_t Tx = HID ? T - int32_t(X[NW]) : T;
         uint32_t lb[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            lb[r] = fold_bound<G, XS, NW, NWF>(X, Y[r]);
-            if (HID) lb[r] += X[NW] + idY[r];
-        }
+        for (int r = 0; r < R; ++r) lb[r] = fold_bound<G, XS, NW, NWF>(X, Y[r], HID ? idY[r] : 0u);
 #pragma unroll
         for (int g0 = 0; g0 < R; g0 += GR) {
             uint32_t gmin = lb[g0];
 #pragma unroll
             for (int r = 1; r < GR; ++r) gmin = min(gmin, lb[g0 + r]);
-            if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= T)) {
+            if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= Tx)) {
 #pragma unroll
                 for (int r = 0; r < GR; ++r) {
                     uint32_t w = xor_weight<0, NW, XS, NW>(X, Y[g0 + r]);
