@@ -2064,9 +2064,15 @@ static uint32_t fold_words(const GammaDev& g) {
     return (g.nw >= 2 && fw + 1 == g.nw) ? g.nw - 1 : g.nw;
 }
 
+// margin of the stage-1 limits, in standard deviations of the sampled bound
+#ifndef MDG_SIGMA
+#define MDG_SIGMA 3.5
+#endif
+constexpr double kSigma = MDG_SIGMA;
+
 // Stage-1 limits measured on the round's own codewords: 128 uniform random
 // c-subsets of Gamma_j's compacted rows (SplitMix64 seeded by (j, c)), lower bounds
-// lb_G = sum of popc over G fold groups (+ identity count), lim_G = mean - 4 sd.
+// lb_G = sum of popc over G fold groups (+ identity count), lim_G = mean - 3.5 sd - 1.
 // Sampling captures the column structure the density model misses (the partial
 // Gamma's rows are e_r plus subsets of the pivot columns: dense in half the columns).
 static void sampled_fold_limits(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t c,
@@ -2128,7 +2134,7 @@ static void sampled_fold_limits(Engine::Impl& im, uint32_t j, uint32_t k, uint32
             if ((v == 1 && fw == nw) || (G == 2 && fw < 3) || (G == 4 && fw < 5)) { out[v][gi] = -1; continue; }
             const double mean = sum[v][gi] / kSamples;
             const double var = std::max(0.0, sq[v][gi] / kSamples - mean * mean);
-            out[v][gi] = int32_t(std::floor(mean - 4.0 * std::sqrt(var) - 1.0));
+            out[v][gi] = int32_t(std::floor(mean - kSigma * std::sqrt(var) - 1.0));
         }
         if (out[v][1] <= out[v][0]) out[v][1] = -1;
         if (out[v][2] <= std::max(out[v][0], out[v][1])) out[v][2] = -1;
