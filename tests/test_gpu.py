@@ -521,3 +521,26 @@ def test_fused_levels_equal_per_round_launches(mdg):
             assert a.witness_ok and b.witness_ok
     fused.close()
     single.close()
+
+
+@pytest.mark.parametrize("n,k,seed,cap", [(512, 16, 1, 0), (1024, 8, 2, 0), (100, 99, 3, 0),
+                                          (64, 64, 4, 0), (300, 150, 5, 3), (301, 150, 6, 3),
+                                          (200, 3, 7, 0), (40, 1, 8, 0), (96, 2, 9, 0),
+                                          (1000, 40, 10, 2), (130, 64, 11, 4)])
+def test_unusual_shapes_vs_oracle(mdg, device, n, k, seed, cap):
+    """Shapes far from the BASELINE configs -- many Gammas (m up to 96, beyond the fused-level
+    limit), one-row codes, n = k and n = k + 1, 32-word compacted rows, partial blocks --
+    through the front door in both round modes, against the C oracle's trace."""
+    G = mdg.gen_matrix(n, k, seed, True)
+    ref = port.min_weight(port.gen_matrix(n, k, seed, True), n, 10, seed, level_cap=cap)
+    for exact in (True, False):
+        res = mdg.min_weight(G, n, 10, seed, level_cap=cap, device=device, exact_rounds=exact)
+        assert (res.d, res.capped, res.m, res.k_last) == (ref.d, ref.capped, ref.m, ref.k_last)
+        assert res.levels == ref.levels and res.gamma_hash == ref.gamma_hash
+        U, want = n - k + 1, []
+        for c, j, w, u_after in ref.rounds:
+            want.append([c, j, w if exact else min(w, U), u_after])
+            U = u_after
+        assert res.rounds == want
+        if not res.capped:
+            assert res.witness_ok
