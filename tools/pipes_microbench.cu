@@ -37,6 +37,19 @@ __global__ void pipe_kernel(uint32_t seed, int iters) {
                 asm volatile("min.u32 %0, %0, %1;" : "+r"(a[i]) : "r"(b));
             } else if (OP == 4) { // IMAD (fma pipe)
                 asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[i]) : "r"(b), "r"(c));
+            } else if (OP == 6) { // PRMT (byte permute)
+                asm volatile("prmt.b32 %0, %0, %1, 0x5410;" : "+r"(a[i]) : "r"(b));
+            } else if (OP == 7) { // SHF funnel shift (rotate)
+                asm volatile("shf.l.wrap.b32 %0, %0, %1, 16;" : "+r"(a[i]) : "r"(b));
+            } else if (OP == 8) { // LOP3 and IMNMX interleaved: separate pipes?
+                if (i & 1) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[i]) : "r"(b), "r"(c));
+                else asm volatile("min.u32 %0, %0, %1;" : "+r"(a[i]) : "r"(b));
+            } else if (OP == 9) { // LOP3 and POPC interleaved 4:1
+                if ((i & 3) == 3) asm volatile("popc.b32 %0, %0;" : "+r"(a[i]));
+                else asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[i]) : "r"(b), "r"(c));
+            } else if (OP == 10) { // LOP3 and PRMT interleaved 1:1
+                if (i & 1) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[i]) : "r"(b), "r"(c));
+                else asm volatile("prmt.b32 %0, %0, %1, 0x5410;" : "+r"(a[i]) : "r"(b));
             } else if (OP == 5) { // POPC of a 64-bit value (2x POPC + add)
                 uint64_t v = ((uint64_t)a[i] << 32) | b;
                 uint32_t r;
@@ -88,5 +101,10 @@ int main() {
     run<3>("imnmx", sms);
     run<4>("imad", sms);
     run<5>("popc64", sms);
+    run<6>("prmt", sms);
+    run<7>("shf_rot", sms);
+    run<8>("lop3+imnmx_1:1", sms);
+    run<9>("lop3+popc_3:1", sms);
+    run<10>("lop3+prmt_1:1", sms);
     return 0;
 }
