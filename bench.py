@@ -195,13 +195,23 @@ def main():
     import torch
     import paper_1911_08963_b200 as mdg
 
+    # MDG_BENCH_BACKEND=gloo: plumbing check of the multi-rank path with several ranks on the
+    # GPUs present (ranks share a GPU; their kernels never wait on each other) -- not a
+    # scaling measurement
+    backend = os.environ.get("MDG_BENCH_BACKEND", "nccl")
+    if backend == "gloo":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    red_dev = "cpu" if backend == "gloo" else f"cuda:{local}"
     dist = None
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", rank=rank, world_size=world,
-                                device_id=torch.device("cuda", local))
+        if backend == "gloo":
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+        else:
+            dist.init_process_group("nccl", rank=rank, world_size=world,
+                                    device_id=torch.device("cuda", local))
     kernel = mdg.KERNEL_TAB if args.kernel == "tab" else mdg.KERNEL_RD
 
     # expected answers (tests/golden, produced from the reference): d per seed
@@ -330,7 +340,9 @@ def main():
     # per-round key combined by an in-stream NCCL allreduce(min) (mdg_min_weight_dist);
     # reported beside the sharded throughput, not part of it
     split = None
-    if world > 1:
+    if world > 1 and backend == "gloo":
+        split = {"skipped": "MDG_BENCH_BACKEND=gloo plumbing run (ranks share a GPU; NCCL needs one GPU per rank)"}
+    elif world > 1:
         try:
             sd = mdg.Device(local)
             u = [mdg.nccl_unique_id() if rank == 0 else None]
@@ -350,7 +362,7 @@ def main():
                     raise RuntimeError("round-split parity failure")
                 if step >= args.warmup:
                     sms_.append(ev0.elapsed_time(ev1))
-            t = torch.tensor([max(sms_)], dtype=torch.float64, device=f"cuda:{local}")
+            t = torch.tensor([max(sms_)], dtype=torch.float64, device=red_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             split = {"what": "config-2 seed 1 through mdg_min_weight_dist: each round's tiles split "
                              f"across {world} ranks, NCCL allreduce(min) of the round key in stream",
@@ -365,13 +377,13 @@ def main():
     tot_ms = sum(ms_steps)
     tot_e2e = sum(e2e_ms)
     if dist is not None:
-        t = torch.tensor([tot_ms, tot_e2e, float(c7_ms)], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([tot_ms, tot_e2e, float(c7_ms)], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        c = torch.tensor([cw_total, e2e_cw, c7_cw, launches_total], dtype=torch.float64,
-                         device=f"cuda:{local}")
+        c = torch.tensor([cw_total, e2e_cw, c7_cw, launches_total, h2d, d2h], dtype=torch.float64,
+                         device=red_dev)
         dist.all_reduce(c, op=dist.ReduceOp.SUM)
         tot_ms, tot_e2e, c7_ms = [float(x) for x in t.tolist()]
-        cw_total, e2e_cw, c7_cw, launches_total = [int(x) for x in c.tolist()]
+        cw_total, e2e_cw, c7_cw, launches_total, h2d, d2h = [int(x) for x in c.tolist()]
 
     if rank == 0:
         value = cw_total / (tot_ms * 1e-3)
