@@ -21,6 +21,11 @@ int usage() {
                  "  mindist mindist FILE [--algorithm gpu|brute] [--kernel tab|rd] [--trials T]\n"
                  "                       [--seed S] [--level-cap C] [--device D] [--exact-rounds]\n"
                  "                       [--gamma-search host|gpu] [--pretty]\n"
+                 "    accepted for the reference's command line (cli.cpp:264-277), validated as there\n"
+                 "    and not used by the GPU engine: --algorithm basic|optimized|stack|saved|\n"
+                 "    saved_unrolled (run the GPU engine: same d and trace), --s 1..8, --unroll 1..3,\n"
+                 "    --workers W>=1, --schedule serial|dynamic|dynamic_2cm|static_cyclic|static_snake,\n"
+                 "    --prefix P, --order lex|left_lex\n"
                  "  mindist gen --n N --k K --seed S [--plain]\n";
     return 2;
 }
@@ -84,8 +89,29 @@ int main(int argc, char** argv) {
         if (a == "--algorithm") {
             if (v == "brute") {
                 brute = true;
-            } else if (v != "gpu") {
-                std::cerr << "error: unknown algorithm: " << v << " (this build provides gpu, brute)\n";
+            } else if (v != "gpu" && v != "basic" && v != "optimized" && v != "stack" && v != "saved" &&
+                       v != "saved_unrolled") { // engines.cpp:65-73 names: all run the GPU engine
+                std::cerr << "error: unknown algorithm: " << v << "\n";
+                return 2;
+            }
+        } else if (a == "--s" || a == "--unroll" || a == "--workers" || a == "--prefix") {
+            // CPU-engine settings (EngineConfig::validate, engines.cpp:83-92): checked, unused
+            if (!parse_u64(v.c_str(), x)) {
+                std::cerr << "error: bad option " << a << " " << v << "\n";
+                return 2;
+            }
+            if (a == "--s" && (x < 1 || x > 8)) { std::cerr << "error: config: s must be in 1..8\n"; return 2; }
+            if (a == "--unroll" && (x < 1 || x > 3)) { std::cerr << "error: config: unroll must be in 1..3\n"; return 2; }
+            if (a == "--workers" && x < 1) { std::cerr << "error: config: workers must be >= 1\n"; return 2; }
+        } else if (a == "--schedule") { // parallel.cpp:46-53
+            if (v != "serial" && v != "dynamic" && v != "dynamic_2cm" && v != "static_cyclic" &&
+                v != "static_snake") {
+                std::cerr << "error: unknown schedule: " << v << "\n";
+                return 2;
+            }
+        } else if (a == "--order") { // cli.cpp:86-87
+            if (v != "lex" && v != "left_lex") {
+                std::cerr << "error: order must be lex or left_lex\n";
                 return 2;
             }
         } else if (a == "--gamma-search") {

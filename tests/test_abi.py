@@ -55,6 +55,15 @@ def test_cli_binary_errors_exit_2(tmp_path):
     r = subprocess.run([exe, "mindist", str(good), "--algorithm", "fancy", "--seed", "0"],
                        capture_output=True, text=True)
     assert r.returncode == 2 and "error:" in r.stderr
+    # the reference's CPU-engine options are validated like EngineConfig::validate /
+    # schedule_from_name / cli.cpp's order check (exit 2) before any device is touched
+    for opt, val, msg in [("--s", "9", "s must be in 1..8"), ("--unroll", "0", "unroll must be in 1..3"),
+                          ("--workers", "0", "workers must be >= 1"),
+                          ("--schedule", "fast", "unknown schedule"),
+                          ("--order", "colex", "order must be lex or left_lex")]:
+        r = subprocess.run([exe, "mindist", str(good), opt, val, "--seed", "0"], capture_output=True,
+                           text=True)
+        assert r.returncode == 2 and msg in r.stderr, (opt, r.stderr)
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 2
     r = subprocess.run([exe, "gen", "--n", "80", "--k", "40", "--seed", "1"], capture_output=True,

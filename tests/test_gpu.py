@@ -381,6 +381,14 @@ def test_cli_json_record(mdg, tmp_path):
     r = subprocess.run([exe, "mindist", str(f), "--seed", "1", "--pretty", "--exact-rounds"],
                        capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "d:             7" in r.stdout
+    # a reference command line with CPU-engine options runs unchanged on the GPU engine
+    r = subprocess.run([exe, "mindist", str(f), "--algorithm", "saved", "--s", "5", "--unroll", "2",
+                        "--workers", "8", "--schedule", "dynamic", "--prefix", "3", "--order",
+                        "left_lex", "--trials", "10", "--seed", "1", "--gamma-search", "gpu"],
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    rec = json.loads(r.stdout)
+    assert rec["d"] == 7 and rec["levels"] == kats["golay_23_12"]["levels"]
 
 
 def test_cfg4_cap7_engines_agree(mdg, device):
