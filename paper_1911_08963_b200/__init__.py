@@ -616,7 +616,7 @@ def min_weight(G: np.ndarray, n: int, trials: int = 10, seed: int = 0, level_cap
 
 def min_weight_batch(Gs, n, trials: int = 10, seed=0, level_cap: int = 0,
                      kernel: int = KERNEL_TAB, witness: bool = True, device: Optional[Device] = None,
-                     exact_rounds: bool = False, streams: int = 4) -> list:
+                     exact_rounds: bool = False, streams: int = 4, gamma_search: str = "host") -> list:
     """min_weight for many codes on one device (mdg_min_weight_batch): up to `streams` codes
     in flight, each on its own engine/stream, so host Gamma searches overlap device loops.
     Gs: sequence of packed row arrays; n and seed: one value for all codes or one per code.
@@ -635,8 +635,8 @@ def min_weight_batch(Gs, n, trials: int = 10, seed=0, level_cap: int = 0,
     seeds = list(seed) if hasattr(seed, "__len__") else [seed] * count
     if len(seeds) != count:
         raise InvalidArgument("one seed per code")
-    cfgs = (_Config * max(1, count))(*[_config(trials, sd, level_cap, kernel, witness, exact_rounds)
-                                       for sd in seeds])
+    cfgs = (_Config * max(1, count))(*[_config(trials, sd, level_cap, kernel, witness, exact_rounds,
+                                               gamma_search) for sd in seeds])
     hs = (C.c_void_p * max(1, count))()
     _check(lib().mdg_min_weight_batch(device.handle, count, ptrs, ks, nn, cfgs, streams, hs))
     return [_collect(C.c_void_p(hs[i])) for i in range(count)]

@@ -1770,6 +1770,8 @@ constexpr int kSlots = 4096; // per-round scratch slots {best key, evaluated, co
 
 struct Engine::Impl {
     cudaStream_t stream = nullptr;
+    void* scratch = nullptr;   // Engine::scratch (GPU permutation search)
+    size_t scratch_cap = 0;
     bool prune = true; // stage-1 bound pruning (mdg_set_pruning)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, tev0 = nullptr, tev1 = nullptr;
     Engine::Counters cnt;
@@ -1879,6 +1881,7 @@ Engine::~Engine() {
         try { nccl().CommDestroy(impl_->comm); } catch (...) {}
     }
     cudaFree(impl_->red_dev);
+    cudaFree(impl_->scratch);
     cudaFree(impl_->d_state);
     cudaFree(impl_->d_recs);
     cudaFreeHost(impl_->h_state);
@@ -2597,6 +2600,17 @@ Engine::BruteResult Engine::brute_force(uint32_t k, uint32_t n, const uint64_t* 
 Engine::Counters Engine::counters() const { return impl_->cnt; }
 void Engine::set_pruning(bool on) { impl_->prune = on; }
 struct CUstream_st* Engine::stream() const { return impl_->stream; }
+void* Engine::scratch(size_t bytes) {
+    Impl& im = *impl_;
+    if (im.scratch_cap < bytes) {
+        CK(cudaStreamSynchronize(im.stream));
+        cudaFree(im.scratch);
+        im.scratch = nullptr;
+        CK(cudaMalloc(&im.scratch, bytes));
+        im.scratch_cap = bytes;
+    }
+    return im.scratch;
+}
 void Engine::count_launch() { impl_->cnt.launches += 1; }
 void Engine::reset_counters() { impl_->cnt = Counters{}; }
 void Engine::timer_start() {

@@ -117,6 +117,7 @@ public:
     uint64_t permutation_search(const uint64_t* rows, uint32_t k, uint32_t n, uint32_t trials,
                                 uint64_t seed);
     struct CUstream_st* stream() const; // the engine's CUDA stream
+    void* scratch(size_t bytes);         // a persistent device buffer (grows; never freed early)
     void count_launch();
 
     // counters (kernel launches, host<->device bytes) and a CUDA-event timer

@@ -175,10 +175,8 @@ uint64_t Engine::permutation_search(const uint64_t* rows, uint32_t k, uint32_t n
         for (uint32_t c = 0; c < n; ++c)
             if ((rows[size_t(r) * W + (c >> 6)] >> (c & 63)) & 1u)
                 cols[size_t(c) * KW + (r >> 6)] |= uint64_t{1} << (r & 63);
-    uint64_t* d_cols = nullptr;
-    unsigned long long* d_best = nullptr;
-    CK(cudaMalloc(&d_cols, cols.size() * 8 + 8));
-    d_best = reinterpret_cast<unsigned long long*>(d_cols + cols.size());
+    uint64_t* d_cols = static_cast<uint64_t*>(scratch(cols.size() * 8 + 8));
+    unsigned long long* d_best = reinterpret_cast<unsigned long long*>(d_cols + cols.size());
     cudaStream_t st = stream();
     CK(cudaMemcpyAsync(d_cols, cols.data(), cols.size() * 8, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(d_best, 0, 8, st));
@@ -202,7 +200,6 @@ uint64_t Engine::permutation_search(const uint64_t* rows, uint32_t k, uint32_t n
     uint64_t key = 0;
     CK(cudaMemcpyAsync(&key, d_best, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    cudaFree(d_cols);
     return key;
 }
 
