@@ -98,6 +98,9 @@ struct Bounds {
 
 GammaSet compute_gamma_matrices(const BitMatrix& G);
 GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint64_t seed);
+// True when gs has the largest (m, k_last) any column order of a k x n matrix allows
+// (then best_gamma_over_permutations returns the identity's set for every trial count).
+bool gamma_set_is_maximal(const GammaSet& gs, uint32_t n, uint32_t k);
 // The column order of trial t of best_gamma_over_permutations(G, trials, seed) (n columns):
 // identity shuffled by Fisher-Yates with the generator advanced past the t earlier trials.
 std::vector<uint32_t> trial_permutation(uint32_t n, uint64_t seed, uint64_t t);

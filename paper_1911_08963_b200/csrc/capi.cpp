@@ -139,6 +139,7 @@ void upload(Engine& eng, const GammaSet& gs) {
 GammaSet best_gamma_gpu(Engine& eng, const BitMatrix& B, uint32_t trials, uint64_t seed) {
     if (trials < 1) throw std::invalid_argument("best_gamma_over_permutations: trials must be >= 1");
     GammaSet best = compute_gamma_matrices(B);
+    if (gamma_set_is_maximal(best, B.cols(), B.rows())) return best;
     const uint64_t key = eng.permutation_search(B.data(), B.rows(), B.cols(), trials, seed);
     const uint32_t m = uint32_t(key >> 53), kl = uint32_t((key >> 42) & 0x7FF);
     const uint64_t t = ((uint64_t{1} << 42) - 1) - (key & ((uint64_t{1} << 42) - 1));

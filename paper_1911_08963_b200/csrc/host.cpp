@@ -287,9 +287,20 @@ GammaSet gamma_for_permutation(const BitMatrix& G, const std::vector<uint32_t>& 
     return g;
 }
 
+// The largest (m, k_last) any column order can give: blocks take k columns each, so
+// m <= ceil(n / k) and then k_last <= min(k, n - (m - 1) k). A candidate replaces the
+// current best only when strictly larger (gamma.cpp:88-91), so once the identity order
+// reaches this maximum no trial can change the result -- the trials are skipped.
+bool gamma_set_is_maximal(const GammaSet& gs, uint32_t n, uint32_t k) {
+    const uint32_t m_max = (n + k - 1) / k;
+    const uint32_t kl_max = std::min(k, n - (m_max - 1) * k);
+    return gs.m() == m_max && gs.k_last == kl_max;
+}
+
 GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint64_t seed) {
     if (trials < 1) throw std::invalid_argument("best_gamma_over_permutations: trials must be >= 1");
     GammaSet best = compute_gamma_matrices(G);
+    if (gamma_set_is_maximal(best, G.cols(), G.rows())) return best;
     SplitMix64 rng(seed);
     const uint32_t n = G.cols();
     std::vector<std::vector<uint32_t>> perms(trials);
