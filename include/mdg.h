@@ -39,7 +39,9 @@ extern "C" {
 
 /* Round kernel selector. MDG_KERNEL_TAB: pivot-split Cartesian enumeration
  * (saved suffix table in HBM x prefix chunk in shared memory; the default).
- * MDG_KERNEL_RD: per-thread revolving-door walk of a contiguous rank range. */
+ * MDG_KERNEL_RD: the same tiles with each tile's prefixes a contiguous rank
+ * range of the revolving-door order, walked with one (row out ^ row in) XOR
+ * per step on the codewords held in registers. Identical results. */
 #define MDG_KERNEL_TAB 0
 #define MDG_KERNEL_RD 1
 

@@ -204,7 +204,7 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
     bounds.upper = singleton_upper(n, k);
     const bool nccl_reduce = reduce == &mdg_nccl_reduce_min;
     eng.timer_start();
-    if (eng.kernel() == Kernel::tab && (world == 1 || nccl_reduce)) {
+    if (world == 1 || nccl_reduce) {
         // device-chained level loop: same semantics as run_bz_loop, no host sync per round;
         // with the NCCL reducer the per-round allreduce(min) is enqueued in-stream
         Engine::ChainResult cr = eng.chain_loop(bounds.upper, bounds.lower, cfg.level_cap,

@@ -339,6 +339,8 @@ struct TabArgs {
     uint32_t cutoff;               // only weights < cutoff matter (0 = exact round)
     int32_t fold_lim[3];           // G = 1, 2, 4 fold groups usable while T <= fold_lim (host)
     int32_t fold_lim_d[3];         // the same with the last word left out (-1: not applicable)
+    uint32_t rd;                   // 1: prefixes in revolving-door order; the round kernels walk
+                                   //    them with one (row out ^ row in) XOR per step
     uint64_t tile_lo, tile_hi;
     unsigned long long* best_key;
     unsigned long long* evaluated;
@@ -471,11 +473,57 @@ __device__ __forceinline__ void build_prefix(const TabArgs& a, uint32_t e, uint6
     for (int w = 0; w < XS; ++w) dst[w] = w < NW ? acc[w] : (HID && w == NW ? id : 0u);
 }
 
-// smem-side item t of the tile: a prefix (normal) or a suffix-table entry (transposed)
+// XOR-sum of the rows of the rank-th t-subset of [0, e) in revolving-door order (Knuth
+// 7.2.1.3 Algorithm R; the t-subsets of [0, e) are the first C(e, t) ranks of the order for
+// any larger ground set, host.cpp rd_unrank) into acc; returns its identity-row count.
+template <int NW>
+__device__ __forceinline__ uint32_t rd_subset_sum(const TabArgs& a, uint32_t e, uint32_t t,
+                                                  uint64_t rank, uint32_t (&acc)[NW]) {
+    uint32_t id = 0;
+    uint64_t r = rank;
+    for (uint32_t i = t; i >= 1; --i) {
+        // smallest x >= i-1 with C(x+1, i) > r
+        uint32_t lo = i - 1, hi = e - 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (BT(a.binom, mid + 1, i) > r) hi = mid; else lo = mid + 1;
+        }
+        xor_row<NW>(a.rows, lo, acc);
+        id += lo < a.id_rows;
+        r = BT(a.binom, lo + 1, i) - 1 - r;
+    }
+    return id;
+}
+
+// smem-side item t of the tile: a prefix (normal) or a suffix-table entry (transposed).
+// Revolving-door plans (a.rd): prefix x = x0 + t is row e plus the x-th (p-1)-subset of
+// [0, e) in revolving-door order; with `walk` (the round kernels) item t > 0 holds instead
+// the difference to prefix x - 1 -- the XOR of the row leaving and the row entering -- and
+// its identity-count change, so the kernel advances each codeword with one XOR per step.
 template <int NW, bool HID>
 __device__ __forceinline__ void build_smem_item(const TabArgs& a, const TileInfo& ti, uint32_t t,
-                                                uint32_t* dst) {
+                                                uint32_t* dst, bool walk = false) {
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
+    if (a.rd) {
+        const uint64_t x = ti.x0 + t;
+        uint32_t acc[NW];
+        uint32_t id;
+        if (walk && t > 0) {
+            uint32_t prev[NW];
+#pragma unroll
+            for (int w = 0; w < NW; ++w) acc[w] = prev[w] = 0;
+            id = rd_subset_sum<NW>(a, ti.e, a.p - 1, x, acc);
+            id -= rd_subset_sum<NW>(a, ti.e, a.p - 1, x - 1, prev); // signed change, mod 2^32
+#pragma unroll
+            for (int w = 0; w < NW; ++w) acc[w] ^= prev[w];
+        } else {
+            load_row<NW>(a.rows, ti.e, acc);
+            id = (ti.e < a.id_rows) + rd_subset_sum<NW>(a, ti.e, a.p - 1, x, acc);
+        }
+#pragma unroll
+        for (int w = 0; w < XS; ++w) dst[w] = w < NW ? acc[w] : (HID && w == NW ? id : 0u);
+        return;
+    }
     if (!ti.tr) {
         build_prefix<NW, HID>(a, ti.e, ti.x0 + t, dst);
         return;
@@ -632,6 +680,101 @@ __device__ __forceinline__ uint32_t tile_min(const uint32_t* xs, uint32_t x_begi
     return best;
 }
 
+// ------------------------------------------------ revolving-door walk (Kernel::rd)
+// Stage-1 bound of an accumulated codeword: OR-folds of G word groups of A (first NWF words).
+template <int G, int NW, int NWF = NW>
+__device__ __forceinline__ uint32_t fold_or_bound(const uint32_t (&A)[NW], uint32_t lb) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const int b = g * NWF / G, e = (g + 1) * NWF / G;
+        if (b < e) {
+            uint32_t f = A[b];
+#pragma unroll
+            for (int i = b + 1; i < e; ++i) f |= A[i];
+            lb += __popc(f);
+        }
+    }
+    return lb;
+}
+
+template <int NW>
+__device__ __forceinline__ uint32_t popc_words(const uint32_t (&A)[NW]) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) w += __popc(A[i]);
+    return w;
+}
+
+// The revolving-door walk of a tile: register item r starts as its suffix sum and takes
+// smem item 0 (the first prefix) and then, step by step, each (row out ^ row in) difference
+// -- consecutive prefixes in revolving-door order differ by one row swap -- so every step
+// is one XOR per word on codewords held in registers (north_star's formulation). Bound
+// pruning as tile_min (G: 0 = exact; 1/2/4 groups, | kFoldDrop). A and idA are consumed.
+template <int NW, bool HID, int G, int NWF = NW>
+__device__ __forceinline__ uint32_t walk_min(const uint32_t* xs, uint32_t nx,
+                                             uint32_t (&A)[r_for(NW)][NW], uint32_t (&idA)[r_for(NW)],
+                                             int32_t T) {
+    constexpr int R = r_for(NW);
+    constexpr int XS = stride_for(NW + (HID ? 1 : 0));
+    constexpr int GR = R >= MDG_VOTE_GROUP ? MDG_VOTE_GROUP : R;
+    uint32_t best = 0xFFFFFFFFu;
+    for (uint32_t xi = 0; xi < nx; ++xi) {
+        uint32_t X[XS];
+        vload<XS>(xs + xi * XS, X);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) A[r][w] ^= X[w];
+            if (HID) idA[r] += X[NW];
+        }
+        if (G == 0) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) best = min(best, popc_words<NW>(A[r]) + (HID ? idA[r] : 0u));
+            continue;
+        }
+        uint32_t lb[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) lb[r] = fold_or_bound<(G > 0 ? G : 1), NW, NWF>(A[r], HID ? idA[r] : 0u);
+#pragma unroll
+        for (int g0 = 0; g0 < R; g0 += GR) {
+            uint32_t gmin = lb[g0];
+#pragma unroll
+            for (int r = 1; r < GR; ++r) gmin = min(gmin, lb[g0 + r]);
+            if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= T)) {
+#pragma unroll
+                for (int r = 0; r < GR; ++r)
+                    best = min(best, popc_words<NW>(A[g0 + r]) + (HID ? idA[g0 + r] : 0u));
+                T = min(T, int32_t(best));
+            }
+        }
+    }
+    return best;
+}
+
+template <int NW, bool HID>
+__device__ __forceinline__ uint32_t tile_min_walk(const uint32_t* xs, uint32_t nx,
+                                                  uint32_t (&A)[r_for(NW)][NW],
+                                                  uint32_t (&idA)[r_for(NW)], int32_t T, int G) {
+    if (T < 0) return 0xFFFFFFFFu;
+    if constexpr (NW >= 2) {
+        if (G == (1 | kFoldDrop)) return walk_min<NW, HID, 1, NW - 1>(xs, nx, A, idA, T);
+    }
+    if constexpr (NW >= 4) {
+        if (G == (2 | kFoldDrop)) return walk_min<NW, HID, 2, NW - 1>(xs, nx, A, idA, T);
+    }
+    if constexpr (NW >= 6) {
+        if (G == (4 | kFoldDrop)) return walk_min<NW, HID, 4, NW - 1>(xs, nx, A, idA, T);
+    }
+    if (G == 1) return walk_min<NW, HID, 1>(xs, nx, A, idA, T);
+    if constexpr (NW >= 3) {
+        if (G == 2) return walk_min<NW, HID, 2>(xs, nx, A, idA, T);
+    }
+    if constexpr (NW >= 5) {
+        if (G == 4) return walk_min<NW, HID, 4>(xs, nx, A, idA, T);
+    }
+    return walk_min<NW, HID, 0>(xs, nx, A, idA, T);
+}
+
 // fold groups for bound T: the smallest G whose stage-1 bound still rejects almost every
 // codeword at T (lim[] from the host's density estimate; -1 = unusable), else 0 (exact)
 // Cheapest first: fewer groups (POPCs) first, and at equal G the fold without the last
@@ -671,7 +814,7 @@ __global__ void __launch_bounds__(kThreads, NW <= 2 ? MDG_MINBLK_SMALL : 4) tab_
     // the previous round. Later tiles: dynamic scheduler (atomic counter).
     if (threadIdx.x < 32) decode_tile_warp<YC>(a, a.tile_lo + blockIdx.x, ti);
     __syncthreads();
-    if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(a, ti, threadIdx.x, xs + threadIdx.x * XS);
+    if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(a, ti, threadIdx.x, xs + threadIdx.x * XS, true);
     uint32_t Y[R][NW], idY[R];
     bool valid[R];
     load_suffixes<NW, HID>(a, ti, Y, idY, valid);
@@ -709,7 +852,7 @@ __global__ void __launch_bounds__(kThreads, NW <= 2 ? MDG_MINBLK_SMALL : 4) tab_
             }
             __syncthreads();
             if (ti.stop) break;
-            if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(a, ti, threadIdx.x, xs + threadIdx.x * XS);
+            if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(a, ti, threadIdx.x, xs + threadIdx.x * XS, true);
             load_suffixes<NW, HID>(a, ti, Y, idY, valid);
         }
         if (threadIdx.x == 0) {
@@ -724,7 +867,8 @@ __global__ void __launch_bounds__(kThreads, NW <= 2 ? MDG_MINBLK_SMALL : 4) tab_
         __syncthreads();
         const uint64_t tile = ti.tile;
 
-        uint32_t best = tile_min<NW, HID>(xs, 0, ti.nx, Y, idY, ti.T, ti.G);
+        uint32_t best = a.rd ? tile_min_walk<NW, HID>(xs, ti.nx, Y, idY, ti.T, ti.G)
+                             : tile_min<NW, HID>(xs, 0, ti.nx, Y, idY, ti.T, ti.G);
         if (best != 0xFFFFFFFFu) best += a.add_const;
         best = __reduce_min_sync(0xFFFFFFFFu, best);
         if (lane == 0 && best != 0xFFFFFFFFu && (cutoff == 0 || best < cutoff)) {
@@ -808,7 +952,7 @@ tab_level(TabArgs a, const __grid_constant__ LevelDesc L) {
     __syncthreads();
     if (threadIdx.x < 32) decode_tile_warp<YC>(sa, uint64_t(blockIdx.x) % L.T, ti);
     __syncthreads();
-    if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(sa, ti, threadIdx.x, xs + threadIdx.x * XS);
+    if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(sa, ti, threadIdx.x, xs + threadIdx.x * XS, true);
     uint32_t Y[R][NW], idY[R];
     bool valid[R];
     load_suffixes<NW, HID>(sa, ti, Y, idY, valid);
@@ -863,14 +1007,15 @@ tab_level(TabArgs a, const __grid_constant__ LevelDesc L) {
         __syncthreads();
         if (!skip_tile) {
             if (!first) {
-                if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(sa, ti, threadIdx.x, xs + threadIdx.x * XS);
+                if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(sa, ti, threadIdx.x, xs + threadIdx.x * XS, true);
                 load_suffixes<NW, HID>(sa, ti, Y, idY, valid);
                 __syncthreads();
             }
             const uint64_t tile = ti.tile;
             const uint32_t add = sa.add_const;
             unsigned long long* best_key = L.r[cur_j].slot;
-            uint32_t best = tile_min<NW, HID>(xs, 0, ti.nx, Y, idY, ti.T, ti.G);
+            uint32_t best = a.rd ? tile_min_walk<NW, HID>(xs, ti.nx, Y, idY, ti.T, ti.G)
+                             : tile_min<NW, HID>(xs, 0, ti.nx, Y, idY, ti.T, ti.G);
             if (best != 0xFFFFFFFFu) best += add;
             best = __reduce_min_sync(0xFFFFFFFFu, best);
             if (lane == 0 && best != 0xFFFFFFFFu && (cutoff == 0 || best < cutoff))
@@ -986,174 +1131,6 @@ __global__ void __launch_bounds__(kThreads) tab_hist(TabArgs a) {
     if (threadIdx.x == 0 && done_local) atomicAdd(a.evaluated, done_local);
 }
 
-// ------------------------------------------------------- revolving door
-// Each thread walks RD_CHUNK consecutive ranks of the revolving-door order
-// (Knuth 7.2.1.3 Algorithm R; host.cpp rd_unrank) starting from its unranked
-// first combination. Gamma_j rows live in shared memory; one 3-input XOR per
-// word per step (row out ^ row in).
-constexpr int kRdThreads = 256;
-
-struct RdArgs {
-    const uint32_t* rows;
-    const uint64_t* binom;
-    uint32_t k, c, id_rows, add_const, stop_at;
-    uint64_t total;              // C(k, c)
-    uint64_t chunk;              // ranks per task (rd_chunk)
-    uint32_t smem_binom;         // 1: the (k+1) x (c+1) binomials are staged in smem
-    uint64_t task_lo, task_hi;   // chunk range
-    unsigned long long* best_key;
-    unsigned long long* evaluated;
-    unsigned long long* find_out;
-    uint32_t find_target;
-};
-
-// T: binomial table with row stride `stride` (x-major), x <= k
-__device__ __forceinline__ void rd_unrank_dev(const uint64_t* T, uint32_t stride, uint32_t k,
-                                              uint32_t c, uint64_t rank, uint32_t* idx) {
-    uint64_t r = rank;
-    for (uint32_t t = c; t >= 1; --t) {
-        // smallest x >= t-1 with C(x+1, t) > r  (binary search on x in [t-1, k-1])
-        uint32_t lo = t - 1, hi = k - 1;
-        while (lo < hi) {
-            uint32_t mid = (lo + hi) >> 1;
-            if (T[size_t(mid + 1) * stride + t] > r) hi = mid; else lo = mid + 1;
-        }
-        idx[t - 1] = lo;
-        r = T[size_t(lo + 1) * stride + t] - 1 - r;
-    }
-}
-
-// Algorithm R successor on c_1 < ... < c_t (cc[0] = c_1), cc[t] = k sentinel.
-// Returns false at the end; sets out/in rows.
-__device__ __forceinline__ bool rd_next(uint32_t* cc, uint32_t t, uint32_t& out, uint32_t& in) {
-    if (t & 1) {
-        if (cc[0] + 1 < cc[1]) { out = cc[0]; in = cc[0] + 1; cc[0] += 1; return true; }
-    } else {
-        if (cc[0] > 0) { out = cc[0]; in = cc[0] - 1; cc[0] -= 1; return true; }
-    }
-    // j = 2..t: R4 when (j + t) odd, R5 when (j + t) even
-    for (uint32_t j = 2; j <= t; ++j) {
-        if ((j + t) & 1) { // R4: try to decrease c_j (c_j = c_{j-1} + 1)
-            if (cc[j - 1] >= j) {
-                out = cc[j - 1]; in = j - 2;
-                cc[j - 1] = cc[j - 2]; cc[j - 2] = j - 2;
-                return true;
-            }
-        } else {           // R5: try to increase c_j (c_{j-1} = j - 2)
-            if (cc[j - 1] + 1 < cc[j]) {
-                out = j - 2; in = cc[j - 1] + 1;
-                cc[j - 2] = cc[j - 1]; cc[j - 1] += 1;
-                return true;
-            }
-        }
-    }
-    return false;
-}
-
-template <int NW, bool FIND>
-__global__ void __launch_bounds__(kRdThreads) rd_round(RdArgs a) {
-    // smem: [binomials C(x, t), x <= k, t <= c (when a.smem_binom)] [k x NW rows]
-    //       [(k-1) x NW adjacent pairs]
-    extern __shared__ __align__(16) unsigned long long rd_smem[];
-    const uint32_t bstride = a.smem_binom ? a.c + 1 : kBT;
-    const size_t bwords = a.smem_binom ? size_t(a.k + 1) * bstride : 0;
-    uint64_t* sbin = reinterpret_cast<uint64_t*>(rd_smem);
-    uint32_t* srows = reinterpret_cast<uint32_t*>(rd_smem + bwords);
-    for (size_t i = threadIdx.x; i < bwords; i += blockDim.x)
-        sbin[i] = BT(a.binom, uint32_t(i / bstride), uint32_t(i % bstride));
-    for (uint32_t i = threadIdx.x; i < a.k * NW; i += blockDim.x) srows[i] = a.rows[i];
-    for (uint32_t i = threadIdx.x; i + NW < a.k * NW; i += blockDim.x)
-        srows[a.k * NW + i] = a.rows[i] ^ a.rows[i + NW];
-    __syncthreads();
-    const uint64_t* tbin = a.smem_binom ? sbin : a.binom;
-    const uint32_t lane = threadIdx.x & 31;
-    unsigned long long seen = ~0ull, done_local = 0;
-    uint32_t cc[kMaxC + 1];
-    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-    for (uint64_t chunk = a.task_lo + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;; chunk += stride) {
-        // warp-uniform loop exit: all lanes of a warp iterate together
-        bool active = chunk < a.task_hi;
-        if (!FIND) {
-            unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
-            if ((g >> kKeyShift) <= a.stop_at) active = false;
-        }
-        if (__all_sync(0xFFFFFFFFu, !active)) break;
-        uint32_t best = 0xFFFFFFFFu;
-        uint64_t best_rank = ~0ull;
-        if (active) {
-            const uint64_t r0 = chunk * a.chunk;
-            uint64_t r1 = umin64(r0 + a.chunk, a.total);
-            rd_unrank_dev(tbin, bstride, a.k, a.c, r0, cc);
-            cc[a.c] = a.k;
-            uint32_t cw[NW];
-#pragma unroll
-            for (int w = 0; w < NW; ++w) cw[w] = 0;
-            uint32_t id = 0;
-            for (uint32_t i = 0; i < a.c; ++i) {
-#pragma unroll
-                for (int w = 0; w < NW; ++w) cw[w] ^= srows[cc[i] * NW + w];
-                id += cc[i] < a.id_rows;
-            }
-            // c_1 and c_2 live in registers: the easy step of Algorithm R (~90 % of
-            // steps) moves only c_1 to an adjacent row, one pair-table load (rows
-            // c, c+1 pre-XORed in smem); the other steps fall back to the array.
-            const bool odd = a.c & 1u;
-            uint32_t c0 = cc[0], c1 = cc[1];
-            const uint32_t* spair = srows + a.k * NW;
-            for (uint64_t rk = r0;;) {
-                uint32_t w = id + a.add_const + popsum<NW>(cw);
-                if (FIND) {
-                    if (w == a.find_target && rk < best_rank) best_rank = rk;
-                } else {
-                    best = min(best, w);
-                }
-                if (++rk >= r1) break;
-                if (!FIND && ((rk - r0) & 1023u) == 0) { // poll the bound inside long chunks
-                    unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
-                    if ((g >> kKeyShift) <= a.stop_at || (best <= a.stop_at)) {
-                        r1 = rk; // stop here; the codewords up to rk were evaluated
-                        break;
-                    }
-                }
-                uint32_t o, n;
-                if (odd ? (c0 + 1 < c1) : (c0 > 0)) {
-                    o = c0;
-                    n = odd ? c0 + 1 : c0 - 1;
-                    const uint32_t lo = odd ? c0 : c0 - 1;
-                    c0 = n;
-#pragma unroll
-                    for (int i = 0; i < NW; ++i) cw[i] ^= spair[lo * NW + i];
-                } else {
-                    cc[0] = c0;
-                    rd_next(cc, a.c, o, n);
-                    c0 = cc[0];
-                    c1 = cc[1];
-#pragma unroll
-                    for (int i = 0; i < NW; ++i) cw[i] ^= srows[o * NW + i] ^ srows[n * NW + i];
-                }
-                id += (n < a.id_rows) - (o < a.id_rows);
-            }
-            done_local += r1 - r0;
-        }
-        if (FIND) {
-            if (best_rank != ~0ull) atomicMin(a.find_out, best_rank);
-        } else {
-            uint32_t wmin = __reduce_min_sync(0xFFFFFFFFu, best);
-            // lowest chunk id among lanes achieving the warp min (deterministic key)
-            unsigned long long mykey = (best == wmin && active)
-                ? ((static_cast<unsigned long long>(wmin) << kKeyShift) | chunk) : ~0ull;
-            for (int off = 16; off; off >>= 1) {
-                unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, mykey, off);
-                mykey = o < mykey ? o : mykey;
-            }
-            if (lane == 0 && mykey < seen) {
-                unsigned long long old = atomicMin(a.best_key, mykey);
-                seen = old < mykey ? old : mykey;
-            }
-        }
-    }
-    if (!FIND && done_local) atomicAdd(a.evaluated, done_local);
-}
 
 
 // ------------------------------------------------------------ brute force
@@ -1196,6 +1173,7 @@ struct SpanArgs {
     unsigned long long* find_out;
     uint32_t find_target;
 };
+
 
 template <int NW, bool FIND>
 __global__ void __launch_bounds__(kThreads, 4) span_round(SpanArgs a) {
@@ -1434,25 +1412,6 @@ __global__ void init_slots(unsigned long long* s, int n) {
     }
 }
 
-template <int NW, bool FIND>
-struct RdLaunchT {
-    static void run(const RdArgs& a, int grid, cudaStream_t st) {
-        size_t bin = size_t(a.k + 1) * (a.c + 1) * 8;
-        size_t smem = size_t(2 * a.k) * NW * 4; // rows + adjacent pairs
-        if (smem > 227 * 1024)
-            throw std::invalid_argument("rd kernel: Gamma exceeds shared memory; use the tab kernel");
-        RdArgs b = a;
-        b.smem_binom = smem + bin <= 160 * 1024 ? 1u : 0u;
-        if (b.smem_binom) smem += bin;
-        auto fn = rd_round<NW, FIND>;
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        fn<<<grid, kRdThreads, smem, st>>>(b);
-    }
-};
-template <int NW, bool FIND>
-struct RdLaunch : RdLaunchT<NW, FIND> {};
-
 } // namespace
 
 // ================================================================ host side
@@ -1463,13 +1422,6 @@ uint32_t template_width(uint32_t nw32) {
     throw std::invalid_argument("row width exceeds the device limit (n - rank <= 1024)");
 }
 
-// ranks per revolving-door task: ~2^18 tasks (about 1.8 per resident thread),
-// 256..8192 steps each so the per-task unrank stays a small share
-uint64_t rd_chunk(uint64_t total) {
-    uint64_t chunk = 256;
-    while (chunk < 8192 && total / chunk > (uint64_t{1} << 18)) chunk *= 2;
-    return chunk;
-}
 
 uint32_t tab_yc(uint32_t nw32) { return uint32_t(r_for(int(nw32))) * kThreads; }
 uint32_t tab_tx() { return kTX; }
@@ -1531,9 +1483,9 @@ static uint64_t tile_overhead() {
 
 // total cost in codeword-slots: masked register lanes + a per-tile overhead
 static uint64_t plan_cost(uint32_t k, uint32_t c, uint32_t s, uint32_t TX, uint32_t YC,
-                          uint64_t* tiles_out) {
+                          uint64_t* tiles_out, bool allow_tr = true) {
     uint32_t p = c - s;
-    const bool can = transpose_enabled() && xtab_ok(k, p - 1);
+    const bool can = allow_tr && transpose_enabled() && xtab_ok(k, p - 1);
     uint64_t cost = 0, tiles = 0;
     for (uint32_t e = p - 1; e + s <= k - 1; ++e) {
         uint64_t NX = hb(e, p - 1), NY = hb(k - 1 - e, s);
@@ -1549,17 +1501,18 @@ static uint64_t plan_cost(uint32_t k, uint32_t c, uint32_t s, uint32_t TX, uint3
 // Suffix size s minimizes the tile cost (suffix table <= 4M entries); the
 // prefix chunk TX is the largest of 256/128/64/32/16 that still yields >= 8
 // tiles per resident block, so the dynamic scheduler's tail stays short.
-TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_blocks) {
+TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_blocks, bool rd) {
     TabPlan pl;
     pl.k = k;
     pl.c = c;
+    pl.rd = rd; // revolving-door prefix walk: the prefixes stay on the smem side (no transposition)
     pl.YC = tab_yc(nw32);
     uint32_t best_s = 0;
     if (c >= 2) {
         uint64_t best_cost = ~uint64_t{0};
         for (uint32_t s = 1; s <= c - 1; ++s) {
             if (hb(k, s) > (uint64_t{1} << 22) && s > 1) break;
-            uint64_t cost = plan_cost(k, c, s, kTX, pl.YC, nullptr);
+            uint64_t cost = plan_cost(k, c, s, kTX, pl.YC, nullptr, !rd);
             if (cost < best_cost) { best_cost = cost; best_s = s; }
         }
     }
@@ -1583,10 +1536,10 @@ TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_b
     pl.TX = kMinTX;
     for (uint32_t tx = kTX; tx >= kMinTX; tx /= 2) {
         uint64_t tiles = 0;
-        plan_cost(k, c, pl.s, tx, pl.YC, &tiles);
+        plan_cost(k, c, pl.s, tx, pl.YC, &tiles, !rd);
         if (tiles >= uint64_t(resident_blocks) * kTilesPerBlock || tx <= kMinTX) { pl.TX = tx; break; }
     }
-    const bool can = transpose_enabled() && xtab_ok(k, pl.p - 1);
+    const bool can = !rd && transpose_enabled() && xtab_ok(k, pl.p - 1);
     pl.prefix.assign(1, 0);
     pl.tr.clear();
     for (uint32_t e = pl.emin; e <= pl.emax; ++e) {
@@ -1628,7 +1581,8 @@ void tab_decode(const TabPlan& pl, uint64_t tile, uint32_t x_local, uint32_t y_l
     uint64_t x = tr ? rg : sm, y = tr ? sm : rg;                   // prefix / suffix index
     std::vector<uint32_t> out;
     std::vector<uint32_t> tmp(pl.c + 1);
-    if (pl.p > 1) colex_unrank_host(x, pl.p - 1, e, tmp.data());
+    if (pl.p > 1 && pl.rd) rd_unrank(pl.p - 1, x, tmp.data()); // revolving-door prefix order
+    else if (pl.p > 1) colex_unrank_host(x, pl.p - 1, e, tmp.data());
     for (uint32_t q = 0; q + 1 < pl.p; ++q) out.push_back(tmp[q]);
     out.push_back(e);
     if (pl.s) {
@@ -1770,6 +1724,7 @@ constexpr int kSlots = 4096; // per-round scratch slots {best key, evaluated, co
 
 struct Engine::Impl {
     cudaStream_t stream = nullptr;
+    bool rd = false;           // revolving-door prefix walk (Kernel::rd) instead of prefix sums
     void* scratch = nullptr;   // Engine::scratch (GPU permutation search)
     size_t scratch_cap = 0;
     bool prune = true; // stage-1 bound pruning (mdg_set_pruning)
@@ -1783,7 +1738,7 @@ struct Engine::Impl {
     size_t hist_cap = 0;
     std::vector<GammaDev> gammas;
     std::map<std::tuple<uint32_t, uint32_t, bool>, uint32_t*> tables; // (j, size, reverse) -> table
-    std::map<std::tuple<uint32_t, uint32_t, uint32_t, bool>, PlanEntry> plans; // (k, c, nw, hid)
+    std::map<std::tuple<uint32_t, uint32_t, uint32_t, bool, bool>, PlanEntry> plans; // (k, c, nw, hid, rd)
     std::map<std::pair<uint32_t, bool>, int> occ;                     // (nw, hid)
     std::map<std::pair<uint32_t, uint32_t>, std::array<int32_t, 6>> fold_cache; // (j, c)
     ncclComm_t comm = nullptr;
@@ -1829,11 +1784,11 @@ struct Engine::Impl {
         return o * sms;
     }
     const PlanEntry& plan(uint32_t k, uint32_t c, const GammaDev& g, int sms) {
-        auto key = std::make_tuple(k, c, g.nw, g.hid);
+        auto key = std::make_tuple(k, c, g.nw, g.hid, rd);
         auto it = plans.find(key);
         if (it != plans.end()) return it->second;
         PlanEntry pe;
-        pe.plan = make_tab_plan(k, c, g.nw, uint32_t(resident(g.nw, g.hid, sms)));
+        pe.plan = make_tab_plan(k, c, g.nw, uint32_t(resident(g.nw, g.hid, sms)), rd);
         const size_t pb = pe.plan.prefix.size() * 8, tb = pe.plan.tr.size();
         pe.d_prefix = static_cast<uint64_t*>(plan_arena.alloc(pb + tb));
         CK(cudaMemcpyAsync(pe.d_prefix, pe.plan.prefix.data(), pb, cudaMemcpyHostToDevice, stream));
@@ -2000,7 +1955,7 @@ static std::vector<TableNeed> table_needs(Engine::Impl& im, uint32_t m, uint32_t
         for (uint32_t j = 0; j < m; ++j) {
             const PlanEntry& pe = im.plan(k, c, im.gammas[j], sms);
             want(j, pe.plan.s, true);
-            if (xtab_ok(k, pe.plan.p - 1)) want(j, pe.plan.p - 1, false);
+            if (!pe.plan.rd && xtab_ok(k, pe.plan.p - 1)) want(j, pe.plan.p - 1, false);
         }
     return need;
 }
@@ -2157,13 +2112,13 @@ static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe
     sampled_fold_limits(im, uint32_t(&g - im.gammas.data()), k, c, a.fold_lim, a.fold_lim_d);
     if (!im.prune) // exact weights only
         for (int q = 0; q < 3; ++q) a.fold_lim[q] = a.fold_lim_d[q] = -1;
-    a.xtab = ensure_xtab(im, uint32_t(&g - im.gammas.data()), k, pe.plan.p - 1);
+    a.rd = pe.plan.rd ? 1u : 0u;
+    a.xtab = pe.plan.rd ? nullptr : ensure_xtab(im, uint32_t(&g - im.gammas.data()), k, pe.plan.p - 1);
     return a;
 }
 
 uint64_t Engine::tasks(uint32_t j, uint32_t c) {
     check_round(j, c);
-    if (kernel_ == Kernel::rd) return ceil_div(binomial(k_, c), rd_chunk(binomial(k_, c)));
     return impl_->plan(k_, c, impl_->gammas[j], sms_).plan.tiles();
 }
 
@@ -2175,56 +2130,25 @@ RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t tas
     const GammaDev& g = im.gammas[j];
     RoundResult rr;
     rr.combinations = binomial(k_, c);
-    if (kernel_ == Kernel::tab) {
-        const PlanEntry& pe = im.plan(k_, c, g, sms_);
-        uint64_t lo = std::min(task_lo, pe.plan.tiles()), hi = std::min(task_hi, pe.plan.tiles());
-        rr.task_lo = lo;
-        rr.task_hi = hi;
-        uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
-        unsigned long long* slot = im.take_slot();
-        TabArgs a = tab_args(im, g, pe, yt, k_, c);
-        a.stop_at = stop_at;
-        a.cutoff = cutoff;
-        a.tile_lo = lo; a.tile_hi = hi;
-        a.best_key = slot; a.evaluated = slot + 1; a.counter = slot + 2;
-        CK(cudaEventRecord(im.ev0, im.stream));
-        if (hi > lo) {
-            dispatch_nw_hid<TabLaunch>(g.nw, g.hid, a, hi - lo, im.stream, 0, size_t(0), sms_);
-            CK(cudaGetLastError());
-            im.cnt.launches += 1;
-        }
-        CK(cudaEventRecord(im.ev1, im.stream));
-        im.read_slot(slot);
-    } else {
-        uint64_t total = binomial(k_, c);
-        uint64_t chunks = ceil_div(total, rd_chunk(total));
-        uint64_t lo = std::min(task_lo, chunks), hi = std::min(task_hi, chunks);
-        rr.task_lo = lo;
-        rr.task_hi = hi;
-        unsigned long long* slot = im.take_slot();
-        RdArgs a{};
-        a.rows = g.rows; a.binom = im.binom; a.k = k_; a.c = c; a.id_rows = g.id_rows;
-        a.add_const = 0; // rd counts identity rows itself
-        a.stop_at = stop_at; a.total = total; a.chunk = rd_chunk(total);
-        a.task_lo = lo; a.task_hi = hi;
-        a.best_key = slot; a.evaluated = slot + 1;
-        CK(cudaEventRecord(im.ev0, im.stream));
-        if (hi > lo) {
-            uint64_t threads = hi - lo;
-            int grid = int(std::min<uint64_t>(ceil_div(threads, kRdThreads), uint64_t(sms_) * 8));
-            switch (g.nw) {
-#define RD_CASE(N) case N: RdLaunch<N, false>::run(a, grid, im.stream); break;
-                RD_CASE(1) RD_CASE(2) RD_CASE(3) RD_CASE(4) RD_CASE(5) RD_CASE(6) RD_CASE(7) RD_CASE(8)
-                RD_CASE(10) RD_CASE(12) RD_CASE(14) RD_CASE(16) RD_CASE(20) RD_CASE(24) RD_CASE(28) RD_CASE(32)
-#undef RD_CASE
-                default: throw std::invalid_argument("row width beyond the device limit");
-            }
-            CK(cudaGetLastError());
-            im.cnt.launches += 1;
-        }
-        CK(cudaEventRecord(im.ev1, im.stream));
-        im.read_slot(slot);
+    const PlanEntry& pe = im.plan(k_, c, g, sms_);
+    uint64_t lo = std::min(task_lo, pe.plan.tiles()), hi = std::min(task_hi, pe.plan.tiles());
+    rr.task_lo = lo;
+    rr.task_hi = hi;
+    uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
+    unsigned long long* slot = im.take_slot();
+    TabArgs a = tab_args(im, g, pe, yt, k_, c);
+    a.stop_at = stop_at;
+    a.cutoff = cutoff;
+    a.tile_lo = lo; a.tile_hi = hi;
+    a.best_key = slot; a.evaluated = slot + 1; a.counter = slot + 2;
+    CK(cudaEventRecord(im.ev0, im.stream));
+    if (hi > lo) {
+        dispatch_nw_hid<TabLaunch>(g.nw, g.hid, a, hi - lo, im.stream, 0, size_t(0), sms_);
+        CK(cudaGetLastError());
+        im.cnt.launches += 1;
     }
+    CK(cudaEventRecord(im.ev1, im.stream));
+    im.read_slot(slot);
     CK(cudaStreamSynchronize(im.stream));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, im.ev0, im.ev1));
@@ -2295,51 +2219,27 @@ std::vector<uint32_t> Engine::witness(uint32_t j, uint32_t c, const RoundResult&
     const uint32_t target = uint32_t(rr.key >> kKeyShift);
     std::vector<uint32_t> idx(c);
     unsigned long long* slot = im.take_slot();
-    if (kernel_ == Kernel::tab) {
-        const PlanEntry& pe = im.plan(k_, c, g, sms_);
-        if (task >= pe.plan.tiles()) throw std::invalid_argument("witness: key names no task of this round");
-        uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
-        TabArgs a = tab_args(im, g, pe, yt, k_, c);
-        a.tile_lo = task; a.tile_hi = task + 1;
-        a.find_out = slot + 3;
-        a.find_target = target;
-        dispatch_nw_hid<TabLaunch>(g.nw, g.hid, a, uint64_t(1), im.stream, 1, size_t(0), sms_);
-        CK(cudaGetLastError());
-        im.cnt.launches += 1;
-        im.read_slot(slot);
-        CK(cudaStreamSynchronize(im.stream));
-        uint64_t f = im.host_slot[3];
-        if (f == ~0ull) throw std::logic_error("witness: winning tile holds no codeword of the round minimum");
-        tab_decode(pe.plan, task, uint32_t(f >> 32), uint32_t(f & 0xFFFFFFFFu), idx.data());
-    } else {
-        RdArgs a{};
-        a.rows = g.rows; a.binom = im.binom; a.k = k_; a.c = c; a.id_rows = g.id_rows;
-        a.add_const = 0; a.total = binomial(k_, c); a.chunk = rd_chunk(a.total);
-        a.task_lo = task; a.task_hi = task + 1;
-        a.find_out = slot + 3;
-        a.find_target = target;
-        switch (g.nw) {
-#define RD_CASE(N) case N: RdLaunch<N, true>::run(a, 1, im.stream); break;
-            RD_CASE(1) RD_CASE(2) RD_CASE(3) RD_CASE(4) RD_CASE(5) RD_CASE(6) RD_CASE(7) RD_CASE(8)
-            RD_CASE(10) RD_CASE(12) RD_CASE(14) RD_CASE(16) RD_CASE(20) RD_CASE(24) RD_CASE(28) RD_CASE(32)
-#undef RD_CASE
-            default: throw std::invalid_argument("row width beyond the device limit");
-        }
-        CK(cudaGetLastError());
-        im.cnt.launches += 1;
-        im.read_slot(slot);
-        CK(cudaStreamSynchronize(im.stream));
-        uint64_t f = im.host_slot[3];
-        if (f == ~0ull) throw std::logic_error("witness: winning chunk holds no codeword of the round minimum");
-        rd_unrank(c, f, idx.data());
-    }
+    const PlanEntry& pe = im.plan(k_, c, g, sms_);
+    if (task >= pe.plan.tiles()) throw std::invalid_argument("witness: key names no task of this round");
+    uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
+    TabArgs a = tab_args(im, g, pe, yt, k_, c);
+    a.tile_lo = task; a.tile_hi = task + 1;
+    a.find_out = slot + 3;
+    a.find_target = target;
+    dispatch_nw_hid<TabLaunch>(g.nw, g.hid, a, uint64_t(1), im.stream, 1, size_t(0), sms_);
+    CK(cudaGetLastError());
+    im.cnt.launches += 1;
+    im.read_slot(slot);
+    CK(cudaStreamSynchronize(im.stream));
+    uint64_t f = im.host_slot[3];
+    if (f == ~0ull) throw std::logic_error("witness: winning tile holds no codeword of the round minimum");
+    tab_decode(pe.plan, task, uint32_t(f >> 32), uint32_t(f & 0xFFFFFFFFu), idx.data());
     return idx;
 }
 
 Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_cap, bool exact,
                                        uint32_t k_last, uint32_t rank, uint32_t world,
                                        bool allreduce, uint64_t split_min) {
-    if (kernel_ != Kernel::tab) throw std::logic_error("chain_loop: tab kernel only");
     allreduce = allreduce || world > 1;
     if (allreduce && !impl_->comm) throw std::logic_error("chain_loop: NCCL communicator not initialised");
     CK(cudaSetDevice(device_));
@@ -2599,6 +2499,10 @@ Engine::BruteResult Engine::brute_force(uint32_t k, uint32_t n, const uint64_t* 
 
 Engine::Counters Engine::counters() const { return impl_->cnt; }
 void Engine::set_pruning(bool on) { impl_->prune = on; }
+void Engine::set_kernel(Kernel kern) {
+    kernel_ = kern;
+    impl_->rd = kern == Kernel::rd;
+}
 struct CUstream_st* Engine::stream() const { return impl_->stream; }
 void* Engine::scratch(size_t bytes) {
     Impl& im = *impl_;

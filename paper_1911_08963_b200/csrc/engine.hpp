@@ -43,6 +43,7 @@ struct TabPlan {
     uint32_t TX = 0, YC = 0;
     std::vector<uint64_t> prefix; // tiles before pivot emin + i; size npiv + 1
     std::vector<uint8_t> tr;      // per pivot: 1 = transposed tiles (suffixes in smem)
+    bool rd = false;              // prefixes in revolving-door order (Kernel::rd)
     uint64_t tiles() const { return prefix.empty() ? 0 : prefix.back(); }
 };
 
@@ -59,7 +60,7 @@ public:
     uint32_t k() const { return k_; }
     uint32_t n() const { return n_; }
 
-    void set_kernel(Kernel kern) { kernel_ = kern; }
+    void set_kernel(Kernel kern);
     void set_pruning(bool on);
     Kernel kernel() const { return kernel_; }
 
@@ -140,12 +141,11 @@ private:
     std::unique_ptr<Impl> impl_;
 };
 
-TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_blocks);
+TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_blocks, bool rd = false);
 uint32_t tab_yc(uint32_t nw32);
 uint32_t tab_tx();
 // kernel template width for a row of nw32 words (rows are zero-padded up to it)
 uint32_t template_width(uint32_t nw32);
-uint64_t rd_chunk(uint64_t total);
 // reconstruct the combination of tile `tile`, local prefix x / suffix y
 void tab_decode(const TabPlan& plan, uint64_t tile, uint32_t x_local, uint32_t y_local,
                 uint32_t* idx);
