@@ -14,16 +14,20 @@
 //     "saved additions" table (engines.cpp:96-151) turned into a GPU operand.
 //
 // Kernels (all integer; no tensor cores):
-//   tab_round<NW,HID>  persistent grid over tiles (prefix chunk x suffix chunk);
-//                      prefix sums built in smem per tile, each lane holds R
-//                      suffix sums in registers, one XOR + POPC per word per
-//                      codeword; warp __reduce_min_sync; global 64-bit
-//                      atomicMin of (weight << 40 | tile); every tile polls the
-//                      global bound for early exit.
+//   tab_round<NW,HID>  persistent grid over tiles (prefix chunk x suffix chunk, or
+//                      transposed); smem items built per tile, each lane holds R
+//                      register items, one XOR per word + OR-fold bound + POPC per
+//                      codeword, exact weights only where the bound can still win;
+//                      warp __reduce_min_sync; global 64-bit atomicMin of
+//                      (weight << 40 | tile); tile fetches poll the bound for early
+//                      exit; in a chained loop the last block closes the round.
+//                      With a revolving-door plan (Kernel::rd) the prefixes are a
+//                      contiguous revolving-door rank range walked with one
+//                      (row out ^ row in) XOR per step.
+//   tab_level<NW,HID>  all rounds of a small level in one launch.
 //   tab_find           re-evaluates the winning tile to name the witness.
-//   tab_hist           same walk, per-warp shared-memory weight histograms.
-//   rd_round / rd_find revolving-door walk of contiguous rank ranges (the
-//                      north_star formulation; cross-check engine).
+//   tab_hist           the full weight histogram of a round (per-warp smem bins).
+//   tables_build       prefix / suffix tables; span_build / span_round: brute force.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
