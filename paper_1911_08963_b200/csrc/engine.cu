@@ -58,7 +58,16 @@ constexpr int kWarps = 8;           // warps per block (tab kernels)
 constexpr int kThreads = kWarps * 32;
 constexpr int kTX = 256;            // prefixes per tile (= threads that build them)
 constexpr int kFindX = 4;           // smem-side items per block of the witness search
-constexpr int kFoldDrop = 16;       // fold-group flag: stage 1 leaves out the last word
+constexpr int kFoldDrop = 16;       // fold-option flag: stage 1 leaves out the last word
+constexpr int kFoldHalf = 32;       // fold-option flag: stage 1 folds the first ceil(NW/2) words
+constexpr int kFoldOpts = 9;        // (G in 1, 2, 4) x (all, drop, half)
+
+// Stage-1 options of a round, cheapest first (host-sampled): a tile takes the first whose
+// limit admits its bound T. code = G | kFoldDrop | kFoldHalf; lim -1 = unused slot.
+struct FoldPlan {
+    int32_t lim[kFoldOpts];
+    int32_t code[kFoldOpts];
+};
 constexpr uint32_t kBT = kMaxC + 1; // binomial table row stride
 constexpr int kKeyShift = 40;
 
@@ -341,8 +350,7 @@ struct TabArgs {
     const uint8_t* tr;             // per pivot: 1 = transposed tiles (null: none)
     uint32_t k, p, s, emin, npiv, id_rows, add_const, stop_at, tx;
     uint32_t cutoff;               // only weights < cutoff matter (0 = exact round)
-    int32_t fold_lim[3];           // G = 1, 2, 4 fold groups usable while T <= fold_lim (host)
-    int32_t fold_lim_d[3];         // the same with the last word left out (-1: not applicable)
+    FoldPlan fold;                 // stage-1 options (host-sampled), cheapest first
     uint32_t rd;                   // 1: prefixes in revolving-door order; the round kernels walk
                                    //    them with one (row out ^ row in) XOR per step
     uint64_t tile_lo, tile_hi;
@@ -654,21 +662,31 @@ __device__ __forceinline__ uint32_t tile_min(const uint32_t* xs, uint32_t x_begi
     constexpr int R = r_for(NW);
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
     if (T < 0) return 0xFFFFFFFFu; // every codeword here is above the bound
-    if constexpr (NW >= 2) { // G | kFoldDrop: stage 1 skips the (nearly empty) last word
-        if (G == (1 | kFoldDrop)) return tile_min_pruned<NW, HID, 1, NW - 1>(xs, x_begin, nx, Y, idY, T);
-    }
-    if constexpr (NW >= 4) {
-        if (G == (2 | kFoldDrop)) return tile_min_pruned<NW, HID, 2, NW - 1>(xs, x_begin, nx, Y, idY, T);
-    }
-    if constexpr (NW >= 6) {
-        if (G == (4 | kFoldDrop)) return tile_min_pruned<NW, HID, 4, NW - 1>(xs, x_begin, nx, Y, idY, T);
-    }
+    constexpr int ND = NW >= 2 ? NW - 1 : NW, NH = (NW + 1) / 2; // drop / half fold widths
     if (G == 1) return tile_min_pruned<NW, HID, 1>(xs, x_begin, nx, Y, idY, T);
     if constexpr (NW >= 3) {
         if (G == 2) return tile_min_pruned<NW, HID, 2>(xs, x_begin, nx, Y, idY, T);
     }
     if constexpr (NW >= 5) {
         if (G == 4) return tile_min_pruned<NW, HID, 4>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (NW >= 2) {
+        if (G == (1 | kFoldDrop)) return tile_min_pruned<NW, HID, 1, ND>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (ND >= 3 && NW >= 2) {
+        if (G == (2 | kFoldDrop)) return tile_min_pruned<NW, HID, 2, ND>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (ND >= 5 && NW >= 2) {
+        if (G == (4 | kFoldDrop)) return tile_min_pruned<NW, HID, 4, ND>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (NW >= 3) {
+        if (G == (1 | kFoldHalf)) return tile_min_pruned<NW, HID, 1, NH>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (NH >= 3 && NW >= 3) {
+        if (G == (2 | kFoldHalf)) return tile_min_pruned<NW, HID, 2, NH>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (NH >= 5 && NW >= 3) {
+        if (G == (4 | kFoldHalf)) return tile_min_pruned<NW, HID, 4, NH>(xs, x_begin, nx, Y, idY, T);
     }
     uint32_t best = 0xFFFFFFFFu;
     for (uint32_t xi = x_begin; xi < nx; ++xi) {
@@ -760,14 +778,24 @@ __device__ __forceinline__ uint32_t tile_min_walk(const uint32_t* xs, uint32_t n
                                                   uint32_t (&A)[r_for(NW)][NW],
                                                   uint32_t (&idA)[r_for(NW)], int32_t T, int G) {
     if (T < 0) return 0xFFFFFFFFu;
+    constexpr int ND = NW >= 2 ? NW - 1 : NW, NH = (NW + 1) / 2;
     if constexpr (NW >= 2) {
-        if (G == (1 | kFoldDrop)) return walk_min<NW, HID, 1, NW - 1>(xs, nx, A, idA, T);
+        if (G == (1 | kFoldDrop)) return walk_min<NW, HID, 1, ND>(xs, nx, A, idA, T);
     }
-    if constexpr (NW >= 4) {
-        if (G == (2 | kFoldDrop)) return walk_min<NW, HID, 2, NW - 1>(xs, nx, A, idA, T);
+    if constexpr (ND >= 3 && NW >= 2) {
+        if (G == (2 | kFoldDrop)) return walk_min<NW, HID, 2, ND>(xs, nx, A, idA, T);
     }
-    if constexpr (NW >= 6) {
-        if (G == (4 | kFoldDrop)) return walk_min<NW, HID, 4, NW - 1>(xs, nx, A, idA, T);
+    if constexpr (ND >= 5 && NW >= 2) {
+        if (G == (4 | kFoldDrop)) return walk_min<NW, HID, 4, ND>(xs, nx, A, idA, T);
+    }
+    if constexpr (NW >= 3) {
+        if (G == (1 | kFoldHalf)) return walk_min<NW, HID, 1, NH>(xs, nx, A, idA, T);
+    }
+    if constexpr (NH >= 3 && NW >= 3) {
+        if (G == (2 | kFoldHalf)) return walk_min<NW, HID, 2, NH>(xs, nx, A, idA, T);
+    }
+    if constexpr (NH >= 5 && NW >= 3) {
+        if (G == (4 | kFoldHalf)) return walk_min<NW, HID, 4, NH>(xs, nx, A, idA, T);
     }
     if (G == 1) return walk_min<NW, HID, 1>(xs, nx, A, idA, T);
     if constexpr (NW >= 3) {
@@ -789,13 +817,10 @@ __device__ __forceinline__ int pick_groups(int32_t T, const int32_t (&lim)[3]) {
     if (T <= lim[2]) return 4;
     return 0;
 }
-__device__ __forceinline__ int pick_groups(int32_t T, const int32_t (&lim)[3], const int32_t (&limd)[3]) {
-    if (T <= limd[0]) return 1 | kFoldDrop;
-    if (T <= lim[0]) return 1;
-    if (T <= limd[1]) return 2 | kFoldDrop;
-    if (T <= lim[1]) return 2;
-    if (T <= limd[2]) return 4 | kFoldDrop;
-    if (T <= lim[2]) return 4;
+__device__ __forceinline__ int pick_fold(int32_t T, const FoldPlan& fp) {
+#pragma unroll
+    for (int i = 0; i < kFoldOpts; ++i)
+        if (T <= fp.lim[i]) return fp.code[i];
     return 0;
 }
 
@@ -866,7 +891,7 @@ __global__ void __launch_bounds__(kThreads, NW <= 2 ? MDG_MINBLK_SMALL : 4) tab_
             if (int64_t(gw) < lim) lim = gw;
             lim -= a.add_const;
             ti.T = lim < -1 ? -1 : (lim > 0x7FFFFFFF ? 0x7FFFFFFF : int32_t(lim));
-            ti.G = pick_groups(ti.T, a.fold_lim, a.fold_lim_d);
+            ti.G = pick_fold(ti.T, a.fold);
         }
         __syncthreads();
         const uint64_t tile = ti.tile;
@@ -913,7 +938,7 @@ struct LevelRound {
     const uint32_t* xtab;
     unsigned long long* slot; // {best key, evaluated, -, -, -}
     ChainRec* rec;
-    int32_t fold_lim[3], fold_lim_d[3];
+    FoldPlan fold;
     uint32_t id_rows, add_const;
 };
 struct LevelDesc {
@@ -941,12 +966,7 @@ tab_level(TabArgs a, const __grid_constant__ LevelDesc L) {
         sa.xtab = r.xtab;
         sa.id_rows = r.id_rows;
         sa.add_const = r.add_const;
-        sa.fold_lim[0] = r.fold_lim[0];
-        sa.fold_lim[1] = r.fold_lim[1];
-        sa.fold_lim[2] = r.fold_lim[2];
-        sa.fold_lim_d[0] = r.fold_lim_d[0];
-        sa.fold_lim_d[1] = r.fold_lim_d[1];
-        sa.fold_lim_d[2] = r.fold_lim_d[2];
+        sa.fold = r.fold;
         cur_j = j;
     };
     if (threadIdx.x == 0) {
@@ -1005,7 +1025,7 @@ tab_level(TabArgs a, const __grid_constant__ LevelDesc L) {
             if (!exact && prev != 0xFFFFFFFFu && int64_t(prev) - 1 < lim) lim = int64_t(prev) - 1;
             lim -= sa.add_const;
             ti.T = lim < -1 ? -1 : (lim > 0x7FFFFFFF ? 0x7FFFFFFF : int32_t(lim));
-            ti.G = pick_groups(ti.T, sa.fold_lim, sa.fold_lim_d);
+            ti.G = pick_fold(ti.T, sa.fold);
             if (!skip_tile) atomicAdd(L.r[j].slot + 1, uint64_t(ti.nx) * ti.nyv);
         }
         __syncthreads();
@@ -1744,7 +1764,7 @@ struct Engine::Impl {
     std::map<std::tuple<uint32_t, uint32_t, bool>, uint32_t*> tables; // (j, size, reverse) -> table
     std::map<std::tuple<uint32_t, uint32_t, uint32_t, bool, bool>, PlanEntry> plans; // (k, c, nw, hid, rd)
     std::map<std::pair<uint32_t, bool>, int> occ;                     // (nw, hid)
-    std::map<std::pair<uint32_t, uint32_t>, std::array<int32_t, 6>> fold_cache; // (j, c)
+    std::map<std::pair<uint32_t, uint32_t>, FoldPlan> fold_cache; // (j, c)
     ncclComm_t comm = nullptr;
     uint64_t* red_dev = nullptr;
     size_t red_cap = 0;
@@ -2017,14 +2037,6 @@ static const uint32_t* ensure_xtab(Engine::Impl& im, uint32_t j, uint32_t k, uin
     return ensure_table(im, j, k, pm1, false);
 }
 
-// Words of Gamma g's compacted rows that the stage-1 fold covers: all NW template words,
-// or NW - 1 when the last one holds fewer than 12 bits (template padding or a short tail):
-// folding it would cost a LOP3 per codeword for at most a few bits of bound.
-static uint32_t fold_words(const GammaDev& g) {
-    const uint32_t full = g.n_compact / 32, tail = g.n_compact % 32;
-    const uint32_t fw = full + (tail >= 12 ? 1u : 0u);
-    return (g.nw >= 2 && fw + 1 == g.nw) ? g.nw - 1 : g.nw;
-}
 
 // margin of the stage-1 limits, in standard deviations of the sampled bound
 #ifndef MDG_SIGMA
@@ -2037,26 +2049,29 @@ constexpr double kSigma = MDG_SIGMA;
 // lb_G = sum of popc over G fold groups (+ identity count), lim_G = mean - 3.5 sd - 1.
 // Sampling captures the column structure the density model misses (the partial
 // Gamma's rows are e_r plus subsets of the pivot columns: dense in half the columns).
-static void sampled_fold_limits(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t c,
-                                int32_t (&lim)[3], int32_t (&limd)[3]) {
+static FoldPlan sampled_fold_plan(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t c) {
     auto key = std::make_pair(j, c);
     auto it = im.fold_cache.find(key);
-    if (it != im.fold_cache.end()) {
-        std::copy(it->second.begin(), it->second.begin() + 3, lim);
-        std::copy(it->second.begin() + 3, it->second.end(), limd);
-        return;
-    }
+    if (it != im.fold_cache.end()) return it->second;
+    FoldPlan fp;
+    for (int q = 0; q < kFoldOpts; ++q) fp.lim[q] = -1, fp.code[q] = 0;
     const GammaDev& g = im.gammas[j];
     if (hb(k, c) < (uint64_t{1} << 20)) { // a small round: exact weights cost nothing, skip sampling
-        for (int q = 0; q < 3; ++q) lim[q] = limd[q] = -1;
-        im.fold_cache[key] = {-1, -1, -1, -1, -1, -1};
-        return;
+        im.fold_cache[key] = fp;
+        return fp;
     }
     const uint32_t nw = g.nw;
-    const uint32_t fwd = fold_words(g); // < nw: the fold may leave the last word out
-    const uint32_t fws[2] = {nw, fwd};
-    const int Gs[3] = {1, 2, 4};
-    double sum[2][3] = {}, sq[2][3] = {};
+    // fold widths: all words, all but the last, the first half (the kernel's variants)
+    struct Opt { uint32_t fw; int G; int code; double sum = 0, sq = 0; };
+    std::vector<Opt> opts;
+    const uint32_t widths[3] = {nw, nw >= 2 ? nw - 1 : 0, nw >= 3 ? (nw + 1) / 2 : 0};
+    const int flags[3] = {0, kFoldDrop, kFoldHalf};
+    for (int v = 0; v < 3; ++v) {
+        const uint32_t fw = widths[v];
+        if (fw == 0 || (v == 2 && fw >= widths[1])) continue;
+        for (int G : {1, 2, 4})
+            if ((G == 1) || (G == 2 && fw >= 3) || (G == 4 && fw >= 5)) opts.push_back({fw, G, G | flags[v]});
+    }
     constexpr int kSamples = 128;
     SplitMix64 rng(0x9E3779B97F4A7C15ull ^ (uint64_t(j) << 32) ^ c);
     std::vector<uint32_t> acc(nw), pick;
@@ -2074,36 +2089,45 @@ static void sampled_fold_limits(Engine::Impl& im, uint32_t j, uint32_t k, uint32
             for (uint32_t w = 0; w < nw; ++w) acc[w] ^= g.host_rows[size_t(r) * nw + w];
         }
         for (uint32_t r : pick) used[r] = 0;
-        for (int v = 0; v < 2; ++v)
-            for (int gi = 0; gi < 3; ++gi) {
-                const int G = Gs[gi];
-                const uint32_t fw = fws[v];
-                uint32_t lb = g.hid ? id : 0;
-                for (int q = 0; q < G; ++q) {
-                    uint32_t f = 0;
-                    for (uint32_t w = uint32_t(q) * fw / G; w < uint32_t(q + 1) * fw / G; ++w) f |= acc[w];
-                    lb += uint32_t(__builtin_popcount(f));
-                }
-                sum[v][gi] += lb;
-                sq[v][gi] += double(lb) * lb;
+        for (Opt& o : opts) {
+            uint32_t lb = g.hid ? id : 0;
+            for (int q = 0; q < o.G; ++q) {
+                uint32_t f = 0;
+                for (uint32_t w = uint32_t(q) * o.fw / o.G; w < uint32_t(q + 1) * o.fw / o.G; ++w) f |= acc[w];
+                lb += uint32_t(__builtin_popcount(f));
             }
-    }
-    int32_t out[2][3];
-    for (int v = 0; v < 2; ++v) {
-        const uint32_t fw = fws[v];
-        for (int gi = 0; gi < 3; ++gi) {
-            const int G = Gs[gi];
-            if ((v == 1 && fw == nw) || (G == 2 && fw < 3) || (G == 4 && fw < 5)) { out[v][gi] = -1; continue; }
-            const double mean = sum[v][gi] / kSamples;
-            const double var = std::max(0.0, sq[v][gi] / kSamples - mean * mean);
-            out[v][gi] = int32_t(std::floor(mean - kSigma * std::sqrt(var) - 1.0));
+            o.sum += lb;
+            o.sq += double(lb) * lb;
         }
-        if (out[v][1] <= out[v][0]) out[v][1] = -1;
-        if (out[v][2] <= std::max(out[v][0], out[v][1])) out[v][2] = -1;
     }
-    std::copy(out[0], out[0] + 3, lim);
-    std::copy(out[1], out[1] + 3, limd);
-    im.fold_cache[key] = {lim[0], lim[1], lim[2], limd[0], limd[1], limd[2]};
+    // cheapest first (a LOP3 per folded word, a POPC -- 4x scarcer -- per group); keep the
+    // options whose limit beats every cheaper one's
+    std::vector<std::pair<int, std::pair<int32_t, int>>> ranked; // cost, (lim, code)
+    for (const Opt& o : opts) {
+        const double mean = o.sum / kSamples;
+        const double var = std::max(0.0, o.sq / kSamples - mean * mean);
+        const int32_t lim = int32_t(std::floor(mean - kSigma * std::sqrt(var) - 1.0));
+        if (lim >= 0) ranked.push_back({int(o.fw) + 4 * o.G, {lim, o.code}});
+    }
+    std::sort(ranked.begin(), ranked.end());
+    int n = 0;
+    int32_t best_lim = -1;
+    for (const auto& r : ranked) {
+        if (r.second.first <= best_lim) continue;
+        best_lim = r.second.first;
+        fp.lim[n] = r.second.first;
+        fp.code[n] = r.second.second;
+        ++n;
+    }
+    if (std::getenv("MDG_PLAN_DEBUG")) {
+        std::fprintf(stderr, "[mdg fold] j=%u c=%u nw=%u:", j, c, nw);
+        for (int q = 0; q < n; ++q)
+            std::fprintf(stderr, " (G=%d%s T<=%d)", fp.code[q] & 15,
+                         (fp.code[q] & kFoldDrop) ? " drop" : (fp.code[q] & kFoldHalf) ? " half" : "", fp.lim[q]);
+        std::fprintf(stderr, "\n");
+    }
+    im.fold_cache[key] = fp;
+    return fp;
 }
 
 static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe, uint32_t* yt,
@@ -2113,9 +2137,9 @@ static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe
     a.k = k; a.p = pe.plan.p; a.s = pe.plan.s; a.emin = pe.plan.emin;
     a.npiv = uint32_t(pe.plan.prefix.size() - 1);
     a.id_rows = g.id_rows; a.add_const = (g.id_rows == k) ? c : 0; a.tx = pe.plan.TX;
-    sampled_fold_limits(im, uint32_t(&g - im.gammas.data()), k, c, a.fold_lim, a.fold_lim_d);
+    a.fold = sampled_fold_plan(im, uint32_t(&g - im.gammas.data()), k, c);
     if (!im.prune) // exact weights only
-        for (int q = 0; q < 3; ++q) a.fold_lim[q] = a.fold_lim_d[q] = -1;
+        for (int q = 0; q < kFoldOpts; ++q) a.fold.lim[q] = -1;
     a.rd = pe.plan.rd ? 1u : 0u;
     a.xtab = pe.plan.rd ? nullptr : ensure_xtab(im, uint32_t(&g - im.gammas.data()), k, pe.plan.p - 1);
     return a;
@@ -2328,10 +2352,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
                 r.xtab = aj.xtab;
                 r.slot = im.take_slot();
                 r.rec = im.d_recs + nrec + j;
-                r.fold_lim[0] = aj.fold_lim[0];
-                r.fold_lim[1] = aj.fold_lim[1];
-                r.fold_lim[2] = aj.fold_lim[2];
-                for (int q = 0; q < 3; ++q) r.fold_lim_d[q] = aj.fold_lim_d[q];
+                r.fold = aj.fold;
                 r.id_rows = aj.id_rows;
                 r.add_const = aj.add_const;
             }
