@@ -15,6 +15,8 @@ public:
     using std::runtime_error::runtime_error;
 };
 
+// tab: prefix-sum tiles (prefix table x suffix table); rd: the same tiles with each tile's
+// prefixes a revolving-door rank range walked one row swap at a time. Identical results.
 enum class Kernel : int { tab = 0, rd = 1 };
 
 // Limits of the device path (checked up front, std::invalid_argument).
@@ -72,7 +74,7 @@ public:
                       uint64_t task_hi = UINT64_MAX, uint32_t cutoff = 0);
     RoundResult round_hist(uint32_t j, uint32_t c, uint64_t* hist);
 
-    // The whole level loop with rounds chained on the stream ("tab" kernel):
+    // The whole level loop with rounds chained on the stream (either kernel):
     // a device-side state carries U / L / done, a finalize kernel per round
     // applies run_bz_loop's updates, and the host only synchronizes after
     // enough enqueued work (or at the end) to look at `done`. world > 1 adds an
