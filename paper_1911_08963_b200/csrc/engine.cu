@@ -1748,6 +1748,17 @@ constexpr int kSlots = 4096; // per-round scratch slots {best key, evaluated, co
 
 struct Engine::Impl {
     cudaStream_t stream = nullptr;
+    void* stage = nullptr;     // pinned host staging for uploads (grows)
+    size_t stage_cap = 0;
+    uint32_t* staging(size_t bytes) {
+        if (stage_cap < bytes) {
+            if (stage) cudaFreeHost(stage);
+            stage = nullptr;
+            CK(cudaHostAlloc(&stage, bytes, cudaHostAllocDefault));
+            stage_cap = bytes;
+        }
+        return static_cast<uint32_t*>(stage);
+    }
     bool rd = false;           // revolving-door prefix walk (Kernel::rd) instead of prefix sums
     void* scratch = nullptr;   // Engine::scratch (GPU permutation search)
     size_t scratch_cap = 0;
@@ -1864,6 +1875,7 @@ Engine::~Engine() {
     cudaFree(impl_->d_state);
     cudaFree(impl_->d_recs);
     cudaFreeHost(impl_->h_state);
+    if (impl_->stage) cudaFreeHost(impl_->stage);
     for (auto e : impl_->evpool) cudaEventDestroy(e);
     cudaFree(impl_->hist_dev);
     cudaFree(impl_->binom);
@@ -1907,14 +1919,30 @@ void Engine::load(uint32_t m, uint32_t k, uint32_t n, const uint64_t* rows, cons
         gd.hid = rk > 0 && rk < k;
         auto& hr = host[j];
         hr.assign(size_t(k) * gd.nw, 0);
+        // compacted row = bits [0, off) then bits [off + rk, n): two word-level bit-range copies
+        auto get64 = [&](const uint64_t* row, uint32_t pos) -> uint64_t { // 64 bits from pos (0-padded)
+            const uint32_t w = pos / 64, sh = pos % 64;
+            uint64_t v = w < W ? row[w] >> sh : 0;
+            if (sh && w + 1 < W) v |= row[w + 1] << (64 - sh);
+            return v;
+        };
+        const uint32_t cut = ranks ? rk : 0, head = ranks ? off : n;
         for (uint32_t r = 0; r < k; ++r) {
-            uint32_t o = 0;
-            for (uint32_t col = 0; col < n; ++col) {
-                if (ranks && col >= off && col < off + rk) continue;
-                if ((G[size_t(r) * W + col / 64] >> (col % 64)) & 1u)
-                    hr[size_t(r) * gd.nw + o / 32] |= 1u << (o % 32);
-                ++o;
-            }
+            const uint64_t* row = G + size_t(r) * W;
+            uint32_t* dst = hr.data() + size_t(r) * gd.nw;
+            auto put = [&](uint32_t from, uint32_t len, uint32_t to) { // bits [from, from+len) -> to
+                for (uint32_t done = 0; done < len;) {
+                    const uint32_t take = std::min<uint32_t>(32, len - done);
+                    uint32_t v = uint32_t(get64(row, from + done));
+                    if (take < 32) v &= (1u << take) - 1u;
+                    const uint32_t p = to + done, w = p / 32, sh = p % 32;
+                    dst[w] |= v << sh;
+                    if (sh && sh + take > 32) dst[w + 1] |= v >> (32 - sh);
+                    done += take;
+                }
+            };
+            put(0, std::min(head, n), 0);
+            if (ranks && off + cut < n) put(off + cut, n - off - cut, off);
         }
         uint64_t ones = 0;
         for (uint32_t x : hr) ones += uint32_t(__builtin_popcount(x));
@@ -1926,12 +1954,19 @@ void Engine::load(uint32_t m, uint32_t k, uint32_t n, const uint64_t* rows, cons
     impl_->tables.clear();
     impl_->fold_cache.clear();
     impl_->arena.reset(); // the stream is idle (synchronized above)
+    // all Gammas in one device block, one copy from a pinned staging buffer
+    size_t total = 0;
+    for (uint32_t j = 0; j < m; ++j) total += (host[j].size() + 63) / 64 * 64; // 256-B aligned
+    uint32_t* block = static_cast<uint32_t*>(impl_->arena.alloc(total * 4));
+    uint32_t* stage = impl_->staging(total * 4);
+    size_t o = 0;
     for (uint32_t j = 0; j < m; ++j) {
-        next[j].rows = static_cast<uint32_t*>(impl_->arena.alloc(host[j].size() * 4));
-        CK(cudaMemcpyAsync(next[j].rows, host[j].data(), host[j].size() * 4, cudaMemcpyHostToDevice,
-                           impl_->stream));
-        impl_->cnt.h2d += host[j].size() * 4;
+        std::memcpy(stage + o, host[j].data(), host[j].size() * 4);
+        next[j].rows = block + o;
+        o += (host[j].size() + 63) / 64 * 64;
     }
+    CK(cudaMemcpyAsync(block, stage, total * 4, cudaMemcpyHostToDevice, impl_->stream));
+    impl_->cnt.h2d += total * 4;
     CK(cudaStreamSynchronize(impl_->stream));
     impl_->gammas = std::move(next);
     m_ = m;
