@@ -107,6 +107,8 @@ std::vector<uint32_t> trial_permutation(uint32_t n, uint64_t seed, uint64_t t);
 // compute_gamma_matrices on G's columns in the order `perm`, column_perm composed with perm
 // (one candidate of the permutation search, gamma.cpp:85-91).
 GammaSet gamma_for_permutation(const BitMatrix& G, const std::vector<uint32_t>& perm);
+// fn(i) for i in [0, n) on the library's host thread pool (the calling thread joins in)
+void parallel_for(uint32_t n, const std::function<void(uint32_t)>& fn);
 uint32_t lower_bound(uint32_t m, uint32_t g, uint32_t k, uint32_t k_last);
 uint32_t singleton_upper(uint32_t n, uint32_t k);
 BitMatrix permute_columns(const BitMatrix& m, const std::vector<uint32_t>& perm);

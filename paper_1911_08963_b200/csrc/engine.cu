@@ -2084,17 +2084,33 @@ constexpr double kSigma = MDG_SIGMA;
 // lb_G = sum of popc over G fold groups (+ identity count), lim_G = mean - 3.5 sd - 1.
 // Sampling captures the column structure the density model misses (the partial
 // Gamma's rows are e_r plus subsets of the pivot columns: dense in half the columns).
+static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k, uint32_t c);
+
 static FoldPlan sampled_fold_plan(Engine::Impl& im, uint32_t j, uint32_t k, uint32_t c) {
     auto key = std::make_pair(j, c);
     auto it = im.fold_cache.find(key);
     if (it != im.fold_cache.end()) return it->second;
+    FoldPlan fp = compute_fold_plan(im, j, k, c);
+    im.fold_cache[key] = fp;
+    return fp;
+}
+
+// the fold plans of all Gammas of level c, sampled in parallel on the host pool
+static void prefetch_fold_plans(Engine::Impl& im, uint32_t m, uint32_t k, uint32_t c) {
+    std::vector<uint32_t> todo;
+    for (uint32_t j = 0; j < m; ++j)
+        if (!im.fold_cache.count(std::make_pair(j, c))) todo.push_back(j);
+    if (todo.size() < 2) return;
+    std::vector<FoldPlan> out(todo.size());
+    parallel_for(uint32_t(todo.size()), [&](uint32_t i) { out[i] = compute_fold_plan(im, todo[i], k, c); });
+    for (size_t i = 0; i < todo.size(); ++i) im.fold_cache[std::make_pair(todo[i], c)] = out[i];
+}
+
+static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k, uint32_t c) {
     FoldPlan fp;
     for (int q = 0; q < kFoldOpts; ++q) fp.lim[q] = -1, fp.code[q] = 0;
     const GammaDev& g = im.gammas[j];
-    if (hb(k, c) < (uint64_t{1} << 20)) { // a small round: exact weights cost nothing, skip sampling
-        im.fold_cache[key] = fp;
-        return fp;
-    }
+    if (hb(k, c) < (uint64_t{1} << 20)) return fp; // a small round: exact weights cost nothing
     const uint32_t nw = g.nw;
     // fold widths: all words, all but the last, the first half (the kernel's variants)
     struct Opt { uint32_t fw; int G; int code; double sum = 0, sq = 0; };
@@ -2161,7 +2177,6 @@ static FoldPlan sampled_fold_plan(Engine::Impl& im, uint32_t j, uint32_t k, uint
                          (fp.code[q] & kFoldDrop) ? " drop" : (fp.code[q] & kFoldHalf) ? " half" : "", fp.lim[q]);
         std::fprintf(stderr, "\n");
     }
-    im.fold_cache[key] = fp;
     return fp;
 }
 
@@ -2364,6 +2379,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
             prebuild_tables(im, m_, k_, g, g, sms_);
             built_to = g;
         }
+        prefetch_fold_plans(im, m_, k_, g);
         // small levels of Gammas of one row width: all m rounds in one launch (tab_level)
         bool fuse_level = !allreduce && m_ >= 2 && m_ <= uint32_t(kMaxFuse) && fuse_max_ > 0 &&
                           double(m_) * double(binomial(k_, g)) <= fuse_max_;

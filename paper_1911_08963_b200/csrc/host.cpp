@@ -281,6 +281,12 @@ std::vector<uint32_t> trial_permutation(uint32_t n, uint64_t seed, uint64_t t) {
     return perm;
 }
 
+void parallel_for(uint32_t n, const std::function<void(uint32_t)>& fn) {
+    if (n >= 2 && HostPool::get().size() > 1) HostPool::get().run(n, fn);
+    else
+        for (uint32_t i = 0; i < n; ++i) fn(i);
+}
+
 GammaSet gamma_for_permutation(const BitMatrix& G, const std::vector<uint32_t>& perm) {
     GammaSet g = gamma_blocks(permute_columns(G, perm));
     for (uint32_t j = 0; j < g.column_perm.size(); ++j) g.column_perm[j] = perm[g.column_perm[j]];
