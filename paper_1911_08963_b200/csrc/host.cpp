@@ -258,9 +258,12 @@ GammaSet compute_gamma_matrices(const BitMatrix& G) {
     const uint32_t k = G.rows();
     const uint32_t n = G.cols();
     if (k == 0 || k > n) throw std::invalid_argument("compute_gamma_matrices: need 1 <= k <= n");
-    if (rank_of(G) != k)
+    // gamma.cpp checks rank_of(G) == k first; the first block's elimination searches every
+    // column for its pivots, so its rank is rank(G) -- the same check without a second pass
+    GammaSet gs = gamma_blocks(G);
+    if (gs.ranks.empty() || gs.ranks[0] != k)
         throw std::invalid_argument("compute_gamma_matrices: rank-deficient generator matrix");
-    return gamma_blocks(G);
+    return gs;
 }
 
 // gamma.cpp:77-94 — identity plus `trials` Fisher–Yates shuffles
@@ -303,6 +306,113 @@ bool gamma_set_is_maximal(const GammaSet& gs, uint32_t n, uint32_t k) {
     return gs.m() == m_max && gs.k_last == kl_max;
 }
 
+// (m, k_last) of compute_gamma_matrices on the columns of G in the order `order`, without
+// the systematization (gsearch.cu's kernel, on the host): block j's pivots are the greedy
+// independent columns from position j*k on (row operations keep column dependencies), a
+// pick at position pc swaps with `target` like gamma.cpp's column swap, and what the
+// forward-only scan skips is dependent and stays so. cols: n column vectors, KW words each.
+template <uint32_t KW>
+static std::pair<uint32_t, uint32_t> block_shape_w(const uint64_t* cols, uint32_t n, uint32_t k,
+                                                   std::vector<uint32_t>& order) {
+    thread_local std::vector<uint64_t> basis;
+    thread_local std::vector<uint32_t> piv;
+    basis.resize(size_t(k) * KW);
+    piv.resize(k);
+    uint32_t m = 0, k_last = 0;
+    for (uint32_t o = 0; o < n; o += k) {
+        uint32_t cnt = 0, target = o, s = o;
+        while (cnt < k && target < n) {
+            bool found = false;
+            for (; s < n; ++s) {
+                uint64_t v[KW];
+                const uint64_t* src = cols + size_t(order[s]) * KW;
+                for (uint32_t w = 0; w < KW; ++w) v[w] = src[w];
+                for (uint32_t i = 0; i < cnt; ++i) {
+                    const uint32_t p = piv[i];
+                    if ((v[p >> 6] >> (p & 63)) & 1u) {
+                        const uint64_t* b = basis.data() + size_t(i) * KW;
+                        for (uint32_t w = 0; w < KW; ++w) v[w] ^= b[w];
+                    }
+                }
+                uint32_t lowest = UINT32_MAX;
+                for (uint32_t w = 0; w < KW; ++w)
+                    if (v[w]) { lowest = w * 64 + uint32_t(__builtin_ctzll(v[w])); break; }
+                if (lowest != UINT32_MAX) {
+                    for (uint32_t w = 0; w < KW; ++w) basis[size_t(cnt) * KW + w] = v[w];
+                    piv[cnt] = lowest;
+                    std::swap(order[target], order[s]);
+                    ++cnt;
+                    ++target;
+                    ++s;
+                    found = true;
+                    break;
+                }
+            }
+            if (!found) break;
+        }
+        if (cnt == 0) break;
+        ++m;
+        k_last = cnt;
+        if (cnt < k) break;
+    }
+    return {m, k_last};
+}
+
+// column-vector stride for k rows: a template width (the layout block_shape expects)
+static uint32_t shape_words(uint32_t k) {
+    const uint32_t kw = (k + 63) / 64;
+    return kw <= 4 ? kw : kw <= 8 ? 8 : kw <= 16 ? 16 : kw <= 32 ? 32 : (kw + 63) / 64 * 64;
+}
+
+static std::pair<uint32_t, uint32_t> block_shape(const std::vector<uint64_t>& cols, uint32_t KW, uint32_t n,
+                                                 uint32_t k, std::vector<uint32_t> order) {
+    switch (KW) {
+        case 1: return block_shape_w<1>(cols.data(), n, k, order);
+        case 2: return block_shape_w<2>(cols.data(), n, k, order);
+        case 3: return block_shape_w<3>(cols.data(), n, k, order);
+        case 4: return block_shape_w<4>(cols.data(), n, k, order);
+        case 8: return block_shape_w<8>(cols.data(), n, k, order);
+        case 16: return block_shape_w<16>(cols.data(), n, k, order);
+        case 32: return block_shape_w<32>(cols.data(), n, k, order);
+        default: break;
+    }
+    // very tall matrices: plain loop over KW words
+    std::vector<uint64_t> basis(size_t(k) * KW), v(KW);
+    std::vector<uint32_t> piv(k);
+    uint32_t m = 0, k_last = 0;
+    for (uint32_t o = 0; o < n; o += k) {
+        uint32_t cnt = 0, target = o, s = o;
+        while (cnt < k && target < n) {
+            bool found = false;
+            for (; s < n; ++s) {
+                std::copy(cols.begin() + size_t(order[s]) * KW, cols.begin() + size_t(order[s] + 1) * KW, v.begin());
+                for (uint32_t i = 0; i < cnt; ++i)
+                    if ((v[piv[i] >> 6] >> (piv[i] & 63)) & 1u)
+                        for (uint32_t w = 0; w < KW; ++w) v[w] ^= basis[size_t(i) * KW + w];
+                uint32_t lowest = UINT32_MAX;
+                for (uint32_t w = 0; w < KW && lowest == UINT32_MAX; ++w)
+                    if (v[w]) lowest = w * 64 + uint32_t(__builtin_ctzll(v[w]));
+                if (lowest != UINT32_MAX) {
+                    std::copy(v.begin(), v.end(), basis.begin() + size_t(cnt) * KW);
+                    piv[cnt] = lowest;
+                    std::swap(order[target], order[s]);
+                    ++cnt;
+                    ++target;
+                    ++s;
+                    found = true;
+                    break;
+                }
+            }
+            if (!found) break;
+        }
+        if (cnt == 0) break;
+        ++m;
+        k_last = cnt;
+        if (cnt < k) break;
+    }
+    return {m, k_last};
+}
+
 GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint64_t seed) {
     if (trials < 1) throw std::invalid_argument("best_gamma_over_permutations: trials must be >= 1");
     GammaSet best = compute_gamma_matrices(G);
@@ -319,20 +429,34 @@ GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint6
             std::swap(perm[i - 1], perm[j]);
         }
     }
-    std::vector<GammaSet> cands(trials);
-    std::function<void(uint32_t)> work = [&](uint32_t t) {
-        cands[t] = gamma_blocks(permute_columns(G, perms[t]));
-        for (uint32_t j = 0; j < cands[t].column_perm.size(); ++j)
-            cands[t].column_perm[j] = perms[t][cands[t].column_perm[j]];
-    };
-    if (uint64_t(G.rows()) * n >= 1024 && trials >= 2 && HostPool::get().size() > 1)
+    // Each candidate needs only its (m, k_last) to be compared (gamma.cpp:88-91): computed on
+    // the column vectors by the greedy block scan (block_shape); the winner alone is
+    // systematized in full, as the GPU search does.
+    const uint32_t k = G.rows();
+    const uint32_t KW = shape_words(k);
+    std::vector<uint64_t> cols(size_t(n) * KW, 0);
+    for (uint32_t r = 0; r < k; ++r)
+        for (uint32_t c = 0; c < n; ++c)
+            if ((G.row(r)[c >> 6] >> (c & 63)) & 1u) cols[size_t(c) * KW + (r >> 6)] |= uint64_t{1} << (r & 63);
+    std::vector<std::pair<uint32_t, uint32_t>> mk(trials);
+    std::function<void(uint32_t)> work = [&](uint32_t t) { mk[t] = block_shape(cols, KW, n, k, perms[t]); };
+    if (uint64_t(k) * n >= 1024 && trials >= 2 && HostPool::get().size() > 1)
         HostPool::get().run(trials, work);
     else
         for (uint32_t t = 0; t < trials; ++t) work(t);
+    int64_t win = -1;
+    uint32_t bm = best.m(), bk = best.k_last;
     for (uint32_t t = 0; t < trials; ++t)
-        if (cands[t].m() > best.m() || (cands[t].m() == best.m() && cands[t].k_last > best.k_last))
-            best = std::move(cands[t]);
-    return best;
+        if (mk[t].first > bm || (mk[t].first == bm && mk[t].second > bk)) {
+            bm = mk[t].first;
+            bk = mk[t].second;
+            win = t;
+        }
+    if (win < 0) return best;
+    GammaSet cand = gamma_for_permutation(G, perms[size_t(win)]);
+    if (cand.m() != bm || cand.k_last != bk)
+        throw std::logic_error("best_gamma_over_permutations: block scan disagrees with the systematization");
+    return cand;
 }
 
 // gamma.cpp:96-100
