@@ -552,3 +552,24 @@ def test_unusual_shapes_vs_oracle(mdg, device, n, k, seed, cap):
         assert res.rounds == want
         if not res.capped:
             assert res.witness_ok
+
+
+def test_histogram_and_witness_rd_plan(mdg, device):
+    """Revolving-door plans (prefixes in revolving-door order) give the same histograms and
+    valid witnesses on full and partial Gammas."""
+    for (n, k, seed) in [(70, 20, 5), (300, 200, 11), (256, 100, 3)]:
+        G = mdg.gen_matrix(n, k, seed, True)
+        gs = mdg.GammaSet.build(G, n, 3, seed)
+        device.load_gset(gs)
+        for j in range(gs.m):
+            g = gs.gamma(j)
+            for c in (2, 3):
+                device.set_kernel(mdg.KERNEL_TAB)
+                a, ha = device.round_hist(j, c, n)
+                device.set_kernel(mdg.KERNEL_RD)
+                b, hb = device.round_hist(j, c, n)
+                assert ha.tolist() == hb.tolist() and a.min_weight == b.min_weight, (n, k, j, c)
+                o = device.round(j, c)
+                idx = device.round_witness(j, c, o)
+                assert len(set(idx)) == c and popcount_rows(g, idx)[0] == o.min_weight
+        device.set_kernel(mdg.KERNEL_TAB)
