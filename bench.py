@@ -44,11 +44,11 @@ sys.path.insert(0, ROOT)
 
 N, K, SEEDS = 128, 64, list(range(1, 9))
 POPC_PER_S_MEASURED = 4642.3e9   # profiles/r01_pipes_microbench.jsonl (B200, 148 SMs)
-# XU (POPC) operations the bound-pruned level-7 kernel executes per codeword, from the
-# committed ncu capture of that launch (profiles/r01f_tab_level_c7_ncu.txt: the fused
-# level-7 launch, both rounds)
-XU_PER_CW_PRUNED = 1.037
-DRAM_BYTES_PER_LAUNCH = 8425728  # same capture: dram__bytes_read.sum + dram__bytes_write.sum
+# XU (POPC) operations the bound-pruned level-7 round kernel executes per codeword, from the
+# committed ncu capture of that launch (profiles/r01e_tab_round_c7_ncu.txt: tab_round<2,false>
+# on the config-2 seed-1 level-7 round, cutoff U = 15)
+XU_PER_CW_PRUNED = 1.035
+DRAM_BYTES_PER_LAUNCH = 4225024  # same capture: dram__bytes_read.sum + dram__bytes_write.sum
 WORKLOAD = "cfg2: random [128,64] codes G=(I|A), mt19937_64 seeds 1..8, BZ to termination (exact d)"
 
 
@@ -254,16 +254,26 @@ def main():
         torch.cuda.synchronize()
         return ev0.elapsed_time(ev1), sum(r.evaluated for r in runs), sum(r.launches for r in runs)
 
+    # the level-7 rounds of every code with the bound U they run under in the loop (the U
+    # after the code's previous round), from one traced loop per code
+    c7_rounds = []
+    for x in range(len(devs)):
+        r = one_loop(x)
+        U = N - K + 1
+        for (c, j, w, U_after) in r.rounds:
+            if c == 7:
+                c7_rounds.append((x, j, U))
+            U = U_after
+
     def kernel_pass():
-        """The dominant kernel alone (roofline): level-7 rounds of each code, loops run one
-        after another so every launch has the GPU to itself."""
+        """The dominant kernel alone (roofline): each level-7 round as one tab_round launch,
+        bounded by its loop U, timed with CUDA events on the engine's stream, one launch at a
+        time so each has the GPU to itself."""
         c7_cw, c7_ms = 0, 0.0
-        for x in range(len(devs)):
-            r = one_loop(x)
-            for (c, j, w, U), ev, ms in zip(r.rounds, r.round_evaluated, r.round_ms):
-                if c == 7:
-                    c7_cw += ev
-                    c7_ms += ms
+        for (x, j, U) in c7_rounds:
+            o = devs[x].round_bounded(j, 7, U)
+            c7_cw += o.evaluated
+            c7_ms += o.device_ms
         return c7_cw, c7_ms
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=f"cuda:{local}")
@@ -396,15 +406,16 @@ def main():
         roofline = {
             "bound": "int_popc", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gcw/s",
             "frac": achieved / peak, "traffic": DRAM_BYTES_PER_LAUNCH, "traffic_unit": "DRAM bytes per launch (ncu)",
-            "kernel": ("tab_level<2,false>: both level-7 rounds of a code in one launch (2 x 621,216,192 "
-                       "codewords), bound-pruned (cutoff U), profiled in "
-                       "profiles/r01f_tab_level_c7_ncu.txt"),
+            "kernel": ("tab_round<2,false>: one level-7 round per launch (621,216,192 codewords), "
+                       "bound-pruned by the loop's U, CUDA-event timed on the engine stream "
+                       "(in the chained loop both rounds of the level run as one tab_level launch, "
+                       "profiles/r01f_tab_level_c7_ncu.txt)"),
             "peak_basis": ("measured B200 POPC (XU pipe) rate 16/clk/SM = 4.64e12/s "
-                           "(tools/pipes_microbench.cu) / 1.037 XU ops per codeword executed by this "
-                           "kernel (ncu, profiles/r01f_tab_level_c7_ncu.txt)"),
+                           "(tools/pipes_microbench.cu) / 1.035 XU ops per codeword executed by this "
+                           "kernel (ncu, profiles/r01e_tab_round_c7_ncu.txt)"),
             "op_mix_per_codeword": ("2 LOP3 (XOR, fused OR-fold) + 1 POPC of the fold (a lower bound on "
                                     "the weight) + group min / warp vote; the exact weight only for warp "
-                                    "groups that can still beat the bound (1.037 POPC per codeword measured)"),
+                                    "groups that can still beat the bound (1.035 POPC per codeword measured)"),
             "frac_vs_unpruned_popc_roofline": achieved / (popc / nw),
             "unpruned_c7": ({
                 "what": "exact config-2 level-7 round with early exit and bound pruning off "
@@ -418,7 +429,7 @@ def main():
                 "frac_elided": ex_cw / (min(ex_ms) * 1e-3) / (popc / nw),
                 "elided_def": "identity block elided: 64 compacted bits = 2 POPC per codeword",
             } if ex_ms else None),
-            "traffic_note": "DRAM 8.4 MB per launch (the tables, read once), 0.3% of HBM bandwidth: compute-bound",
+            "traffic_note": "DRAM 4.2 MB per launch (the tables, read once), 0.3% of HBM bandwidth: compute-bound",
         }
         if clocks.get("sm_mhz"):
             roofline["frac_at_measured_clock"] = achieved / (peak * clocks["sm_mhz"] / 1965.0)
