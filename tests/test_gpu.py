@@ -573,3 +573,32 @@ def test_histogram_and_witness_rd_plan(mdg, device):
                 idx = device.round_witness(j, c, o)
                 assert len(set(idx)) == c and popcount_rows(g, idx)[0] == o.min_weight
         device.set_kernel(mdg.KERNEL_TAB)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_random_sparse_codes_vs_oracle(mdg, device, kernel):
+    """Random codes of random shapes and densities (sparse rows exercise the partial-word
+    fold options, partial Gammas, transposed tiles and fused levels) in both round modes:
+    d, trace and witness against the C oracle."""
+    rng = np.random.default_rng(1234 + kernel)
+    checked = 0
+    while checked < 120:
+        k = int(rng.integers(4, 23))
+        n = int(rng.integers(k + 1, 3 * k + 12))
+        dens = float(rng.choice([0.08, 0.15, 0.3, 0.5]))
+        try:
+            rows = _sparse_code(rng, k, n, dens)
+        except Exception:
+            continue
+        seed = int(rng.integers(0, 1000))
+        ref = port.min_weight(rows, n, 10, seed)
+        for exact in (True, False):
+            res = mdg.min_weight(rows, n, 10, seed, kernel=kernel, device=device, exact_rounds=exact)
+            assert (res.d, res.m, res.k_last, res.levels) == (ref.d, ref.m, ref.k_last, ref.levels), (n, k, dens, seed)
+            U, want = n - k + 1, []
+            for c, j, w, u_after in ref.rounds:
+                want.append([c, j, w if exact else min(w, U), u_after])
+                U = u_after
+            assert res.rounds == want, (n, k, dens, seed, exact)
+            assert res.witness_ok
+        checked += 1
