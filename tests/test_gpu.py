@@ -602,3 +602,27 @@ def test_random_sparse_codes_vs_oracle(mdg, device, kernel):
             assert res.rounds == want, (n, k, dens, seed, exact)
             assert res.witness_ok
         checked += 1
+
+
+def test_min_weight_batch_many_mixed(mdg, device):
+    """Many codes of mixed shapes through the batch front door with 8 streams: each result
+    equals the single-code front door's (trace, d, Gamma set)."""
+    mats, ns, seeds = [], [], []
+    for case in load_golden("seeded")[:48]:
+        rows, n = mdg.parse_matrix(case["matrix"])
+        mats.append(rows)
+        ns.append(n)
+        seeds.append(case["seed"])
+    for (n, k, s) in [(128, 64, 3), (256, 32, 7), (80, 40, 1), (300, 200, 11)]:
+        mats.append(mdg.gen_matrix(n, k, s, True))
+        ns.append(n)
+        seeds.append(s)
+    caps = [0] * (len(mats) - 1) + [4]
+    runs = mdg.min_weight_batch(mats[:-1], ns[:-1], trials=10, seed=seeds[:-1], device=device, streams=8)
+    runs.append(mdg.min_weight_batch([mats[-1]], ns[-1], trials=10, seed=seeds[-1], level_cap=4,
+                                     device=device)[0])
+    for i, r in enumerate(runs):
+        one = mdg.min_weight(mats[i], ns[i], 10, seeds[i], level_cap=caps[i], device=device)
+        assert (r.d, r.rounds, r.levels, r.gamma_hash, r.capped) == \
+               (one.d, one.rounds, one.levels, one.gamma_hash, one.capped), i
+        assert r.witness_ok or r.capped
