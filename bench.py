@@ -52,6 +52,19 @@ DRAM_BYTES_PER_LAUNCH = 4225024  # same capture: dram__bytes_read.sum + dram__by
 WORKLOAD = "cfg2: random [128,64] codes G=(I|A), mt19937_64 seeds 1..8, BZ to termination (exact d)"
 
 
+def hbm_check(achieved_cw_s):
+    """The HBM roofline for the same launch, against MEASURED_PEAKS.json (driver-written): the
+    launch's DRAM bytes per second over the measured copy bandwidth."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm = float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return None
+    launch_s = 621216192 / achieved_cw_s if achieved_cw_s else 0.0
+    gbs = DRAM_BYTES_PER_LAUNCH / launch_s / 1e9 if launch_s else 0.0
+    return {"dram_gbs": gbs, "hbm_peak_gbs": hbm, "frac": gbs / hbm, "source": "MEASURED_PEAKS.json hbm_gbs"}
+
+
 def env_int(name, default):
     try:
         return int(os.environ.get(name, default))
@@ -430,6 +443,7 @@ def main():
                 "elided_def": "identity block elided: 64 compacted bits = 2 POPC per codeword",
             } if ex_ms else None),
             "traffic_note": "DRAM 4.2 MB per launch (the tables, read once), 0.3% of HBM bandwidth: compute-bound",
+            "hbm_check": hbm_check(achieved),
         }
         if clocks.get("sm_mhz"):
             roofline["frac_at_measured_clock"] = achieved / (peak * clocks["sm_mhz"] / 1965.0)
