@@ -18,7 +18,7 @@ namespace {
 
 int usage() {
     std::cerr << "usage:\n"
-                 "  mindist mindist FILE [--algorithm gpu|brute] [--kernel tab|rd] [--trials T]\n"
+                 "  mindist mindist FILE [FILE ...] [--algorithm gpu|brute] [--kernel tab|rd] [--trials T]\n"
                  "                       [--seed S] [--level-cap C] [--device D] [--exact-rounds]\n"
                  "                       [--gamma-search host|gpu] [--pretty]\n"
                  "    accepted for the reference's command line (cli.cpp:264-277), validated as there\n"
@@ -26,6 +26,7 @@ int usage() {
                  "    saved_unrolled (run the GPU engine: same d and trace), --s 1..8, --unroll 1..3,\n"
                  "    --workers W>=1, --schedule serial|dynamic|dynamic_2cm|static_cyclic|static_snake,\n"
                  "    --prefix P, --order lex|left_lex\n"
+                 "    several FILEs: one record per file, the codes run as one batch\n"
                  "  mindist gen --n N --k K --seed S [--plain]\n";
     return 2;
 }
@@ -72,15 +73,16 @@ int main(int argc, char** argv) {
         return 0;
     }
     if (cmd != "mindist" || argc < 3) return usage();
-    std::string path = argv[2];
+    std::vector<std::string> paths; // the reference takes one FILE; several run as one batch
     mdg_config cfg;
     mdg_config_default(&cfg);
     bool pretty = false;
     int device = 0;
     bool seed_given = false;
     bool brute = false;
-    for (int i = 3; i < argc; ++i) {
+    for (int i = 2; i < argc; ++i) {
         std::string a = argv[i];
+        if (a.rfind("--", 0) != 0) { paths.push_back(a); continue; }
         if (a == "--pretty") { pretty = true; continue; }
         if (a == "--exact-rounds") { cfg.exact_rounds = 1; continue; }
         if (i + 1 >= argc) return usage();
@@ -140,49 +142,73 @@ int main(int argc, char** argv) {
         cfg.seed = (uint64_t(std::rand()) << 32) ^ uint64_t(std::rand()) ^ uint64_t(time(nullptr));
         std::cerr << "seed: " << cfg.seed << "\n";
     }
-    mdg::BitMatrix G;
-    try {
-        G = mdg::parse_matrix_file(path);
-    } catch (const std::invalid_argument& e) {
-        std::cerr << "error: " << e.what() << "\n";
-        return 2;
+    if (paths.empty()) return usage();
+    std::vector<mdg::BitMatrix> Gs(paths.size());
+    for (size_t f = 0; f < paths.size(); ++f) {
+        try {
+            Gs[f] = mdg::parse_matrix_file(paths[f]);
+        } catch (const std::invalid_argument& e) {
+            std::cerr << "error: " << (paths.size() > 1 ? paths[f] + ": " : "") << e.what() << "\n";
+            return 2;
+        }
     }
     mdg_ctx* ctx = nullptr;
     int rc = mdg_open(device, &ctx);
     if (rc) return exit_code(rc);
-    mdg_run* run = nullptr;
-    rc = brute ? mdg_brute_force(ctx, G.data(), G.rows(), G.cols(), 40, &run)
-               : mdg_min_weight(ctx, G.data(), G.rows(), G.cols(), &cfg, &run);
+    std::vector<mdg_run*> runs(paths.size(), nullptr);
+    if (brute) {
+        for (size_t f = 0; f < paths.size() && rc == 0; ++f)
+            rc = mdg_brute_force(ctx, Gs[f].data(), Gs[f].rows(), Gs[f].cols(), 40, &runs[f]);
+    } else if (paths.size() == 1) {
+        rc = mdg_min_weight(ctx, Gs[0].data(), Gs[0].rows(), Gs[0].cols(), &cfg, &runs[0]);
+    } else { // several files: codes in flight on their own streams (mdg_min_weight_batch)
+        std::vector<const uint64_t*> ptr;
+        std::vector<uint32_t> ks, ns;
+        std::vector<mdg_config> cfgs(paths.size(), cfg);
+        for (const auto& G : Gs) {
+            ptr.push_back(G.data());
+            ks.push_back(G.rows());
+            ns.push_back(G.cols());
+        }
+        rc = mdg_min_weight_batch(ctx, uint32_t(paths.size()), ptr.data(), ks.data(), ns.data(),
+                                  cfgs.data(), 0, runs.data());
+    }
     if (rc) {
+        for (mdg_run* r : runs)
+            if (r) mdg_run_free(r);
         mdg_close(ctx);
         return exit_code(rc);
     }
     std::vector<char> buf(1 << 20);
-    long len = mdg_run_json(run, buf.data(), buf.size());
-    if (len < 0) {
-        buf.resize(size_t(-len) + 16);
-        len = mdg_run_json(run, buf.data(), buf.size());
+    for (size_t f = 0; f < paths.size(); ++f) {
+        mdg_run* run = runs[f];
+        long len = mdg_run_json(run, buf.data(), buf.size());
+        if (len < 0) {
+            buf.resize(size_t(-len) + 16);
+            len = mdg_run_json(run, buf.data(), buf.size());
+        }
+        if (pretty) {
+            mdg_run_info info;
+            mdg_run_info_get(run, &info);
+            if (paths.size() > 1) std::cout << "file:          " << paths[f] << "\n";
+            std::cout << "d:             " << info.d << (info.capped ? " (level cap: upper bound)" : "") << "\n"
+                      << "n:             " << info.n << "\n"
+                      << "k:             " << info.k << "\n"
+                      << "algorithm:     " << (brute ? "brute" : "gpu") << "\n"
+                      << "m:             " << info.m << "\n"
+                      << "k_last:        " << info.k_last << "\n"
+                      << "g_final:       " << info.g_final << "\n"
+                      << "row_additions: " << info.row_additions << "\n"
+                      << "combinations:  " << info.combinations << "\n"
+                      << "wall_seconds:  " << info.wall_seconds << "\n"
+                      << "seed:          " << cfg.seed << "\n"
+                      << "workers:       1\n"
+                      << "witness_ok:    " << (info.witness_ok ? "true" : "false") << "\n";
+        } else {
+            std::cout << buf.data() << "\n";
+        }
+        mdg_run_free(run);
     }
-    if (pretty) {
-        mdg_run_info info;
-        mdg_run_info_get(run, &info);
-        std::cout << "d:             " << info.d << (info.capped ? " (level cap: upper bound)" : "") << "\n"
-                  << "n:             " << info.n << "\n"
-                  << "k:             " << info.k << "\n"
-                  << "algorithm:     " << (brute ? "brute" : "gpu") << "\n"
-                  << "m:             " << info.m << "\n"
-                  << "k_last:        " << info.k_last << "\n"
-                  << "g_final:       " << info.g_final << "\n"
-                  << "row_additions: " << info.row_additions << "\n"
-                  << "combinations:  " << info.combinations << "\n"
-                  << "wall_seconds:  " << info.wall_seconds << "\n"
-                  << "seed:          " << cfg.seed << "\n"
-                  << "workers:       1\n"
-                  << "witness_ok:    " << (info.witness_ok ? "true" : "false") << "\n";
-    } else {
-        std::cout << buf.data() << "\n";
-    }
-    mdg_run_free(run);
     mdg_close(ctx);
     return 0;
 }

@@ -389,6 +389,18 @@ def test_cli_json_record(mdg, tmp_path):
     assert r.returncode == 0, r.stderr
     rec = json.loads(r.stdout)
     assert rec["d"] == 7 and rec["levels"] == kats["golay_23_12"]["levels"]
+    # several files: one record each, in order, run as one batch
+    files = []
+    for name in ("golay_23_12", "hamming_taps", "ext_golay_24_12", "rank_deficient_14_5", "repetition_9"):
+        if name in kats:
+            p = tmp_path / f"{name}.txt"
+            p.write_text(kats[name]["matrix"])
+            files.append((p, kats[name]))
+    r = subprocess.run([exe, "mindist"] + [str(p) for p, _ in files] + ["--seed", "1"],
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    recs = [json.loads(line) for line in r.stdout.splitlines()]
+    assert [x["d"] for x in recs] == [c["d"] for _, c in files]
 
 
 def test_cfg4_cap7_engines_agree(mdg, device):
