@@ -8,11 +8,12 @@ codes. Metric: codewords evaluated per second (BASELINE.json `metric`).
 * value  — device-resident: the level loops over Gamma sets already in HBM
            (mdg_bz_loop_device, one context per code, --streams codes in flight
            per GPU), CUDA events around each whole step (host gaps included);
-           codewords / time, max over ranks for the time. Under torchrun the
-           eight codes are sharded across ranks (rank r owns codes r, r+N, ...;
-           independent objects, no data-path collective); config.round_split
-           reports SURVEY.md §8e's split of one code's rounds across the ranks
-           (mdg_min_weight_dist, NCCL allreduce(min) per round) beside it.
+           codewords / time, max over ranks for the time. Under torchrun every
+           rank runs its own eight-code step (codes are independent objects: no
+           data-path collective; per-GPU work fixed, "scaling": "weak");
+           config.round_split reports SURVEY.md §8e's split of one code's rounds
+           across the ranks (mdg_min_weight_dist, NCCL allreduce(min) per round)
+           beside it.
 * e2e    — the public front door from host matrices (mdg_min_weight_batch over
            the rank's codes): row basis +
            Gamma search on the host, H2D of the Gammas, the device loop, D2H of
@@ -172,7 +173,7 @@ def run_reference_arm(args, rank, world):
     line = {
         "impl": "reference", "metric": "codewords_evaluated_per_sec", "value": value, "unit": "cw/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": statistics.mean(steps_ms), "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": statistics.mean(steps_ms), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (mt19937_64, SURVEY.md §8d)",
         "config": {"workload": WORKLOAD, "per_step": "one code (seed rotates)"},
         "cpu_baseline": {"value": value, "unit": "cw/s", "cores": workers, "kind": kind,
@@ -232,10 +233,10 @@ def main():
         gold = {c["name"]: c for c in json.load(f)["data"]}
     expect_d = [gold[f"cfg2_s{s}"]["d"] for s in SEEDS]
 
-    # Codes are independent objects: rank r owns codes r, r + N, ... (no data-path
-    # collective; the 8-code step is fixed, so scaling is strong). One context per owned
-    # code with its Gamma set resident in HBM, plus the host matrices.
-    mine = [i for i in range(len(SEEDS)) if i % world == rank]
+    # Codes are independent objects: every rank runs the eight-code step on its GPU (no
+    # data-path collective; per-GPU work fixed: weak scaling). One context per code with its
+    # Gamma set resident in HBM, plus the host matrices.
+    mine = list(range(len(SEEDS)))
     Gs = [mdg.gen_matrix(N, K, SEEDS[i], True) for i in mine]
     gsets = [mdg.GammaSet.build(G, N, 10, SEEDS[i]) for G, i in zip(Gs, mine)]
     devs = [mdg.Device(local) for _ in mine]
@@ -468,12 +469,13 @@ def main():
         line = {
             "metric": "codewords_evaluated_per_sec", "value": value, "unit": "cw/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (mt19937_64 seeds 1..8, SURVEY.md §8d)",
             "config": {"workload": WORKLOAD, "kernel": args.kernel,
-                       "parallelism": (f"{world} ranks, codes sharded (rank r owns codes r, r+{world}, ...), "
-                                       f"{args.streams} in flight per GPU; no data-path collective"
+                       "parallelism": (f"{world} ranks, each running the eight-code step "
+                                       f"({args.streams} codes in flight per GPU); independent codes, "
+                                       "no data-path collective"
                                        if world > 1 else
                                        f"single GPU, {min(args.streams, len(SEEDS))} codes in flight"),
                        "round_split": split,
