@@ -435,9 +435,14 @@ GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint6
     const uint32_t k = G.rows();
     const uint32_t KW = shape_words(k);
     std::vector<uint64_t> cols(size_t(n) * KW, 0);
-    for (uint32_t r = 0; r < k; ++r)
-        for (uint32_t c = 0; c < n; ++c)
-            if ((G.row(r)[c >> 6] >> (c & 63)) & 1u) cols[size_t(c) * KW + (r >> 6)] |= uint64_t{1} << (r & 63);
+    for (uint32_t r = 0; r < k; ++r) {
+        const uint64_t* row = G.row(r);
+        for (uint32_t w = 0; w < G.words(); ++w)
+            for (uint64_t bits = row[w]; bits; bits &= bits - 1) {
+                const uint32_t c = w * 64 + uint32_t(__builtin_ctzll(bits));
+                if (c < n) cols[size_t(c) * KW + (r >> 6)] |= uint64_t{1} << (r & 63);
+            }
+    }
     std::vector<std::pair<uint32_t, uint32_t>> mk(trials);
     std::function<void(uint32_t)> work = [&](uint32_t t) { mk[t] = block_shape(cols, KW, n, k, perms[t]); };
     if (uint64_t(k) * n >= 1024 && trials >= 2 && HostPool::get().size() > 1)
