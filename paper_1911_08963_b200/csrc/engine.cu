@@ -60,13 +60,14 @@ constexpr int kTX = 256;            // prefixes per tile (= threads that build t
 constexpr int kFindX = 4;           // smem-side items per block of the witness search
 constexpr int kFoldDrop = 16;       // fold-option flag: stage 1 leaves out the last word
 constexpr int kFoldHalf = 32;       // fold-option flag: stage 1 folds the first ceil(NW/2) words
-constexpr int kFoldOpts = 9;        // (G in 1, 2, 4) x (all, drop, half)
+constexpr int kFoldPair = 64;       // fold-option flag: two register items share one POPC
+                                    // (popc of the AND of their folds bounds both weights)
+constexpr int kPlanT = 128;         // stage-1 choice per tile bound T < kPlanT (above: exact)
 
-// Stage-1 options of a round, cheapest first (host-sampled): a tile takes the first whose
-// limit admits its bound T. code = G | kFoldDrop | kFoldHalf; lim -1 = unused slot.
+// Stage-1 option of a round per tile bound T (host-sampled expected cost, the cheapest):
+// code = G | kFoldDrop | kFoldHalf | kFoldPair, 0 = exact weights.
 struct FoldPlan {
-    int32_t lim[kFoldOpts];
-    int32_t code[kFoldOpts];
+    uint8_t code[kPlanT];
 };
 constexpr uint32_t kBT = kMaxC + 1; // binomial table row stride
 constexpr int kKeyShift = 40;
@@ -606,8 +607,49 @@ __device__ __forceinline__ uint32_t fold_bound(const uint32_t (&X)[S], const uin
     return lb;
 }
 
+// Pair bound: sum_g popc(fold_g(X ^ Ya) & fold_g(X ^ Yb)) is at most each of the two
+// fold bounds, so it bounds both weights from below with G POPCs for the two codewords
+// (one AND per group more). With dense folds (bit set w.p. 3/4 for two words) the AND
+// keeps 9/16 of the bits: a weaker bound that still rejects nearly every pair at the
+// deep levels' small T, and the XU pipe (POPC, 16/clk/SM) stops binding.
+template <int G, int S, int NW, int NWF = NW>
+__device__ __forceinline__ uint32_t fold_bound_pair(const uint32_t (&X)[S], const uint32_t (&Ya)[NW],
+                                                    const uint32_t (&Yb)[NW], uint32_t lb) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const int b = g * NWF / G, e = (g + 1) * NWF / G;
+        if (b < e) {
+            uint32_t fa = X[b] ^ Ya[b], fb = X[b] ^ Yb[b];
+#pragma unroll
+            for (int i = b + 1; i < e; ++i) {
+                fa = or_xor(fa, X[i], Ya[i]);
+                fb = or_xor(fb, X[i], Yb[i]);
+            }
+            lb += __popc(fa & fb);
+        }
+    }
+    return lb;
+}
+
+// Exact weights of register items [r0, r0 + n) against smem item X; lowers best and T.
+template <int NW, bool HID, int XS, int R>
+__device__ __forceinline__ void group_exact(const uint32_t (&X)[XS], const uint32_t (&Y)[R][NW],
+                                            const uint32_t (&idY)[R], int r0, int n,
+                                            uint32_t& best, int32_t& T) {
+#pragma unroll
+    for (int r = 0; r < n; ++r) {
+        uint32_t w = xor_weight<0, NW, XS, NW>(X, Y[r0 + r]);
+        if (HID) w += X[NW] + idY[r0 + r];
+        best = min(best, w);
+    }
+    T = min(T, int32_t(best));
+}
+
 // The bound-pruned walk with G fold groups over the first NWF words (see tile_min).
-template <int NW, bool HID, int G, int NWF = NW>
+// PAIR: a pre-filter of one bound per two register items (fold_bound_pair) over vote groups
+// of GP items; a group it cannot reject takes the single-item fold bounds (vote groups of
+// GR), and only their survivors the exact weight.
+template <int NW, bool HID, int G, int NWF = NW, bool PAIR = false>
 __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t x_begin, uint32_t nx,
                                                     const uint32_t (&Y)[r_for(NW)][NW],
                                                     const uint32_t (&idY)[r_for(NW)], int32_t T) {
@@ -616,7 +658,12 @@ __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t
 #ifndef MDG_VOTE_GROUP
 #define MDG_VOTE_GROUP 4
 #endif
-    constexpr int GR = R >= MDG_VOTE_GROUP ? MDG_VOTE_GROUP : R; // suffixes per warp vote
+#ifndef MDG_PAIR_VOTE_GROUP
+#define MDG_PAIR_VOTE_GROUP 8
+#endif
+    constexpr int GR = R >= MDG_VOTE_GROUP ? MDG_VOTE_GROUP : R;           // single-bound vote
+    constexpr int GP = R >= MDG_PAIR_VOTE_GROUP ? MDG_PAIR_VOTE_GROUP : R; // pair-bound vote
+    static_assert(!PAIR || (GP % 2 == 0 && GP % GR == 0), "pair vote groups");
     uint32_t best = 0xFFFFFFFFu;
     for (uint32_t xi = x_begin; xi < nx; ++xi) {
         uint32_t X[XS];
@@ -624,70 +671,52 @@ __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t
         // partial identity block: the register item's count starts the popcount sum (one
         // IADD3 with the fold POPCs) and the smem item's comes off the bound once per row
         const int32_t Tx = HID ? T - int32_t(X[NW]) : T;
-        uint32_t lb[R];
+        if constexpr (PAIR) {
+            uint32_t lp[R / 2];
 #pragma unroll
-        for (int r = 0; r < R; ++r) lb[r] = fold_bound<G, XS, NW, NWF>(X, Y[r], HID ? idY[r] : 0u);
+            for (int b = 0; b < R / 2; ++b)
+                lp[b] = fold_bound_pair<G, XS, NW, NWF>(X, Y[2 * b], Y[2 * b + 1],
+                                                        HID ? min(idY[2 * b], idY[2 * b + 1]) : 0u);
 #pragma unroll
-        for (int g0 = 0; g0 < R; g0 += GR) {
-            uint32_t gmin = lb[g0];
+            for (int g0 = 0; g0 < R; g0 += GP) {
+                uint32_t gmin = lp[g0 / 2];
 #pragma unroll
-            for (int r = 1; r < GR; ++r) gmin = min(gmin, lb[g0 + r]);
-            if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= Tx)) {
+                for (int b = 1; b < GP / 2; ++b) gmin = min(gmin, lp[g0 / 2 + b]);
+                if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= Tx)) {
 #pragma unroll
-                for (int r = 0; r < GR; ++r) {
-                    uint32_t w = xor_weight<0, NW, XS, NW>(X, Y[g0 + r]);
-                    if (HID) w += X[NW] + idY[g0 + r];
-                    best = min(best, w);
+                    for (int h0 = g0; h0 < g0 + GP; h0 += GR) {
+                        uint32_t hmin = 0xFFFFFFFFu;
+#pragma unroll
+                        for (int r = 0; r < GR; ++r)
+                            hmin = min(hmin, fold_bound<G, XS, NW, NWF>(X, Y[h0 + r], HID ? idY[h0 + r] : 0u));
+                        const int32_t Th = HID ? T - int32_t(X[NW]) : T; // T may have dropped
+                        if (__any_sync(0xFFFFFFFFu, int32_t(hmin) <= Th))
+                            group_exact<NW, HID>(X, Y, idY, h0, GR, best, T);
+                    }
                 }
-                T = min(T, int32_t(best));
+            }
+        } else {
+            uint32_t lb[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) lb[r] = fold_bound<G, XS, NW, NWF>(X, Y[r], HID ? idY[r] : 0u);
+#pragma unroll
+            for (int g0 = 0; g0 < R; g0 += GR) {
+                uint32_t gmin = lb[g0];
+#pragma unroll
+                for (int r = 1; r < GR; ++r) gmin = min(gmin, lb[g0 + r]);
+                if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= Tx)) group_exact<NW, HID>(X, Y, idY, g0, GR, best, T);
             }
         }
     }
     return best;
 }
 
-// Minimum of (compacted weight + identity count) over prefixes xs[x_begin, nx) x the
-// lane's R suffixes, considering only values <= T (T < 0: none). Values above T may be
-// reported as "none" (0xFFFFFFFF) or exactly — never as anything smaller than the
-// truth. G (warp-uniform): 0 = exact weights for every codeword; 1, 2, 4 = stage-1
-// lower bound from that many OR-fold groups, exact weight only for warp groups of 4
-// suffixes in which some lane can still reach T (a real warp-uniform branch: a
-// per-codeword vote gets if-converted and the predicated POPCs would still occupy the
-// XU pipe). T must be warp-uniform on entry.
 template <int NW, bool HID>
-__device__ __forceinline__ uint32_t tile_min(const uint32_t* xs, uint32_t x_begin, uint32_t nx,
-                                             const uint32_t (&Y)[r_for(NW)][NW],
-                                             const uint32_t (&idY)[r_for(NW)], int32_t T,
-                                             int G) {
+__device__ __forceinline__ uint32_t tile_min_exact(const uint32_t* xs, uint32_t x_begin, uint32_t nx,
+                                                   const uint32_t (&Y)[r_for(NW)][NW],
+                                                   const uint32_t (&idY)[r_for(NW)]) {
     constexpr int R = r_for(NW);
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
-    if (T < 0) return 0xFFFFFFFFu; // every codeword here is above the bound
-    constexpr int ND = NW >= 2 ? NW - 1 : NW, NH = (NW + 1) / 2; // drop / half fold widths
-    if (G == 1) return tile_min_pruned<NW, HID, 1>(xs, x_begin, nx, Y, idY, T);
-    if constexpr (NW >= 3) {
-        if (G == 2) return tile_min_pruned<NW, HID, 2>(xs, x_begin, nx, Y, idY, T);
-    }
-    if constexpr (NW >= 5) {
-        if (G == 4) return tile_min_pruned<NW, HID, 4>(xs, x_begin, nx, Y, idY, T);
-    }
-    if constexpr (NW >= 2) {
-        if (G == (1 | kFoldDrop)) return tile_min_pruned<NW, HID, 1, ND>(xs, x_begin, nx, Y, idY, T);
-    }
-    if constexpr (ND >= 3 && NW >= 2) {
-        if (G == (2 | kFoldDrop)) return tile_min_pruned<NW, HID, 2, ND>(xs, x_begin, nx, Y, idY, T);
-    }
-    if constexpr (ND >= 5 && NW >= 2) {
-        if (G == (4 | kFoldDrop)) return tile_min_pruned<NW, HID, 4, ND>(xs, x_begin, nx, Y, idY, T);
-    }
-    if constexpr (NW >= 3) {
-        if (G == (1 | kFoldHalf)) return tile_min_pruned<NW, HID, 1, NH>(xs, x_begin, nx, Y, idY, T);
-    }
-    if constexpr (NH >= 3 && NW >= 3) {
-        if (G == (2 | kFoldHalf)) return tile_min_pruned<NW, HID, 2, NH>(xs, x_begin, nx, Y, idY, T);
-    }
-    if constexpr (NH >= 5 && NW >= 3) {
-        if (G == (4 | kFoldHalf)) return tile_min_pruned<NW, HID, 4, NH>(xs, x_begin, nx, Y, idY, T);
-    }
     uint32_t best = 0xFFFFFFFFu;
     for (uint32_t xi = x_begin; xi < nx; ++xi) {
         uint32_t X[XS];
@@ -700,6 +729,60 @@ __device__ __forceinline__ uint32_t tile_min(const uint32_t* xs, uint32_t x_begi
         }
     }
     return best;
+}
+
+// the stage-1 variant for fold code G (pair flag already decoded into PAIR); exact if none
+template <int NW, bool HID, bool PAIR>
+__device__ __forceinline__ uint32_t tile_min_folds(const uint32_t* xs, uint32_t x_begin, uint32_t nx,
+                                                   const uint32_t (&Y)[r_for(NW)][NW],
+                                                   const uint32_t (&idY)[r_for(NW)], int32_t T, int G) {
+    constexpr int ND = NW >= 2 ? NW - 1 : NW, NH = (NW + 1) / 2; // drop / half fold widths
+    if (G == 1) return tile_min_pruned<NW, HID, 1, NW, PAIR>(xs, x_begin, nx, Y, idY, T);
+    if constexpr (NW >= 3) {
+        if (G == 2) return tile_min_pruned<NW, HID, 2, NW, PAIR>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (NW >= 5) {
+        if (G == 4) return tile_min_pruned<NW, HID, 4, NW, PAIR>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (NW >= 2) {
+        if (G == (1 | kFoldDrop)) return tile_min_pruned<NW, HID, 1, ND, PAIR>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (ND >= 3 && NW >= 2) {
+        if (G == (2 | kFoldDrop)) return tile_min_pruned<NW, HID, 2, ND, PAIR>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (ND >= 5 && NW >= 2) {
+        if (G == (4 | kFoldDrop)) return tile_min_pruned<NW, HID, 4, ND, PAIR>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (NW >= 3) {
+        if (G == (1 | kFoldHalf)) return tile_min_pruned<NW, HID, 1, NH, PAIR>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (NH >= 3 && NW >= 3) {
+        if (G == (2 | kFoldHalf)) return tile_min_pruned<NW, HID, 2, NH, PAIR>(xs, x_begin, nx, Y, idY, T);
+    }
+    if constexpr (NH >= 5 && NW >= 3) {
+        if (G == (4 | kFoldHalf)) return tile_min_pruned<NW, HID, 4, NH, PAIR>(xs, x_begin, nx, Y, idY, T);
+    }
+    return tile_min_exact<NW, HID>(xs, x_begin, nx, Y, idY);
+}
+
+// Minimum of (compacted weight + identity count) over prefixes xs[x_begin, nx) x the
+// lane's R suffixes, considering only values <= T (T < 0: none). Values above T may be
+// reported as "none" (0xFFFFFFFF) or exactly — never as anything smaller than the
+// truth. G (warp-uniform): 0 = exact weights for every codeword; 1, 2, 4 = stage-1
+// lower bound from that many OR-fold groups (| kFoldPair: one bound per two register
+// items), exact weight only for warp groups of 4 suffixes in which some lane can still
+// reach T (a real warp-uniform branch: a per-codeword vote gets if-converted and the
+// predicated POPCs would still occupy the XU pipe). T must be warp-uniform on entry.
+template <int NW, bool HID>
+__device__ __forceinline__ uint32_t tile_min(const uint32_t* xs, uint32_t x_begin, uint32_t nx,
+                                             const uint32_t (&Y)[r_for(NW)][NW],
+                                             const uint32_t (&idY)[r_for(NW)], int32_t T,
+                                             int G) {
+    if (T < 0) return 0xFFFFFFFFu; // every codeword here is above the bound
+    if constexpr (r_for(NW) >= 2) {
+        if (G & kFoldPair) return tile_min_folds<NW, HID, true>(xs, x_begin, nx, Y, idY, T, G & ~kFoldPair);
+    }
+    return tile_min_folds<NW, HID, false>(xs, x_begin, nx, Y, idY, T, G & ~kFoldPair);
 }
 
 // ------------------------------------------------ revolving-door walk (Kernel::rd)
@@ -778,6 +861,7 @@ __device__ __forceinline__ uint32_t tile_min_walk(const uint32_t* xs, uint32_t n
                                                   uint32_t (&A)[r_for(NW)][NW],
                                                   uint32_t (&idA)[r_for(NW)], int32_t T, int G) {
     if (T < 0) return 0xFFFFFFFFu;
+    G &= ~kFoldPair; // the walk bounds each item on its own (at least as tight as a pair bound)
     constexpr int ND = NW >= 2 ? NW - 1 : NW, NH = (NW + 1) / 2;
     if constexpr (NW >= 2) {
         if (G == (1 | kFoldDrop)) return walk_min<NW, HID, 1, ND>(xs, nx, A, idA, T);
@@ -818,10 +902,7 @@ __device__ __forceinline__ int pick_groups(int32_t T, const int32_t (&lim)[3]) {
     return 0;
 }
 __device__ __forceinline__ int pick_fold(int32_t T, const FoldPlan& fp) {
-#pragma unroll
-    for (int i = 0; i < kFoldOpts; ++i)
-        if (T <= fp.lim[i]) return fp.code[i];
-    return 0;
+    return (T >= 0 && T < kPlanT) ? int(fp.code[T]) : 0;
 }
 
 #ifndef MDG_MINBLK_SMALL
@@ -2073,16 +2154,19 @@ static const uint32_t* ensure_xtab(Engine::Impl& im, uint32_t j, uint32_t k, uin
 }
 
 
-// margin of the stage-1 limits, in standard deviations of the sampled bound
-#ifndef MDG_SIGMA
-#define MDG_SIGMA 3.5
+// sd inflation of the normal tail used for overdispersed stage-1 bounds
+#ifndef MDG_SD_SCALE
+#define MDG_SD_SCALE 1.15
 #endif
-constexpr double kSigma = MDG_SIGMA;
+constexpr double kSdScale = MDG_SD_SCALE;
 
-// Stage-1 limits measured on the round's own codewords: 128 uniform random
-// c-subsets of Gamma_j's compacted rows (SplitMix64 seeded by (j, c)), lower bounds
-// lb_G = sum of popc over G fold groups (+ identity count), lim_G = mean - 3.5 sd - 1.
-// Sampling captures the column structure the density model misses (the partial
+// Stage-1 choice per tile bound T, from the round's own codewords: 512 uniform random
+// c-subsets of Gamma_j's compacted rows (SplitMix64 seeded by (j, c)) give mean and sd of
+// each option's lower bound lb_G (sum of popc over G fold groups + identity count) and of
+// its pair bound (the AND of two codewords' folds, the second sharing half the rows as
+// two codewords of a tile share the prefix). Per T the option with the smallest expected
+// pipe time per codeword wins (see the cost model below); exact weights when none beats
+// them. Sampling captures the column structure a density model misses (the partial
 // Gamma's rows are e_r plus subsets of the pivot columns: dense in half the columns).
 static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k, uint32_t c);
 
@@ -2106,14 +2190,24 @@ static void prefetch_fold_plans(Engine::Impl& im, uint32_t m, uint32_t k, uint32
     for (size_t i = 0; i < todo.size(); ++i) im.fold_cache[std::make_pair(todo[i], c)] = out[i];
 }
 
+// POPCs of popsum<n> (Harley-Seal chain)
+static int popsum_popcs(int n) {
+    if (n <= 2) return n < 0 ? 0 : n;
+    const int m = (n - 1) / 2;
+    return 1 + ((n - 1) % 2) + popsum_popcs(m);
+}
+
 static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k, uint32_t c) {
     FoldPlan fp;
-    for (int q = 0; q < kFoldOpts; ++q) fp.lim[q] = -1, fp.code[q] = 0;
+    std::memset(fp.code, 0, sizeof fp.code);
     const GammaDev& g = im.gammas[j];
     if (hb(k, c) < (uint64_t{1} << 20)) return fp; // a small round: exact weights cost nothing
     const uint32_t nw = g.nw;
+    const int R = r_for(int(nw));
+    const int GP = std::min(R, 8); // register items per pair-filter vote (MDG_PAIR_VOTE_GROUP)
+    static const bool no_pair = std::getenv("MDG_NO_PAIR") != nullptr; // A/B switch
     // fold widths: all words, all but the last, the first half (the kernel's variants)
-    struct Opt { uint32_t fw; int G; int code; double sum = 0, sq = 0; };
+    struct Opt { uint32_t fw; int G; int code; double sum = 0, sq = 0, psum = 0, psq = 0; };
     std::vector<Opt> opts;
     const uint32_t widths[3] = {nw, nw >= 2 ? nw - 1 : 0, nw >= 3 ? (nw + 1) / 2 : 0};
     const int flags[3] = {0, kFoldDrop, kFoldHalf};
@@ -2123,60 +2217,109 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
         for (int G : {1, 2, 4})
             if ((G == 1) || (G == 2 && fw >= 3) || (G == 4 && fw >= 5)) opts.push_back({fw, G, G | flags[v]});
     }
-    constexpr int kSamples = 128;
+    constexpr int kSamples = 512;
     SplitMix64 rng(0x9E3779B97F4A7C15ull ^ (uint64_t(j) << 32) ^ c);
-    std::vector<uint32_t> acc(nw), pick;
+    std::vector<uint32_t> acc(nw), acc2(nw), pick;
     std::vector<uint8_t> used(k);
-    for (int t = 0; t < kSamples; ++t) {
-        std::fill(acc.begin(), acc.end(), 0u);
-        uint32_t id = 0;
-        pick.clear();
-        for (uint32_t i = 0; i < c; ++i) { // c distinct rows
+    auto draw = [&](uint32_t keep, std::vector<uint32_t>& out) -> uint32_t { // c distinct rows
+        for (uint32_t i = 0; i < keep; ++i) used[pick[i]] = 1;
+        pick.resize(keep);
+        while (pick.size() < c) {
             uint32_t r;
             do { r = uint32_t(rng.next() % k); } while (used[r]);
             used[r] = 1;
             pick.push_back(r);
-            id += r < g.id_rows;
-            for (uint32_t w = 0; w < nw; ++w) acc[w] ^= g.host_rows[size_t(r) * nw + w];
         }
-        for (uint32_t r : pick) used[r] = 0;
+        std::fill(out.begin(), out.end(), 0u);
+        uint32_t id = 0;
+        for (uint32_t r : pick) {
+            used[r] = 0;
+            id += r < g.id_rows;
+            for (uint32_t w = 0; w < nw; ++w) out[w] ^= g.host_rows[size_t(r) * nw + w];
+        }
+        return id;
+    };
+    for (int t = 0; t < kSamples; ++t) {
+        pick.clear();
+        const uint32_t id = draw(0, acc);
+        const uint32_t id2 = draw(c / 2, acc2); // a second codeword of the tile: shares rows
         for (Opt& o : opts) {
-            uint32_t lb = g.hid ? id : 0;
+            uint32_t lb = g.hid ? id : 0, lp = g.hid ? std::min(id, id2) : 0;
             for (int q = 0; q < o.G; ++q) {
-                uint32_t f = 0;
-                for (uint32_t w = uint32_t(q) * o.fw / o.G; w < uint32_t(q + 1) * o.fw / o.G; ++w) f |= acc[w];
+                uint32_t f = 0, f2 = 0;
+                for (uint32_t w = uint32_t(q) * o.fw / o.G; w < uint32_t(q + 1) * o.fw / o.G; ++w)
+                    f |= acc[w], f2 |= acc2[w];
                 lb += uint32_t(__builtin_popcount(f));
+                lp += uint32_t(__builtin_popcount(f & f2));
             }
             o.sum += lb;
             o.sq += double(lb) * lb;
+            o.psum += lp;
+            o.psq += double(lp) * lp;
         }
     }
-    // cheapest first (a LOP3 per folded word, a POPC -- 4x scarcer -- per group); keep the
-    // options whose limit beats every cheaper one's
-    std::vector<std::pair<int, std::pair<int32_t, int>>> ranked; // cost, (lim, code)
-    for (const Opt& o : opts) {
-        const double mean = o.sum / kSamples;
-        const double var = std::max(0.0, o.sq / kSamples - mean * mean);
-        const int32_t lim = int32_t(std::floor(mean - kSigma * std::sqrt(var) - 1.0));
-        if (lim >= 0) ranked.push_back({int(o.fw) + 4 * o.G, {lim, o.code}});
+    // Expected pipe time per codeword in ALU-op units, max(ALU ops, 4 x POPCs) (the XU pipe
+    // issues POPC at a quarter of the LOP3 rate; the two pipes overlap). Exact weight: NW
+    // XORs, the carry-save chain, one add per POPC, the min; stage 1: one LOP3 per folded
+    // word, an IADD3 per two groups, ~1.4 ops of vote-group min / compare / vote / smem
+    // load per item (~0.9 with pairs); a vote that falls through costs its items the next
+    // stage. P(fall through) = 1 - (1 - p)^(bounds per vote), p = P(lb <= T).
+    auto csa = [](auto&& self, int n) -> int { return n <= 2 ? 0 : (n - 1) / 2 + self(self, (n - 1) / 2); };
+    const int pe = popsum_popcs(int(nw));
+    const double exact = std::max(double(nw) + 2.0 * csa(csa, int(nw)) + pe + 2.0, 4.0 * pe);
+    // P(lb <= T): lb is a popcount of nearly independent bits, so a binomial with the sampled
+    // mean and variance (N = mean / q, q = 1 - var / mean) models its tail; overdispersed
+    // samples (var >= mean: structured columns) fall back to an inflated normal tail
+    auto tail = [](double mean, double var, int T) -> double {
+        if (var <= 0) return T >= mean ? 1.0 : 0.0;
+        const double q = 1.0 - var / mean;
+        if (!(q > 0.05)) {
+            const double sd = kSdScale * std::sqrt(var);
+            return 0.5 * std::erfc(-(T + 0.5 - mean) / (sd * std::sqrt(2.0)));
+        }
+        const int N = std::max(1, int(std::lround(mean / q)));
+        const double qq = std::min(1.0 - 1e-9, mean / N);
+        double p = 0;
+        for (int i = 0; i <= std::min(T, N); ++i)
+            p += std::exp(std::lgamma(N + 1.0) - std::lgamma(i + 1.0) - std::lgamma(N - i + 1.0) +
+                          i * std::log(qq) + (N - i) * std::log1p(-qq));
+        return std::min(1.0, p);
+    };
+    auto fall = [](double p, double bounds) {
+        return -std::expm1(bounds * std::log1p(-std::min(p, 1.0 - 1e-12)));
+    };
+    const int GR = std::min(R, 4);
+    int last = -2;
+    std::string dbg;
+    for (int T = 0; T < kPlanT; ++T) {
+        double best = exact;
+        int code = 0;
+        for (const Opt& o : opts) {
+            const double m1 = o.sum / kSamples, v1 = std::max(0.0, o.sq / kSamples - m1 * m1);
+            const double adds = (o.G + 1) / 2;
+            const double f1 = fall(tail(m1, v1, T), 32.0 * GR);
+            const double single = std::max(o.fw + adds + 1.4, 4.0 * o.G) + f1 * exact;
+            if (single < best) best = single, code = o.code;
+            if (R < 2 || no_pair) continue;
+            const double m2 = o.psum / kSamples, v2 = std::max(0.0, o.psq / kSamples - m2 * m2);
+            const double f2 = fall(tail(m2, v2, T), 32.0 * (GP / 2));
+            // a fall-through group takes the single bounds (folds already computed: POPCs only)
+            const double pair = std::max(o.fw + 0.5 * o.G + 0.5 * adds + 0.9, 2.0 * o.G) +
+                                f2 * (std::max(adds + 1.4, 4.0 * o.G) + f1 * exact);
+            if (pair < best) best = pair, code = o.code | kFoldPair;
+        }
+        fp.code[T] = uint8_t(code);
+        if (code != last) {
+            char b[64];
+            std::snprintf(b, sizeof b, " T>=%d:%s%d%s%s", T, code ? "G" : "exact", code & 15,
+                          (code & kFoldDrop) ? "d" : (code & kFoldHalf) ? "h" : "", (code & kFoldPair) ? "p" : "");
+            dbg += b;
+            last = code;
+        }
     }
-    std::sort(ranked.begin(), ranked.end());
-    int n = 0;
-    int32_t best_lim = -1;
-    for (const auto& r : ranked) {
-        if (r.second.first <= best_lim) continue;
-        best_lim = r.second.first;
-        fp.lim[n] = r.second.first;
-        fp.code[n] = r.second.second;
-        ++n;
-    }
-    if (std::getenv("MDG_PLAN_DEBUG")) {
-        std::fprintf(stderr, "[mdg fold] j=%u c=%u nw=%u:", j, c, nw);
-        for (int q = 0; q < n; ++q)
-            std::fprintf(stderr, " (G=%d%s T<=%d)", fp.code[q] & 15,
-                         (fp.code[q] & kFoldDrop) ? " drop" : (fp.code[q] & kFoldHalf) ? " half" : "", fp.lim[q]);
-        std::fprintf(stderr, "\n");
-    }
+    if (const char* f = std::getenv("MDG_FORCE_FOLD")) // development: one code for every T
+        std::memset(fp.code, std::atoi(f), sizeof fp.code);
+    if (std::getenv("MDG_PLAN_DEBUG")) std::fprintf(stderr, "[mdg fold] j=%u c=%u nw=%u:%s\n", j, c, nw, dbg.c_str());
     return fp;
 }
 
@@ -2189,7 +2332,7 @@ static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe
     a.id_rows = g.id_rows; a.add_const = (g.id_rows == k) ? c : 0; a.tx = pe.plan.TX;
     a.fold = sampled_fold_plan(im, uint32_t(&g - im.gammas.data()), k, c);
     if (!im.prune) // exact weights only
-        for (int q = 0; q < kFoldOpts; ++q) a.fold.lim[q] = -1;
+        std::memset(a.fold.code, 0, sizeof a.fold.code);
     a.rd = pe.plan.rd ? 1u : 0u;
     a.xtab = pe.plan.rd ? nullptr : ensure_xtab(im, uint32_t(&g - im.gammas.data()), k, pe.plan.p - 1);
     return a;
