@@ -20,8 +20,9 @@ codes. Metric: codewords evaluated per second (BASELINE.json `metric`).
            every round result and the witness; CUDA-event timed the same way.
 * roofline — the dominant kernel (tab_round on the c = 7 rounds, measured in a
            separate pass with one loop at a time): achieved
-           codewords/s vs the POPC issue-rate roofline measured on B200
-           (profiles/pipes_microbench.jsonl: 4642 Gpopc/s = 16 POPC/clk/SM).
+           codewords/s vs the integer issue-rate roofline of its op mix: ALU pipe
+           (LOP3, 64/clk/SM) and XU pipe (POPC, 16/clk/SM) rates measured on B200
+           (profiles/r01_pipes_microbench.jsonl) over the ops per codeword ncu counts.
 * cpu_baseline — the reference's own engine (oracle/_ref, unmodified sources)
            on this host's cores, one code of the same workload.
 
@@ -44,12 +45,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 N, K, SEEDS = 128, 64, list(range(1, 9))
-POPC_PER_S_MEASURED = 4642.3e9   # profiles/r01_pipes_microbench.jsonl (B200, 148 SMs)
-# XU (POPC) operations the bound-pruned level-7 round kernel executes per codeword, from the
-# committed ncu capture of that launch (profiles/r01e_tab_round_c7_ncu.txt: tab_round<2,false>
-# on the config-2 seed-1 level-7 round, cutoff U = 15)
-XU_PER_CW_PRUNED = 1.035
-DRAM_BYTES_PER_LAUNCH = 4225024  # same capture: dram__bytes_read.sum + dram__bytes_write.sum
+POPC_PER_S_MEASURED = 4642.3e9   # profiles/r01_pipes_microbench.jsonl (B200, 148 SMs): XU pipe
+ALU_PER_S_MEASURED = 18146.5e9   # same file: LOP3 on the ALU pipe (64/clk/SM)
+# Pipe operations the bound-pruned level-7 round kernel executes per codeword, from the committed
+# ncu capture of that launch (profiles/r01h_tab_round_c7_ncu.txt: tab_round<2,false> on the
+# config-2 seed-1 level-7 round at the loop's U = 16): ALU-pipe ops (LOP3 folds, the pair AND,
+# vote-group min / compare) and XU ops (POPC). The ALU pipe binds (86 % busy, XU 57 %).
+ALU_PER_CW_PRUNED = 3.403
+XU_PER_CW_PRUNED = 0.562
+DRAM_BYTES_PER_LAUNCH = 4250368  # same capture: dram__bytes_read.sum + dram__bytes_write.sum
 WORKLOAD = "cfg2: random [128,64] codes G=(I|A), mt19937_64 seeds 1..8, BZ to termination (exact d)"
 
 
@@ -416,20 +420,27 @@ def main():
         nw = 2  # popcounts per codeword of the unpruned kernel (64 non-identity columns)
         achieved = c7_cw / (c7_ms * 1e-3) / world if c7_ms > 0 else 0.0
         popc = POPC_PER_S_MEASURED * sms / 148
-        peak = popc / XU_PER_CW_PRUNED
+        alu = ALU_PER_S_MEASURED * sms / 148
+        peak_alu, peak_xu = alu / ALU_PER_CW_PRUNED, popc / XU_PER_CW_PRUNED
+        peak = min(peak_alu, peak_xu)
         roofline = {
-            "bound": "int_popc", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gcw/s",
+            "bound": "int_alu" if peak_alu <= peak_xu else "int_popc",
+            "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gcw/s",
             "frac": achieved / peak, "traffic": DRAM_BYTES_PER_LAUNCH, "traffic_unit": "DRAM bytes per launch (ncu)",
             "kernel": ("tab_round<2,false>: one level-7 round per launch (621,216,192 codewords), "
                        "bound-pruned by the loop's U, CUDA-event timed on the engine stream "
                        "(in the chained loop both rounds of the level run as one tab_level launch, "
-                       "profiles/r01f_tab_level_c7_ncu.txt)"),
-            "peak_basis": ("measured B200 POPC (XU pipe) rate 16/clk/SM = 4.64e12/s "
-                           "(tools/pipes_microbench.cu) / 1.035 XU ops per codeword executed by this "
-                           "kernel (ncu, profiles/r01e_tab_round_c7_ncu.txt)"),
-            "op_mix_per_codeword": ("2 LOP3 (XOR, fused OR-fold) + 1 POPC of the fold (a lower bound on "
-                                    "the weight) + group min / warp vote; the exact weight only for warp "
-                                    "groups that can still beat the bound (1.035 POPC per codeword measured)"),
+                       "profiles/r01h_tab_level_c7_ncu.txt)"),
+            "peak_basis": ("integer issue-rate roofline of this kernel's op mix: min(ALU pipe 64/clk/SM = "
+                           "1.81e13 LOP3/s / 3.403 ALU ops per codeword, XU pipe 16/clk/SM = 4.64e12 POPC/s / "
+                           "0.562 POPC per codeword); rates measured on B200 (tools/pipes_microbench.cu), "
+                           "ops per codeword from ncu (profiles/r01h_tab_round_c7_ncu.txt)"),
+            "peak_alu": peak_alu / 1e9, "peak_xu": peak_xu / 1e9,
+            "op_mix_per_codeword": ("stage 1: 2 LOP3 (XOR, fused OR-fold) per codeword + 1 LOP3 (AND) and 1 POPC "
+                                    "per pair of codewords (popc(fold_a & fold_b) bounds both weights), "
+                                    "vote-group min / warp vote; single-codeword folds (1 POPC) for vote groups "
+                                    "the pair bound cannot reject; exact weight only where a codeword can still "
+                                    "beat the bound"),
             "frac_vs_unpruned_popc_roofline": achieved / (popc / nw),
             "unpruned_c7": ({
                 "what": "exact config-2 level-7 round with early exit and bound pruning off "
@@ -443,7 +454,7 @@ def main():
                 "frac_elided": ex_cw / (min(ex_ms) * 1e-3) / (popc / nw),
                 "elided_def": "identity block elided: 64 compacted bits = 2 POPC per codeword",
             } if ex_ms else None),
-            "traffic_note": "DRAM 4.2 MB per launch (the tables, read once), 0.3% of HBM bandwidth: compute-bound",
+            "traffic_note": "DRAM 4.25 MB per launch (the tables, read once), 0.5% of HBM bandwidth: compute-bound",
             "hbm_check": hbm_check(achieved),
         }
         if clocks.get("sm_mhz"):

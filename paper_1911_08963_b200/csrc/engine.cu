@@ -2270,20 +2270,32 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
     // P(lb <= T): lb is a popcount of nearly independent bits, so a binomial with the sampled
     // mean and variance (N = mean / q, q = 1 - var / mean) models its tail; overdispersed
     // samples (var >= mean: structured columns) fall back to an inflated normal tail
-    auto tail = [](double mean, double var, int T) -> double {
-        if (var <= 0) return T >= mean ? 1.0 : 0.0;
-        const double q = 1.0 - var / mean;
-        if (!(q > 0.05)) {
+    // CDF of the bound at T = 0 .. kPlanT-1 in one pass (pmf recurrence, log domain)
+    auto tail = [](double mean, double var, std::array<double, kPlanT>& cdf) {
+        const double q = var > 0 ? 1.0 - var / mean : 0.0;
+        if (var <= 0) {
+            for (int T = 0; T < kPlanT; ++T) cdf[T] = T >= mean ? 1.0 : 0.0;
+        } else if (!(q > 0.05)) {
             const double sd = kSdScale * std::sqrt(var);
-            return 0.5 * std::erfc(-(T + 0.5 - mean) / (sd * std::sqrt(2.0)));
+            for (int T = 0; T < kPlanT; ++T) cdf[T] = 0.5 * std::erfc(-(T + 0.5 - mean) / (sd * std::sqrt(2.0)));
+        } else {
+            const int N = std::min(4094, std::max(1, int(std::lround(mean / q))));
+            const double qq = std::min(1.0 - 1e-9, mean / N);
+            static const std::vector<double> logi = [] { // log(i); N <= 4094 >= any bound
+                std::vector<double> v(4096, 0.0);
+                for (size_t i = 1; i < v.size(); ++i) v[i] = std::log(double(i));
+                return v;
+            }();
+            double lp = N * std::log1p(-qq), acc = 0; // log pmf(0)
+            const double odds = std::log(qq) - std::log1p(-qq);
+            int T = 0;
+            for (; T < kPlanT && T <= N && acc < 1.0; ++T) {
+                acc += std::exp(lp);
+                cdf[T] = std::min(1.0, acc);
+                if (T < N) lp += logi[N - T] - logi[T + 1] + odds;
+            }
+            for (; T < kPlanT; ++T) cdf[T] = std::min(1.0, acc);
         }
-        const int N = std::max(1, int(std::lround(mean / q)));
-        const double qq = std::min(1.0 - 1e-9, mean / N);
-        double p = 0;
-        for (int i = 0; i <= std::min(T, N); ++i)
-            p += std::exp(std::lgamma(N + 1.0) - std::lgamma(i + 1.0) - std::lgamma(N - i + 1.0) +
-                          i * std::log(qq) + (N - i) * std::log1p(-qq));
-        return std::min(1.0, p);
     };
     auto fall = [](double p, double bounds) {
         return -std::expm1(bounds * std::log1p(-std::min(p, 1.0 - 1e-12)));
@@ -2291,18 +2303,25 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
     const int GR = std::min(R, 4);
     int last = -2;
     std::string dbg;
+    const size_t no = opts.size();
+    std::vector<std::array<double, kPlanT>> c1(no), c2(no);
+    for (size_t i = 0; i < no; ++i) {
+        const Opt& o = opts[i];
+        const double m1 = o.sum / kSamples, m2 = o.psum / kSamples;
+        tail(m1, std::max(0.0, o.sq / kSamples - m1 * m1), c1[i]);
+        tail(m2, std::max(0.0, o.psq / kSamples - m2 * m2), c2[i]);
+    }
     for (int T = 0; T < kPlanT; ++T) {
         double best = exact;
         int code = 0;
-        for (const Opt& o : opts) {
-            const double m1 = o.sum / kSamples, v1 = std::max(0.0, o.sq / kSamples - m1 * m1);
+        for (size_t i = 0; i < no; ++i) {
+            const Opt& o = opts[i];
             const double adds = (o.G + 1) / 2;
-            const double f1 = fall(tail(m1, v1, T), 32.0 * GR);
+            const double f1 = fall(c1[i][T], 32.0 * GR);
             const double single = std::max(o.fw + adds + 1.4, 4.0 * o.G) + f1 * exact;
             if (single < best) best = single, code = o.code;
             if (R < 2 || no_pair) continue;
-            const double m2 = o.psum / kSamples, v2 = std::max(0.0, o.psq / kSamples - m2 * m2);
-            const double f2 = fall(tail(m2, v2, T), 32.0 * (GP / 2));
+            const double f2 = fall(c2[i][T], 32.0 * (GP / 2));
             // a fall-through group takes the single bounds (folds already computed: POPCs only)
             const double pair = std::max(o.fw + 0.5 * o.G + 0.5 * adds + 0.9, 2.0 * o.G) +
                                 f2 * (std::max(adds + 1.4, 4.0 * o.G) + f1 * exact);
