@@ -631,6 +631,35 @@ __device__ __forceinline__ uint32_t fold_bound_pair(const uint32_t (&X)[S], cons
     return lb;
 }
 
+template <uint32_t LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(r) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+    return r;
+}
+
+// Pair bound of a two-word fold group in 3 LOP3 instead of 5. Per bit the AND of the two
+// folds is 1 iff the smem item's bit pair x = (x0, x1) is neither a's nor b's. With
+// d = x ^ a and c = a ^ b: c = 00 -> d0 | d1; c = 10 -> d1 (x0 is free); c = 01 -> d0;
+// c = 11 -> d0 ^ d1 (x in {a, ~a}). So with per-pair constants K0 = ~(c0 & ~c1),
+// K1 = ~(c1 & ~c0), KX = c0 & c1 (register side, built once per tile):
+//   u = (x0 ^ a0) & K0, v = (x1 ^ a1) & K1, bound bits = KX ? u ^ v : u | v.
+struct Pair2 { uint32_t k0, k1, kx; };
+__device__ __forceinline__ Pair2 pair2_consts(uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1) {
+    const uint32_t c0 = a0 ^ b0, c1 = a1 ^ b1;
+    Pair2 k{~(c0 & ~c1), ~(c1 & ~c0), c0 & c1};
+    // opaque to the compiler: under register pressure it would rebuild them from the
+    // register items inside the smem loop (2 LOP3 each) instead of keeping them
+    asm volatile("" : "+r"(k.k0), "+r"(k.k1), "+r"(k.kx));
+    return k;
+}
+__device__ __forceinline__ uint32_t pair2_bits(uint32_t x0, uint32_t x1, uint32_t a0, uint32_t a1,
+                                               const Pair2& k) {
+    const uint32_t u = lop3<0x28>(x0, a0, k.k0); // (x0 ^ a0) & k0
+    const uint32_t v = lop3<0x28>(x1, a1, k.k1); // (x1 ^ a1) & k1
+    return lop3<0x7C>(u, v, k.kx);               // kx ? u ^ v : u | v
+}
+
 // Exact weights of register items [r0, r0 + n) against smem item X; lowers best and T.
 template <int NW, bool HID, int XS, int R>
 __device__ __forceinline__ void group_exact(const uint32_t (&X)[XS], const uint32_t (&Y)[R][NW],
@@ -664,6 +693,11 @@ __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t
     constexpr int GR = R >= MDG_VOTE_GROUP ? MDG_VOTE_GROUP : R;           // single-bound vote
     constexpr int GP = R >= MDG_PAIR_VOTE_GROUP ? MDG_PAIR_VOTE_GROUP : R; // pair-bound vote
     static_assert(!PAIR || (GP % 2 == 0 && GP % GR == 0), "pair vote groups");
+    Pair2 K2[(PAIR && G == 1 && NWF == 2) ? R / 2 : 1];
+    if constexpr (PAIR && G == 1 && NWF == 2) {
+#pragma unroll
+        for (int b = 0; b < R / 2; ++b) K2[b] = pair2_consts(Y[2 * b][0], Y[2 * b][1], Y[2 * b + 1][0], Y[2 * b + 1][1]);
+    }
     uint32_t best = 0xFFFFFFFFu;
     for (uint32_t xi = x_begin; xi < nx; ++xi) {
         uint32_t X[XS];
@@ -674,9 +708,13 @@ __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t
         if constexpr (PAIR) {
             uint32_t lp[R / 2];
 #pragma unroll
-            for (int b = 0; b < R / 2; ++b)
-                lp[b] = fold_bound_pair<G, XS, NW, NWF>(X, Y[2 * b], Y[2 * b + 1],
-                                                        HID ? min(idY[2 * b], idY[2 * b + 1]) : 0u);
+            for (int b = 0; b < R / 2; ++b) {
+                const uint32_t id = HID ? min(idY[2 * b], idY[2 * b + 1]) : 0u;
+                if constexpr (G == 1 && NWF == 2)
+                    lp[b] = id + __popc(pair2_bits(X[0], X[1], Y[2 * b][0], Y[2 * b][1], K2[b]));
+                else
+                    lp[b] = fold_bound_pair<G, XS, NW, NWF>(X, Y[2 * b], Y[2 * b + 1], id);
+            }
 #pragma unroll
             for (int g0 = 0; g0 < R; g0 += GP) {
                 uint32_t gmin = lp[g0 / 2];
@@ -2323,7 +2361,9 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
             if (R < 2 || no_pair) continue;
             const double f2 = fall(c2[i][T], 32.0 * (GP / 2));
             // a fall-through group takes the single bounds (folds already computed: POPCs only)
-            const double pair = std::max(o.fw + 0.5 * o.G + 0.5 * adds + 0.9, 2.0 * o.G) +
+            // (a single two-word group takes 3 LOP3 per pair, pair2_bits; else 2 fw + G)
+            const double lops = (o.G == 1 && o.fw == 2) ? 1.5 : o.fw + 0.5 * o.G;
+            const double pair = std::max(lops + 0.5 * adds + 0.9, 2.0 * o.G) +
                                 f2 * (std::max(adds + 1.4, 4.0 * o.G) + f1 * exact);
             if (pair < best) best = pair, code = o.code | kFoldPair;
         }

@@ -1,10 +1,7 @@
 # A/B of the stage-1 pair pre-filter (development): config-2 rounds at T = 7, 8, 9, 10,
-# the sweep rounds and config 4 level 6, with and without MDG_NO_PAIR, and the old library
+# the sweep rounds and config 4 level 6, against a baseline library (tools/variants/)
 export PYTHONUNBUFFERED=1
-MDG_PLAN_DEBUG=1 python tools/sweep.py 2>&1 | grep "mdg fold" | sort | uniq
-MDG_PLAN_DEBUG=1 python tools/ncu_target.py --n 300 --k 200 --seed 11 --c 6 --j 1 --cutoff 24 --reps 1 2>&1 | grep "mdg fold"
-MDG_PLAN_DEBUG=1 python tools/ncu_target.py --n 300 --k 200 --seed 11 --c 6 --j 0 --cutoff 24 --reps 1 2>&1 | grep "mdg fold"
-for v in "" "MDG_FORCE_FOLD=65"; do
+for v in "" "MDG_FORCE_FOLD=1"; do
   echo "== $v"
   for cc in "7 15" "7 16" "6 16" "5 16"; do
     set -- $cc
