@@ -33,6 +33,7 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -607,30 +608,6 @@ __device__ __forceinline__ uint32_t fold_bound(const uint32_t (&X)[S], const uin
     return lb;
 }
 
-// Pair bound: sum_g popc(fold_g(X ^ Ya) & fold_g(X ^ Yb)) is at most each of the two
-// fold bounds, so it bounds both weights from below with G POPCs for the two codewords
-// (one AND per group more). With dense folds (bit set w.p. 3/4 for two words) the AND
-// keeps 9/16 of the bits: a weaker bound that still rejects nearly every pair at the
-// deep levels' small T, and the XU pipe (POPC, 16/clk/SM) stops binding.
-template <int G, int S, int NW, int NWF = NW>
-__device__ __forceinline__ uint32_t fold_bound_pair(const uint32_t (&X)[S], const uint32_t (&Ya)[NW],
-                                                    const uint32_t (&Yb)[NW], uint32_t lb) {
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-        const int b = g * NWF / G, e = (g + 1) * NWF / G;
-        if (b < e) {
-            uint32_t fa = X[b] ^ Ya[b], fb = X[b] ^ Yb[b];
-#pragma unroll
-            for (int i = b + 1; i < e; ++i) {
-                fa = or_xor(fa, X[i], Ya[i]);
-                fb = or_xor(fb, X[i], Yb[i]);
-            }
-            lb += __popc(fa & fb);
-        }
-    }
-    return lb;
-}
-
 template <uint32_t LUT>
 __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t r;
@@ -638,8 +615,12 @@ __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
     return r;
 }
 
-// Pair bound of a two-word fold group in 3 LOP3 instead of 5. Per bit the AND of the two
-// folds is 1 iff the smem item's bit pair x = (x0, x1) is neither a's nor b's. With
+// Pair bound: popc(fold(X ^ Ya) & fold(X ^ Yb)) is at most each of the two fold bounds, so
+// it bounds both weights from below with one POPC for two codewords. With dense folds (a bit
+// set w.p. 3/4 for two words) the AND keeps 9/16 of the bits: a weaker bound that still
+// rejects nearly every pair at the deep levels' small T, and the XU pipe stops binding.
+// For a two-word fold it takes 3 LOP3 instead of 5: per bit the AND of the two folds is 1
+// iff the smem item's bit pair x = (x0, x1) is neither a's nor b's. With
 // d = x ^ a and c = a ^ b: c = 00 -> d0 | d1; c = 10 -> d1 (x0 is free); c = 01 -> d0;
 // c = 11 -> d0 ^ d1 (x in {a, ~a}). So with per-pair constants K0 = ~(c0 & ~c1),
 // K1 = ~(c1 & ~c0), KX = c0 & c1 (register side, built once per tile):
@@ -675,8 +656,8 @@ __device__ __forceinline__ void group_exact(const uint32_t (&X)[XS], const uint3
 }
 
 // The bound-pruned walk with G fold groups over the first NWF words (see tile_min).
-// PAIR: a pre-filter of one bound per two register items (fold_bound_pair) over vote groups
-// of GP items; a group it cannot reject takes the single-item fold bounds (vote groups of
+// PAIR (one fold group of two words): a pre-filter of one bound per two register items
+// (pair2_bits) over vote groups of GP items; a group it cannot reject takes the single-item fold bounds (vote groups of
 // GR), and only their survivors the exact weight.
 template <int NW, bool HID, int G, int NWF = NW, bool PAIR = false>
 __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t x_begin, uint32_t nx,
@@ -693,8 +674,9 @@ __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t
     constexpr int GR = R >= MDG_VOTE_GROUP ? MDG_VOTE_GROUP : R;           // single-bound vote
     constexpr int GP = R >= MDG_PAIR_VOTE_GROUP ? MDG_PAIR_VOTE_GROUP : R; // pair-bound vote
     static_assert(!PAIR || (GP % 2 == 0 && GP % GR == 0), "pair vote groups");
-    Pair2 K2[(PAIR && G == 1 && NWF == 2) ? R / 2 : 1];
-    if constexpr (PAIR && G == 1 && NWF == 2) {
+    static_assert(!PAIR || (G == 1 && NWF == 2), "pair bounds: one two-word fold group");
+    Pair2 K2[PAIR ? R / 2 : 1];
+    if constexpr (PAIR) {
 #pragma unroll
         for (int b = 0; b < R / 2; ++b) K2[b] = pair2_consts(Y[2 * b][0], Y[2 * b][1], Y[2 * b + 1][0], Y[2 * b + 1][1]);
     }
@@ -710,10 +692,7 @@ __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t
 #pragma unroll
             for (int b = 0; b < R / 2; ++b) {
                 const uint32_t id = HID ? min(idY[2 * b], idY[2 * b + 1]) : 0u;
-                if constexpr (G == 1 && NWF == 2)
-                    lp[b] = id + __popc(pair2_bits(X[0], X[1], Y[2 * b][0], Y[2 * b][1], K2[b]));
-                else
-                    lp[b] = fold_bound_pair<G, XS, NW, NWF>(X, Y[2 * b], Y[2 * b + 1], id);
+                lp[b] = id + __popc(pair2_bits(X[0], X[1], Y[2 * b][0], Y[2 * b][1], K2[b]));
             }
 #pragma unroll
             for (int g0 = 0; g0 < R; g0 += GP) {
@@ -769,36 +748,36 @@ __device__ __forceinline__ uint32_t tile_min_exact(const uint32_t* xs, uint32_t 
     return best;
 }
 
-// the stage-1 variant for fold code G (pair flag already decoded into PAIR); exact if none
-template <int NW, bool HID, bool PAIR>
+// the stage-1 variant for fold code G (without the pair flag); exact if none
+template <int NW, bool HID>
 __device__ __forceinline__ uint32_t tile_min_folds(const uint32_t* xs, uint32_t x_begin, uint32_t nx,
                                                    const uint32_t (&Y)[r_for(NW)][NW],
                                                    const uint32_t (&idY)[r_for(NW)], int32_t T, int G) {
     constexpr int ND = NW >= 2 ? NW - 1 : NW, NH = (NW + 1) / 2; // drop / half fold widths
-    if (G == 1) return tile_min_pruned<NW, HID, 1, NW, PAIR>(xs, x_begin, nx, Y, idY, T);
+    if (G == 1) return tile_min_pruned<NW, HID, 1, NW>(xs, x_begin, nx, Y, idY, T);
     if constexpr (NW >= 3) {
-        if (G == 2) return tile_min_pruned<NW, HID, 2, NW, PAIR>(xs, x_begin, nx, Y, idY, T);
+        if (G == 2) return tile_min_pruned<NW, HID, 2, NW>(xs, x_begin, nx, Y, idY, T);
     }
     if constexpr (NW >= 5) {
-        if (G == 4) return tile_min_pruned<NW, HID, 4, NW, PAIR>(xs, x_begin, nx, Y, idY, T);
+        if (G == 4) return tile_min_pruned<NW, HID, 4, NW>(xs, x_begin, nx, Y, idY, T);
     }
     if constexpr (NW >= 2) {
-        if (G == (1 | kFoldDrop)) return tile_min_pruned<NW, HID, 1, ND, PAIR>(xs, x_begin, nx, Y, idY, T);
+        if (G == (1 | kFoldDrop)) return tile_min_pruned<NW, HID, 1, ND>(xs, x_begin, nx, Y, idY, T);
     }
     if constexpr (ND >= 3 && NW >= 2) {
-        if (G == (2 | kFoldDrop)) return tile_min_pruned<NW, HID, 2, ND, PAIR>(xs, x_begin, nx, Y, idY, T);
+        if (G == (2 | kFoldDrop)) return tile_min_pruned<NW, HID, 2, ND>(xs, x_begin, nx, Y, idY, T);
     }
     if constexpr (ND >= 5 && NW >= 2) {
-        if (G == (4 | kFoldDrop)) return tile_min_pruned<NW, HID, 4, ND, PAIR>(xs, x_begin, nx, Y, idY, T);
+        if (G == (4 | kFoldDrop)) return tile_min_pruned<NW, HID, 4, ND>(xs, x_begin, nx, Y, idY, T);
     }
     if constexpr (NW >= 3) {
-        if (G == (1 | kFoldHalf)) return tile_min_pruned<NW, HID, 1, NH, PAIR>(xs, x_begin, nx, Y, idY, T);
+        if (G == (1 | kFoldHalf)) return tile_min_pruned<NW, HID, 1, NH>(xs, x_begin, nx, Y, idY, T);
     }
     if constexpr (NH >= 3 && NW >= 3) {
-        if (G == (2 | kFoldHalf)) return tile_min_pruned<NW, HID, 2, NH, PAIR>(xs, x_begin, nx, Y, idY, T);
+        if (G == (2 | kFoldHalf)) return tile_min_pruned<NW, HID, 2, NH>(xs, x_begin, nx, Y, idY, T);
     }
     if constexpr (NH >= 5 && NW >= 3) {
-        if (G == (4 | kFoldHalf)) return tile_min_pruned<NW, HID, 4, NH, PAIR>(xs, x_begin, nx, Y, idY, T);
+        if (G == (4 | kFoldHalf)) return tile_min_pruned<NW, HID, 4, NH>(xs, x_begin, nx, Y, idY, T);
     }
     return tile_min_exact<NW, HID>(xs, x_begin, nx, Y, idY);
 }
@@ -817,10 +796,12 @@ __device__ __forceinline__ uint32_t tile_min(const uint32_t* xs, uint32_t x_begi
                                              const uint32_t (&idY)[r_for(NW)], int32_t T,
                                              int G) {
     if (T < 0) return 0xFFFFFFFFu; // every codeword here is above the bound
-    if constexpr (r_for(NW) >= 2) {
-        if (G & kFoldPair) return tile_min_folds<NW, HID, true>(xs, x_begin, nx, Y, idY, T, G & ~kFoldPair);
+    // pair codes exist for a single two-word fold group only: all of NW = 2, the first two
+    // words of NW = 3 (drop) or 4 (half) -- the host plans no other
+    if constexpr (NW >= 2 && NW <= 4 && r_for(NW) >= 2) {
+        if (G & kFoldPair) return tile_min_pruned<NW, HID, 1, 2, true>(xs, x_begin, nx, Y, idY, T);
     }
-    return tile_min_folds<NW, HID, false>(xs, x_begin, nx, Y, idY, T, G & ~kFoldPair);
+    return tile_min_folds<NW, HID>(xs, x_begin, nx, Y, idY, T, G & ~kFoldPair);
 }
 
 // ------------------------------------------------ revolving-door walk (Kernel::rd)
@@ -2198,7 +2179,7 @@ static const uint32_t* ensure_xtab(Engine::Impl& im, uint32_t j, uint32_t k, uin
 #endif
 constexpr double kSdScale = MDG_SD_SCALE;
 
-// Stage-1 choice per tile bound T, from the round's own codewords: 512 uniform random
+// Stage-1 choice per tile bound T, from the round's own codewords: 128 uniform random
 // c-subsets of Gamma_j's compacted rows (SplitMix64 seeded by (j, c)) give mean and sd of
 // each option's lower bound lb_G (sum of popc over G fold groups + identity count) and of
 // its pair bound (the AND of two codewords' folds, the second sharing half the rows as
@@ -2217,15 +2198,22 @@ static FoldPlan sampled_fold_plan(Engine::Impl& im, uint32_t j, uint32_t k, uint
     return fp;
 }
 
-// the fold plans of all Gammas of level c, sampled in parallel on the host pool
-static void prefetch_fold_plans(Engine::Impl& im, uint32_t m, uint32_t k, uint32_t c) {
-    std::vector<uint32_t> todo;
-    for (uint32_t j = 0; j < m; ++j)
-        if (!im.fold_cache.count(std::make_pair(j, c))) todo.push_back(j);
+// the fold plans of all Gammas of levels [c, c_hi] not yet cached, sampled in parallel on
+// the host pool (one job)
+static void prefetch_fold_plans(Engine::Impl& im, uint32_t m, uint32_t k, uint32_t c, uint32_t c_hi) {
+    std::vector<std::pair<uint32_t, uint32_t>> todo;
+    for (uint32_t g = c; g <= std::min(c_hi, std::min(k, uint32_t(kMaxC))); ++g)
+        for (uint32_t j = 0; j < m; ++j)
+            if (!im.fold_cache.count(std::make_pair(j, g))) todo.push_back({j, g});
     if (todo.size() < 2) return;
+    const auto t0 = std::chrono::steady_clock::now();
     std::vector<FoldPlan> out(todo.size());
-    parallel_for(uint32_t(todo.size()), [&](uint32_t i) { out[i] = compute_fold_plan(im, todo[i], k, c); });
-    for (size_t i = 0; i < todo.size(); ++i) im.fold_cache[std::make_pair(todo[i], c)] = out[i];
+    parallel_for(uint32_t(todo.size()),
+                 [&](uint32_t i) { out[i] = compute_fold_plan(im, todo[i].first, k, todo[i].second); });
+    for (size_t i = 0; i < todo.size(); ++i) im.fold_cache[todo[i]] = out[i];
+    if (std::getenv("MDG_PLAN_DEBUG"))
+        std::fprintf(stderr, "[mdg fold] %zu plans (levels %u..%u) in %.1f us\n", todo.size(), c, c_hi,
+                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
 }
 
 // POPCs of popsum<n> (Harley-Seal chain)
@@ -2255,7 +2243,7 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
         for (int G : {1, 2, 4})
             if ((G == 1) || (G == 2 && fw >= 3) || (G == 4 && fw >= 5)) opts.push_back({fw, G, G | flags[v]});
     }
-    constexpr int kSamples = 512;
+    constexpr int kSamples = 128;
     SplitMix64 rng(0x9E3779B97F4A7C15ull ^ (uint64_t(j) << 32) ^ c);
     std::vector<uint32_t> acc(nw), acc2(nw), pick;
     std::vector<uint8_t> used(k);
@@ -2264,7 +2252,7 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
         pick.resize(keep);
         while (pick.size() < c) {
             uint32_t r;
-            do { r = uint32_t(rng.next() % k); } while (used[r]);
+            do { r = uint32_t(((rng.next() >> 32) * k) >> 32); } while (used[r]); // no division
             used[r] = 1;
             pick.push_back(r);
         }
@@ -2277,10 +2265,16 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
         }
         return id;
     };
+    const auto tp0 = std::chrono::steady_clock::now();
+    const bool pairs = R >= 2 && !no_pair && std::any_of(opts.begin(), opts.end(), [](const Opt& o) {
+        return o.G == 1 && o.fw == 2; // pair2_bits: one two-word fold group
+    });
     for (int t = 0; t < kSamples; ++t) {
         pick.clear();
         const uint32_t id = draw(0, acc);
-        const uint32_t id2 = draw(c / 2, acc2); // a second codeword of the tile: shares rows
+        // a second codeword of the tile for the pair bound: shares rows, as two codewords of a
+        // tile share the prefix
+        const uint32_t id2 = pairs ? draw(c / 2, acc2) : id;
         for (Opt& o : opts) {
             uint32_t lb = g.hid ? id : 0, lp = g.hid ? std::min(id, id2) : 0;
             for (int q = 0; q < o.G; ++q) {
@@ -2288,7 +2282,7 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
                 for (uint32_t w = uint32_t(q) * o.fw / o.G; w < uint32_t(q + 1) * o.fw / o.G; ++w)
                     f |= acc[w], f2 |= acc2[w];
                 lb += uint32_t(__builtin_popcount(f));
-                lp += uint32_t(__builtin_popcount(f & f2));
+                if (pairs) lp += uint32_t(__builtin_popcount(f & f2));
             }
             o.sum += lb;
             o.sq += double(lb) * lb;
@@ -2324,23 +2318,34 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
                 for (size_t i = 1; i < v.size(); ++i) v[i] = std::log(double(i));
                 return v;
             }();
-            double lp = N * std::log1p(-qq), acc = 0; // log pmf(0)
-            const double odds = std::log(qq) - std::log1p(-qq);
+            // pmf(T+1) = pmf(T) (N - T) / (T + 1) * q / (1 - q): in logs while pmf is below
+            // the double range, then by multiplication (one exp per option)
+            double lp = N * std::log1p(-qq), acc = 0, pm = 0; // log pmf(0)
+            const double odds = qq / (1.0 - qq), lodds = std::log(odds);
             int T = 0;
             for (; T < kPlanT && T <= N && acc < 1.0; ++T) {
-                acc += std::exp(lp);
+                if (pm == 0 && lp > -700) pm = std::exp(lp);
+                acc += pm;
                 cdf[T] = std::min(1.0, acc);
-                if (T < N) lp += logi[N - T] - logi[T + 1] + odds;
+                if (T < N) {
+                    if (pm == 0) lp += logi[N - T] - logi[T + 1] + lodds;
+                    else pm *= double(N - T) / double(T + 1) * odds;
+                }
             }
             for (; T < kPlanT; ++T) cdf[T] = std::min(1.0, acc);
         }
     };
-    auto fall = [](double p, double bounds) {
-        return -std::expm1(bounds * std::log1p(-std::min(p, 1.0 - 1e-12)));
+    // 1 - (1 - p)^bounds for bounds = 32 x a power of two (vote groups of 1..8 items), by
+    // repeated squaring: the plan is on the host's critical path between levels
+    auto fall = [](double p, int bounds) {
+        double q = 1.0 - std::min(p, 1.0);
+        for (int b = 1; b < bounds; b *= 2) q *= q;
+        return 1.0 - q;
     };
     const int GR = std::min(R, 4);
     int last = -2;
     std::string dbg;
+    const auto tp1 = std::chrono::steady_clock::now();
     const size_t no = opts.size();
     std::vector<std::array<double, kPlanT>> c1(no), c2(no);
     for (size_t i = 0; i < no; ++i) {
@@ -2355,15 +2360,14 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
         for (size_t i = 0; i < no; ++i) {
             const Opt& o = opts[i];
             const double adds = (o.G + 1) / 2;
-            const double f1 = fall(c1[i][T], 32.0 * GR);
+            const double f1 = fall(c1[i][T], 32 * GR);
             const double single = std::max(o.fw + adds + 1.4, 4.0 * o.G) + f1 * exact;
             if (single < best) best = single, code = o.code;
-            if (R < 2 || no_pair) continue;
-            const double f2 = fall(c2[i][T], 32.0 * (GP / 2));
+            if (!pairs || o.G != 1 || o.fw != 2) continue; // pair2_bits: one 2-word group
+            const double f2 = fall(c2[i][T], 32 * (GP / 2));
             // a fall-through group takes the single bounds (folds already computed: POPCs only)
-            // (a single two-word group takes 3 LOP3 per pair, pair2_bits; else 2 fw + G)
-            const double lops = (o.G == 1 && o.fw == 2) ? 1.5 : o.fw + 0.5 * o.G;
-            const double pair = std::max(lops + 0.5 * adds + 0.9, 2.0 * o.G) +
+            // 3 LOP3 per pair (pair2_bits)
+            const double pair = std::max(1.5 + 0.5 * adds + 0.9, 2.0 * o.G) +
                                 f2 * (std::max(adds + 1.4, 4.0 * o.G) + f1 * exact);
             if (pair < best) best = pair, code = o.code | kFoldPair;
         }
@@ -2378,7 +2382,12 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
     }
     if (const char* f = std::getenv("MDG_FORCE_FOLD")) // development: one code for every T
         std::memset(fp.code, std::atoi(f), sizeof fp.code);
-    if (std::getenv("MDG_PLAN_DEBUG")) std::fprintf(stderr, "[mdg fold] j=%u c=%u nw=%u:%s\n", j, c, nw, dbg.c_str());
+    if (std::getenv("MDG_PLAN_DEBUG")) {
+        const auto tp2 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[mdg fold] j=%u c=%u nw=%u (sampling %.1f us, choice %.1f us):%s\n", j, c, nw,
+                     std::chrono::duration<double, std::micro>(tp1 - tp0).count(),
+                     std::chrono::duration<double, std::micro>(tp2 - tp1).count(), dbg.c_str());
+    }
     return fp;
 }
 
@@ -2581,7 +2590,10 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
             prebuild_tables(im, m_, k_, g, g, sms_);
             built_to = g;
         }
-        prefetch_fold_plans(im, m_, k_, g);
+        // this level's plans (only the first sampled level waits for them) and the next
+        // level's, computed while the GPU runs the levels already enqueued
+        if (hb(k_, g) >= (uint64_t{1} << 20))
+            prefetch_fold_plans(im, m_, k_, g, level_cap ? std::min(level_cap, g + 1) : g + 1);
         // small levels of Gammas of one row width: all m rounds in one launch (tab_level)
         bool fuse_level = !allreduce && m_ >= 2 && m_ <= uint32_t(kMaxFuse) && fuse_max_ > 0 &&
                           double(m_) * double(binomial(k_, g)) <= fuse_max_;
