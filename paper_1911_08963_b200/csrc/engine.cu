@@ -2227,6 +2227,10 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
     FoldPlan fp;
     std::memset(fp.code, 0, sizeof fp.code);
     const GammaDev& g = im.gammas[j];
+    if (const char* f = std::getenv("MDG_FORCE_FOLD")) { // tests / A-B: one code for every T
+        std::memset(fp.code, std::atoi(f), sizeof fp.code);
+        return fp;
+    }
     if (hb(k, c) < (uint64_t{1} << 20)) return fp; // a small round: exact weights cost nothing
     const uint32_t nw = g.nw;
     const int R = r_for(int(nw));
@@ -2380,8 +2384,6 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
             last = code;
         }
     }
-    if (const char* f = std::getenv("MDG_FORCE_FOLD")) // development: one code for every T
-        std::memset(fp.code, std::atoi(f), sizeof fp.code);
     if (std::getenv("MDG_PLAN_DEBUG")) {
         const auto tp2 = std::chrono::steady_clock::now();
         std::fprintf(stderr, "[mdg fold] j=%u c=%u nw=%u (sampling %.1f us, choice %.1f us):%s\n", j, c, nw,

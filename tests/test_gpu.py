@@ -638,3 +638,43 @@ def test_min_weight_batch_many_mixed(mdg, device):
         assert (r.d, r.rounds, r.levels, r.gamma_hash, r.capped) == \
                (one.d, one.rounds, one.levels, one.gamma_hash, one.capped), i
         assert r.witness_ok or r.capped
+
+
+@pytest.mark.parametrize("code", [1, 1 | 64, 1 | 16 | 64, 1 | 32 | 64, 2 | 16, 4])
+def test_forced_fold_options_vs_oracle(mdg, device, code):
+    """Every stage-1 variant, forced on every tile bound T (MDG_FORCE_FOLD; the plan normally
+    picks them per T only for large rounds): the pair pre-filter (| 64) over one two-word
+    fold group -- all of NW = 2, the first two words of NW = 3 (drop, | 16) and NW = 4 (half,
+    | 32) -- and its fall-through to single folds and exact weights, on raw and systematic
+    matrices of 1..8 words, bounded at cutoffs around the true minimum."""
+    import os
+    rng = np.random.default_rng(99 + code)
+    os.environ["MDG_FORCE_FOLD"] = str(code)
+    try:
+        for n in (40, 64, 80, 96, 128, 150, 200, 256):
+            k = int(rng.integers(10, 20))
+            W = (n + 63) // 64
+            rows = rng.integers(0, 2**63, size=(k, W), dtype=np.uint64)
+            if n % 64:
+                rows[:, -1] &= np.uint64((1 << (n % 64)) - 1)
+            if rng.random() < 0.5:  # sparse rows: the bound admits more candidates
+                rows &= rng.integers(0, 2**63, size=(k, W), dtype=np.uint64)
+            device.load_gammas(rows, n, ranks=None)
+            for c in (2, 3, 4, 5):
+                w, _ = port.round_min(rows, n, c)
+                assert device.round(0, c).min_weight == w, (n, k, c, code)
+                for cutoff in (w, w + 1, w + 3, w + 12, n + 1):
+                    out = device.round_bounded(0, c, cutoff)
+                    assert out.min_weight == min(w, cutoff), (n, k, c, cutoff, code)
+                    assert out.bounded == (w >= cutoff), (n, k, c, cutoff, code)
+                    if not out.bounded:
+                        idx = device.round_witness(0, c, out)
+                        assert popcount_rows(rows, idx)[0] == w
+        for name in ("cfg1", "cfg2_s1", "cfg2_s8"):
+            case = next(c for c in load_golden("configs") if c["name"] == name)
+            g = case["gen"]
+            G = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
+            res = mdg.min_weight(G, g["n"], case["trials"], case["seed"], device=device, exact_rounds=True)
+            _check_run(res, case, name, True)
+    finally:
+        del os.environ["MDG_FORCE_FOLD"]
