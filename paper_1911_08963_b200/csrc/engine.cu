@@ -1651,7 +1651,7 @@ TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_b
     // tuning knobs (defaults measured on B200): tiles per resident block, smallest chunk
     static const uint32_t kTilesPerBlock = [] {
         const char* e = std::getenv("MDG_TILES_PER_BLOCK");
-        return e ? uint32_t(std::max(1, std::atoi(e))) : 8u;
+        return e ? uint32_t(std::max(1, std::atoi(e))) : 2u;
     }();
     static const uint32_t kMinTX = [] {
         const char* e = std::getenv("MDG_MIN_TX");
