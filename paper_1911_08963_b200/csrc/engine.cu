@@ -655,10 +655,50 @@ __device__ __forceinline__ void group_exact(const uint32_t (&X)[XS], const uint3
     T = min(T, int32_t(best));
 }
 
+// Pair bounds of smem item X against the register items (one per two items, pair2_bits).
+template <int NW, bool HID, int XS, int R>
+__device__ __forceinline__ void pair_bounds(const uint32_t (&X)[XS], const uint32_t (&Y)[R][NW],
+                                            const uint32_t (&idY)[R], const Pair2 (&K2)[R / 2],
+                                            uint32_t (&lp)[R / 2]) {
+#pragma unroll
+    for (int b = 0; b < R / 2; ++b) {
+        const uint32_t id = HID ? min(idY[2 * b], idY[2 * b + 1]) : 0u;
+        lp[b] = id + __popc(pair2_bits(X[0], X[1], Y[2 * b][0], Y[2 * b][1], K2[b]));
+    }
+}
+
+// A smem item whose pair bounds were not all rejected by a vote: per vote group of GP items
+// the pair bounds again, then the single-item folds (vote groups of GR), then exact weights.
+template <int NW, bool HID, int G, int NWF, int XS, int R, int GP, int GR>
+__device__ __forceinline__ void pair_fall_through(const uint32_t (&X)[XS], const uint32_t (&Y)[R][NW],
+                                                  const uint32_t (&idY)[R], const uint32_t (&lp)[R / 2],
+                                                  uint32_t& best, int32_t& T) {
+#pragma unroll
+    for (int g0 = 0; g0 < R; g0 += GP) {
+        uint32_t gmin = lp[g0 / 2];
+#pragma unroll
+        for (int b = 1; b < GP / 2; ++b) gmin = min(gmin, lp[g0 / 2 + b]);
+        const int32_t Tx = HID ? T - int32_t(X[NW]) : T;
+        if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= Tx)) {
+#pragma unroll
+            for (int h0 = g0; h0 < g0 + GP; h0 += GR) {
+                uint32_t hmin = 0xFFFFFFFFu;
+#pragma unroll
+                for (int r = 0; r < GR; ++r)
+                    hmin = min(hmin, fold_bound<G, XS, NW, NWF>(X, Y[h0 + r], HID ? idY[h0 + r] : 0u));
+                const int32_t Th = HID ? T - int32_t(X[NW]) : T; // T may have dropped
+                if (__any_sync(0xFFFFFFFFu, int32_t(hmin) <= Th))
+                    group_exact<NW, HID>(X, Y, idY, h0, GR, best, T);
+            }
+        }
+    }
+}
+
 // The bound-pruned walk with G fold groups over the first NWF words (see tile_min).
 // PAIR (one fold group of two words): a pre-filter of one bound per two register items
-// (pair2_bits) over vote groups of GP items; a group it cannot reject takes the single-item fold bounds (vote groups of
-// GR), and only their survivors the exact weight.
+// (pair2_bits); two smem items share one warp vote over all their pair bounds (half the
+// vote / min / loop overhead per codeword), and an item the vote cannot reject falls
+// through to pair_fall_through.
 template <int NW, bool HID, int G, int NWF = NW, bool PAIR = false>
 __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t x_begin, uint32_t nx,
                                                     const uint32_t (&Y)[r_for(NW)][NW],
@@ -675,54 +715,55 @@ __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t
     constexpr int GP = R >= MDG_PAIR_VOTE_GROUP ? MDG_PAIR_VOTE_GROUP : R; // pair-bound vote
     static_assert(!PAIR || (GP % 2 == 0 && GP % GR == 0), "pair vote groups");
     static_assert(!PAIR || (G == 1 && NWF == 2), "pair bounds: one two-word fold group");
-    Pair2 K2[PAIR ? R / 2 : 1];
+    uint32_t best = 0xFFFFFFFFu;
+    uint32_t xi = x_begin;
     if constexpr (PAIR) {
+        Pair2 K2[R / 2];
 #pragma unroll
         for (int b = 0; b < R / 2; ++b) K2[b] = pair2_consts(Y[2 * b][0], Y[2 * b][1], Y[2 * b + 1][0], Y[2 * b + 1][1]);
+#ifndef MDG_PAIR_X2
+#define MDG_PAIR_X2 1
+#endif
+        if (MDG_PAIR_X2) {
+            for (; xi + 1 < nx; xi += 2) {
+                uint32_t X0[XS], X1[XS], l0[R / 2], l1[R / 2];
+                vload<XS>(xs + xi * XS, X0);
+                vload<XS>(xs + (xi + 1) * XS, X1);
+                pair_bounds<NW, HID>(X0, Y, idY, K2, l0);
+                pair_bounds<NW, HID>(X1, Y, idY, K2, l1);
+                uint32_t m0 = l0[0], m1 = l1[0];
+#pragma unroll
+                for (int b = 1; b < R / 2; ++b) m0 = min(m0, l0[b]), m1 = min(m1, l1[b]);
+                const int32_t T0 = HID ? T - int32_t(X0[NW]) : T, T1 = HID ? T - int32_t(X1[NW]) : T;
+                if (__any_sync(0xFFFFFFFFu, int32_t(m0) <= T0 || int32_t(m1) <= T1)) {
+                    pair_fall_through<NW, HID, G, NWF, XS, R, GP, GR>(X0, Y, idY, l0, best, T);
+                    pair_fall_through<NW, HID, G, NWF, XS, R, GP, GR>(X1, Y, idY, l1, best, T);
+                }
+            }
+        }
+        for (; xi < nx; ++xi) {
+            uint32_t X[XS], l[R / 2];
+            vload<XS>(xs + xi * XS, X);
+            pair_bounds<NW, HID>(X, Y, idY, K2, l);
+            pair_fall_through<NW, HID, G, NWF, XS, R, GP, GR>(X, Y, idY, l, best, T);
+        }
+        return best;
     }
-    uint32_t best = 0xFFFFFFFFu;
-    for (uint32_t xi = x_begin; xi < nx; ++xi) {
+    for (; xi < nx; ++xi) {
         uint32_t X[XS];
         vload<XS>(xs + xi * XS, X);
         // partial identity block: the register item's count starts the popcount sum (one
         // IADD3 with the fold POPCs) and the smem item's comes off the bound once per row
         const int32_t Tx = HID ? T - int32_t(X[NW]) : T;
-        if constexpr (PAIR) {
-            uint32_t lp[R / 2];
+        uint32_t lb[R];
 #pragma unroll
-            for (int b = 0; b < R / 2; ++b) {
-                const uint32_t id = HID ? min(idY[2 * b], idY[2 * b + 1]) : 0u;
-                lp[b] = id + __popc(pair2_bits(X[0], X[1], Y[2 * b][0], Y[2 * b][1], K2[b]));
-            }
+        for (int r = 0; r < R; ++r) lb[r] = fold_bound<G, XS, NW, NWF>(X, Y[r], HID ? idY[r] : 0u);
 #pragma unroll
-            for (int g0 = 0; g0 < R; g0 += GP) {
-                uint32_t gmin = lp[g0 / 2];
+        for (int g0 = 0; g0 < R; g0 += GR) {
+            uint32_t gmin = lb[g0];
 #pragma unroll
-                for (int b = 1; b < GP / 2; ++b) gmin = min(gmin, lp[g0 / 2 + b]);
-                if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= Tx)) {
-#pragma unroll
-                    for (int h0 = g0; h0 < g0 + GP; h0 += GR) {
-                        uint32_t hmin = 0xFFFFFFFFu;
-#pragma unroll
-                        for (int r = 0; r < GR; ++r)
-                            hmin = min(hmin, fold_bound<G, XS, NW, NWF>(X, Y[h0 + r], HID ? idY[h0 + r] : 0u));
-                        const int32_t Th = HID ? T - int32_t(X[NW]) : T; // T may have dropped
-                        if (__any_sync(0xFFFFFFFFu, int32_t(hmin) <= Th))
-                            group_exact<NW, HID>(X, Y, idY, h0, GR, best, T);
-                    }
-                }
-            }
-        } else {
-            uint32_t lb[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) lb[r] = fold_bound<G, XS, NW, NWF>(X, Y[r], HID ? idY[r] : 0u);
-#pragma unroll
-            for (int g0 = 0; g0 < R; g0 += GR) {
-                uint32_t gmin = lb[g0];
-#pragma unroll
-                for (int r = 1; r < GR; ++r) gmin = min(gmin, lb[g0 + r]);
-                if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= Tx)) group_exact<NW, HID>(X, Y, idY, g0, GR, best, T);
-            }
+            for (int r = 1; r < GR; ++r) gmin = min(gmin, lb[g0 + r]);
+            if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= Tx)) group_exact<NW, HID>(X, Y, idY, g0, GR, best, T);
         }
     }
     return best;

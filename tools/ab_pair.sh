@@ -1,7 +1,7 @@
 # A/B of the stage-1 pair pre-filter (development): config-2 rounds at T = 7, 8, 9, 10,
 # the sweep rounds and config 4 level 6, against a baseline library (tools/variants/)
 export PYTHONUNBUFFERED=1
-for v in "" "MDG_LIB=tools/variants/libmdg_r16.so" "MDG_LIB=tools/variants/libmdg_r16g16.so"; do
+for v in "" "MDG_LIB=tools/variants/libmdg_nox2.so"; do
   echo "== $v"
   for cc in "7 15" "7 16" "6 16" "5 16"; do
     set -- $cc
