@@ -61,12 +61,13 @@ constexpr int kTX = 256;            // prefixes per tile (= threads that build t
 constexpr int kFindX = 4;           // smem-side items per block of the witness search
 constexpr int kFoldDrop = 16;       // fold-option flag: stage 1 leaves out the last word
 constexpr int kFoldHalf = 32;       // fold-option flag: stage 1 folds the first ceil(NW/2) words
+constexpr int kFold3 = 128;         // fold-option flag: one group over the first 3 words (NW >= 7)
 constexpr int kFoldPair = 64;       // fold-option flag: two register items share one POPC
                                     // (popc of the AND of their folds bounds both weights)
 constexpr int kPlanT = 128;         // stage-1 choice per tile bound T < kPlanT (above: exact)
 
 // Stage-1 option of a round per tile bound T (host-sampled expected cost, the cheapest):
-// code = G | kFoldDrop | kFoldHalf | kFoldPair, 0 = exact weights.
+// code = G | kFoldDrop | kFoldHalf | kFold3 | kFoldPair, 0 = exact weights.
 struct FoldPlan {
     uint8_t code[kPlanT];
 };
@@ -820,6 +821,9 @@ __device__ __forceinline__ uint32_t tile_min_folds(const uint32_t* xs, uint32_t 
     if constexpr (NH >= 5 && NW >= 3) {
         if (G == (4 | kFoldHalf)) return tile_min_pruned<NW, HID, 4, NH>(xs, x_begin, nx, Y, idY, T);
     }
+    if constexpr (NW >= 7) {
+        if (G == (1 | kFold3)) return tile_min_pruned<NW, HID, 1, 3>(xs, x_begin, nx, Y, idY, T);
+    }
     return tile_min_exact<NW, HID>(xs, x_begin, nx, Y, idY);
 }
 
@@ -940,6 +944,9 @@ __device__ __forceinline__ uint32_t tile_min_walk(const uint32_t* xs, uint32_t n
     }
     if constexpr (NH >= 5 && NW >= 3) {
         if (G == (4 | kFoldHalf)) return walk_min<NW, HID, 4, NH>(xs, nx, A, idA, T);
+    }
+    if constexpr (NW >= 7) {
+        if (G == (1 | kFold3)) return walk_min<NW, HID, 1, 3>(xs, nx, A, idA, T);
     }
     if (G == 1) return walk_min<NW, HID, 1>(xs, nx, A, idA, T);
     if constexpr (NW >= 3) {
@@ -2288,6 +2295,7 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
         for (int G : {1, 2, 4})
             if ((G == 1) || (G == 2 && fw >= 3) || (G == 4 && fw >= 5)) opts.push_back({fw, G, G | flags[v]});
     }
+    if (nw >= 7) opts.push_back({3, 1, 1 | kFold3}); // one group over the first three words
     constexpr int kSamples = 128;
     SplitMix64 rng(0x9E3779B97F4A7C15ull ^ (uint64_t(j) << 32) ^ c);
     std::vector<uint32_t> acc(nw), acc2(nw), pick;
@@ -2348,11 +2356,14 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
     // mean and variance (N = mean / q, q = 1 - var / mean) models its tail; overdispersed
     // samples (var >= mean: structured columns) fall back to an inflated normal tail
     // CDF of the bound at T = 0 .. kPlanT-1 in one pass (pmf recurrence, log domain)
-    auto tail = [](double mean, double var, std::array<double, kPlanT>& cdf) {
+    // (a partial Gamma's bound adds the identity count of the row set -- hypergeometric, not
+    // a popcount -- so it takes the normal tail too)
+    const bool normal = g.hid;
+    auto tail = [normal](double mean, double var, std::array<double, kPlanT>& cdf) {
         const double q = var > 0 ? 1.0 - var / mean : 0.0;
         if (var <= 0) {
             for (int T = 0; T < kPlanT; ++T) cdf[T] = T >= mean ? 1.0 : 0.0;
-        } else if (!(q > 0.05)) {
+        } else if (normal || !(q > 0.05)) {
             const double sd = kSdScale * std::sqrt(var);
             for (int T = 0; T < kPlanT; ++T) cdf[T] = 0.5 * std::erfc(-(T + 0.5 - mean) / (sd * std::sqrt(2.0)));
         } else {
@@ -2420,7 +2431,8 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
         if (code != last) {
             char b[64];
             std::snprintf(b, sizeof b, " T>=%d:%s%d%s%s", T, code ? "G" : "exact", code & 15,
-                          (code & kFoldDrop) ? "d" : (code & kFoldHalf) ? "h" : "", (code & kFoldPair) ? "p" : "");
+                          (code & kFoldDrop) ? "d" : (code & kFoldHalf) ? "h" : (code & kFold3) ? "3" : "",
+                          (code & kFoldPair) ? "p" : "");
             dbg += b;
             last = code;
         }

@@ -640,7 +640,7 @@ def test_min_weight_batch_many_mixed(mdg, device):
         assert r.witness_ok or r.capped
 
 
-@pytest.mark.parametrize("code", [1, 1 | 64, 1 | 16 | 64, 1 | 32 | 64, 2 | 16, 4])
+@pytest.mark.parametrize("code", [1, 1 | 64, 1 | 16 | 64, 1 | 32 | 64, 2 | 16, 4, 1 | 128])
 def test_forced_fold_options_vs_oracle(mdg, device, code):
     """Every stage-1 variant, forced on every tile bound T (MDG_FORCE_FOLD; the plan normally
     picks them per T only for large rounds): the pair pre-filter (| 64) over one two-word
