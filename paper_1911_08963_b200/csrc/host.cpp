@@ -311,15 +311,21 @@ bool gamma_set_is_maximal(const GammaSet& gs, uint32_t n, uint32_t k) {
 // independent columns from position j*k on (row operations keep column dependencies), a
 // pick at position pc swaps with `target` like gamma.cpp's column swap, and what the
 // forward-only scan skips is dependent and stays so. cols: n column vectors, KW words each.
+//
+// The basis is kept fully reduced (each basis vector is zero at every other pivot), so a
+// column reduces by XORing the basis vectors of the pivot bits it has set -- read off once,
+// no data-dependent branch per basis vector -- and a new pivot is cleared from the others
+// with masked XORs. Same independence test as an echelon basis, several times faster.
 template <uint32_t KW>
 static std::pair<uint32_t, uint32_t> block_shape_w(const uint64_t* cols, uint32_t n, uint32_t k,
                                                    std::vector<uint32_t>& order) {
-    thread_local std::vector<uint64_t> basis;
-    thread_local std::vector<uint32_t> piv;
-    basis.resize(size_t(k) * KW);
-    piv.resize(k);
+    thread_local std::vector<uint64_t> basis; // by pivot bit: KW words each
+    thread_local std::vector<uint32_t> pivs;  // pivots in insertion order
+    basis.resize(size_t(64) * KW * KW);
+    pivs.resize(k);
     uint32_t m = 0, k_last = 0;
     for (uint32_t o = 0; o < n; o += k) {
+        uint64_t pmask[KW] = {};
         uint32_t cnt = 0, target = o, s = o;
         while (cnt < k && target < n) {
             bool found = false;
@@ -327,19 +333,24 @@ static std::pair<uint32_t, uint32_t> block_shape_w(const uint64_t* cols, uint32_
                 uint64_t v[KW];
                 const uint64_t* src = cols + size_t(order[s]) * KW;
                 for (uint32_t w = 0; w < KW; ++w) v[w] = src[w];
-                for (uint32_t i = 0; i < cnt; ++i) {
-                    const uint32_t p = piv[i];
-                    if ((v[p >> 6] >> (p & 63)) & 1u) {
-                        const uint64_t* b = basis.data() + size_t(i) * KW;
-                        for (uint32_t w = 0; w < KW; ++w) v[w] ^= b[w];
+                for (uint32_t w = 0; w < KW; ++w)
+                    for (uint64_t mb = src[w] & pmask[w]; mb; mb &= mb - 1) {
+                        const uint64_t* b = basis.data() + (size_t(w) * 64 + uint32_t(__builtin_ctzll(mb))) * KW;
+                        for (uint32_t x = 0; x < KW; ++x) v[x] ^= b[x];
                     }
-                }
                 uint32_t lowest = UINT32_MAX;
                 for (uint32_t w = 0; w < KW; ++w)
                     if (v[w]) { lowest = w * 64 + uint32_t(__builtin_ctzll(v[w])); break; }
                 if (lowest != UINT32_MAX) {
-                    for (uint32_t w = 0; w < KW; ++w) basis[size_t(cnt) * KW + w] = v[w];
-                    piv[cnt] = lowest;
+                    const uint32_t lw = lowest >> 6, lb = lowest & 63;
+                    for (uint32_t i = 0; i < cnt; ++i) { // clear the new pivot from the others
+                        uint64_t* b = basis.data() + size_t(pivs[i]) * KW;
+                        const uint64_t sel = uint64_t{0} - ((b[lw] >> lb) & 1u);
+                        for (uint32_t x = 0; x < KW; ++x) b[x] ^= v[x] & sel;
+                    }
+                    for (uint32_t x = 0; x < KW; ++x) basis[size_t(lowest) * KW + x] = v[x];
+                    pmask[lw] |= uint64_t{1} << lb;
+                    pivs[cnt] = lowest;
                     std::swap(order[target], order[s]);
                     ++cnt;
                     ++target;
@@ -415,10 +426,30 @@ static std::pair<uint32_t, uint32_t> block_shape(const std::vector<uint64_t>& co
 
 GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint64_t seed) {
     if (trials < 1) throw std::invalid_argument("best_gamma_over_permutations: trials must be >= 1");
-    GammaSet best = compute_gamma_matrices(G);
-    if (gamma_set_is_maximal(best, G.cols(), G.rows())) return best;
-    SplitMix64 rng(seed);
     const uint32_t n = G.cols();
+    const uint32_t k = G.rows();
+    const uint32_t KW = shape_words(k);
+    std::vector<uint64_t> cols(size_t(n) * KW, 0);
+    for (uint32_t r = 0; r < k; ++r) {
+        const uint64_t* row = G.row(r);
+        for (uint32_t w = 0; w < G.words(); ++w)
+            for (uint64_t bits = row[w]; bits; bits &= bits - 1) {
+                const uint32_t c = w * 64 + uint32_t(__builtin_ctzll(bits));
+                if (c < n) cols[size_t(c) * KW + (r >> 6)] |= uint64_t{1} << (r & 63);
+            }
+    }
+    // the identity order's (m, k_last) by the block scan too: only the winner is systematized
+    std::vector<uint32_t> ident(n);
+    for (uint32_t i = 0; i < n; ++i) ident[i] = i;
+    const std::pair<uint32_t, uint32_t> id_mk = block_shape(cols, KW, n, k, ident);
+    const uint32_t m_max = (n + k - 1) / k;
+    if (id_mk.first == 0 || (id_mk.first == m_max && id_mk.second == std::min(k, n - (m_max - 1) * k))) {
+        GammaSet best = compute_gamma_matrices(G); // (throws the reference's errors)
+        if (best.m() != id_mk.first || best.k_last != id_mk.second)
+            throw std::logic_error("best_gamma_over_permutations: block scan disagrees with the systematization");
+        return best; // maximal: no trial can replace it (gamma_set_is_maximal)
+    }
+    SplitMix64 rng(seed);
     std::vector<std::vector<uint32_t>> perms(trials);
     for (uint32_t t = 0; t < trials; ++t) {
         std::vector<uint32_t>& perm = perms[t];
@@ -432,17 +463,6 @@ GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint6
     // Each candidate needs only its (m, k_last) to be compared (gamma.cpp:88-91): computed on
     // the column vectors by the greedy block scan (block_shape); the winner alone is
     // systematized in full, as the GPU search does.
-    const uint32_t k = G.rows();
-    const uint32_t KW = shape_words(k);
-    std::vector<uint64_t> cols(size_t(n) * KW, 0);
-    for (uint32_t r = 0; r < k; ++r) {
-        const uint64_t* row = G.row(r);
-        for (uint32_t w = 0; w < G.words(); ++w)
-            for (uint64_t bits = row[w]; bits; bits &= bits - 1) {
-                const uint32_t c = w * 64 + uint32_t(__builtin_ctzll(bits));
-                if (c < n) cols[size_t(c) * KW + (r >> 6)] |= uint64_t{1} << (r & 63);
-            }
-    }
     std::vector<std::pair<uint32_t, uint32_t>> mk(trials);
     std::function<void(uint32_t)> work = [&](uint32_t t) { mk[t] = block_shape(cols, KW, n, k, perms[t]); };
     if (uint64_t(k) * n >= 1024 && trials >= 2 && HostPool::get().size() > 1)
@@ -450,15 +470,14 @@ GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint6
     else
         for (uint32_t t = 0; t < trials; ++t) work(t);
     int64_t win = -1;
-    uint32_t bm = best.m(), bk = best.k_last;
+    uint32_t bm = id_mk.first, bk = id_mk.second;
     for (uint32_t t = 0; t < trials; ++t)
         if (mk[t].first > bm || (mk[t].first == bm && mk[t].second > bk)) {
             bm = mk[t].first;
             bk = mk[t].second;
             win = t;
         }
-    if (win < 0) return best;
-    GammaSet cand = gamma_for_permutation(G, perms[size_t(win)]);
+    GammaSet cand = win < 0 ? compute_gamma_matrices(G) : gamma_for_permutation(G, perms[size_t(win)]);
     if (cand.m() != bm || cand.k_last != bk)
         throw std::logic_error("best_gamma_over_permutations: block scan disagrees with the systematization");
     return cand;

@@ -9,7 +9,7 @@ import paper_1911_08963_b200 as mdg  # noqa: E402
 
 dev = mdg.Device(0)
 Gs = [mdg.gen_matrix(128, 64, s, True) for s in range(1, 9)]
-for gsearch in ("host", "gpu"):
+for gsearch in (sys.argv[1:] or ["host", "gpu"]):
     for streams in (4,):
         ts = []
         for rep in range(6):
