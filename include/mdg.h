@@ -69,7 +69,7 @@ typedef struct {
     uint32_t stopped_early;   /* 1 when the early-exit bound fired */
     uint32_t bounded;         /* 1: no codeword below the cutoff; min_weight == cutoff is a bound */
     uint32_t reserved;
-    uint64_t argmin_key;      /* opaque (weight << 40 | task); input of mdg_round_witness */
+    uint64_t argmin_key;      /* opaque (weight << 52 | position of the winner); input of mdg_round_witness */
     uint64_t combinations;    /* C(k,c): the reference's RoundStats.combinations */
     uint64_t evaluated;       /* codewords actually evaluated on this device */
     uint64_t task_lo, task_hi;/* task range this call covered (partition units) */

@@ -180,7 +180,7 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
             if (rc != 0) throw std::runtime_error("mdg: cross-rank reduction failed");
             rr.key = key;
             rr.bounded = false;
-            rr.w = key == ~0ull ? UINT32_MAX : uint32_t(key >> 40);
+            rr.w = key == ~0ull ? UINT32_MAX : uint32_t(key >> kKeyShift);
             if (cutoff && (key == ~0ull || rr.w >= cutoff)) {
                 rr.w = cutoff;
                 rr.key = ~0ull;

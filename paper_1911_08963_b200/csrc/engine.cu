@@ -19,13 +19,14 @@
 //                      register items, one XOR per word + OR-fold bound + POPC per
 //                      codeword, exact weights only where the bound can still win;
 //                      warp __reduce_min_sync; global 64-bit atomicMin of
-//                      (weight << 40 | tile); tile fetches poll the bound for early
+//                      (weight << 52 | tile | position); tile fetches poll the bound for early
 //                      exit; in a chained loop the last block closes the round.
 //                      With a revolving-door plan (Kernel::rd) the prefixes are a
 //                      contiguous revolving-door rank range walked with one
 //                      (row out ^ row in) XOR per step.
 //   tab_level<NW,HID>  all rounds of a small level in one launch.
-//   tab_find           re-evaluates the winning tile to name the witness.
+//   tab_find           re-evaluates the winning tile to name the witness (keys without
+//                      the position: revolving-door plans, rounds of >= 2^32 tiles).
 //   tab_hist           the full weight histogram of a round (per-warp smem bins).
 //   tables_build       prefix / suffix tables; span_build / span_round: brute force.
 #include <cuda_runtime.h>
@@ -72,7 +73,6 @@ struct FoldPlan {
     uint8_t code[kPlanT];
 };
 constexpr uint32_t kBT = kMaxC + 1; // binomial table row stride
-constexpr int kKeyShift = 40;
 
 __host__ __device__ constexpr int r_for(int nw) { return nw <= 4 ? 8 : (nw <= 8 ? 4 : (nw <= 16 ? 2 : 1)); }
 __host__ __device__ constexpr int stride_for(int words) {
@@ -354,6 +354,7 @@ struct TabArgs {
     uint32_t k, p, s, emin, npiv, id_rows, add_const, stop_at, tx;
     uint32_t cutoff;               // only weights < cutoff matter (0 = exact round)
     FoldPlan fold;                 // stage-1 options (host-sampled), cheapest first
+    uint32_t pos_key;              // 1: round keys carry the winner's position (kPosFlag layout)
     uint32_t rd;                   // 1: prefixes in revolving-door order; the round kernels walk
                                    //    them with one (row out ^ row in) XOR per step
     uint64_t tile_lo, tile_hi;
@@ -642,18 +643,33 @@ __device__ __forceinline__ uint32_t pair2_bits(uint32_t x0, uint32_t x1, uint32_
     return lop3<0x7C>(u, v, k.kx);               // kx ? u ^ v : u | v
 }
 
-// Exact weights of register items [r0, r0 + n) against smem item X; lowers best and T.
+// The tile searches track the lane's best as weight * 256 + (smem index of its first
+// occurrence): one shift-add and the same min per exactly weighed group. The kernel then
+// names the register item (warp_round_key) and the round key carries the position, so no
+// witness re-search is needed. (A factor of 257 would make it an IMAD on the FMA pipe, but
+// measured 9 % slower on the pruned level-7 round.) kNone: nothing at or below the bound.
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+#ifndef MDG_PACKX
+#define MDG_PACKX 256
+#endif
+constexpr uint32_t kPackX = MDG_PACKX;
+__device__ __forceinline__ uint32_t pack_best(uint32_t w, uint32_t xi) { return w * kPackX + xi; }
+__device__ __forceinline__ uint32_t best_weight(uint32_t b) { return b == kNone ? kNone : b / kPackX; }
+
+// Exact weights of register items [r0, r0 + n) against smem item xi; lowers best and T.
 template <int NW, bool HID, int XS, int R>
 __device__ __forceinline__ void group_exact(const uint32_t (&X)[XS], const uint32_t (&Y)[R][NW],
-                                            const uint32_t (&idY)[R], int r0, int n,
+                                            const uint32_t (&idY)[R], int r0, int n, uint32_t xi,
                                             uint32_t& best, int32_t& T) {
+    uint32_t m = kNone;
 #pragma unroll
     for (int r = 0; r < n; ++r) {
         uint32_t w = xor_weight<0, NW, XS, NW>(X, Y[r0 + r]);
         if (HID) w += X[NW] + idY[r0 + r];
-        best = min(best, w);
+        m = min(m, w);
     }
-    T = min(T, int32_t(best));
+    best = min(best, pack_best(m, xi));
+    T = min(T, int32_t(m));
 }
 
 // Pair bounds of smem item X against the register items (one per two items, pair2_bits).
@@ -673,7 +689,7 @@ __device__ __forceinline__ void pair_bounds(const uint32_t (&X)[XS], const uint3
 template <int NW, bool HID, int G, int NWF, int XS, int R, int GP, int GR>
 __device__ __forceinline__ void pair_fall_through(const uint32_t (&X)[XS], const uint32_t (&Y)[R][NW],
                                                   const uint32_t (&idY)[R], const uint32_t (&lp)[R / 2],
-                                                  uint32_t& best, int32_t& T) {
+                                                  uint32_t xi, uint32_t& best, int32_t& T) {
 #pragma unroll
     for (int g0 = 0; g0 < R; g0 += GP) {
         uint32_t gmin = lp[g0 / 2];
@@ -689,7 +705,7 @@ __device__ __forceinline__ void pair_fall_through(const uint32_t (&X)[XS], const
                     hmin = min(hmin, fold_bound<G, XS, NW, NWF>(X, Y[h0 + r], HID ? idY[h0 + r] : 0u));
                 const int32_t Th = HID ? T - int32_t(X[NW]) : T; // T may have dropped
                 if (__any_sync(0xFFFFFFFFu, int32_t(hmin) <= Th))
-                    group_exact<NW, HID>(X, Y, idY, h0, GR, best, T);
+                    group_exact<NW, HID>(X, Y, idY, h0, GR, xi, best, T);
             }
         }
     }
@@ -737,8 +753,8 @@ __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t
                 for (int b = 1; b < R / 2; ++b) m0 = min(m0, l0[b]), m1 = min(m1, l1[b]);
                 const int32_t T0 = HID ? T - int32_t(X0[NW]) : T, T1 = HID ? T - int32_t(X1[NW]) : T;
                 if (__any_sync(0xFFFFFFFFu, int32_t(m0) <= T0 || int32_t(m1) <= T1)) {
-                    pair_fall_through<NW, HID, G, NWF, XS, R, GP, GR>(X0, Y, idY, l0, best, T);
-                    pair_fall_through<NW, HID, G, NWF, XS, R, GP, GR>(X1, Y, idY, l1, best, T);
+                    pair_fall_through<NW, HID, G, NWF, XS, R, GP, GR>(X0, Y, idY, l0, xi, best, T);
+                    pair_fall_through<NW, HID, G, NWF, XS, R, GP, GR>(X1, Y, idY, l1, xi + 1, best, T);
                 }
             }
         }
@@ -746,7 +762,7 @@ __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t
             uint32_t X[XS], l[R / 2];
             vload<XS>(xs + xi * XS, X);
             pair_bounds<NW, HID>(X, Y, idY, K2, l);
-            pair_fall_through<NW, HID, G, NWF, XS, R, GP, GR>(X, Y, idY, l, best, T);
+            pair_fall_through<NW, HID, G, NWF, XS, R, GP, GR>(X, Y, idY, l, xi, best, T);
         }
         return best;
     }
@@ -764,7 +780,7 @@ __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t
             uint32_t gmin = lb[g0];
 #pragma unroll
             for (int r = 1; r < GR; ++r) gmin = min(gmin, lb[g0 + r]);
-            if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= Tx)) group_exact<NW, HID>(X, Y, idY, g0, GR, best, T);
+            if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= Tx)) group_exact<NW, HID>(X, Y, idY, g0, GR, xi, best, T);
         }
     }
     return best;
@@ -776,16 +792,18 @@ __device__ __forceinline__ uint32_t tile_min_exact(const uint32_t* xs, uint32_t 
                                                    const uint32_t (&idY)[r_for(NW)]) {
     constexpr int R = r_for(NW);
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
-    uint32_t best = 0xFFFFFFFFu;
+    uint32_t best = kNone;
     for (uint32_t xi = x_begin; xi < nx; ++xi) {
         uint32_t X[XS];
         vload<XS>(xs + xi * XS, X);
+        uint32_t m = kNone;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             uint32_t w = xor_weight<0, NW, XS, NW>(X, Y[r]);
             if (HID) w += X[NW] + idY[r];
-            best = min(best, w);
+            m = min(m, w);
         }
+        best = min(best, pack_best(m, xi));
     }
     return best;
 }
@@ -897,8 +915,10 @@ __device__ __forceinline__ uint32_t walk_min(const uint32_t* xs, uint32_t nx,
             if (HID) idA[r] += X[NW];
         }
         if (G == 0) {
+            uint32_t m = kNone;
 #pragma unroll
-            for (int r = 0; r < R; ++r) best = min(best, popc_words<NW>(A[r]) + (HID ? idA[r] : 0u));
+            for (int r = 0; r < R; ++r) m = min(m, popc_words<NW>(A[r]) + (HID ? idA[r] : 0u));
+            best = min(best, pack_best(m, xi));
             continue;
         }
         uint32_t lb[R];
@@ -910,10 +930,12 @@ __device__ __forceinline__ uint32_t walk_min(const uint32_t* xs, uint32_t nx,
 #pragma unroll
             for (int r = 1; r < GR; ++r) gmin = min(gmin, lb[g0 + r]);
             if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= T)) {
+                uint32_t m = kNone;
 #pragma unroll
                 for (int r = 0; r < GR; ++r)
-                    best = min(best, popc_words<NW>(A[g0 + r]) + (HID ? idA[g0 + r] : 0u));
-                T = min(T, int32_t(best));
+                    m = min(m, popc_words<NW>(A[g0 + r]) + (HID ? idA[g0 + r] : 0u));
+                best = min(best, pack_best(m, xi));
+                T = min(T, int32_t(m));
             }
         }
     }
@@ -970,6 +992,49 @@ __device__ __forceinline__ int pick_groups(int32_t T, const int32_t (&lim)[3]) {
 }
 __device__ __forceinline__ int pick_fold(int32_t T, const FoldPlan& fp) {
     return (T >= 0 && T < kPlanT) ? int(fp.code[T]) : 0;
+}
+
+// The warp's contribution to a round key from the lanes' packed bests (pack_best): with
+// pos_key the smallest (smem index, register index) of the warp's minimum --
+// the lane re-evaluates its R register items at its best smem index and takes the first
+// valid one of that weight (duplicated lanes past the tile's edge are not positions; the
+// item they duplicate is evaluated by its own lane) -- packed as (weight << 19 | xi << 11 |
+// yl), reduced over the warp. Returns the warp's key (kKeyShift / kPosFlag layout, engine.hpp)
+// or ~0 if it has nothing below the cutoff.
+template <int NW, bool HID>
+__device__ __forceinline__ unsigned long long warp_round_key(uint32_t bc, const uint32_t* xs,
+                                                             const uint32_t (&Y)[r_for(NW)][NW],
+                                                             const uint32_t (&idY)[r_for(NW)],
+                                                             uint32_t nyv, uint32_t add,
+                                                             uint32_t cutoff, uint32_t pos_key, uint64_t tile) {
+    constexpr int R = r_for(NW);
+    constexpr int XS = stride_for(NW + (HID ? 1 : 0));
+    uint32_t comb = kNone;
+    if (bc != kNone) {
+        const uint32_t w = best_weight(bc), xi = bc - w * kPackX;
+        if (pos_key) {
+            uint32_t X[XS];
+            vload<XS>(xs + xi * XS, X);
+            uint32_t yl = kNone;
+#pragma unroll
+            for (int r = R - 1; r >= 0; --r) {
+                uint32_t wr = xor_weight<0, NW, XS, NW>(X, Y[r]);
+                if (HID) wr += X[NW] + idY[r];
+                const uint32_t y = uint32_t(r) * kThreads + threadIdx.x; // valid below nyv
+                if (y < nyv && wr == w) yl = y;
+            }
+            if (yl != kNone) comb = ((w + add) << kPosBits) | (xi << 11) | yl;
+        } else {
+            comb = w + add;
+        }
+    }
+    comb = __reduce_min_sync(0xFFFFFFFFu, comb);
+    if (comb == kNone) return ~0ull;
+    const uint32_t w = pos_key ? comb >> kPosBits : comb;
+    if (cutoff != 0 && w >= cutoff) return ~0ull;
+    return pos_key ? (static_cast<unsigned long long>(w) << kKeyShift) | kPosFlag | (tile << kPosBits) |
+                         (comb & ((1u << kPosBits) - 1))
+                   : (static_cast<unsigned long long>(w) << kKeyShift) | tile;
 }
 
 #ifndef MDG_MINBLK_SMALL
@@ -1044,12 +1109,11 @@ __global__ void __launch_bounds__(kThreads, NW <= 2 ? MDG_MINBLK_SMALL : 4) tab_
         __syncthreads();
         const uint64_t tile = ti.tile;
 
-        uint32_t best = a.rd ? tile_min_walk<NW, HID>(xs, ti.nx, Y, idY, ti.T, ti.G)
-                             : tile_min<NW, HID>(xs, 0, ti.nx, Y, idY, ti.T, ti.G);
-        if (best != 0xFFFFFFFFu) best += a.add_const;
-        best = __reduce_min_sync(0xFFFFFFFFu, best);
-        if (lane == 0 && best != 0xFFFFFFFFu && (cutoff == 0 || best < cutoff)) {
-            unsigned long long key = (static_cast<unsigned long long>(best) << kKeyShift) | tile;
+        const uint32_t bc = a.rd ? tile_min_walk<NW, HID>(xs, ti.nx, Y, idY, ti.T, ti.G)
+                                 : tile_min<NW, HID>(xs, 0, ti.nx, Y, idY, ti.T, ti.G);
+        const unsigned long long key =
+            warp_round_key<NW, HID>(bc, xs, Y, idY, ti.nyv, a.add_const, cutoff, a.pos_key, tile);
+        if (lane == 0 && key != ~0ull) {
             if (key < seen) {
                 unsigned long long old = atomicMin(a.best_key, key);
                 seen = old < key ? old : key;
@@ -1186,12 +1250,11 @@ tab_level(TabArgs a, const __grid_constant__ LevelDesc L) {
             const uint64_t tile = ti.tile;
             const uint32_t add = sa.add_const;
             unsigned long long* best_key = L.r[cur_j].slot;
-            uint32_t best = a.rd ? tile_min_walk<NW, HID>(xs, ti.nx, Y, idY, ti.T, ti.G)
-                             : tile_min<NW, HID>(xs, 0, ti.nx, Y, idY, ti.T, ti.G);
-            if (best != 0xFFFFFFFFu) best += add;
-            best = __reduce_min_sync(0xFFFFFFFFu, best);
-            if (lane == 0 && best != 0xFFFFFFFFu && (cutoff == 0 || best < cutoff))
-                atomicMin(best_key, (static_cast<unsigned long long>(best) << kKeyShift) | tile);
+            const uint32_t bc = a.rd ? tile_min_walk<NW, HID>(xs, ti.nx, Y, idY, ti.T, ti.G)
+                                     : tile_min<NW, HID>(xs, 0, ti.nx, Y, idY, ti.T, ti.G);
+            const unsigned long long key =
+                warp_round_key<NW, HID>(bc, xs, Y, idY, ti.nyv, add, cutoff, a.pos_key, tile);
+            if (lane == 0 && key != ~0ull) atomicMin(best_key, key);
         }
         __syncthreads(); // xs / ti / sa reused by the next tile
     }
@@ -1439,7 +1502,7 @@ __global__ void __launch_bounds__(kThreads, 4) span_round(SpanArgs a) {
             // the bound must be warp-uniform: tile_min branches on it around warp votes
             const uint32_t wbest = __reduce_min_sync(0xFFFFFFFFu, best);
             const int32_t T = wbest == 0xFFFFFFFFu ? s_T : min(s_T, int32_t(wbest));
-            best = min(best, tile_min<NW, false>(xs, xb, nx, Y, idY, T, pick_groups(T, a.fold_lim)));
+            best = min(best, best_weight(tile_min<NW, false>(xs, xb, nx, Y, idY, T, pick_groups(T, a.fold_lim))));
             best = __reduce_min_sync(0xFFFFFFFFu, best);
             if (lane == 0 && best != 0xFFFFFFFFu) {
                 unsigned long long key = (static_cast<unsigned long long>(best) << kKeyShift) | s_tile;
@@ -2457,6 +2520,7 @@ static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe
     if (!im.prune) // exact weights only
         std::memset(a.fold.code, 0, sizeof a.fold.code);
     a.rd = pe.plan.rd ? 1u : 0u;
+    a.pos_key = (!pe.plan.rd && pe.plan.tiles() <= 0xFFFFFFFFull) ? 1u : 0u; // see kPosFlag
     a.xtab = pe.plan.rd ? nullptr : ensure_xtab(im, uint32_t(&g - im.gammas.data()), k, pe.plan.p - 1);
     return a;
 }
@@ -2559,12 +2623,18 @@ std::vector<uint32_t> Engine::witness(uint32_t j, uint32_t c, const RoundResult&
     CK(cudaSetDevice(device_));
     Impl& im = *impl_;
     const GammaDev& g = im.gammas[j];
-    const uint64_t task = rr.key & ((uint64_t{1} << kKeyShift) - 1);
+    const bool pos = (rr.key & kPosFlag) != 0;
+    const uint64_t task = pos ? (rr.key >> kPosBits) & 0xFFFFFFFFull : rr.key & (kPosFlag - 1);
     const uint32_t target = uint32_t(rr.key >> kKeyShift);
     std::vector<uint32_t> idx(c);
-    unsigned long long* slot = im.take_slot();
     const PlanEntry& pe = im.plan(k_, c, g, sms_);
     if (task >= pe.plan.tiles()) throw std::invalid_argument("witness: key names no task of this round");
+    if (pos) { // the kernel named the position: smem-side index << 11 | register-side index
+        const uint32_t p = uint32_t(rr.key & ((1u << kPosBits) - 1));
+        tab_decode(pe.plan, task, p >> 11, p & 0x7FFu, idx.data());
+        return idx;
+    }
+    unsigned long long* slot = im.take_slot();
     uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
     TabArgs a = tab_args(im, g, pe, yt, k_, c);
     a.tile_lo = task; a.tile_hi = task + 1;

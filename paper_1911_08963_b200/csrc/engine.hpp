@@ -24,6 +24,16 @@ constexpr uint32_t kMaxK = 1024;        // rows of a Gamma
 constexpr uint32_t kMaxC = 64;          // level
 constexpr uint32_t kMaxWords32 = 32;    // 32-bit words of a compacted row (n' <= 1024)
 
+// Round keys (64-bit, min-reduced over blocks and ranks): the weight in bits 52..63 (weights
+// are <= 2048); bit 51 set (kPosFlag): the task (< 2^32) in bits 19..50 and the winner's
+// position in that tile in bits 0..18 (smem-side index << 11 | register-side index, the
+// smallest of the tile's minimum); bit 51 clear: the task in bits 0..50 and the witness is
+// searched again (tab_find). The minimum key is the lowest task, then position, of the
+// round minimum either way.
+constexpr int kKeyShift = 52;
+constexpr unsigned long long kPosFlag = 1ull << 51;
+constexpr int kPosBits = 19;
+
 struct RoundResult {
     uint32_t w = UINT32_MAX;
     bool stopped = false;
