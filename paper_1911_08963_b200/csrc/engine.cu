@@ -2520,7 +2520,8 @@ static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe
     if (!im.prune) // exact weights only
         std::memset(a.fold.code, 0, sizeof a.fold.code);
     a.rd = pe.plan.rd ? 1u : 0u;
-    a.pos_key = (!pe.plan.rd && pe.plan.tiles() <= 0xFFFFFFFFull) ? 1u : 0u; // see kPosFlag
+    static const bool no_pos = std::getenv("MDG_NO_POS_KEY") != nullptr; // tests: the tab_find path
+    a.pos_key = (!no_pos && !pe.plan.rd && pe.plan.tiles() <= 0xFFFFFFFFull) ? 1u : 0u; // see kPosFlag
     a.xtab = pe.plan.rd ? nullptr : ensure_xtab(im, uint32_t(&g - im.gammas.data()), k, pe.plan.p - 1);
     return a;
 }

@@ -678,3 +678,49 @@ def test_forced_fold_options_vs_oracle(mdg, device, code):
             _check_run(res, case, name, True)
     finally:
         del os.environ["MDG_FORCE_FOLD"]
+
+
+def test_position_keys_name_the_tab_find_witness(mdg, device):
+    """Round keys carry the winner's position (kPosFlag); the witness decoded from them equals
+    the one tab_find re-searches (the lowest position of the round minimum in the lowest
+    tile), on raw and systematic matrices, exact and bounded rounds. The library reads
+    MDG_NO_POS_KEY once, so the tab_find side runs in a subprocess."""
+    import json
+    import os
+    import subprocess
+    import sys
+    script = r'''
+import json, sys
+import numpy as np
+sys.path.insert(0, %r)
+import paper_1911_08963_b200 as mdg
+rng = np.random.default_rng(5)
+dev = mdg.Device(0)
+out = []
+for n in (40, 64, 100, 128, 200, 256):
+    k = int(rng.integers(12, 24))
+    W = (n + 63) // 64
+    rows = rng.integers(0, 2**63, size=(k, W), dtype=np.uint64)
+    if n %% 64:
+        rows[:, -1] &= np.uint64((1 << (n %% 64)) - 1)
+    dev.load_gammas(rows, n, ranks=None)
+    for c in (2, 3, 4, 5):
+        for cut in (0, 3, 1000):
+            o = dev.round_bounded(0, c, cut) if cut else dev.round(0, c)
+            if o.bounded:
+                continue
+            out.append([n, c, cut, o.min_weight, sorted(dev.round_witness(0, c, o)), o.argmin_key >> 51 & 1])
+print(json.dumps(out))
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = {}
+    for mode in ("pos", "find"):
+        env = dict(os.environ)
+        if mode == "find":
+            env["MDG_NO_POS_KEY"] = "1"
+        r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        runs[mode] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert len(runs["pos"]) == len(runs["find"]) > 40
+    assert all(x[5] == 1 for x in runs["pos"]) and all(x[5] == 0 for x in runs["find"])
+    for a, b in zip(runs["pos"], runs["find"]):
+        assert a[:5] == b[:5], (a, b)
