@@ -897,7 +897,7 @@ __device__ __forceinline__ uint32_t popc_words(const uint32_t (&A)[NW]) {
 // -- consecutive prefixes in revolving-door order differ by one row swap -- so every step
 // is one XOR per word on codewords held in registers (north_star's formulation). Bound
 // pruning as tile_min (G: 0 = exact; 1/2/4 groups, | kFoldDrop). A and idA are consumed.
-template <int NW, bool HID, int G, int NWF = NW>
+template <int NW, bool HID, int G, int NWF = NW, bool PAIR = false>
 __device__ __forceinline__ uint32_t walk_min(const uint32_t* xs, uint32_t nx,
                                              uint32_t (&A)[r_for(NW)][NW], uint32_t (&idA)[r_for(NW)],
                                              int32_t T) {
@@ -920,6 +920,18 @@ __device__ __forceinline__ uint32_t walk_min(const uint32_t* xs, uint32_t nx,
             for (int r = 0; r < R; ++r) m = min(m, popc_words<NW>(A[r]) + (HID ? idA[r] : 0u));
             best = min(best, pack_best(m, xi));
             continue;
+        }
+        if constexpr (PAIR) { // one bound per two codewords: popc(fold_a & fold_b), 2 LOP3 per pair
+            static_assert(G == 1 && NWF == 2 && R % 2 == 0, "walk pair bound: one two-word fold");
+            uint32_t pmin = kNone;
+#pragma unroll
+            for (int b = 0; b < R / 2; ++b) {
+                const uint32_t fa = A[2 * b][0] | A[2 * b][1];
+                uint32_t g;
+                asm("lop3.b32 %0, %1, %2, %3, 0xA8;" : "=r"(g) : "r"(A[2 * b + 1][0]), "r"(A[2 * b + 1][1]), "r"(fa));
+                pmin = min(pmin, __popc(g) + (HID ? min(idA[2 * b], idA[2 * b + 1]) : 0u));
+            }
+            if (!__any_sync(0xFFFFFFFFu, int32_t(pmin) <= T)) continue;
         }
         uint32_t lb[R];
 #pragma unroll
@@ -947,7 +959,9 @@ __device__ __forceinline__ uint32_t tile_min_walk(const uint32_t* xs, uint32_t n
                                                   uint32_t (&A)[r_for(NW)][NW],
                                                   uint32_t (&idA)[r_for(NW)], int32_t T, int G) {
     if (T < 0) return 0xFFFFFFFFu;
-    G &= ~kFoldPair; // the walk bounds each item on its own (at least as tight as a pair bound)
+    if constexpr (NW >= 2 && NW <= 4) // pair codes: one two-word fold group (see tile_min)
+        if ((G & kFoldPair) && (G & 15) == 1) return walk_min<NW, HID, 1, 2, true>(xs, nx, A, idA, T);
+    G &= ~kFoldPair;
     constexpr int ND = NW >= 2 ? NW - 1 : NW, NH = (NW + 1) / 2;
     if constexpr (NW >= 2) {
         if (G == (1 | kFoldDrop)) return walk_min<NW, HID, 1, ND>(xs, nx, A, idA, T);
