@@ -247,33 +247,64 @@ struct TableJobs {
     TableJob job[kMaxTableJobs];
 };
 
+// Each thread builds kTabRun consecutive entries: it unranks the first (a binary search per
+// element, dependent loads of the binomial table) and steps through the rest by the colex
+// successor -- the lowest element that can grow grows by one and the ones below it reset to
+// 0, 1, ... -- XORing only the rows that leave and enter (about two per entry instead of s).
+constexpr uint32_t kTabRun = 8;
+constexpr uint32_t kTabMaxS = 8; // longer subsets: every entry unranked
+
 template <int NW, bool HID>
 __global__ void tables_build(const __grid_constant__ TableJobs J, const uint64_t* __restrict__ T) {
     constexpr int YS = stride_for(NW + (HID ? 1 : 0));
-    const uint64_t gi = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (gi >= J.total) return;
-    uint32_t jb = 0;
-    for (uint32_t i = 1; i < J.n; ++i)
-        if (J.job[i].begin <= gi) jb = i;
-    const TableJob& jo = J.job[jb];
-    const uint64_t y = gi - jo.begin;
+    const uint64_t g0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * kTabRun;
+    if (g0 >= J.total) return;
     uint32_t acc[NW];
+    uint32_t id = 0, jb = 0, c[kTabMaxS];
+    uint64_t job_end = 0, y = 0;
+    for (uint64_t gi = g0; gi < g0 + kTabRun && gi < J.total; ++gi, ++y) {
+        const bool fresh = gi == g0 || gi == job_end;
+        if (fresh) { // locate the job and unrank its entry
+            jb = 0;
+            for (uint32_t i = 1; i < J.n; ++i)
+                if (J.job[i].begin <= gi) jb = i;
+            job_end = jb + 1 < J.n ? J.job[jb + 1].begin : J.total;
+            y = gi - J.job[jb].begin;
+        }
+        const TableJob& jo = J.job[jb];
+        if (fresh || jo.s > kTabMaxS) {
 #pragma unroll
-    for (int w = 0; w < NW; ++w) acc[w] = 0;
-    uint32_t id = 0;
-    uint64_t r = y;
-    uint32_t hi = J.k;
-    for (uint32_t i = jo.s; i >= 1; --i) {
-        uint32_t x = colex_top(T, r, i, hi);
-        r -= BT(T, x, i);
-        hi = x;
-        uint32_t q = jo.reverse ? J.k - 1 - x : x;
-        xor_row<NW>(jo.rows, q, acc);
-        id += q < jo.id_rows;
+            for (int w = 0; w < NW; ++w) acc[w] = 0;
+            id = 0;
+            uint64_t r = y;
+            uint32_t hi = J.k;
+            for (uint32_t i = jo.s; i >= 1; --i) {
+                uint32_t x = colex_top(T, r, i, hi);
+                r -= BT(T, x, i);
+                hi = x;
+                if (i <= kTabMaxS) c[i - 1] = x;
+                uint32_t q = jo.reverse ? J.k - 1 - x : x;
+                xor_row<NW>(jo.rows, q, acc);
+                id += q < jo.id_rows;
+            }
+        } else { // colex successor of c[0..s) (ascending)
+            uint32_t j = 0;
+            while (j + 1 < jo.s && c[j] + 1 == c[j + 1]) ++j;
+            for (uint32_t t = 0; t <= j; ++t) {
+                const uint32_t nv = t < j ? t : c[j] + 1;
+                if (nv == c[t]) continue;
+                const uint32_t qo = jo.reverse ? J.k - 1 - c[t] : c[t];
+                const uint32_t qn = jo.reverse ? J.k - 1 - nv : nv;
+                xor_row<NW>(jo.rows, qo, acc);
+                xor_row<NW>(jo.rows, qn, acc);
+                id += (qn < jo.id_rows) - (qo < jo.id_rows);
+                c[t] = nv;
+            }
+        }
+        uint32_t* o = jo.out + y * YS;
+#pragma unroll
+        for (int w = 0; w < YS; ++w) o[w] = w < NW ? acc[w] : (HID && w == NW ? id : 0u);
     }
-    uint32_t* o = jo.out + y * YS;
-#pragma unroll
-    for (int w = 0; w < YS; ++w) o[w] = w < NW ? acc[w] : (HID && w == NW ? id : 0u);
 }
 
 // Device-side state of the level loop (run_bz_loop, engines.cpp:447-476) when
@@ -1581,7 +1612,7 @@ struct YtabLaunch {
 template <int NW, bool HID>
 struct TablesLaunch {
     static void run(const TableJobs& J, const uint64_t* T, cudaStream_t st) {
-        uint64_t blocks = (J.total + 255) / 256;
+        uint64_t blocks = (J.total + 256 * kTabRun - 1) / (256 * kTabRun);
         tables_build<NW, HID><<<dim3(uint32_t(blocks)), 256, 0, st>>>(J, T);
     }
 };
