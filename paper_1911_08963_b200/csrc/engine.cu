@@ -16,8 +16,10 @@
 // Kernels (all integer; no tensor cores):
 //   tab_round<NW,HID>  persistent grid over tiles (prefix chunk x suffix chunk, or
 //                      transposed); smem items built per tile, each lane holds R
-//                      register items, one XOR per word + OR-fold bound + POPC per
-//                      codeword, exact weights only where the bound can still win;
+//                      register items; stage 1 bounds the weight from below (OR-folds
+//                      of the words of X ^ Y, or one AND of two codewords' folds per
+//                      pair: 3 LOP3 + 1 POPC for two codewords), the plan choosing per
+//                      tile bound T; exact weights only where the bound can still win;
 //                      warp __reduce_min_sync; global 64-bit atomicMin of
 //                      (weight << 52 | tile | position); tile fetches poll the bound for early
 //                      exit; in a chained loop the last block closes the round.
