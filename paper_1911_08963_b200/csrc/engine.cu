@@ -1031,7 +1031,8 @@ __device__ __forceinline__ uint32_t tile_min_walk(const uint32_t* xs, uint32_t n
 // codeword at T (lim[] from the host's density estimate; -1 = unusable), else 0 (exact)
 // Cheapest first: fewer groups (POPCs) first, and at equal G the fold without the last
 // (nearly empty) word (limd, kFoldDrop: one LOP3 less per codeword).
-__device__ __forceinline__ int pick_groups(int32_t T, const int32_t (&lim)[3]) {
+__device__ __forceinline__ int pick_groups(int32_t T, const int32_t (&lim)[4]) {
+    if (T <= lim[3]) return 1 | kFoldPair; // pair bound over words 0-1 (NW 2..4, see tile_min)
     if (T <= lim[0]) return 1;
     if (T <= lim[1]) return 2;
     if (T <= lim[2]) return 4;
@@ -1443,7 +1444,7 @@ __global__ void span_build(const uint32_t* __restrict__ rows, uint32_t first, ui
 }
 
 struct SpanArgs {
-    int32_t fold_lim[3];
+    int32_t fold_lim[4];           // G = 1, 2, 4; [3]: pair bound over words 0-1 (NW 2..4)
     const uint32_t* ta;
     const uint32_t* tb;
     uint64_t na, nb, nty;
@@ -1957,7 +1958,7 @@ private:
 // 1 - (1 - rho_c)^m, so popc(folds) ~ mean E_G, variance V_G; pruning with G groups
 // is worth it while the bound T <= E_G - 4 sqrt(V_G) (then almost no codeword passes).
 // G must leave some group with two or more words (G=2 needs NW >= 3, G=4 needs NW >= 5).
-static void fold_limits(uint32_t bits, uint32_t nw, double rho_c, int32_t (&lim)[3]) {
+static void fold_limits(uint32_t bits, uint32_t nw, double rho_c, int32_t (&lim)[4]) {
     const int Gs[3] = {1, 2, 4};
     for (int gi = 0; gi < 3; ++gi) {
         const int G = Gs[gi];
@@ -1979,6 +1980,20 @@ static void fold_limits(uint32_t bits, uint32_t nw, double rho_c, int32_t (&lim)
     // a larger G only helps if it raises the limit
     if (lim[1] <= lim[0]) lim[1] = -1;
     if (lim[2] <= std::max(lim[0], lim[1])) lim[2] = -1;
+    // pair pre-filter over words 0-1 (tile_min's pair variant; NW 2..4): a bit of the AND of
+    // two codewords' folds is set w.p. q^2; used while T is 3.5 sd below its mean (a vote
+    // that falls through takes the single folds, then exact weights)
+    lim[3] = -1;
+    if (nw >= 2 && nw <= 4) {
+        double mean = 0, var = 0;
+        for (uint32_t p = 0; p < 32; ++p) {
+            const uint32_t m = (p < bits ? 1u : 0u) + (32 + p < bits ? 1u : 0u);
+            const double q = 1.0 - std::pow(1.0 - rho_c, double(m)), q2 = q * q;
+            mean += q2;
+            var += q2 * (1.0 - q2);
+        }
+        lim[3] = int32_t(std::floor(mean - 3.5 * std::sqrt(var)));
+    }
 }
 
 // density of an XOR of c rows of density rho (independent bits)
