@@ -111,7 +111,8 @@ int mdg_round_witness(mdg_ctx* ctx, uint32_t j, uint32_t c, const mdg_round_out*
 int mdg_set_kernel(mdg_ctx* ctx, int kernel);
 /* Bound pruning of the tab kernel (on by default): off computes every
  * codeword's exact weight (results are identical; for roofline measurements
- * of the unpruned kernel). */
+ * of the unpruned kernel). The two settings use different tile plans: ask for
+ * a round's witness (mdg_round_witness) under the setting the round ran with. */
 int mdg_set_pruning(mdg_ctx* ctx, int on);
 
 /* ----------------------------------------------------------- host objects */

@@ -1784,7 +1784,8 @@ static uint64_t plan_cost(uint32_t k, uint32_t c, uint32_t s, uint32_t TX, uint3
 // Suffix size s minimizes the tile cost (suffix table <= 4M entries); the
 // prefix chunk TX is the largest of 256/128/64/32/16 that still yields >= 8
 // tiles per resident block, so the dynamic scheduler's tail stays short.
-TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_blocks, bool rd) {
+TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_blocks, bool rd,
+                      uint32_t tiles_per_block) {
     TabPlan pl;
     pl.k = k;
     pl.c = c;
@@ -1820,7 +1821,8 @@ TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_b
     for (uint32_t tx = kTX; tx >= kMinTX; tx /= 2) {
         uint64_t tiles = 0;
         plan_cost(k, c, pl.s, tx, pl.YC, &tiles, !rd);
-        if (tiles >= uint64_t(resident_blocks) * kTilesPerBlock || tx <= kMinTX) { pl.TX = tx; break; }
+        const uint32_t tpb = tiles_per_block ? tiles_per_block : kTilesPerBlock;
+        if (tiles >= uint64_t(resident_blocks) * tpb || tx <= kMinTX) { pl.TX = tx; break; }
     }
     const bool can = !rd && transpose_enabled() && xtab_ok(k, pl.p - 1);
     pl.prefix.assign(1, 0);
@@ -2046,7 +2048,7 @@ struct Engine::Impl {
     size_t hist_cap = 0;
     std::vector<GammaDev> gammas;
     std::map<std::tuple<uint32_t, uint32_t, bool>, uint32_t*> tables; // (j, size, reverse) -> table
-    std::map<std::tuple<uint32_t, uint32_t, uint32_t, bool, bool>, PlanEntry> plans; // (k, c, nw, hid, rd)
+    std::map<std::tuple<uint32_t, uint32_t, uint32_t, bool, bool, bool>, PlanEntry> plans; // (k, c, nw, hid, rd, prune)
     std::map<std::pair<uint32_t, bool>, int> occ;                     // (nw, hid)
     std::map<std::pair<uint32_t, uint32_t>, FoldPlan> fold_cache; // (j, c)
     ncclComm_t comm = nullptr;
@@ -2092,11 +2094,11 @@ struct Engine::Impl {
         return o * sms;
     }
     const PlanEntry& plan(uint32_t k, uint32_t c, const GammaDev& g, int sms) {
-        auto key = std::make_tuple(k, c, g.nw, g.hid, rd);
+        auto key = std::make_tuple(k, c, g.nw, g.hid, rd, prune);
         auto it = plans.find(key);
         if (it != plans.end()) return it->second;
         PlanEntry pe;
-        pe.plan = make_tab_plan(k, c, g.nw, uint32_t(resident(g.nw, g.hid, sms)), rd);
+        pe.plan = make_tab_plan(k, c, g.nw, uint32_t(resident(g.nw, g.hid, sms)), rd, prune ? 0u : 8u);
         const size_t pb = pe.plan.prefix.size() * 8, tb = pe.plan.tr.size();
         pe.d_prefix = static_cast<uint64_t*>(plan_arena.alloc(pb + tb));
         CK(cudaMemcpyAsync(pe.d_prefix, pe.plan.prefix.data(), pb, cudaMemcpyHostToDevice, stream));

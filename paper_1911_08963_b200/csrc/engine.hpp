@@ -153,7 +153,10 @@ private:
     std::unique_ptr<Impl> impl_;
 };
 
-TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_blocks, bool rd = false);
+// tiles_per_block: the smallest tile count per resident block the plan aims for (0: the
+// default, 2 -- or MDG_TILES_PER_BLOCK; exact-weight rounds take 8: their tiles run ~3x longer)
+TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_blocks, bool rd = false,
+                      uint32_t tiles_per_block = 0);
 uint32_t tab_yc(uint32_t nw32);
 uint32_t tab_tx();
 // kernel template width for a row of nw32 words (rows are zero-padded up to it)
