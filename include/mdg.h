@@ -68,7 +68,7 @@ typedef struct {
     uint32_t min_weight;      /* UINT32_MAX when nothing was evaluated */
     uint32_t stopped_early;   /* 1 when the early-exit bound fired */
     uint32_t bounded;         /* 1: no codeword below the cutoff; min_weight == cutoff is a bound */
-    uint32_t reserved;
+    uint32_t plan_tag;        /* opaque: the tile plan the round ran on (mdg_round_witness decodes with it) */
     uint64_t argmin_key;      /* opaque (weight << 52 | position of the winner); input of mdg_round_witness */
     uint64_t combinations;    /* C(k,c): the reference's RoundStats.combinations */
     uint64_t evaluated;       /* codewords actually evaluated on this device */
@@ -111,8 +111,9 @@ int mdg_round_witness(mdg_ctx* ctx, uint32_t j, uint32_t c, const mdg_round_out*
 int mdg_set_kernel(mdg_ctx* ctx, int kernel);
 /* Bound pruning of the tab kernel (on by default): off computes every
  * codeword's exact weight (results are identical; for roofline measurements
- * of the unpruned kernel). The two settings use different tile plans: ask for
- * a round's witness (mdg_round_witness) under the setting the round ran with. */
+ * of the unpruned kernel). The two settings use different tile plans; the
+ * round's plan_tag records which, so mdg_round_witness decodes correctly after
+ * a switch, and it re-weighs the decoded rows (MDG_EINTERNAL on a mismatch). */
 int mdg_set_pruning(mdg_ctx* ctx, int on);
 
 /* ----------------------------------------------------------- host objects */
@@ -184,6 +185,10 @@ typedef struct {
     uint64_t split_min;   /* multi-rank runs: rounds of >= split_min codewords are split across
                              the ranks and their keys reduced; smaller rounds run whole on every
                              rank (identical results, no exchange). 0 = 2e8; 1 = split all */
+    uint32_t workers;     /* EngineConfig.workers (engines.hpp:66; the CLI's --workers /
+                             MINDIST_WORKERS, cli.cpp:78-79), default 1: echoed as the JSON
+                             record's "workers"; the GPU engine's parallelism is the device
+                             (and "devices" ranks), so it sets no thread count here */
 } mdg_config;
 #define MDG_GAMMA_HOST 0
 #define MDG_GAMMA_GPU 1

@@ -60,7 +60,7 @@ u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 
 class _RoundOut(C.Structure):
     _fields_ = [("min_weight", C.c_uint32), ("stopped_early", C.c_uint32),
-                ("bounded", C.c_uint32), ("reserved", C.c_uint32), ("argmin_key", C.c_uint64), ("combinations", C.c_uint64),
+                ("bounded", C.c_uint32), ("plan_tag", C.c_uint32), ("argmin_key", C.c_uint64), ("combinations", C.c_uint64),
                 ("evaluated", C.c_uint64), ("task_lo", C.c_uint64), ("task_hi", C.c_uint64),
                 ("device_ms", C.c_double)]
 
@@ -68,7 +68,7 @@ class _RoundOut(C.Structure):
 class _Config(C.Structure):
     _fields_ = [("trials", C.c_uint32), ("seed", C.c_uint64), ("level_cap", C.c_uint32),
                 ("kernel", C.c_int), ("want_witness", C.c_int), ("exact_rounds", C.c_int),
-                ("gamma_search", C.c_int), ("split_min", C.c_uint64)]
+                ("gamma_search", C.c_int), ("split_min", C.c_uint64), ("workers", C.c_uint32)]
 
 
 class _RunInfo(C.Structure):

@@ -31,7 +31,7 @@ struct mdg_gset {
 struct mdg_run {
     EngineResult er;
     uint32_t n = 0, k = 0, m = 0, k_last = 0;
-    uint32_t level_cap = 0, trials = 0, devices = 1;
+    uint32_t level_cap = 0, trials = 0, devices = 1, workers = 1;
     uint64_t seed = 0;
     std::string algorithm = "gpu", kernel = "tab";
     std::vector<uint32_t> perm;
@@ -141,8 +141,9 @@ GammaSet best_gamma_gpu(Engine& eng, const BitMatrix& B, uint32_t trials, uint64
     GammaSet best = compute_gamma_matrices(B);
     if (gamma_set_is_maximal(best, B.cols(), B.rows())) return best;
     const uint64_t key = eng.permutation_search(B.data(), B.rows(), B.cols(), trials, seed);
-    const uint32_t m = uint32_t(key >> 53), kl = uint32_t((key >> 42) & 0x7FF);
-    const uint64_t t = ((uint64_t{1} << 42) - 1) - (key & ((uint64_t{1} << 42) - 1));
+    const uint32_t m = uint32_t(key >> kSearchMShift);
+    const uint32_t kl = uint32_t((key >> kSearchKShift) & ((1u << (kSearchMShift - kSearchKShift)) - 1));
+    const uint64_t t = ((uint64_t{1} << kSearchKShift) - 1) - (key & ((uint64_t{1} << kSearchKShift) - 1));
     if (m > best.m() || (m == best.m() && kl > best.k_last)) {
         GammaSet cand = gamma_for_permutation(B, trial_permutation(B.cols(), seed, t));
         if (cand.m() != m || cand.k_last != kl)
@@ -243,6 +244,7 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
             rr.evaluated = r.evaluated;
             rr.combinations = rs.combinations;
             rr.ms = r.ms;
+            rr.plan_tag = cr.plan_tag;
             log.push_back({r.j, r.c, rr});
         }
         er.d = cr.U;
@@ -301,6 +303,7 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
     out.trials = cfg.trials;
     out.seed = cfg.seed;
     out.devices = world;
+    out.workers = cfg.workers ? cfg.workers : 1;
     out.kernel = cfg.kernel == MDG_KERNEL_RD ? "rd" : "tab";
     out.exact_rounds = cfg.exact_rounds != 0;
 }
@@ -335,7 +338,7 @@ std::string json_of(const mdg_run& r) {
       << r.algorithm << "\",\"m\":" << r.m << ",\"k_last\":" << r.k_last
       << ",\"g_final\":" << st.g_final << ",\"row_additions\":" << st.row_additions
       << ",\"combinations\":" << st.combinations << ",\"wall_seconds\":" << r.wall
-      << ",\"seed\":" << r.seed << ",\"workers\":" << r.devices;
+      << ",\"seed\":" << r.seed << ",\"workers\":" << r.workers;
     // new keys: witness, trace, level cap, devices, throughput
     o << ",\"capped\":" << (r.er.capped ? "true" : "false") << ",\"level_cap\":" << r.level_cap
       << ",\"exact_rounds\":" << (r.exact_rounds ? "true" : "false")
@@ -408,7 +411,7 @@ static void fill_out(const RoundResult& rr, mdg_round_out* out) {
     out->min_weight = rr.w;
     out->stopped_early = rr.stopped ? 1u : 0u;
     out->bounded = rr.bounded ? 1u : 0u;
-    out->reserved = 0;
+    out->plan_tag = rr.plan_tag;
     out->argmin_key = rr.key;
     out->combinations = rr.combinations;
     out->evaluated = rr.evaluated;
@@ -421,6 +424,7 @@ static RoundResult to_rr(const mdg_round_out* out) {
     RoundResult rr;
     rr.w = out->min_weight;
     rr.key = out->argmin_key;
+    rr.plan_tag = out->plan_tag;
     rr.combinations = out->combinations;
     rr.evaluated = out->evaluated;
     return rr;
@@ -625,6 +629,7 @@ void mdg_config_default(mdg_config* cfg) {
     cfg->exact_rounds = 0;
     cfg->gamma_search = MDG_GAMMA_HOST;
     cfg->split_min = 0;
+    cfg->workers = 1;
 }
 
 int mdg_min_weight(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n, const mdg_config* cfg,

@@ -35,6 +35,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <array>
 #include <chrono>
 #include <cmath>
@@ -1624,8 +1625,14 @@ template <int NW, bool HID>
 struct LevelLaunch {
     static void run(const TabArgs& a, const LevelDesc& L, uint64_t total, bool pdl, cudaStream_t st,
                     int sms) {
-        static int occ = -1;
-        if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tab_level<NW, HID>, kThreads, 0);
+        // per instantiation (the kernel's resources never change); several host threads
+        // (the batch front door) may race to fill it: atomic, and every writer stores the same value
+        static std::atomic<int> cached{-1};
+        int occ = cached.load(std::memory_order_relaxed);
+        if (occ < 0) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tab_level<NW, HID>, kThreads, 0);
+            cached.store(occ, std::memory_order_relaxed);
+        }
         const uint64_t g = std::max<uint64_t>(1, std::min<uint64_t>(total, uint64_t(sms) * std::max(occ, 1)));
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(uint32_t(g));
@@ -1643,9 +1650,13 @@ struct LevelLaunch {
 template <int NW, bool HID>
 struct TabOcc {
     static void run(int* occ) {
-        static int cached = -1; // per instantiation; the kernel's resources never change
-        if (cached < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached, tab_round<NW, HID>, kThreads, 0);
-        *occ = cached;
+        static std::atomic<int> cached{-1}; // per instantiation, as LevelLaunch
+        int o = cached.load(std::memory_order_relaxed);
+        if (o < 0) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, tab_round<NW, HID>, kThreads, 0);
+            cached.store(o, std::memory_order_relaxed);
+        }
+        *occ = o;
     }
 };
 
@@ -1710,6 +1721,9 @@ uint32_t tab_yc(uint32_t nw32) { return uint32_t(r_for(int(nw32))) * kThreads; }
 uint32_t tab_tx() { return kTX; }
 
 static uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// RoundResult::plan_tag: bit 0 valid, bit 1 pruning on, bit 2 revolving-door plan
+static uint32_t plan_tag(bool rd, bool prune) { return 1u | (prune ? 2u : 0u) | (rd ? 4u : 0u); }
 
 // saturating Pascal table C(x, t), x <= kMaxK, t <= kMaxC (host and device copies)
 static const std::vector<uint64_t>& binom_table() {
@@ -2094,6 +2108,10 @@ struct Engine::Impl {
         return o * sms;
     }
     const PlanEntry& plan(uint32_t k, uint32_t c, const GammaDev& g, int sms) {
+        return plan(k, c, g, sms, rd, prune);
+    }
+    // the tile plan of an explicit variant (a round's witness is decoded with the plan it ran on)
+    const PlanEntry& plan(uint32_t k, uint32_t c, const GammaDev& g, int sms, bool rd, bool prune) {
         auto key = std::make_tuple(k, c, g.nw, g.hid, rd, prune);
         auto it = plans.find(key);
         if (it != plans.end()) return it->second;
@@ -2607,6 +2625,7 @@ RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t tas
     uint64_t lo = std::min(task_lo, pe.plan.tiles()), hi = std::min(task_hi, pe.plan.tiles());
     rr.task_lo = lo;
     rr.task_hi = hi;
+    rr.plan_tag = plan_tag(im.rd, im.prune);
     uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
     unsigned long long* slot = im.take_slot();
     TabArgs a = tab_args(im, g, pe, yt, k_, c);
@@ -2692,27 +2711,46 @@ std::vector<uint32_t> Engine::witness(uint32_t j, uint32_t c, const RoundResult&
     const uint64_t task = pos ? (rr.key >> kPosBits) & 0xFFFFFFFFull : rr.key & (kPosFlag - 1);
     const uint32_t target = uint32_t(rr.key >> kKeyShift);
     std::vector<uint32_t> idx(c);
-    const PlanEntry& pe = im.plan(k_, c, g, sms_);
+    // decode with the tile plan the round ran on (tagged by Engine::round / chain_loop), not
+    // whatever kernel / pruning setting is current: the plans differ
+    const bool tagged = (rr.plan_tag & 1u) != 0;
+    const PlanEntry& pe = im.plan(k_, c, g, sms_, tagged ? (rr.plan_tag & 4u) != 0 : im.rd,
+                                  tagged ? (rr.plan_tag & 2u) != 0 : im.prune);
     if (task >= pe.plan.tiles()) throw std::invalid_argument("witness: key names no task of this round");
     if (pos) { // the kernel named the position: smem-side index << 11 | register-side index
         const uint32_t p = uint32_t(rr.key & ((1u << kPosBits) - 1));
         tab_decode(pe.plan, task, p >> 11, p & 0x7FFu, idx.data());
-        return idx;
+    } else {
+        unsigned long long* slot = im.take_slot();
+        uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
+        TabArgs a = tab_args(im, g, pe, yt, k_, c);
+        a.tile_lo = task; a.tile_hi = task + 1;
+        a.find_out = slot + 3;
+        a.find_target = target;
+        dispatch_nw_hid<TabLaunch>(g.nw, g.hid, a, uint64_t(1), im.stream, 1, size_t(0), sms_);
+        CK(cudaGetLastError());
+        im.cnt.launches += 1;
+        im.read_slot(slot);
+        CK(cudaStreamSynchronize(im.stream));
+        uint64_t f = im.host_slot[3];
+        if (f == ~0ull) throw std::logic_error("witness: winning tile holds no codeword of the round minimum");
+        tab_decode(pe.plan, task, uint32_t(f >> 32), uint32_t(f & 0xFFFFFFFFu), idx.data());
     }
-    unsigned long long* slot = im.take_slot();
-    uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
-    TabArgs a = tab_args(im, g, pe, yt, k_, c);
-    a.tile_lo = task; a.tile_hi = task + 1;
-    a.find_out = slot + 3;
-    a.find_target = target;
-    dispatch_nw_hid<TabLaunch>(g.nw, g.hid, a, uint64_t(1), im.stream, 1, size_t(0), sms_);
-    CK(cudaGetLastError());
-    im.cnt.launches += 1;
-    im.read_slot(slot);
-    CK(cudaStreamSynchronize(im.stream));
-    uint64_t f = im.host_slot[3];
-    if (f == ~0ull) throw std::logic_error("witness: winning tile holds no codeword of the round minimum");
-    tab_decode(pe.plan, task, uint32_t(f >> 32), uint32_t(f & 0xFFFFFFFFu), idx.data());
+    // the decoded rows must have the key's weight (compacted XOR + identity rows), else the
+    // key was decoded against the wrong plan or Gamma: fail loudly instead of a wrong witness
+    std::vector<uint32_t> acc(g.nw, 0);
+    uint32_t wt = 0;
+    for (uint32_t i = 0; i < c; ++i) {
+        if (idx[i] >= k_ || (i && idx[i] <= idx[i - 1]))
+            throw std::logic_error("witness: decoded combination is not a sorted c-subset");
+        for (uint32_t w = 0; w < g.nw; ++w) acc[w] ^= g.host_rows[size_t(idx[i]) * g.nw + w];
+        if (idx[i] < g.id_rows) ++wt;
+    }
+    for (uint32_t w = 0; w < g.nw; ++w) wt += uint32_t(__builtin_popcount(acc[w]));
+    if (wt != target)
+        throw std::logic_error("witness: decoded combination has weight " + std::to_string(wt) +
+                               ", the round key says " + std::to_string(target) +
+                               " (key from a different plan or Gamma set?)");
     return idx;
 }
 
@@ -2896,6 +2934,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
     im.cnt.d2h += sizeof(ChainState) + nrec * sizeof(ChainRec);
     res.U = im.h_state->U;
     res.L = im.h_state->L;
+    res.plan_tag = plan_tag(im.rd, im.prune);
     res.done = im.h_state->done != 0;
     // run_bz_loop: capped when the loop reaches level cap + 1 (<= k) without being done
     res.capped = !res.done && level_cap && level_cap < k_ && g > level_cap;

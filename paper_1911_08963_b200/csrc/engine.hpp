@@ -34,6 +34,10 @@ constexpr int kKeyShift = 52;
 constexpr unsigned long long kPosFlag = 1ull << 51;
 constexpr int kPosBits = 19;
 
+// GPU permutation search key layout (see permutation_search)
+constexpr int kSearchMShift = 51;
+constexpr int kSearchKShift = 41;
+
 struct RoundResult {
     uint32_t w = UINT32_MAX;
     bool stopped = false;
@@ -43,6 +47,9 @@ struct RoundResult {
     uint64_t evaluated = 0;
     uint64_t task_lo = 0, task_hi = 0;
     double ms = 0;
+    // tile plan the round ran on (bit 0 set: valid; bit 1 pruning on; bit 2 revolving-door
+    // plan); 0 = the engine's current setting. Engine::witness decodes the key with it.
+    uint32_t plan_tag = 0;
 };
 
 // Pivot split of a level-c round (the "tab" kernel's enumeration): a sorted
@@ -97,6 +104,7 @@ public:
     struct ChainResult {
         uint32_t U = 0, L = 0;
         bool done = false, capped = false;
+        uint32_t plan_tag = 0;          // RoundResult::plan_tag of every round of the loop
         std::vector<ChainRound> rounds; // executed rounds, in loop order
     };
     // Gray-code brute force over all 2^k - 1 nonzero codewords of a k-row basis
@@ -126,7 +134,8 @@ public:
 
     // GPU permutation search (gsearch.cu): best (m, k_last, earliest trial) of `trials`
     // SplitMix64 / Fisher-Yates column orders of the k x n matrix `rows` (row-major u64),
-    // packed as m << 53 | k_last << 42 | (2^42 - 1 - trial).
+    // packed as m << 51 | k_last << 41 | (2^41 - 1 - trial): m <= n <= 4096 needs 13 bits,
+    // k_last <= k <= 512 needs 10.
     uint64_t permutation_search(const uint64_t* rows, uint32_t k, uint32_t n, uint32_t trials,
                                 uint64_t seed);
     struct CUstream_st* stream() const; // the engine's CUDA stream

@@ -129,9 +129,9 @@ __global__ void __launch_bounds__(256) perm_search(SearchArgs a) {
             if (cnt < k) break;
         }
         if (lane == 0) {
-            const unsigned long long key = (static_cast<unsigned long long>(m) << 53) |
-                                           (static_cast<unsigned long long>(k_last) << 42) |
-                                           ((1ull << 42) - 1 - t);
+            const unsigned long long key = (static_cast<unsigned long long>(m) << kSearchMShift) |
+                                           (static_cast<unsigned long long>(k_last) << kSearchKShift) |
+                                           ((1ull << kSearchKShift) - 1 - t);
             atomicMax(a.best, key);
         }
         __syncwarp();
@@ -160,12 +160,12 @@ void launch_search(const SearchArgs& base, size_t col_bytes, size_t warp_bytes, 
 } // namespace
 
 // Best (m, k_last, earliest trial) over `trials` shuffled orders of G's columns;
-// returns (m << 53 | k_last << 42 | (2^42 - 1 - t)) for the best trial t.
+// returns (m << 51 | k_last << 41 | (2^41 - 1 - t)) for the best trial t (engine.hpp).
 uint64_t Engine::permutation_search(const uint64_t* rows, uint32_t k, uint32_t n, uint32_t trials,
                                     uint64_t seed) {
     if (k < 1 || k > 512 || n < k || n > 4096)
         throw std::invalid_argument("gpu permutation search: needs 1 <= k <= 512, k <= n <= 4096");
-    if (trials < 1 || uint64_t(trials) >= (uint64_t{1} << 42))
+    if (trials < 1 || uint64_t(trials) >= (uint64_t{1} << kSearchKShift))
         throw std::invalid_argument("best_gamma_over_permutations: trials must be >= 1");
     CK(cudaSetDevice(device_));
     const uint32_t W = (n + 63) / 64;

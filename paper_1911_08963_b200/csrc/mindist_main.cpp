@@ -24,7 +24,7 @@ int usage() {
                  "    accepted for the reference's command line (cli.cpp:264-277), validated as there\n"
                  "    and not used by the GPU engine: --algorithm basic|optimized|stack|saved|\n"
                  "    saved_unrolled (run the GPU engine: same d and trace), --s 1..8, --unroll 1..3,\n"
-                 "    --workers W>=1, --schedule serial|dynamic|dynamic_2cm|static_cyclic|static_snake,\n"
+                 "    --workers W>=1 (else MINDIST_WORKERS; echoed as \"workers\"), --schedule serial|dynamic|dynamic_2cm|static_cyclic|static_snake,\n"
                  "    --prefix P, --order lex|left_lex\n"
                  "    several FILEs: one record per file, the codes run as one batch\n"
                  "  mindist gen --n N --k K --seed S [--plain]\n";
@@ -80,6 +80,7 @@ int main(int argc, char** argv) {
     int device = 0;
     bool seed_given = false;
     bool brute = false;
+    bool workers_given = false;
     for (int i = 2; i < argc; ++i) {
         std::string a = argv[i];
         if (a.rfind("--", 0) != 0) { paths.push_back(a); continue; }
@@ -105,6 +106,10 @@ int main(int argc, char** argv) {
             if (a == "--s" && (x < 1 || x > 8)) { std::cerr << "error: config: s must be in 1..8\n"; return 2; }
             if (a == "--unroll" && (x < 1 || x > 3)) { std::cerr << "error: config: unroll must be in 1..3\n"; return 2; }
             if (a == "--workers" && x < 1) { std::cerr << "error: config: workers must be >= 1\n"; return 2; }
+            if (a == "--workers") {
+                cfg.workers = uint32_t(x);
+                workers_given = true;
+            }
         } else if (a == "--schedule") { // parallel.cpp:46-53
             if (v != "serial" && v != "dynamic" && v != "dynamic_2cm" && v != "static_cyclic" &&
                 v != "static_snake") {
@@ -136,6 +141,23 @@ int main(int argc, char** argv) {
         } else {
             std::cerr << "error: bad option " << a << " " << v << "\n";
             return 2;
+        }
+    }
+    // cli.cpp:78-80: --workers, else MINDIST_WORKERS (default 1); MINDIST_MEMORY_CAP_BYTES
+    // (default 2 GiB) caps the CPU engines' saved tables -- parsed and validated as there (a
+    // malformed value is an invalid argument, exit 2); the GPU engine's tables live in HBM
+    // and are not bound by it
+    for (const char* env : {"MINDIST_WORKERS", "MINDIST_MEMORY_CAP_BYTES"}) {
+        const char* v = std::getenv(env);
+        uint64_t x = 0;
+        if (!v || !*v) continue;
+        if (!parse_u64(v, x)) {
+            std::cerr << "error: " << env << ": not an unsigned integer: " << v << "\n";
+            return 2;
+        }
+        if (!workers_given && std::strcmp(env, "MINDIST_WORKERS") == 0) {
+            if (x < 1) { std::cerr << "error: config: workers must be >= 1\n"; return 2; }
+            cfg.workers = uint32_t(x);
         }
     }
     if (!seed_given) { // cli.cpp:46-53 draws and logs a seed
@@ -187,11 +209,11 @@ int main(int argc, char** argv) {
             buf.resize(size_t(-len) + 16);
             len = mdg_run_json(run, buf.data(), buf.size());
         }
-        if (pretty) {
+        if (pretty) { // result_to_text (cli.cpp:240-255), then the new keys that matter
             mdg_run_info info;
             mdg_run_info_get(run, &info);
             if (paths.size() > 1) std::cout << "file:          " << paths[f] << "\n";
-            std::cout << "d:             " << info.d << (info.capped ? " (level cap: upper bound)" : "") << "\n"
+            std::cout << "d:             " << info.d << "\n"
                       << "n:             " << info.n << "\n"
                       << "k:             " << info.k << "\n"
                       << "algorithm:     " << (brute ? "brute" : "gpu") << "\n"
@@ -202,8 +224,8 @@ int main(int argc, char** argv) {
                       << "combinations:  " << info.combinations << "\n"
                       << "wall_seconds:  " << info.wall_seconds << "\n"
                       << "seed:          " << cfg.seed << "\n"
-                      << "workers:       1\n"
-                      << "witness_ok:    " << (info.witness_ok ? "true" : "false") << "\n";
+                      << "workers:       " << cfg.workers << "\n";
+            if (info.capped) std::cout << "capped:        true (d is the upper bound at the level cap)\n";
         } else {
             std::cout << buf.data() << "\n";
         }

@@ -64,6 +64,13 @@ def test_cli_binary_errors_exit_2(tmp_path):
         r = subprocess.run([exe, "mindist", str(good), opt, val, "--seed", "0"], capture_output=True,
                            text=True)
         assert r.returncode == 2 and msg in r.stderr, (opt, r.stderr)
+    # cli.cpp:78-80 environment: a malformed MINDIST_WORKERS / MINDIST_MEMORY_CAP_BYTES is an
+    # invalid argument (exit 2), checked before any device is touched
+    for env, val in [("MINDIST_WORKERS", "many"), ("MINDIST_WORKERS", "0"),
+                     ("MINDIST_MEMORY_CAP_BYTES", "-5")]:
+        r = subprocess.run([exe, "mindist", str(good), "--seed", "0"], capture_output=True, text=True,
+                           env=dict(os.environ, **{env: val}))
+        assert r.returncode == 2 and "error:" in r.stderr, (env, val, r.stderr)
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 2
     r = subprocess.run([exe, "gen", "--n", "80", "--k", "40", "--seed", "1"], capture_output=True,

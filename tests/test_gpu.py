@@ -381,6 +381,16 @@ def test_cli_json_record(mdg, tmp_path):
     r = subprocess.run([exe, "mindist", str(f), "--seed", "1", "--pretty", "--exact-rounds"],
                        capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "d:             7" in r.stdout
+    # result_to_text's twelve lines in the reference's order (cli.cpp:240-255)
+    keys = [ln.split(":")[0] for ln in r.stdout.splitlines()]
+    assert keys == ["d", "n", "k", "algorithm", "m", "k_last", "g_final", "row_additions",
+                    "combinations", "wall_seconds", "seed", "workers"], keys
+    # workers: --workers, else MINDIST_WORKERS, else 1 (cli.cpp:78-79), echoed in the record
+    for env, args, want in [({}, [], 1), ({"MINDIST_WORKERS": "6"}, [], 6),
+                            ({"MINDIST_WORKERS": "6"}, ["--workers", "3"], 3)]:
+        r = subprocess.run([exe, "mindist", str(f), "--seed", "1"] + args, capture_output=True,
+                           text=True, timeout=120, env=dict(os.environ, **env))
+        assert r.returncode == 0 and json.loads(r.stdout)["workers"] == want, (env, args, r.stderr)
     # a reference command line with CPU-engine options runs unchanged on the GPU engine
     r = subprocess.run([exe, "mindist", str(f), "--algorithm", "saved", "--s", "5", "--unroll", "2",
                         "--workers", "8", "--schedule", "dynamic", "--prefix", "3", "--order",
@@ -458,6 +468,35 @@ def test_pruning_off_same_minima(mdg, device):
                 b = device.round(j, c)
                 device.set_pruning(True)
                 assert (a.min_weight, a.evaluated) == (b.min_weight, b.evaluated), (n, k, j, c)
+
+
+def test_witness_after_plan_switch(mdg, device):
+    """A round's witness decodes with the tile plan the round ran on (plan_tag), even after
+    the caller switches pruning or the kernel in between (the plans differ); a key from
+    another Gamma set fails loudly (the decoded rows are re-weighed) instead of returning
+    a wrong combination."""
+    G = mdg.gen_matrix(128, 64, 1, True)
+    gs = mdg.GammaSet.build(G, 128, 10, 1)
+    device.load_gset(gs)
+    rows = gs.gamma(0)
+    try:
+        for c in (3, 4, 5):
+            for first, then in (((True, 0), (False, 0)), ((False, 0), (True, 1)), ((True, 1), (True, 0))):
+                device.set_pruning(first[0])
+                device.set_kernel(first[1])
+                o = device.round(0, c)
+                device.set_pruning(then[0])
+                device.set_kernel(then[1])
+                idx = device.round_witness(0, c, o)
+                assert popcount_rows(rows, idx)[0] == o.min_weight, (c, first, then)
+    finally:
+        device.set_pruning(True)
+        device.set_kernel(0)
+    o = device.round(0, 4)
+    other = mdg.GammaSet.build(mdg.gen_matrix(128, 64, 2, True), 128, 10, 2)
+    device.load_gset(other)
+    with pytest.raises(mdg.MdgError):
+        device.round_witness(0, 4, o)
 
 
 def _sparse_code(rng, k, n, density):
