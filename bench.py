@@ -5,15 +5,20 @@ codes, G = (I_64 | A), A from mt19937_64 seeds 1..8; one
 step = the full Brouwer–Zimmermann run to termination (exact d) of all eight
 codes. Metric: codewords evaluated per second (BASELINE.json `metric`).
 
-* value  — device-resident: the level loops over Gamma sets already in HBM
-           (mdg_bz_loop_device, one context per code, --streams codes in flight
-           per GPU), CUDA events around each whole step (host gaps included);
-           codewords / time, max over ranks for the time. Under torchrun every
-           rank runs its own eight-code step (codes are independent objects: no
-           data-path collective; per-GPU work fixed, "scaling": "weak");
-           config.round_split reports SURVEY.md §8e's split of one code's rounds
-           across the ranks (mdg_min_weight_dist, NCCL allreduce(min) per round)
-           beside it.
+* value  — N = 1: device-resident: the level loops over Gamma sets already in
+           HBM (mdg_bz_loop_device, one context per code, --streams codes in
+           flight), CUDA events around each whole step (host gaps included);
+           codewords / time. N > 1 (torchrun): the strong leg below is the
+           headline ("scaling": "strong"); the eight-code step, run by every rank
+           on its own GPU (independent codes, no collective), moves to
+           `weak_step`.
+* strong — at every N: ONE code (config 4 to level cap 7, 4.7e12 codewords)
+           with every round of >= 2e8 codewords split across the ranks and its
+           key min-reduced by an in-stream NCCL allreduce(min)
+           (mdg_min_weight_dist); N = 1 is its baseline. Parity
+           flags against the reference's cap-6 and cap-7 traces.
+* configs — N = 1: time-to-d of configs 1, 3, 4 (caps 5, 6) and the config-5
+           histograms, each with a parity flag against the reference goldens.
 * e2e    — the public front door from host matrices (mdg_min_weight_batch over
            the rank's codes): row basis +
            Gamma search on the host, H2D of the Gammas, the device loop, D2H of
@@ -188,6 +193,109 @@ def run_reference_arm(args, rank, world):
     return 0
 
 
+CFG4 = (300, 200, 11)
+
+
+def _gold(name, file="configs"):
+    with open(os.path.join(ROOT, "tests", "golden", file + ".json")) as f:
+        return next(c for c in json.load(f)["data"] if c["name"] == name)
+
+
+def _trace_matches(res, case):
+    """bounded-round trace (w = min(exact w, U before the round)) and levels vs a golden"""
+    U = case["n"] - case["k"] + 1
+    exp = []
+    for c, j, w, Ua in case["rounds"]:
+        exp.append([c, j, min(w, U), Ua])
+        U = Ua
+    n = min(len(res.rounds), len(exp))
+    return (n == len(exp) and res.rounds[:n] == exp and
+            res.levels[:len(case["levels"])] == case["levels"] and
+            res.gamma_hash == case["gamma_hash"] and res.witness_ok)
+
+
+def strong_leg(mdg, torch, dist, rank, world, local, kernel, barrier, warm=1, steps=3):
+    """One code's rounds split across the ranks (config 4 to cap 7): see main()."""
+    n, k, seed = CFG4
+    G = mdg.gen_matrix(n, k, seed, True)
+    dev = mdg.Device(local)
+    if world > 1:
+        u = [mdg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(u, src=0)
+        dev.nccl_init(u[0], rank, world)
+    gold6 = _gold("cfg4", "configs_cap4_6")
+    try:
+        gold7 = _gold("cfg4", "configs_cap4_7")
+    except (OSError, StopIteration):
+        gold7 = None
+    ms, r = [], None
+    for step in range(warm + steps):
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        if world > 1:
+            r = mdg.min_weight_dist(G, n, rank, world, "nccl", trials=10, seed=seed, level_cap=7,
+                                    kernel=kernel, device=dev)
+        else:
+            r = mdg.min_weight(G, n, 10, seed, level_cap=7, kernel=kernel, device=dev)
+        ev1.record()
+        torch.cuda.synchronize()
+        if step >= warm:
+            ms.append(ev0.elapsed_time(ev1))
+    tot = sum(ms)
+    if dist is not None:
+        t = torch.tensor([tot], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot = float(t.item())
+    dev.close()
+    parity6 = r.capped and r.levels[:6] == gold6["levels"] and _trace_matches(r, {**gold6, "rounds": gold6["rounds"]})
+    parity7 = (r.levels == gold7["levels"] and _trace_matches(r, gold7)) if gold7 else None
+    return {"workload": "cfg4 [300,200] seed 11, BZ to level cap 7: ONE code, every round of >= 2e8 "
+                        "codewords split across the ranks (contiguous tile ranges), its key "
+                        "min-reduced by an in-stream NCCL allreduce(min); N = 1: the same run on one GPU",
+            "ranks": world, "scaling": "strong", "steps": steps,
+            "ms_per_run": tot / steps, "codewords": int(r.combinations),
+            "cw_per_s": r.combinations / (tot / steps * 1e-3),
+            "levels": r.levels, "parity_cap6_vs_reference": bool(parity6),
+            "parity_cap7_vs_reference": parity7,
+            "path": "mdg_min_weight_dist (NCCL)" if world > 1 else "mdg_min_weight"}
+
+
+def configs_table(mdg, dev):
+    """Time-to-d (front door, host Gamma search included, one code at a time) of the other
+    BASELINE configs with parity flags against the reference goldens (tests/golden)."""
+    out = []
+    for name, cap, file in (("cfg1", 0, "configs"), ("cfg3", 0, "configs"), ("cfg4", 5, "configs"),
+                            ("cfg4", 6, "configs_cap4_6")):
+        case = _gold(name, file)
+        g = case["gen"]
+        G = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
+        best = None
+        for _ in range(3):
+            t0 = time.perf_counter()
+            r = mdg.min_weight(G, g["n"], 10, g["seed"], level_cap=cap, device=dev)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        ok = (r.d == (case["U_final"] if cap else case["d"])) and _trace_matches(r, case)
+        out.append({"config": f"{name}" + (f" cap {cap}" if cap else ""), "d": r.d,
+                    "capped": r.capped, "ms": best * 1e3, "codewords": int(r.combinations),
+                    "parity_vs_reference": bool(ok)})
+    # config 5: the histograms of levels 1..5, every bin against the golden
+    with open(os.path.join(ROOT, "tests", "golden", "cfg5_hist.json")) as f:
+        h = json.load(f)["data"]
+    M = mdg.gen_matrix(256, 100, 3, identity=False)
+    dev.load_gammas(M, 256, ranks=None)
+    ms, ok, cw = 0.0, True, 0
+    for lv in h["levels"]:
+        o, hist = dev.round_hist(0, lv["c"], 256)
+        ms += o.device_ms
+        cw += o.evaluated
+        ok = ok and hist.tolist() == lv["hist"] and o.min_weight == lv["min"]
+    out.append({"config": "cfg5 histograms c=1..5", "ms_kernels": ms, "codewords": cw,
+                "cw_per_s_c1_to_5": cw / (ms * 1e-3), "parity_vs_reference": bool(ok)})
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -196,6 +304,8 @@ def main():
     ap.add_argument("--impl", default="mdg", choices=["mdg", "reference"])
     ap.add_argument("--kernel", default="tab", choices=["tab", "rd"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-strong", action="store_true", help="skip the one-code split (strong) leg")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other configs' time-to-d table")
     ap.add_argument("--streams", type=int, default=4,
                     help="codes in flight at once on one GPU (value: threads over resident "
                          "contexts; e2e: mdg_min_weight_batch)")
@@ -364,41 +474,26 @@ def main():
             h2d += sum(r.h2d_bytes for r in runs)
             d2h += sum(r.d2h_bytes for r in runs)
 
-    # SURVEY.md §8e's split of ONE code: every round's tiles divided across the ranks and the
-    # per-round key combined by an in-stream NCCL allreduce(min) (mdg_min_weight_dist);
-    # reported beside the sharded throughput, not part of it
-    split = None
+    # SURVEY.md §8e's split of ONE code (the strong-scaling leg, at every N): config 4 to
+    # level cap 7 (BASELINE.md's throughput / scaling case, 4.7e12 codewords): every round of
+    # >= 2e8 codewords has its tiles split across the ranks and its key min-reduced by an
+    # in-stream NCCL allreduce(min) (mdg_min_weight_dist); N = 1 is its single-GPU baseline.
+    # Sigma C(k, c) over the executed rounds / max-rank wall (CUDA events on the torch stream).
+    strong = None
     if world > 1 and backend == "gloo":
-        split = {"skipped": "MDG_BENCH_BACKEND=gloo plumbing run (ranks share a GPU; NCCL needs one GPU per rank)"}
-    elif world > 1:
+        strong = {"skipped": "MDG_BENCH_BACKEND=gloo plumbing run (ranks share a GPU; NCCL needs one GPU per rank)"}
+    elif not args.no_strong:
         try:
-            sd = mdg.Device(local)
-            u = [mdg.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(u, src=0)
-            sd.nccl_init(u[0], rank, world)
-            G1 = mdg.gen_matrix(N, K, SEEDS[0], True)
-            sms_ = []
-            for step in range(args.warmup + args.steps):
-                barrier()
-                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                ev0.record()
-                r = mdg.min_weight_dist(G1, N, rank, world, "nccl", trials=10, seed=SEEDS[0],
-                                        kernel=kernel, device=sd)
-                ev1.record()
-                torch.cuda.synchronize()
-                if r.d != expect_d[0] or not r.witness_ok:
-                    raise RuntimeError("round-split parity failure")
-                if step >= args.warmup:
-                    sms_.append(ev0.elapsed_time(ev1))
-            t = torch.tensor([max(sms_)], dtype=torch.float64, device=red_dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            split = {"what": "config-2 seed 1 through mdg_min_weight_dist: each round's tiles split "
-                             f"across {world} ranks, NCCL allreduce(min) of the round key in stream",
-                     "ms_per_code": float(t.item()), "codewords": int(r.combinations),
-                     "cw_per_s": r.combinations / (float(t.item()) * 1e-3)}
-            sd.close()
+            strong = strong_leg(mdg, torch, dist, rank, world, local, kernel, barrier,
+                                warm=1, steps=max(1, min(args.steps, 3)))
         except Exception as e:  # reported, never fatal
-            split = {"error": str(e)[:200]}
+            strong = {"error": str(e)[:300]}
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        try:
+            configs = configs_table(mdg, devs[0])
+        except Exception as e:  # reported, never fatal
+            configs = {"error": str(e)[:300]}
     clocks = sampler.stop()
 
     # max over ranks of time, sum over ranks of codewords
@@ -456,6 +551,12 @@ def main():
                 "frac_elided": ex_cw / (min(ex_ms) * 1e-3) / (popc / nw),
                 "elided_def": "identity block elided: 64 compacted bits = 2 POPC per codeword",
             } if ex_ms else None),
+            "frac_fixed_unit": (ex_cw / (min(ex_ms) * 1e-3) / (popc / nw) if ex_ms else None),
+            "frac_fixed_unit_def": ("the exact-weight level-7 kernel (pruning off, every codeword weighed: "
+                                    "2 POPC per codeword on the 64 non-identity columns) over the XU "
+                                    "roofline of that fixed unit, 4.64e12 POPC/s / 2; `frac` above is the "
+                                    "pruned kernel's issue efficiency on its own op mix, which a better "
+                                    "pruning stage can lower"),
             "traffic_note": "DRAM 4.24 MB per launch (the tables, read once), 0.6% of HBM bandwidth: compute-bound",
             "hbm_check": hbm_check(achieved),
         }
@@ -479,26 +580,44 @@ def main():
             except Exception as e:  # reported, never fatal
                 cpu = {"value": None, "unit": "cw/s", "cores": 0, "kind": "unavailable",
                        "sample": str(e)[:200]}
+        weak = {"value": value, "unit": "cw/s", "ms_per_step": tot_ms / args.steps,
+                "workload": WORKLOAD, "scaling": "weak",
+                "parallelism": (f"{world} ranks, each running the eight-code step ({args.streams} "
+                                "codes in flight per GPU); independent codes, no data-path collective"
+                                if world > 1 else
+                                f"single GPU, {min(args.streams, len(SEEDS))} codes in flight")}
+        # N > 1: the headline is the strong leg (one code's rounds split across the ranks,
+        # north_star's per-level partition); the eight-code step stays as `weak_step`
+        strong_ok = isinstance(strong, dict) and "cw_per_s" in strong
+        headline_strong = world > 1 and strong_ok
         line = {
-            "metric": "codewords_evaluated_per_sec", "value": value, "unit": "cw/s",
+            "metric": "codewords_evaluated_per_sec",
+            "value": strong["cw_per_s"] if headline_strong else value, "unit": "cw/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": strong["ms_per_run"] if headline_strong else tot_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong" if headline_strong else "weak",
             "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (mt19937_64 seeds 1..8, SURVEY.md §8d)",
-            "config": {"workload": WORKLOAD, "kernel": args.kernel,
-                       "parallelism": (f"{world} ranks, each running the eight-code step "
-                                       f"({args.streams} codes in flight per GPU); independent codes, "
-                                       "no data-path collective"
-                                       if world > 1 else
-                                       f"single GPU, {min(args.streams, len(SEEDS))} codes in flight"),
-                       "round_split": split,
+            "config": {"workload": strong["workload"] if headline_strong else WORKLOAD,
+                       "kernel": args.kernel,
+                       "parallelism": (f"{world} ranks over NCCL: one code, rounds split" if headline_strong
+                                       else weak["parallelism"]),
+                       "counting": ("value counts codewords the way the reference's RoundStats.combinations "
+                                    "does (C(k,c) per executed round; the device evaluates each against "
+                                    "the running bound, most of them with a pair / fold lower bound only: "
+                                    "bound-screened, not all weighed exactly -- roofline.frac_fixed_unit "
+                                    "is the exact-weight kernel on a fixed unit)"),
                        "l2": "flushed between steps (256 MiB write); working set < 1 MiB",
                        "codewords_per_step": cw_total // args.steps,
                        "ms_per_code_amortized": tot_ms / args.steps / len(SEEDS),
                        "d": expect_d},
+            "weak_step": weak if world > 1 else None,
+            "strong": strong,
+            "configs": configs,
             "e2e": {"value": e2e_value, "unit": "cw/s", "h2d_bytes_per_step": h2d // args.steps,
                     "d2h_bytes_per_step": d2h // args.steps,
                     "ms_per_step": tot_e2e / args.steps,
+                    "workload": WORKLOAD,
                     "path": "mdg_min_weight_batch (C ABI)" +
                             " from pinned host matrices: row basis + Gamma search + H2D + level loop"
                             " + witness + D2H"},

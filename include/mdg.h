@@ -87,6 +87,16 @@ int mdg_round(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t stop_at, mdg_round_
  * tasks [task_lo, task_hi) — the unit the multi-GPU path splits across ranks
  * (parallel.cpp:72-88 prefix tasks / engines.cpp:508-557 contiguous blocks). */
 int mdg_round_tasks(mdg_ctx* ctx, uint32_t j, uint32_t c, uint64_t* n_tasks);
+/* Rank `rank`'s range of a round split `world` ways, as the multi-rank loops cut it: contiguous
+ * tasks holding about 1/world of the codewords each (tasks differ in size: a task count split
+ * would give the first ranks most of the work; engines.cpp:508-557 splits by combinations). */
+int mdg_round_split(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t rank, uint32_t world,
+                    uint64_t* task_lo, uint64_t* task_hi);
+/* The same split on the host alone (no device): the tile plan of a level-c round of k rows of
+ * nw32 compacted 32-bit words for `resident_blocks` resident blocks; *codewords = the range's
+ * codeword count. For planning and tests. */
+int mdg_plan_split(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_blocks, uint32_t rank,
+                   uint32_t world, uint64_t* task_lo, uint64_t* task_hi, uint64_t* codewords);
 int mdg_round_range(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t stop_at, uint64_t task_lo,
                     uint64_t task_hi, mdg_round_out* out);
 
@@ -239,10 +249,35 @@ int mdg_brute_force(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n, uin
 int mdg_min_weight_dist(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n,
                         const mdg_config* cfg, uint32_t rank, uint32_t world,
                         mdg_reduce_fn reduce_min, void* user, mdg_run** out);
-/* NCCL reducer owned by the context (libnccl.so.2 loaded at runtime). */
+/* NCCL reducer owned by the context (libnccl.so.2 loaded at runtime).
+ * mdg_nccl_init also makes the ranks agree on the smallest SM count, so every
+ * rank cuts a split round into the same tiles. */
 int mdg_nccl_unique_id(uint8_t id[128]);
 int mdg_nccl_init(mdg_ctx* ctx, const uint8_t id[128], uint32_t rank, uint32_t world);
 int mdg_nccl_reduce_min(void* ctx, uint64_t* keys, uint32_t count); /* mdg_reduce_fn; user = ctx */
+
+/* In-process exchange group: `world` contexts in ONE process (on one device,
+ * or on devices with peer access), each driven by its own thread, run the
+ * same level loop; a split round's key is min-reduced by a stream-ordered
+ * kernel after cudaStreamWaitEvent on every member's round event (no NCCL, no
+ * kernel waiting on another). Same results as the NCCL path (the reference's
+ * merge of local minima, engines.cpp:432-441 / parallel.cpp:20-31). Attach
+ * each context with its rank, then call mdg_min_weight_dist / mdg_bz_loop_
+ * device_dist from one thread per member with reduce_min =
+ * mdg_group_reduce_min (a marker: calling it directly is an error). */
+typedef struct mdg_group mdg_group;
+int mdg_group_create(uint32_t world, mdg_group** out);   /* 1 <= world <= 16 */
+void mdg_group_free(mdg_group* g);
+int mdg_group_attach(mdg_ctx* ctx, mdg_group* g, uint32_t rank); /* g == NULL detaches */
+int mdg_group_reduce_min(void* user, uint64_t* keys, uint32_t count);
+
+/* Single-process multi-GPU front door: min_weight(G) with every round of at
+ * least cfg->split_min codewords split across the `world` contexts (their
+ * devices; the same device twice is allowed) through an exchange group, one
+ * host thread per context. out[r] receives rank r's record (the same d, trace
+ * and Gamma set on every rank; per-rank evaluated counts). */
+int mdg_min_weight_multi(mdg_ctx* const* ctxs, uint32_t world, const uint64_t* G, uint32_t k,
+                         uint32_t n, const mdg_config* cfg, mdg_run** out);
 
 /* Result accessors. */
 typedef struct {

@@ -24,7 +24,7 @@ import numpy as np
 
 __all__ = [
     "MdgError", "InvalidArgument", "OverflowError_", "CudaFailure", "lib", "Device", "GammaSet",
-    "RoundOut", "RunResult", "min_weight", "min_weight_dist", "run_bz_loop", "lower_bound",
+    "RoundOut", "RunResult", "min_weight", "min_weight_dist", "min_weight_multi", "run_bz_loop", "lower_bound",
     "singleton_upper", "brute_force", "nccl_unique_id", "parse_matrix", "serialize_matrix", "gen_matrix", "binomial",
     "rd_unrank", "rd_rank", "hash_rows", "rank_of", "words", "KERNEL_TAB", "KERNEL_RD",
 ]
@@ -106,6 +106,10 @@ SYMBOLS = {
     "mdg_load_gammas": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, u64p, C.c_void_p]),
     "mdg_round": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(_RoundOut)]),
     "mdg_round_tasks": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64)]),
+    "mdg_round_split": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                  C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "mdg_plan_split": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                 C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "mdg_round_range": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                   C.c_uint64, C.POINTER(_RoundOut)]),
     "mdg_round_bounded": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
@@ -152,6 +156,12 @@ SYMBOLS = {
     "mdg_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "mdg_nccl_init": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint32, C.c_uint32]),
     "mdg_nccl_reduce_min": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_uint32]),
+    "mdg_group_create": (C.c_int, [C.c_uint32, C.POINTER(C.c_void_p)]),
+    "mdg_group_free": (None, [C.c_void_p]),
+    "mdg_group_attach": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32]),
+    "mdg_group_reduce_min": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_uint32]),
+    "mdg_min_weight_multi": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32, u64p, C.c_uint32, C.c_uint32,
+                                       C.POINTER(_Config), C.POINTER(C.c_void_p)]),
     "mdg_run_info_get": (C.c_int, [C.c_void_p, C.POINTER(_RunInfo)]),
     "mdg_run_rounds": (C.c_int, [C.c_void_p, C.POINTER(_RoundRec)]),
     "mdg_run_levels": (C.c_int, [C.c_void_p, C.POINTER(_LevelRec)]),
@@ -416,6 +426,12 @@ class Device:
         _check(lib().mdg_round_tasks(self._h, j, c, C.byref(t)))
         return int(t.value)
 
+    def split_range(self, j: int, c: int, rank: int, world: int) -> tuple:
+        """rank's codeword-balanced task range of round (j, c) (mdg_round_split)"""
+        lo, hi = C.c_uint64(0), C.c_uint64(0)
+        _check(lib().mdg_round_split(self._h, j, c, rank, world, C.byref(lo), C.byref(hi)))
+        return int(lo.value), int(hi.value)
+
     def round_range(self, j: int, c: int, task_lo: int, task_hi: int, stop_at: int = 0) -> RoundOut:
         o = _RoundOut()
         _check(lib().mdg_round_range(self._h, j, c, stop_at, task_lo, task_hi, C.byref(o)))
@@ -664,6 +680,32 @@ def min_weight_dist(G: np.ndarray, n: int, rank: int, world: int,
     return _collect(h)
 
 
+def min_weight_multi(G: np.ndarray, n: int, devices: list, trials: int = 10, seed: int = 0,
+                     level_cap: int = 0, kernel: int = KERNEL_TAB, witness: bool = True,
+                     exact_rounds: bool = False, split_min: int = 0) -> list:
+    """Single-process multi-GPU min_weight (mdg_min_weight_multi): the contexts in `devices`
+    (distinct Device objects; their GPUs may repeat) run one level loop together, every round
+    of at least split_min codewords (0 = 2e8, 1 = every round) split across them and its key
+    min-reduced through an in-process exchange group (stream-ordered events + a min kernel).
+    Returns one RunResult per rank: the same d, trace and Gamma set on every rank."""
+    G = _rows(G)
+    world = len(devices)
+    cfg = _config(trials, seed, level_cap, kernel, witness, exact_rounds)
+    cfg.split_min = split_min
+    ctxs = (C.c_void_p * max(1, world))(*[d.handle.value for d in devices])
+    hs = (C.c_void_p * max(1, world))()
+    _check(lib().mdg_min_weight_multi(ctxs, world, G, G.shape[0], n, C.byref(cfg), hs))
+    return [_collect(C.c_void_p(hs[i])) for i in range(world)]
+
+
+def plan_split(k: int, c: int, nw32: int, resident_blocks: int, rank: int, world: int) -> tuple:
+    """Host-only tile plan split (mdg_plan_split): (task_lo, task_hi, codewords) of rank's range."""
+    lo, hi, cw = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+    _check(lib().mdg_plan_split(k, c, nw32, resident_blocks, rank, world, C.byref(lo), C.byref(hi),
+                                C.byref(cw)))
+    return int(lo.value), int(hi.value), int(cw.value)
+
+
 def brute_force(G: np.ndarray, n: int, brute_cap: int = 40,
                 device: Optional[Device] = None) -> RunResult:
     """min_weight with Algorithm::brute_gray (engines.cpp:480-558, 623-628): all 2^k - 1
@@ -678,6 +720,8 @@ def brute_force(G: np.ndarray, n: int, brute_cap: int = 40,
 def _reducer(reduce_min, device):
     if reduce_min == "nccl":
         return C.cast(lib().mdg_nccl_reduce_min, C.c_void_p), device.handle, None
+    if reduce_min == "group":  # the context was attached to an exchange group
+        return C.cast(lib().mdg_group_reduce_min, C.c_void_p), None, None
 
     def _cb(_user, keys, count):
         try:

@@ -28,6 +28,10 @@ struct mdg_gset {
     GammaSet gs;
 };
 
+struct mdg_group {
+    std::shared_ptr<ExchangeGroup> g;
+};
+
 struct mdg_run {
     EngineResult er;
     uint32_t n = 0, k = 0, m = 0, k_last = 0;
@@ -169,12 +173,13 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
     const uint64_t split_min = cfg.split_min ? cfg.split_min : uint64_t(200000000);
     auto do_round = [&](uint32_t j, uint32_t g, uint32_t stop_at, uint32_t cutoff) {
         RoundResult rr;
-        // a round below split_min codewords runs whole on every rank: no exchange
-        if (world <= 1 || double(binomial(k, g)) < double(split_min)) {
+        // a round below split_min codewords runs whole on every rank: no exchange (and the
+        // in-process group has no host-side reducer: its host-loop rounds -- the witness
+        // search only -- run whole too)
+        if (world <= 1 || double(binomial(k, g)) < double(split_min) || reduce == &mdg_group_reduce_min) {
             rr = eng.round(j, g, stop_at, 0, UINT64_MAX, cutoff);
         } else {
-            uint64_t T = eng.tasks(j, g);
-            uint64_t lo = T * rank / world, hi = T * (rank + 1) / world;
+            const auto [lo, hi] = eng.split_range(j, g, rank, world);
             rr = eng.round(j, g, stop_at, lo, hi, cutoff);
             uint64_t key = rr.key;
             int rc = reduce(user, &key, 1);
@@ -203,14 +208,15 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
     Bounds bounds;
     bounds.lower = 1;
     bounds.upper = singleton_upper(n, k);
-    const bool nccl_reduce = reduce == &mdg_nccl_reduce_min;
+    // NCCL or the in-process exchange group: the reduction is enqueued on the stream
+    const bool device_reduce = reduce == &mdg_nccl_reduce_min || reduce == &mdg_group_reduce_min;
     eng.timer_start();
-    if (world == 1 || nccl_reduce) {
+    if (world == 1 || device_reduce) {
         // device-chained level loop: same semantics as run_bz_loop, no host sync per round;
         // with the NCCL reducer the per-round allreduce(min) is enqueued in-stream
         Engine::ChainResult cr = eng.chain_loop(bounds.upper, bounds.lower, cfg.level_cap,
                                                 cfg.exact_rounds != 0, gs.k_last, rank, world,
-                                                nccl_reduce, split_min);
+                                                device_reduce, split_min);
         EngineResult& er = out.er;
         uint32_t U = bounds.upper;
         for (const auto& r : cr.rounds) {
@@ -441,6 +447,32 @@ int mdg_round_tasks(mdg_ctx* ctx, uint32_t j, uint32_t c, uint64_t* n_tasks) {
     return guard([&] {
         if (!ctx || !n_tasks) throw std::invalid_argument("null argument");
         *n_tasks = ctx->eng->tasks(j, c);
+    });
+}
+
+int mdg_round_split(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t rank, uint32_t world,
+                    uint64_t* task_lo, uint64_t* task_hi) {
+    return guard([&] {
+        if (!ctx || !task_lo || !task_hi) throw std::invalid_argument("null argument");
+        if (world < 1 || rank >= world) throw std::invalid_argument("bad rank / world");
+        const auto r = ctx->eng->split_range(j, c, rank, world);
+        *task_lo = r.first;
+        *task_hi = r.second;
+    });
+}
+
+int mdg_plan_split(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_blocks, uint32_t rank,
+                   uint32_t world, uint64_t* task_lo, uint64_t* task_hi, uint64_t* codewords) {
+    return guard([&] {
+        if (!task_lo || !task_hi || !codewords) throw std::invalid_argument("null argument");
+        if (world < 1 || rank >= world) throw std::invalid_argument("bad rank / world");
+        if (c < 1 || c > k || k > kMaxK || c > kMaxC) throw std::invalid_argument("need 1 <= c <= k <= 1024, c <= 64");
+        binomial(k, c);
+        const TabPlan pl = make_tab_plan(k, c, template_width(std::max(1u, nw32)), std::max(1u, resident_blocks));
+        const auto r = tab_split(pl, rank, world);
+        *task_lo = r.first;
+        *task_hi = r.second;
+        *codewords = tab_codewords_before(pl, r.second) - tab_codewords_before(pl, r.first);
     });
 }
 
@@ -816,6 +848,91 @@ int mdg_brute_force(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n, uin
         run->loop_s = br.ms * 1e-3;
         run->wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         *out = run.release();
+    });
+}
+
+int mdg_group_create(uint32_t world, mdg_group** out) {
+    return guard([&] {
+        if (!out) throw std::invalid_argument("null out");
+        auto g = std::make_unique<mdg_group>();
+        g->g = make_exchange_group(world);
+        *out = g.release();
+    });
+}
+
+void mdg_group_free(mdg_group* g) { delete g; }
+
+int mdg_group_attach(mdg_ctx* ctx, mdg_group* g, uint32_t rank) {
+    return guard([&] {
+        if (!ctx) throw std::invalid_argument("null ctx");
+        ctx->eng->group_attach(g ? g->g : nullptr, rank);
+    });
+}
+
+int mdg_group_reduce_min(void*, uint64_t*, uint32_t) {
+    g_err = "mdg_group_reduce_min is a marker for the device-side group exchange, not a host reducer";
+    return MDG_EINVAL;
+}
+
+int mdg_min_weight_multi(mdg_ctx* const* ctxs, uint32_t world, const uint64_t* G, uint32_t k,
+                         uint32_t n, const mdg_config* cfg, mdg_run** out) {
+    return guard([&] {
+        if (!ctxs || !G || !out) throw std::invalid_argument("null argument");
+        if (world < 1) throw std::invalid_argument("bad rank / world");
+        for (uint32_t r = 0; r < world; ++r) {
+            if (!ctxs[r]) throw std::invalid_argument("null ctx");
+            for (uint32_t q = 0; q < r; ++q)
+                if (ctxs[q] == ctxs[r]) throw std::invalid_argument("a context appears twice");
+            out[r] = nullptr;
+        }
+        mdg_config c;
+        mdg_config_default(&c);
+        if (cfg) c = *cfg;
+        if (c.trials < 1) throw std::invalid_argument("best_gamma_over_permutations: trials must be >= 1");
+        const BitMatrix M = from_rows(G, k, n);
+        auto group = make_exchange_group(world);
+        int plan_sms = ctxs[0]->eng->sm_count();
+        for (uint32_t r = 0; r < world; ++r) plan_sms = std::min(plan_sms, ctxs[r]->eng->sm_count());
+        std::vector<int> old_sms(world);
+        for (uint32_t r = 0; r < world; ++r) { // one tile cut of every split round on all ranks
+            ctxs[r]->eng->group_attach(group, r);
+            old_sms[r] = ctxs[r]->eng->plan_sms();
+            ctxs[r]->eng->set_plan_sms(plan_sms);
+        }
+        std::vector<std::unique_ptr<mdg_run>> runs(world);
+        std::vector<std::exception_ptr> errs(world);
+        auto member = [&](uint32_t r) {
+            try {
+                runs[r] = min_weight_device(*ctxs[r]->eng, M, c, r, world, &mdg_group_reduce_min, nullptr);
+            } catch (const std::exception& e) {
+                errs[r] = std::current_exception();
+                abort_exchange_group(*group, "rank " + std::to_string(r) + ": " + e.what());
+            } catch (...) {
+                errs[r] = std::current_exception();
+                abort_exchange_group(*group, "rank " + std::to_string(r) + " failed");
+            }
+        };
+        std::vector<std::thread> th;
+        for (uint32_t r = 1; r < world; ++r) th.emplace_back(member, r);
+        member(0);
+        for (auto& t : th) t.join();
+        for (uint32_t r = 0; r < world; ++r) {
+            ctxs[r]->eng->group_attach(nullptr, 0);
+            ctxs[r]->eng->set_plan_sms(old_sms[r]);
+        }
+        // the first real failure is the cause; the others' "aborted" errors follow from it
+        for (uint32_t r = 0; r < world; ++r)
+            if (errs[r]) {
+                try {
+                    std::rethrow_exception(errs[r]);
+                } catch (const std::runtime_error& e) {
+                    if (std::string(e.what()).find("exchange group aborted") != std::string::npos) continue;
+                    throw;
+                }
+            }
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+        for (uint32_t r = 0; r < world; ++r) out[r] = runs[r].release();
     });
 }
 

@@ -43,6 +43,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <condition_variable>
 #include <mutex>
 #include <sstream>
 
@@ -366,6 +367,25 @@ __device__ __forceinline__ void finalize_round(ChainState* st, const unsigned lo
         if (st->L >= st->U) st->done = 1;
     }
     *rec = r;
+}
+
+// In-process exchange group (ExchangeGroup): min of every member's round key, read
+// after the stream waited on the members' round events (peer loads for members on other
+// devices), written to this member's slot -- the group's allreduce(min) of one u64.
+constexpr int kMaxGroup = 16;
+struct GroupKeys {
+    const unsigned long long* key[kMaxGroup];
+    uint32_t n;
+};
+__global__ void group_min(GroupKeys g, unsigned long long* slot) {
+    if (threadIdx.x == 0) {
+        unsigned long long m = ~0ull;
+        for (uint32_t i = 0; i < g.n; ++i) {
+            const unsigned long long v = *reinterpret_cast<volatile const unsigned long long*>(g.key[i]);
+            m = v < m ? v : m;
+        }
+        *slot = m;
+    }
 }
 
 // chain start time stamp (device clock), read back with the records
@@ -1364,7 +1384,11 @@ __global__ void __launch_bounds__(kThreads) tab_find(TabArgs a) {
     if (cand != ~0ull) atomicMin(a.find_out, cand);
 }
 
-// full weight histogram (config 5): per-warp privatized bins in smem
+// full weight histogram (config 5): per-warp privatized u32 bins in smem. The lanes past
+// the tile's edge count into a dummy bin (no divergent branch per codeword); the bin
+// address is a 32-bit shared-window offset computed once (a generic pointer costs an S2R
+// and a LEA per increment); the smem bins are flushed into the u64 global histogram before
+// any of them could wrap (a block counts at most 2^32 - 1 codewords between flushes).
 template <int NW, bool HID>
 __global__ void __launch_bounds__(kThreads) tab_hist(TabArgs a) {
     constexpr int R = r_for(NW);
@@ -1372,46 +1396,77 @@ __global__ void __launch_bounds__(kThreads) tab_hist(TabArgs a) {
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
     extern __shared__ __align__(16) uint32_t dyn[];
     uint32_t* xs = dyn;
-    uint32_t* bins = dyn + a.tx * XS; // kWarps x nbins
+    const uint32_t bs = a.nbins + 1;  // per-warp stride: the bins and the dummy
+    uint32_t* bins = dyn + a.tx * XS; // kWarps x bs
     __shared__ TileInfo ti;
-    const uint32_t warp = threadIdx.x >> 5;
-    for (uint32_t i = threadIdx.x; i < kWarps * a.nbins; i += kThreads) bins[i] = 0;
-    unsigned long long done_local = 0;
-    uint32_t* mybins = bins + warp * a.nbins;
+    __shared__ uint32_t flush_now;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t i = threadIdx.x; i < kWarps * bs; i += kThreads) bins[i] = 0;
+    const uint32_t sbase = uint32_t(__cvta_generic_to_shared(bins + warp * bs));
+    const uint32_t add = a.add_const, dummy = a.nbins;
+    unsigned long long done_local = 0, since_flush = 0; // thread 0
+    auto flush = [&]() { // all threads; bins -> global, zeroed
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < a.nbins; b += kThreads) {
+            unsigned long long sum = 0;
+            for (int w = 0; w < kWarps; ++w) {
+                sum += bins[w * bs + b];
+                bins[w * bs + b] = 0;
+            }
+            if (sum) atomicAdd(a.hist + b, sum);
+        }
+        __syncthreads();
+    };
     for (;;) {
-        if (threadIdx.x == 0) {
-            uint64_t t = a.tile_lo + atomicAdd(a.counter, 1ull);
-            ti.stop = t >= a.tile_hi;
-            if (!ti.stop) {
-                decode_tile<YC>(a, t, ti);
-                done_local += uint64_t(ti.nx) * ti.nyv;
+        if (threadIdx.x < 32) {
+            uint32_t stop = 0;
+            uint64_t t = 0;
+            if (lane == 0) {
+                t = a.tile_lo + atomicAdd(a.counter, 1ull);
+                stop = t >= a.tile_hi;
+            }
+            stop = __shfl_sync(0xFFFFFFFFu, stop, 0);
+            t = __shfl_sync(0xFFFFFFFFu, t, 0);
+            if (!stop) decode_tile_warp<YC>(a, t, ti);
+            if (lane == 0) {
+                ti.stop = stop;
+                flush_now = 0;
+                if (!stop) {
+                    const uint64_t cw = uint64_t(ti.nx) * ti.nyv;
+                    done_local += cw;
+                    if (since_flush + cw > 0xFFFFFFFFull) {
+                        flush_now = 1;
+                        since_flush = 0;
+                    }
+                    since_flush += cw;
+                }
             }
         }
         __syncthreads();
         if (ti.stop) break;
+        if (flush_now) flush();
         if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(a, ti, threadIdx.x, xs + threadIdx.x * XS);
         uint32_t Y[R][NW], idY[R];
         bool valid[R];
         load_suffixes<NW, HID>(a, ti, Y, idY, valid);
+        uint32_t base[R]; // the lane's per-item base: the weight offset, or the dummy bin
+#pragma unroll
+        for (int r = 0; r < R; ++r) base[r] = valid[r] ? add + (HID ? idY[r] : 0u) : 0u;
         __syncthreads();
         for (uint32_t xi = 0; xi < ti.nx; ++xi) {
             uint32_t X[XS];
             vload<XS>(xs + xi * XS, X);
+            const uint32_t xid = HID ? X[NW] : 0u;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                uint32_t w = a.add_const + xor_weight<0, NW, XS, NW>(X, Y[r]);
-                if (HID) w += X[NW] + idY[r];
-                if (valid[r]) atomicAdd(mybins + w, 1u);
+                uint32_t w = base[r] + xid + xor_weight<0, NW, XS, NW>(X, Y[r]);
+                w = valid[r] ? w : dummy;
+                asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(sbase + 4u * w));
             }
         }
         __syncthreads();
     }
-    __syncthreads();
-    for (uint32_t b = threadIdx.x; b < a.nbins; b += kThreads) {
-        unsigned long long s = 0;
-        for (int w = 0; w < kWarps; ++w) s += bins[w * a.nbins + b];
-        if (s) atomicAdd(a.hist + b, s);
-    }
+    flush();
     if (threadIdx.x == 0 && done_local) atomicAdd(a.evaluated, done_local);
 }
 
@@ -1661,6 +1716,15 @@ struct TabOcc {
 };
 
 template <int NW, bool HID>
+struct HistOcc { // resident tab_hist blocks per SM at `dyn` bytes of dynamic smem
+    static void run(size_t dyn, int* occ) {
+        auto fn = tab_hist<NW, HID>;
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, kThreads, dyn);
+    }
+};
+
+template <int NW, bool HID>
 struct TabLaunch {
     // grid: number of tiles for mode 0/2 (clamped to the resident-block count)
     static void run(const TabArgs& a, uint64_t grid, cudaStream_t st, int mode, size_t dyn, int sms) {
@@ -1857,6 +1921,50 @@ TabPlan make_tab_plan(uint32_t k, uint32_t c, uint32_t nw32, uint32_t resident_b
     return pl;
 }
 
+// Codewords in tiles [0, t) of a plan: the tiles of pivot e cut its A x B grid (smem side x
+// register side) into TX x YC blocks, row-major, the last row and column partial.
+uint64_t tab_codewords_before(const TabPlan& pl, uint64_t t) {
+    uint64_t cw = 0;
+    const size_t npiv = pl.prefix.size() - 1;
+    for (size_t i = 0; i < npiv && t > pl.prefix[i]; ++i) {
+        const uint32_t e = pl.emin + uint32_t(i);
+        const uint64_t NX = hb(e, pl.p - 1), NY = hb(pl.k - 1 - e, pl.s);
+        const bool tr = i < pl.tr.size() && pl.tr[i];
+        const uint64_t A = tr ? NY : NX, B = tr ? NX : NY;
+        if (t >= pl.prefix[i + 1]) {
+            cw += A * B;
+            continue;
+        }
+        const uint64_t local = t - pl.prefix[i], ntb = ceil_div(B, pl.YC);
+        const uint64_t ta = local / ntb, tb = local % ntb;
+        cw += std::min<uint64_t>(ta * pl.TX, A) * B;
+        cw += std::min<uint64_t>(pl.TX, A - ta * pl.TX) * std::min<uint64_t>(tb * pl.YC, B);
+    }
+    return cw;
+}
+
+// Rank r's contiguous tile range of a split round: boundaries at the tiles where the
+// cumulative codeword count crosses r/world of the round (tiles are not equal-sized: the last
+// pivots' tiles are partial), so every rank gets ~1/world of the codewords, not of the tiles.
+// Deterministic: every rank computes the same boundaries from the same plan.
+std::pair<uint64_t, uint64_t> tab_split(const TabPlan& pl, uint32_t rank, uint32_t world) {
+    const uint64_t T = pl.tiles();
+    if (world <= 1) return {0, T};
+    const uint64_t total = tab_codewords_before(pl, T);
+    auto bound = [&](uint32_t r) -> uint64_t {
+        if (r == 0) return 0;
+        if (r >= world) return T;
+        const uint64_t target = uint64_t((unsigned __int128)total * r / world);
+        uint64_t lo = 0, hi = T; // smallest t with codewords_before(t) >= target
+        while (lo < hi) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            if (tab_codewords_before(pl, mid) >= target) hi = mid; else lo = mid + 1;
+        }
+        return lo;
+    };
+    return {bound(rank), bound(rank + 1)};
+}
+
 // host colex unrank: t-subset of [0, hi) with colex rank r, ascending
 static void colex_unrank_host(uint64_t r, uint32_t t, uint32_t hi, uint32_t* out) {
     for (uint32_t i = t; i >= 1; --i) {
@@ -1926,6 +2034,69 @@ NcclApi& nccl() {
 constexpr int kNcclUint64 = 5; // ncclUint64
 constexpr int kNcclMin = 3;    // ncclMin
 } // namespace
+
+// ------------------------------------------------------------ exchange group
+// SURVEY.md §8e's per-round reduction without NCCL, for `world` engines in ONE process
+// (one host thread each; on one device or on peer-accessible devices). Each split round:
+// the member records an event after its round kernel and publishes (slot, event); a host
+// barrier waits for all members; each member's stream then waits on the others' events
+// and a one-thread kernel takes the min of all members' keys (group_min). No kernel waits
+// on another kernel -- the dependency is stream-ordered. One barrier per round also orders
+// event reuse: a member re-records its event only after every member passed the barrier
+// of the next split round, i.e. after they enqueued their waits on the previous record.
+// Members whose enqueue decisions diverge (a bug: the loop is deterministic) time out.
+struct ExchangeGroup {
+    explicit ExchangeGroup(uint32_t world, double timeout_s)
+        : world(world), timeout_s(timeout_s), slots(world, nullptr), events(world, nullptr) {}
+    const uint32_t world;
+    const double timeout_s;
+    std::mutex mu;
+    std::condition_variable cv;
+    uint64_t generation = 0;
+    uint32_t arrived = 0;
+    bool aborted = false;
+    std::string why;
+    std::vector<unsigned long long*> slots;
+    std::vector<cudaEvent_t> events;
+    std::vector<int> devices;
+
+    // publish (slot, ev) of `rank`, wait for every member of this round; copies out all
+    void exchange(uint32_t rank, unsigned long long* slot, cudaEvent_t ev,
+                  std::vector<unsigned long long*>& all_slots, std::vector<cudaEvent_t>& all_events) {
+        std::unique_lock<std::mutex> lk(mu);
+        if (aborted) throw std::runtime_error("exchange group aborted: " + why);
+        slots[rank] = slot;
+        events[rank] = ev;
+        const uint64_t gen = generation;
+        if (++arrived == world) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else if (!cv.wait_for(lk, std::chrono::duration<double>(timeout_s),
+                                [&] { return generation != gen || aborted; })) {
+            aborted = true;
+            why = "member " + std::to_string(rank) + " timed out at a split round (diverged loop?)";
+            cv.notify_all();
+            throw std::runtime_error("exchange group: " + why);
+        }
+        if (aborted) throw std::runtime_error("exchange group aborted: " + why);
+        all_slots = slots;
+        all_events = events;
+    }
+    void abort(const std::string& reason) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!aborted) why = reason;
+        aborted = true;
+        cv.notify_all();
+    }
+};
+
+std::shared_ptr<ExchangeGroup> make_exchange_group(uint32_t world, double timeout_s) {
+    if (world < 1 || world > uint32_t(kMaxGroup))
+        throw std::invalid_argument("exchange group: 1 <= world <= 16");
+    return std::make_shared<ExchangeGroup>(world, timeout_s);
+}
+void abort_exchange_group(ExchangeGroup& g, const std::string& reason) { g.abort(reason); }
 
 // ------------------------------------------------------------ Engine impl
 // Bump allocator over large cudaMalloc'd chunks: Gamma rows and suffix tables
@@ -2062,10 +2233,13 @@ struct Engine::Impl {
     size_t hist_cap = 0;
     std::vector<GammaDev> gammas;
     std::map<std::tuple<uint32_t, uint32_t, bool>, uint32_t*> tables; // (j, size, reverse) -> table
-    std::map<std::tuple<uint32_t, uint32_t, uint32_t, bool, bool, bool>, PlanEntry> plans; // (k, c, nw, hid, rd, prune)
+    std::map<std::tuple<uint32_t, uint32_t, uint32_t, bool, bool, bool, uint32_t>, PlanEntry> plans; // (k, c, nw, hid, rd, prune, tiles per block)
     std::map<std::pair<uint32_t, bool>, int> occ;                     // (nw, hid)
     std::map<std::pair<uint32_t, uint32_t>, FoldPlan> fold_cache; // (j, c)
     ncclComm_t comm = nullptr;
+    std::shared_ptr<ExchangeGroup> group; // in-process exchange (group_attach)
+    uint32_t group_rank = 0;
+    cudaEvent_t group_ev = nullptr;
     uint64_t* red_dev = nullptr;
     size_t red_cap = 0;
     DevArena arena;                  // Gamma rows + suffix tables (reset per load)
@@ -2111,12 +2285,14 @@ struct Engine::Impl {
         return plan(k, c, g, sms, rd, prune);
     }
     // the tile plan of an explicit variant (a round's witness is decoded with the plan it ran on)
-    const PlanEntry& plan(uint32_t k, uint32_t c, const GammaDev& g, int sms, bool rd, bool prune) {
-        auto key = std::make_tuple(k, c, g.nw, g.hid, rd, prune);
+    const PlanEntry& plan(uint32_t k, uint32_t c, const GammaDev& g, int sms, bool rd, bool prune,
+                          uint32_t tpb = 0, int resident_override = 0) {
+        auto key = std::make_tuple(k, c, g.nw, g.hid, rd, prune, tpb);
         auto it = plans.find(key);
         if (it != plans.end()) return it->second;
         PlanEntry pe;
-        pe.plan = make_tab_plan(k, c, g.nw, uint32_t(resident(g.nw, g.hid, sms)), rd, prune ? 0u : 8u);
+        const int res = resident_override ? resident_override : resident(g.nw, g.hid, sms);
+        pe.plan = make_tab_plan(k, c, g.nw, uint32_t(res), rd, tpb ? tpb : (prune ? 0u : 8u));
         const size_t pb = pe.plan.prefix.size() * 8, tb = pe.plan.tr.size();
         pe.d_prefix = static_cast<uint64_t*>(plan_arena.alloc(pb + tb));
         CK(cudaMemcpyAsync(pe.d_prefix, pe.plan.prefix.data(), pb, cudaMemcpyHostToDevice, stream));
@@ -2140,6 +2316,7 @@ Engine::Engine(int device) : device_(device), impl_(new Impl) {
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device));
     sms_ = prop.multiProcessorCount;
+    plan_sms_ = sms_;
     if (const char* e = std::getenv("MDG_PDL")) pdl_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("MDG_FUSE_MAX")) fuse_max_ = std::atof(e);
     CK(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking));
@@ -2163,6 +2340,7 @@ Engine::~Engine() {
     if (impl_->comm) {
         try { nccl().CommDestroy(impl_->comm); } catch (...) {}
     }
+    if (impl_->group_ev) cudaEventDestroy(impl_->group_ev);
     cudaFree(impl_->red_dev);
     cudaFree(impl_->scratch);
     cudaFree(impl_->d_state);
@@ -2608,9 +2786,14 @@ static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe
     return a;
 }
 
+std::pair<uint64_t, uint64_t> Engine::split_range(uint32_t j, uint32_t c, uint32_t rank, uint32_t world) {
+    check_round(j, c);
+    return tab_split(impl_->plan(k_, c, impl_->gammas[j], plan_sms_).plan, rank, world);
+}
+
 uint64_t Engine::tasks(uint32_t j, uint32_t c) {
     check_round(j, c);
-    return impl_->plan(k_, c, impl_->gammas[j], sms_).plan.tiles();
+    return impl_->plan(k_, c, impl_->gammas[j], plan_sms_).plan.tiles();
 }
 
 RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t task_lo, uint64_t task_hi,
@@ -2621,7 +2804,7 @@ RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t tas
     const GammaDev& g = im.gammas[j];
     RoundResult rr;
     rr.combinations = binomial(k_, c);
-    const PlanEntry& pe = im.plan(k_, c, g, sms_);
+    const PlanEntry& pe = im.plan(k_, c, g, plan_sms_);
     uint64_t lo = std::min(task_lo, pe.plan.tiles()), hi = std::min(task_hi, pe.plan.tiles());
     rr.task_lo = lo;
     rr.task_hi = hi;
@@ -2670,7 +2853,13 @@ RoundResult Engine::round_hist(uint32_t j, uint32_t c, uint64_t* hist) {
     }
     RoundResult rr;
     rr.combinations = binomial(k_, c);
-    const PlanEntry& pe = im.plan(k_, c, g, sms_);
+    // its own tile plan: every codeword is weighed (no pruning), so the plan aims for 4 tiles
+    // per resident tab_hist block (its occupancy is set by the smem bins) -- the pruned
+    // rounds' plan leaves most SMs idle on a config-5 sized round
+    const int XSh = stride_for(int(g.nw) + (g.hid ? 1 : 0));
+    int hocc = 0;
+    dispatch_nw_hid<HistOcc>(g.nw, g.hid, size_t(kTX) * XSh * 4 + size_t(kWarps) * (nbins + 1) * 4, &hocc);
+    const PlanEntry& pe = im.plan(k_, c, g, plan_sms_, im.rd, false, /*tpb=*/4, std::max(1, hocc) * sms_);
     uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
     unsigned long long* slot = im.take_slot();
     CK(cudaMemsetAsync(im.hist_dev, 0, nbins * 8, im.stream));
@@ -2680,7 +2869,7 @@ RoundResult Engine::round_hist(uint32_t j, uint32_t c, uint64_t* hist) {
     a.nbins = nbins;
     a.hist = im.hist_dev;
     int XS = stride_for(int(g.nw) + (g.hid ? 1 : 0));
-    size_t dyn = size_t(pe.plan.TX) * XS * 4 + size_t(kWarps) * nbins * 4;
+    size_t dyn = size_t(pe.plan.TX) * XS * 4 + size_t(kWarps) * (nbins + 1) * 4; // + a dummy bin per warp
     CK(cudaEventRecord(im.ev0, im.stream));
     dispatch_nw_hid<TabLaunch>(g.nw, g.hid, a, pe.plan.tiles(), im.stream, 2, dyn, sms_);
     CK(cudaGetLastError());
@@ -2714,7 +2903,7 @@ std::vector<uint32_t> Engine::witness(uint32_t j, uint32_t c, const RoundResult&
     // decode with the tile plan the round ran on (tagged by Engine::round / chain_loop), not
     // whatever kernel / pruning setting is current: the plans differ
     const bool tagged = (rr.plan_tag & 1u) != 0;
-    const PlanEntry& pe = im.plan(k_, c, g, sms_, tagged ? (rr.plan_tag & 4u) != 0 : im.rd,
+    const PlanEntry& pe = im.plan(k_, c, g, plan_sms_, tagged ? (rr.plan_tag & 4u) != 0 : im.rd,
                                   tagged ? (rr.plan_tag & 2u) != 0 : im.prune);
     if (task >= pe.plan.tiles()) throw std::invalid_argument("witness: key names no task of this round");
     if (pos) { // the kernel named the position: smem-side index << 11 | register-side index
@@ -2758,7 +2947,10 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
                                        uint32_t k_last, uint32_t rank, uint32_t world,
                                        bool allreduce, uint64_t split_min) {
     allreduce = allreduce || world > 1;
-    if (allreduce && !impl_->comm) throw std::logic_error("chain_loop: NCCL communicator not initialised");
+    if (allreduce && !impl_->comm && !impl_->group)
+        throw std::logic_error("chain_loop: no NCCL communicator or exchange group attached");
+    if (impl_->group && (impl_->group->world != world || impl_->group_rank != rank))
+        throw std::invalid_argument("chain_loop: rank / world differ from the attached exchange group");
     CK(cudaSetDevice(device_));
     Impl& im = *impl_;
     // host work per check: ~2e8 codewords (~0.1 ms of device time) between looks at `done`
@@ -2790,11 +2982,11 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
         for (uint32_t c = 1; c <= k_ && c <= kMaxC && (!level_cap || c <= level_cap); ++c) {
             work += double(m_) * double(hb(k_, c));
             if (c > 1 && (work > 2e10 ||
-                          table_bytes(im, k_, table_needs(im, m_, k_, 1, c, sms_)) > (uint64_t{32} << 20)))
+                          table_bytes(im, k_, table_needs(im, m_, k_, 1, c, plan_sms_)) > (uint64_t{32} << 20)))
                 break;
             built_to = c;
         }
-        if (built_to >= 1) prebuild_tables(im, m_, k_, 1, built_to, sms_);
+        if (built_to >= 1) prebuild_tables(im, m_, k_, 1, built_to, plan_sms_);
     }
     uint32_t g = 1;
     bool done = init.done != 0;
@@ -2815,21 +3007,23 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
         }
         const uint32_t lb = lower_bound(m_, g, k_, k_last);
         if (g > built_to) {
-            prebuild_tables(im, m_, k_, g, g, sms_);
+            prebuild_tables(im, m_, k_, g, g, plan_sms_);
             built_to = g;
         }
         // this level's plans (only the first sampled level waits for them) and the next
         // level's, computed while the GPU runs the levels already enqueued
         if (hb(k_, g) >= (uint64_t{1} << 20))
             prefetch_fold_plans(im, m_, k_, g, level_cap ? std::min(level_cap, g + 1) : g + 1);
-        // small levels of Gammas of one row width: all m rounds in one launch (tab_level)
-        bool fuse_level = !allreduce && m_ >= 2 && m_ <= uint32_t(kMaxFuse) && fuse_max_ > 0 &&
+        // small levels of Gammas of one row width: all m rounds in one launch (tab_level);
+        // multi-rank, only a level none of whose rounds is split (every rank runs it whole)
+        const bool level_split = allreduce && double(binomial(k_, g)) >= double(split_min);
+        bool fuse_level = !level_split && m_ >= 2 && m_ <= uint32_t(kMaxFuse) && fuse_max_ > 0 &&
                           double(m_) * double(binomial(k_, g)) <= fuse_max_;
         for (uint32_t j = 1; fuse_level && j < m_; ++j)
             fuse_level = im.gammas[j].nw == im.gammas[0].nw && im.gammas[j].hid == im.gammas[0].hid;
         if (fuse_level) {
             const GammaDev& g0 = im.gammas[0];
-            const PlanEntry& pe = im.plan(k_, g, g0, sms_);
+            const PlanEntry& pe = im.plan(k_, g, g0, plan_sms_);
             LevelDesc L{};
             L.m = m_;
             L.T = pe.plan.tiles();
@@ -2868,7 +3062,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
         }
         for (uint32_t j = 0; j < m_ && !fuse_level; ++j) {
             const GammaDev& gd = im.gammas[j];
-            const PlanEntry& pe = im.plan(k_, g, gd, sms_);
+            const PlanEntry& pe = im.plan(k_, g, gd, plan_sms_);
             uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
             unsigned long long* slot = im.take_slot();
             TabArgs a = tab_args(im, gd, pe, yt, k_, g);
@@ -2877,8 +3071,9 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
             // everywhere with no exchange (the split would cost more in reduction latency)
             const bool split = allreduce && double(binomial(k_, g)) >= double(split_min);
             a.st = im.d_state;
-            a.tile_lo = split ? T * rank / world : 0;
-            a.tile_hi = split ? T * (rank + 1) / world : T;
+            const auto range = split ? tab_split(pe.plan, rank, world) : std::make_pair(uint64_t(0), T);
+            a.tile_lo = range.first;
+            a.tile_hi = range.second;
             a.best_key = slot; a.evaluated = slot + 1; a.counter = slot + 2;
             const bool fuse = !split && a.tile_hi > a.tile_lo;
             if (fuse) { // the round kernel's last block closes the round: one launch per round
@@ -2900,9 +3095,24 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
                 after_round = im.cnt.launches;
                 synced = false;
             }
-            if (split) {
+            if (split && im.comm) {
                 int rc = nccl().AllReduce(slot, slot, 1, kNcclUint64, kNcclMin, im.comm, im.stream);
                 if (rc != 0) throw std::runtime_error(std::string("ncclAllReduce: ") + nccl().GetErrorString(rc));
+            } else if (split) { // in-process exchange group
+                CK(cudaEventRecord(im.group_ev, im.stream));
+                std::vector<unsigned long long*> all;
+                std::vector<cudaEvent_t> evs;
+                im.group->exchange(rank, slot, im.group_ev, all, evs);
+                GroupKeys gk{};
+                gk.n = world;
+                for (uint32_t r = 0; r < world; ++r) {
+                    gk.key[r] = all[r];
+                    if (r != rank) CK(cudaStreamWaitEvent(im.stream, evs[r], 0));
+                }
+                group_min<<<1, 32, 0, im.stream>>>(gk, slot);
+                CK(cudaGetLastError());
+                im.cnt.launches += 1;
+                synced = true; // the next round must not overlap the exchange (no PDL)
             }
             if (!fuse) {
                 chain_finalize<<<1, 32, 0, im.stream>>>(im.d_state, slot, im.d_recs + nrec, g, j,
@@ -3049,6 +3259,48 @@ double Engine::timer_stop_ms() {
     return ms;
 }
 
+void Engine::set_plan_sms(int sms) {
+    if (sms < 1) throw std::invalid_argument("set_plan_sms: need >= 1");
+    if (sms == plan_sms_) return;
+    CK(cudaSetDevice(device_));
+    CK(cudaStreamSynchronize(impl_->stream));
+    plan_sms_ = sms;
+    impl_->plans.clear(); // tile plans depend on it (their arena memory is simply kept)
+}
+
+void Engine::group_attach(std::shared_ptr<ExchangeGroup> g, uint32_t rank) {
+    CK(cudaSetDevice(device_));
+    Impl& im = *impl_;
+    if (!g) { // detach
+        im.group.reset();
+        im.group_rank = 0;
+        return;
+    }
+    if (rank >= g->world) throw std::invalid_argument("group_attach: rank >= world");
+    if (!im.group_ev) CK(cudaEventCreateWithFlags(&im.group_ev, cudaEventDisableTiming));
+    // members on other devices read this engine's round slots (and it theirs): peer access
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        for (int d : g->devices) {
+            if (d == device_) continue;
+            int can = 0;
+            CK(cudaDeviceCanAccessPeer(&can, device_, d));
+            if (!can) throw std::invalid_argument("group_attach: devices " + std::to_string(device_) + " and " +
+                                                  std::to_string(d) + " have no peer access");
+            for (auto [from, to] : {std::make_pair(device_, d), std::make_pair(d, device_)}) {
+                CK(cudaSetDevice(from));
+                cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else CK(e);
+            }
+            CK(cudaSetDevice(device_));
+        }
+        g->devices.push_back(device_);
+    }
+    im.group = std::move(g);
+    im.group_rank = rank;
+}
+
 void Engine::nccl_unique_id(uint8_t id[128]) {
     ncclUniqueId_t u;
     int rc = nccl().GetUniqueId(&u);
@@ -3062,6 +3314,12 @@ void Engine::nccl_init(const uint8_t id[128], uint32_t rank, uint32_t world) {
     std::memcpy(u.internal, id, 128);
     int rc = nccl().CommInitRank(&impl_->comm, int(world), u, int(rank));
     if (rc != 0) throw std::runtime_error(std::string("ncclCommInitRank: ") + nccl().GetErrorString(rc));
+    // every rank must cut a split round into the same tiles: the tile plans depend on the
+    // resident-block count, so the ranks agree on the smallest SM count (identical on a B200
+    // box; a mixed or partitioned node would otherwise split rounds inconsistently)
+    uint64_t sms = uint64_t(sms_);
+    nccl_reduce_min(&sms, 1);
+    set_plan_sms(int(sms));
 }
 
 void Engine::nccl_reduce_min(uint64_t* keys, uint32_t count) {

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "mdg.hpp"
@@ -66,6 +67,12 @@ struct TabPlan {
     uint64_t tiles() const { return prefix.empty() ? 0 : prefix.back(); }
 };
 
+// In-process exchange group (engine.cu): `world` engines in one process reduce each split
+// round's key through stream-ordered events and a min kernel instead of NCCL.
+struct ExchangeGroup;
+std::shared_ptr<ExchangeGroup> make_exchange_group(uint32_t world, double timeout_s = 120.0);
+void abort_exchange_group(ExchangeGroup& g, const std::string& reason);
+
 class Engine {
 public:
     explicit Engine(int device);
@@ -84,6 +91,8 @@ public:
     Kernel kernel() const { return kernel_; }
 
     uint64_t tasks(uint32_t j, uint32_t c);
+    // rank's contiguous task range of round (j, c) split `world` ways by codewords (tab_split)
+    std::pair<uint64_t, uint64_t> split_range(uint32_t j, uint32_t c, uint32_t rank, uint32_t world);
     // cutoff: only weights < cutoff matter (0 = the exact round minimum). With a
     // cutoff the result is min(true minimum, cutoff) and `bounded` is set when no
     // codeword lies below it — what run_bz_loop's U = min(U, w) needs.
@@ -124,6 +133,14 @@ public:
                            bool allreduce = false, uint64_t split_min = 1);
     std::vector<uint32_t> witness(uint32_t j, uint32_t c, const RoundResult& rr);
 
+    // In-process multi-engine runs: attach this engine as member `rank` of an exchange group
+    // (null: detach); chain_loop then reduces split rounds through the group, not NCCL.
+    void group_attach(std::shared_ptr<ExchangeGroup> g, uint32_t rank);
+    // Resident-SM count the tile plans assume (default: this device's). Multi-rank runs agree
+    // on one value so every rank cuts a split round into the same tiles.
+    void set_plan_sms(int sms);
+    int plan_sms() const { return plan_sms_; }
+
     // NCCL (loaded at runtime) for the multi-GPU reduction
     void nccl_init(const uint8_t id[128], uint32_t rank, uint32_t world);
     void nccl_reduce_min(uint64_t* keys, uint32_t count);
@@ -154,7 +171,7 @@ public:
 
 private:
     void check_round(uint32_t j, uint32_t c) const;
-    int device_ = 0, sms_ = 0;
+    int device_ = 0, sms_ = 0, plan_sms_ = 0;
     bool pdl_ = true; // programmatic dependent launch between chained rounds (MDG_PDL=0: off)
     double fuse_max_ = 4e9; // chained levels up to this many codewords run as one launch (MDG_FUSE_MAX)
     uint32_t m_ = 0, k_ = 0, n_ = 0;
@@ -170,6 +187,9 @@ uint32_t tab_yc(uint32_t nw32);
 uint32_t tab_tx();
 // kernel template width for a row of nw32 words (rows are zero-padded up to it)
 uint32_t template_width(uint32_t nw32);
+// codewords in tiles [0, t) of a plan, and rank's codeword-balanced contiguous tile range
+uint64_t tab_codewords_before(const TabPlan& plan, uint64_t t);
+std::pair<uint64_t, uint64_t> tab_split(const TabPlan& plan, uint32_t rank, uint32_t world);
 // reconstruct the combination of tile `tile`, local prefix x / suffix y
 void tab_decode(const TabPlan& plan, uint64_t tile, uint32_t x_local, uint32_t y_local,
                 uint32_t* idx);

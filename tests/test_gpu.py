@@ -313,6 +313,61 @@ def test_dist_two_ranks_threaded(mdg):
             assert calls == [0, 0]  # cfg2 seed 8 never reaches 2e8-codeword rounds
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_min_weight_multi_group_split(mdg, world):
+    """The chained split path (each rank's contiguous tile range of every round of at least
+    split_min codewords, the per-round key min-reduced IN STREAM before the round closes --
+    the production multi-GPU path, here with the in-process exchange group instead of NCCL:
+    cudaStreamWaitEvent on the members' round events, then a min kernel; no kernel waits on
+    another) with `world` contexts on one GPU: d, per-round and per-level trace, Gamma set and
+    witness equal the golden on every rank; the ranks' evaluated counts add up to the
+    single-rank count of the split rounds; levels below split_min still run fused."""
+    devs = [mdg.Device(0) for _ in range(world)]
+    cases = {c["name"]: c for c in load_golden("configs")}
+    cases["cfg4_cap6"] = next(c for c in load_golden("configs_cap4_6") if c["name"] == "cfg4")
+    try:
+        for name in ("cfg1", "cfg2_s1", "cfg2_s8", "cfg3", "cfg4_cap6"):
+            case = cases[name]
+            g = case["gen"]
+            cap = case["level_cap"] if case["capped"] else 0
+            rows = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
+            single = mdg.min_weight(rows, g["n"], 10, g["seed"], level_cap=cap, device=devs[0])
+            for split_min in ((1, 0, 10**6, 1 << 62) if name != "cfg4_cap6" else (0,)):
+                runs = mdg.min_weight_multi(rows, g["n"], devs, trials=10, seed=g["seed"],
+                                            level_cap=cap, split_min=split_min)
+                assert len(runs) == world
+                for r, res in enumerate(runs):
+                    assert res.d == (case["U_final"] if cap else case["d"]), (name, r)
+                    assert res.capped == bool(cap)
+                    _check_run(res, case, f"{name} rank{r} split_min={split_min}", exact=False)
+                if split_min == 1 and name == "cfg2_s1":  # every round split: each rank
+                    # evaluates about 1/world of the codewords of the single-rank run
+                    assert max(r_.evaluated for r_ in runs) < 0.75 * single.evaluated, name
+    finally:
+        for d in devs:
+            d.close()
+
+
+def test_min_weight_multi_errors(mdg):
+    """Argument checks of the single-process multi front door, and a member failure (a level
+    beyond the device limit would be hit by every rank at once; here a bad context list)
+    surfaces as an error on the caller instead of a hang."""
+    rows = mdg.gen_matrix(80, 40, 1, True)
+    d0 = mdg.Device(0)
+    try:
+        with pytest.raises(mdg.InvalidArgument):
+            mdg.min_weight_multi(rows, 80, [d0, d0])  # the same context twice
+        with pytest.raises(mdg.InvalidArgument):
+            mdg.min_weight_multi(rows, 80, [])
+        # the group marker is not a host reducer
+        with pytest.raises(mdg.InvalidArgument):
+            mdg.min_weight_dist(rows, 80, 0, 2, "group", trials=10, seed=1, device=d0)
+        one = mdg.min_weight_multi(rows, 80, [d0], trials=10, seed=1)
+        assert one[0].d == 9
+    finally:
+        d0.close()
+
+
 # ------------------------------------------------------------ brute force
 @pytest.mark.parametrize("kind", ["kats", "seeded"])
 def test_brute_force_vs_reference(mdg, device, kind):
@@ -763,3 +818,37 @@ print(json.dumps(out))
     assert all(x[5] == 1 for x in runs["pos"]) and all(x[5] == 0 for x in runs["find"])
     for a, b in zip(runs["pos"], runs["find"]):
         assert a[:5] == b[:5], (a, b)
+
+
+def test_reference_loop_drives_gpu_round(tmp_path):
+    """INTEGRATION.md §1 built literally (tests/integration/bz_gpu.cpp -> oracle/_ref/bz_gpu):
+    the UNMODIFIED reference's min_weight steps and run_bz_loop (engines.cpp:447-476, linked
+    from oracle/_ref) with the GPU RoundRunner calling mdg_round. Every exact round minimum,
+    U, d and g_final equal the reference's own goldens."""
+    import json
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "oracle", "_ref", "bz_gpu")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/bz_gpu not built (needs /root/reference at build time)")
+    import paper_1911_08963_b200 as mdg
+    cases = [c for c in load_golden("configs") if c["name"] in ("cfg1", "cfg2_s1", "cfg2_s8", "cfg3", "cfg4")]
+    kats = {c["name"]: c for c in load_golden("kats")}
+    for case in cases + [kats["hamming_7_4"], kats["golay_23_12"], kats["ext_golay_24_12"]]:
+        if "gen" in case:
+            g = case["gen"]
+            text = mdg.serialize_matrix(mdg.gen_matrix(g["n"], g["k"], g["seed"], True), g["n"])
+        else:
+            text = case["matrix"]
+        f = tmp_path / f"{case['name']}.txt"
+        f.write_text(text)
+        cmd = [exe, str(f), "--seed", str(case["seed"]), "--trials", str(case["trials"])]
+        if case.get("capped"):
+            cmd += ["--cap", str(case["level_cap"])]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, (case["name"], r.stderr)
+        rec = json.loads(r.stdout)
+        assert rec["rounds"] == case["rounds"], case["name"]
+        assert (rec["m"], rec["k_last"], rec["g_final"]) == (case["m"], case["k_last"], case["g_final"])
+        assert rec["d"] == (case["U_final"] if case.get("capped") else case["d"]), case["name"]

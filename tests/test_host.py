@@ -202,3 +202,28 @@ def test_zero_and_degenerate_inputs(mdg):
         mdg.GammaSet.build(G, 20, 0, 1)
     with pytest.raises(mdg.InvalidArgument):
         mdg.GammaSet.compute(np.zeros((0, 1), dtype=np.uint64), 20)
+
+
+def test_round_split_balances_codewords(mdg):
+    """The multi-rank split of a round (mdg_plan_split, the cut chain_loop / mdg_round_split
+    use): contiguous task ranges covering every task once, their codewords summing to C(k, c),
+    each rank within one tile of 1/world of the codewords -- tiles differ in size (the last
+    pivots' tiles are partial), so a task-count split is not balanced (engines.cpp:508-557
+    splits by combinations for the same reason)."""
+    from math import comb
+    for (k, c, nw, resident) in [(64, 7, 2, 592), (64, 6, 2, 592), (200, 7, 4, 592), (200, 7, 7, 296),
+                                 (200, 5, 4, 296), (32, 9, 7, 296), (100, 5, 8, 592), (40, 3, 2, 592)]:
+        for world in (1, 2, 3, 8):
+            ranges = [mdg.plan_split(k, c, nw, resident, r, world) for r in range(world)]
+            assert ranges[0][0] == 0
+            for a, b in zip(ranges, ranges[1:]):
+                assert a[1] == b[0]
+            assert sum(x[2] for x in ranges) == comb(k, c), (k, c, world)
+            T = ranges[-1][1]
+            tile_max = 256 * 8 * 256  # TX x YC (YC = 256 threads x R <= 8 items)
+            for lo, hi, cw in ranges:
+                assert abs(cw - comb(k, c) / world) <= tile_max, (k, c, nw, world, lo, hi, cw)
+            assert T > 0
+    import pytest
+    with pytest.raises(mdg.InvalidArgument):
+        mdg.plan_split(64, 7, 2, 592, 2, 2)
