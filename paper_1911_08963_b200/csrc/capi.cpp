@@ -9,9 +9,12 @@
 #include <exception>
 #include <thread>
 #include <memory>
+#include <optional>
 #include <sstream>
 #include <string>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "engine.hpp"
 #include "mdg.h"
@@ -54,6 +57,14 @@ struct mdg_run {
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range for the current scope (header-only NVTX3: a no-op unless a profiler is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 template <class F>
 int guard(F&& f) {
@@ -322,13 +333,24 @@ std::unique_ptr<mdg_run> min_weight_device(Engine& eng, const BitMatrix& G, cons
     auto t0 = std::chrono::steady_clock::now();
     auto run = std::make_unique<mdg_run>();
     Engine::Counters c0 = eng.counters();
-    GammaSet gs = cfg.gamma_search == MDG_GAMMA_GPU
-                      ? best_gamma_gpu(eng, row_basis(G), cfg.trials, cfg.seed)
-                      : best_gamma_over_permutations(row_basis(G), cfg.trials, cfg.seed);
+    std::optional<GammaSet> gsearch;
+    {
+        NvtxRange r("mdg gamma search");
+        gsearch.emplace(cfg.gamma_search == MDG_GAMMA_GPU
+                            ? best_gamma_gpu(eng, row_basis(G), cfg.trials, cfg.seed)
+                            : best_gamma_over_permutations(row_basis(G), cfg.trials, cfg.seed));
+    }
+    const GammaSet& gs = *gsearch;
     auto t1 = std::chrono::steady_clock::now();
     run->gamma_s = std::chrono::duration<double>(t1 - t0).count();
-    upload(eng, gs);
-    run_device_loop(eng, gs, cfg, rank, world, reduce, user, *run);
+    {
+        NvtxRange r("mdg upload");
+        upload(eng, gs);
+    }
+    {
+        NvtxRange r("mdg level loop + witness");
+        run_device_loop(eng, gs, cfg, rank, world, reduce, user, *run);
+    }
     Engine::Counters c1 = eng.counters();
     run->cnt.launches = c1.launches - c0.launches;
     run->cnt.h2d = c1.h2d - c0.h2d;

@@ -33,6 +33,7 @@
 //   tables_build       prefix / suffix tables; span_build / span_round: brute force.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -170,6 +171,40 @@ __device__ __forceinline__ uint32_t popsum(const uint32_t (&v)[N]) {
         uint32_t w = __popc(ones);
         if constexpr ((N - 1) % 2 == 1) w += __popc(v[N - 1]);
         return w + 2u * popsum<M>(carries);
+    }
+}
+
+// acc + scale * (sum of the popcounts of N words): the same carry-save chain as popsum, the
+// popcounts combined by multiply-adds whose multipliers are opaque registers (s[0] = scale,
+// s[1] = 2 scale, ...) so ptxas issues them as IMAD on the FMA pipe instead of IADD3 / LEA on
+// the ALU pipe -- the histogram kernel is ALU-bound on its LOP3s (ncu: 85 % busy)
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+template <int N>
+__device__ __forceinline__ uint32_t popsum_mad(const uint32_t (&v)[N], uint32_t acc, const uint32_t* s) {
+    if constexpr (N == 0) {
+        return acc;
+    } else if constexpr (N == 1) {
+        return mad_u32(__popc(v[0]), s[0], acc);
+    } else if constexpr (N == 2) {
+        return mad_u32(__popc(v[1]), s[0], mad_u32(__popc(v[0]), s[0], acc));
+    } else {
+        constexpr int M = (N - 1) / 2;
+        uint32_t carries[M];
+        uint32_t ones = v[0];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const uint32_t b = v[1 + 2 * i], c = v[2 + 2 * i];
+            const uint32_t t = ones ^ b ^ c;
+            carries[i] = (ones & b) | (ones & c) | (b & c);
+            ones = t;
+        }
+        acc = mad_u32(__popc(ones), s[0], acc);
+        if constexpr ((N - 1) % 2 == 1) acc = mad_u32(__popc(v[N - 1]), s[0], acc);
+        return popsum_mad<M>(carries, acc, s + 1);
     }
 }
 
@@ -1385,10 +1420,11 @@ __global__ void __launch_bounds__(kThreads) tab_find(TabArgs a) {
 }
 
 // full weight histogram (config 5): per-warp privatized u32 bins in smem. The lanes past
-// the tile's edge count into a dummy bin (no divergent branch per codeword); the bin
-// address is a 32-bit shared-window offset computed once (a generic pointer costs an S2R
-// and a LEA per increment); the smem bins are flushed into the u64 global histogram before
-// any of them could wrap (a block counts at most 2^32 - 1 codewords between flushes).
+// the tile's edge count into a per-warp scratch copy of the bins (no divergent branch and no
+// select per codeword); the bin address is a 32-bit shared-window offset accumulated by IMADs
+// from the popcounts (popsum_mad: the FMA pipe is idle, the ALU pipe carries the LOP3s); the
+// smem bins are flushed into the u64 global histogram before any could wrap (a block counts
+// at most 2^32 - 1 codewords between flushes).
 template <int NW, bool HID>
 __global__ void __launch_bounds__(kThreads) tab_hist(TabArgs a) {
     constexpr int R = r_for(NW);
@@ -1396,22 +1432,24 @@ __global__ void __launch_bounds__(kThreads) tab_hist(TabArgs a) {
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
     extern __shared__ __align__(16) uint32_t dyn[];
     uint32_t* xs = dyn;
-    const uint32_t bs = a.nbins + 1;  // per-warp stride: the bins and the dummy
-    uint32_t* bins = dyn + a.tx * XS; // kWarps x bs
+    const uint32_t bs = a.nbins;      // per-warp bins, then a per-warp scratch copy
+    uint32_t* bins = dyn + a.tx * XS; // kWarps x 2 x bs
     __shared__ TileInfo ti;
     __shared__ uint32_t flush_now;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t i = threadIdx.x; i < kWarps * bs; i += kThreads) bins[i] = 0;
-    const uint32_t sbase = uint32_t(__cvta_generic_to_shared(bins + warp * bs));
-    const uint32_t add = a.add_const, dummy = a.nbins;
+    for (uint32_t i = threadIdx.x; i < kWarps * 2 * bs; i += kThreads) bins[i] = 0;
+    const uint32_t sreal = uint32_t(__cvta_generic_to_shared(bins + warp * 2 * bs));
+    const uint32_t sjunk = sreal + 4u * bs;
+    uint32_t sc[6] = {4u, 8u, 16u, 32u, 64u, 128u}; // popsum_mad multipliers (bytes per bin << i)
+    asm volatile("" : "+r"(sc[0]), "+r"(sc[1]), "+r"(sc[2]), "+r"(sc[3]), "+r"(sc[4]), "+r"(sc[5]));
     unsigned long long done_local = 0, since_flush = 0; // thread 0
-    auto flush = [&]() { // all threads; bins -> global, zeroed
+    auto flush = [&]() { // all threads; real bins -> global, zeroed
         __syncthreads();
-        for (uint32_t b = threadIdx.x; b < a.nbins; b += kThreads) {
+        for (uint32_t b = threadIdx.x; b < bs; b += kThreads) {
             unsigned long long sum = 0;
             for (int w = 0; w < kWarps; ++w) {
-                sum += bins[w * bs + b];
-                bins[w * bs + b] = 0;
+                sum += bins[w * 2 * bs + b];
+                bins[w * 2 * bs + b] = 0;
             }
             if (sum) atomicAdd(a.hist + b, sum);
         }
@@ -1449,19 +1487,21 @@ __global__ void __launch_bounds__(kThreads) tab_hist(TabArgs a) {
         uint32_t Y[R][NW], idY[R];
         bool valid[R];
         load_suffixes<NW, HID>(a, ti, Y, idY, valid);
-        uint32_t base[R]; // the lane's per-item base: the weight offset, or the dummy bin
+        uint32_t base[R]; // the item's bin row: real bins + weight offset, or the scratch copy
 #pragma unroll
-        for (int r = 0; r < R; ++r) base[r] = valid[r] ? add + (HID ? idY[r] : 0u) : 0u;
+        for (int r = 0; r < R; ++r) base[r] = (valid[r] ? sreal : sjunk) + 4u * (a.add_const + (HID ? idY[r] : 0u));
         __syncthreads();
-        for (uint32_t xi = 0; xi < ti.nx; ++xi) {
+        const uint32_t nx = ti.nx;
+        for (uint32_t xi = 0; xi < nx; ++xi) {
             uint32_t X[XS];
             vload<XS>(xs + xi * XS, X);
-            const uint32_t xid = HID ? X[NW] : 0u;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                uint32_t w = base[r] + xid + xor_weight<0, NW, XS, NW>(X, Y[r]);
-                w = valid[r] ? w : dummy;
-                asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(sbase + 4u * w));
+                uint32_t v[NW];
+#pragma unroll
+                for (int w = 0; w < NW; ++w) v[w] = X[w] ^ Y[r][w];
+                const uint32_t b0 = HID ? mad_u32(X[NW], sc[0], base[r]) : base[r];
+                asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(popsum_mad<NW>(v, b0, sc)));
             }
         }
         __syncthreads();
@@ -2858,7 +2898,7 @@ RoundResult Engine::round_hist(uint32_t j, uint32_t c, uint64_t* hist) {
     // rounds' plan leaves most SMs idle on a config-5 sized round
     const int XSh = stride_for(int(g.nw) + (g.hid ? 1 : 0));
     int hocc = 0;
-    dispatch_nw_hid<HistOcc>(g.nw, g.hid, size_t(kTX) * XSh * 4 + size_t(kWarps) * (nbins + 1) * 4, &hocc);
+    dispatch_nw_hid<HistOcc>(g.nw, g.hid, size_t(kTX) * XSh * 4 + size_t(kWarps) * 2 * nbins * 4, &hocc);
     const PlanEntry& pe = im.plan(k_, c, g, plan_sms_, im.rd, false, /*tpb=*/4, std::max(1, hocc) * sms_);
     uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
     unsigned long long* slot = im.take_slot();
@@ -2869,7 +2909,7 @@ RoundResult Engine::round_hist(uint32_t j, uint32_t c, uint64_t* hist) {
     a.nbins = nbins;
     a.hist = im.hist_dev;
     int XS = stride_for(int(g.nw) + (g.hid ? 1 : 0));
-    size_t dyn = size_t(pe.plan.TX) * XS * 4 + size_t(kWarps) * (nbins + 1) * 4; // + a dummy bin per warp
+    size_t dyn = size_t(pe.plan.TX) * XS * 4 + size_t(kWarps) * 2 * nbins * 4; // bins + scratch per warp
     CK(cudaEventRecord(im.ev0, im.stream));
     dispatch_nw_hid<TabLaunch>(g.nw, g.hid, a, pe.plan.tiles(), im.stream, 2, dyn, sms_);
     CK(cudaGetLastError());
@@ -2948,7 +2988,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
                                        bool allreduce, uint64_t split_min) {
     allreduce = allreduce || world > 1;
     if (allreduce && !impl_->comm && !impl_->group)
-        throw std::logic_error("chain_loop: no NCCL communicator or exchange group attached");
+        throw std::invalid_argument("chain_loop: no NCCL communicator or exchange group attached");
     if (impl_->group && (impl_->group->world != world || impl_->group_rank != rank))
         throw std::invalid_argument("chain_loop: rank / world differ from the attached exchange group");
     CK(cudaSetDevice(device_));
@@ -2992,8 +3032,22 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
     bool done = init.done != 0;
     uint64_t after_round = ~0ull; // launch count right after the last round launch
     bool synced = false;          // a host copy was enqueued since that launch
+    // NVTX: one range per level's host enqueue (header-only NVTX3: no-ops unless a profiler
+    // such as nsys / ncu --nvtx is attached)
+    struct NvtxLevel {
+        bool open = false;
+        void start(uint32_t c) {
+            char name[32];
+            std::snprintf(name, sizeof name, "mdg level %u", c);
+            nvtxRangePushA(name);
+            open = true;
+        }
+        ~NvtxLevel() { if (open) nvtxRangePop(); }
+    };
     while (!done && g <= k_) {
         if (level_cap && g > level_cap) break;
+        NvtxLevel nvtx_level;
+        nvtx_level.start(g);
         bool too_big = g > kMaxC;
         if (!too_big) {
             try { binomial(k_, g); } catch (const std::overflow_error&) { too_big = true; }
