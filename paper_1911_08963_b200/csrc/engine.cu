@@ -448,6 +448,10 @@ struct TabArgs {
                                    //    them with one (row out ^ row in) XOR per step
     uint64_t tile_lo, tile_hi;
     unsigned long long* best_key;
+    unsigned long long* shared_key; // split rounds of an exchange group: the members' common
+                                    // key word (peer memory for members on other devices):
+                                    // every tile result goes there too, every tile fetch polls
+                                    // it -- one rank's find prunes and stops the others
     unsigned long long* evaluated;
     unsigned long long* counter;   // dynamic tile scheduler (next tile - tile_lo)
     unsigned long long* find_out;  // tab_find only
@@ -855,22 +859,54 @@ __device__ __forceinline__ uint32_t tile_min_pruned(const uint32_t* xs, uint32_t
         }
         return best;
     }
-    for (; xi < nx; ++xi) {
-        uint32_t X[XS];
-        vload<XS>(xs + xi * XS, X);
+    // the single-bound vote groups of one smem item (T may drop between groups)
+    auto item_groups = [&](const uint32_t (&X)[XS], const uint32_t (&lb)[R], uint32_t x) {
         // partial identity block: the register item's count starts the popcount sum (one
         // IADD3 with the fold POPCs) and the smem item's comes off the bound once per row
         const int32_t Tx = HID ? T - int32_t(X[NW]) : T;
-        uint32_t lb[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) lb[r] = fold_bound<G, XS, NW, NWF>(X, Y[r], HID ? idY[r] : 0u);
 #pragma unroll
         for (int g0 = 0; g0 < R; g0 += GR) {
             uint32_t gmin = lb[g0];
 #pragma unroll
             for (int r = 1; r < GR; ++r) gmin = min(gmin, lb[g0 + r]);
-            if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= Tx)) group_exact<NW, HID>(X, Y, idY, g0, GR, xi, best, T);
+            if (__any_sync(0xFFFFFFFFu, int32_t(gmin) <= Tx)) group_exact<NW, HID>(X, Y, idY, g0, GR, x, best, T);
         }
+    };
+#ifndef MDG_SINGLE_X2
+#define MDG_SINGLE_X2 1
+#endif
+    if (MDG_SINGLE_X2 && R <= 4) { // R = 8 (NW <= 4): 16 bounds per vote fall through more
+                                   // and the second item's registers cost more than the vote
+                                   // saves (config 4 Gamma_0 level 7: 541 -> 563 ms; Gamma_1,
+                                   // R = 4: 739 -> 707 ms)
+        // two smem items share one warp vote over all their bounds (as the pair path): half
+        // the vote / branch / loop instructions per codeword; a pair the vote cannot reject
+        // takes the per-item groups (T only decreases, so the shared vote is conservative)
+        for (; xi + 1 < nx; xi += 2) {
+            uint32_t X0[XS], X1[XS], l0[R], l1[R];
+            vload<XS>(xs + xi * XS, X0);
+            vload<XS>(xs + (xi + 1) * XS, X1);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                l0[r] = fold_bound<G, XS, NW, NWF>(X0, Y[r], HID ? idY[r] : 0u);
+                l1[r] = fold_bound<G, XS, NW, NWF>(X1, Y[r], HID ? idY[r] : 0u);
+            }
+            uint32_t m0 = l0[0], m1 = l1[0];
+#pragma unroll
+            for (int r = 1; r < R; ++r) m0 = min(m0, l0[r]), m1 = min(m1, l1[r]);
+            const int32_t T0 = HID ? T - int32_t(X0[NW]) : T, T1 = HID ? T - int32_t(X1[NW]) : T;
+            if (__any_sync(0xFFFFFFFFu, int32_t(m0) <= T0 || int32_t(m1) <= T1)) {
+                item_groups(X0, l0, xi);
+                item_groups(X1, l1, xi + 1);
+            }
+        }
+    }
+    for (; xi < nx; ++xi) {
+        uint32_t X[XS], lb[R];
+        vload<XS>(xs + xi * XS, X);
+#pragma unroll
+        for (int r = 0; r < R; ++r) lb[r] = fold_bound<G, XS, NW, NWF>(X, Y[r], HID ? idY[r] : 0u);
+        item_groups(X, lb, xi);
     }
     return best;
 }
@@ -1188,6 +1224,10 @@ __global__ void __launch_bounds__(kThreads, NW <= 2 ? MDG_MINBLK_SMALL : 4) tab_
                     // -- a tile claimed then is simply not evaluated
                     t = a.tile_lo + gridDim.x + atomicAdd(a.counter, 1ull);
                     unsigned long long g = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
+                    if (a.shared_key) {
+                        const unsigned long long sg = *reinterpret_cast<volatile unsigned long long*>(a.shared_key);
+                        g = sg < g ? sg : g;
+                    }
                     gw = uint32_t(g >> kKeyShift);
                     stop = gw <= stop_at || t >= a.tile_hi;
                 }
@@ -1220,6 +1260,10 @@ __global__ void __launch_bounds__(kThreads, NW <= 2 ? MDG_MINBLK_SMALL : 4) tab_
         if (lane == 0 && key != ~0ull) {
             if (key < seen) {
                 unsigned long long old = atomicMin(a.best_key, key);
+                if (a.shared_key) {
+                    const unsigned long long so = atomicMin_system(a.shared_key, key);
+                    old = so < old ? so : old;
+                }
                 seen = old < key ? old : key;
             }
         }
@@ -2099,6 +2143,23 @@ struct ExchangeGroup {
     std::vector<unsigned long long*> slots;
     std::vector<cudaEvent_t> events;
     std::vector<int> devices;
+    // shared round keys (tile results of every member, polled at every tile fetch): a ring on
+    // rank 0's device, entry i % kRing for the i-th split round; rank 0 resets an entry after
+    // the round's exchange (every member's round kernel is then done with it), and stream order
+    // puts that reset before any member's round i + kRing (it follows rank 0's round-(i+1) event)
+    static constexpr uint32_t kRing = 64;
+    unsigned long long* ring = nullptr;
+    int ring_device = -1;
+    bool ring_ok = true; // false: some member pair has no native peer atomics (no shared key)
+    ~ExchangeGroup() {
+        if (ring) {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(ring_device);
+            cudaFree(ring);
+            cudaSetDevice(cur);
+        }
+    }
 
     // publish (slot, ev) of `rank`, wait for every member of this round; copies out all
     void exchange(uint32_t rank, unsigned long long* slot, cudaEvent_t ev,
@@ -2279,6 +2340,7 @@ struct Engine::Impl {
     ncclComm_t comm = nullptr;
     std::shared_ptr<ExchangeGroup> group; // in-process exchange (group_attach)
     uint32_t group_rank = 0;
+    uint64_t group_round = 0;              // split rounds exchanged so far (same on every member)
     cudaEvent_t group_ev = nullptr;
     uint64_t* red_dev = nullptr;
     size_t red_cap = 0;
@@ -3129,6 +3191,8 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
             a.tile_lo = range.first;
             a.tile_hi = range.second;
             a.best_key = slot; a.evaluated = slot + 1; a.counter = slot + 2;
+            if (split && !im.comm && im.group && im.group->ring && im.group->ring_ok) // group: shared key
+                a.shared_key = im.group->ring + im.group_round % ExchangeGroup::kRing;
             const bool fuse = !split && a.tile_hi > a.tile_lo;
             if (fuse) { // the round kernel's last block closes the round: one launch per round
                 a.fin_st = im.d_state;
@@ -3166,6 +3230,12 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
                 group_min<<<1, 32, 0, im.stream>>>(gk, slot);
                 CK(cudaGetLastError());
                 im.cnt.launches += 1;
+                if (im.group->ring) { // rank 0 frees the shared word for round + kRing
+                    if (rank == 0)
+                        CK(cudaMemsetAsync(im.group->ring + im.group_round % ExchangeGroup::kRing, 0xFF,
+                                           sizeof(unsigned long long), im.stream));
+                    ++im.group_round;
+                }
                 synced = true; // the next round must not overlap the exchange (no PDL)
             }
             if (!fuse) {
@@ -3341,6 +3411,9 @@ void Engine::group_attach(std::shared_ptr<ExchangeGroup> g, uint32_t rank) {
             CK(cudaDeviceCanAccessPeer(&can, device_, d));
             if (!can) throw std::invalid_argument("group_attach: devices " + std::to_string(device_) + " and " +
                                                   std::to_string(d) + " have no peer access");
+            int atomics = 0; // the shared round key needs native peer atomics (NVLink)
+            CK(cudaDeviceGetP2PAttribute(&atomics, cudaDevP2PAttrNativeAtomicSupported, device_, d));
+            if (!atomics) g->ring_ok = false;
             for (auto [from, to] : {std::make_pair(device_, d), std::make_pair(d, device_)}) {
                 CK(cudaSetDevice(from));
                 cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
@@ -3350,9 +3423,15 @@ void Engine::group_attach(std::shared_ptr<ExchangeGroup> g, uint32_t rank) {
             CK(cudaSetDevice(device_));
         }
         g->devices.push_back(device_);
+        if (rank == 0 && !g->ring && !std::getenv("MDG_NO_SHARED_BOUND")) {
+            CK(cudaMalloc(&g->ring, ExchangeGroup::kRing * sizeof(unsigned long long)));
+            CK(cudaMemset(g->ring, 0xFF, ExchangeGroup::kRing * sizeof(unsigned long long)));
+            g->ring_device = device_;
+        }
     }
     im.group = std::move(g);
     im.group_rank = rank;
+    im.group_round = 0;
 }
 
 void Engine::nccl_unique_id(uint8_t id[128]) {

@@ -313,15 +313,22 @@ def test_dist_two_ranks_threaded(mdg):
             assert calls == [0, 0]  # cfg2 seed 8 never reaches 2e8-codeword rounds
 
 
+@pytest.mark.parametrize("shared", [True, False])
 @pytest.mark.parametrize("world", [2, 3])
-def test_min_weight_multi_group_split(mdg, world):
+def test_min_weight_multi_group_split(mdg, world, shared, monkeypatch):
     """The chained split path (each rank's contiguous tile range of every round of at least
     split_min codewords, the per-round key min-reduced IN STREAM before the round closes --
     the production multi-GPU path, here with the in-process exchange group instead of NCCL:
     cudaStreamWaitEvent on the members' round events, then a min kernel; no kernel waits on
     another) with `world` contexts on one GPU: d, per-round and per-level trace, Gamma set and
     witness equal the golden on every rank; the ranks' evaluated counts add up to the
-    single-rank count of the split rounds; levels below split_min still run fused."""
+    single-rank count of the split rounds; levels below split_min still run fused. `shared`:
+    the members also share one round key word that every tile result goes to and every tile
+    fetch polls (one rank's find prunes the others' tiles); MDG_NO_SHARED_BOUND turns it off."""
+    if shared:
+        monkeypatch.delenv("MDG_NO_SHARED_BOUND", raising=False)
+    else:
+        monkeypatch.setenv("MDG_NO_SHARED_BOUND", "1")
     devs = [mdg.Device(0) for _ in range(world)]
     cases = {c["name"]: c for c in load_golden("configs")}
     cases["cfg4_cap6"] = next(c for c in load_golden("configs_cap4_6") if c["name"] == "cfg4")
@@ -468,18 +475,20 @@ def test_cli_json_record(mdg, tmp_path):
     assert [x["d"] for x in recs] == [c["d"] for _, c in files]
 
 
-def test_cfg4_cap7_engines_agree(mdg, device):
-    """Config 4 to level cap 7 (4.7e12 codewords; no reference golden — the reference
-    needs ~1 h on 16 cores): the tab engine (bound-pruned) and the revolving-door engine
-    (exact weights, independent enumeration order) give the same (L, U) trace."""
-    G = mdg.gen_matrix(300, 200, 11, True)
-    a = mdg.min_weight(G, 300, 10, 11, level_cap=7, kernel=mdg.KERNEL_TAB, device=device)
-    b = mdg.min_weight(G, 300, 10, 11, level_cap=7, kernel=mdg.KERNEL_RD, device=device)
-    assert a.capped and b.capped and a.d == b.d
-    assert a.levels == b.levels and a.rounds == b.rounds
-    assert a.witness_ok and b.witness_ok
-    cap6 = next(c for c in load_golden("configs_cap4_6") if c["name"] == "cfg4")
-    assert a.levels[:6] == cap6["levels"]
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_cfg4_cap7_vs_reference(mdg, device, kernel):
+    """Config 4 to level cap 7 (4.7e12 codewords, BASELINE.md's throughput and scaling case)
+    against the REFERENCE: tests/golden/configs_cap4_7.json is the reference's own cap-6 trace
+    extended by its level-7 rounds, each computed by the reference's scheduled_round on the
+    reference-built Gamma matrices (oracle/make_cfg4_c7.py, ~2 h on 8 cores). Both kernels
+    (tab: bound-pruned prefix-sum tiles; rd: revolving-door walk) give its bounded-round trace,
+    (L, U) levels and Gamma set; the witness is verified."""
+    case = next(c for c in load_golden("configs_cap4_7") if c["name"] == "cfg4")
+    g = case["gen"]
+    G = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
+    r = mdg.min_weight(G, g["n"], 10, g["seed"], level_cap=7, kernel=kernel, device=device)
+    assert r.capped and r.d == case["U_final"]
+    _check_run(r, case, f"cfg4_cap7 kernel={kernel}", exact=False)
 
 
 @pytest.mark.gpu

@@ -5,7 +5,11 @@
 // Each kernel runs NCH independent dependency chains per thread of a single
 // instruction class, long enough that issue throughput (not latency) binds.
 // ops/clk/SM = (threads * iters * NCH) / (elapsed_s * f_sm * SMs), with f_sm
-// measured in-kernel from clock64() against the CUDA-event wall time.
+// measured in-kernel: clock64() is a per-SM counter, so the span from the first
+// block start to the last block end ON ONE SM (blocks run in several waves) over the
+// CUDA-event wall time. (Round 1 divided block 0's span alone by the wall time: block 0
+// ran one of four waves, which gave f ~ 485 MHz and 4x inflated per-clock rates; its
+// Gops column was right.)
 //
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o pipes tools/pipes_microbench.cu
 #include <cstdio>
@@ -15,7 +19,8 @@
 #define NCH 16
 
 __device__ unsigned long long g_sink;
-__device__ long long g_clk[2048];
+__device__ long long g_clk[2 * 4096];
+__device__ unsigned g_smid[4096];
 
 template <int OP>
 __global__ void pipe_kernel(uint32_t seed, int iters) {
@@ -63,7 +68,13 @@ __global__ void pipe_kernel(uint32_t seed, int iters) {
 #pragma unroll
     for (int i = 0; i < NCH; ++i) acc ^= a[i];
     if (acc == 0xFFFFFFFFu) g_sink = acc;
-    if (threadIdx.x == 0 && blockIdx.x < 2048) g_clk[blockIdx.x] = t1 - t0;
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_clk[2 * blockIdx.x] = t0;
+        g_clk[2 * blockIdx.x + 1] = t1;
+        g_smid[blockIdx.x] = smid;
+    }
 }
 
 template <int OP>
@@ -78,9 +89,17 @@ void run(const char* name, int sms) {
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
-    long long clk[1];
-    cudaMemcpyFromSymbol(clk, g_clk, sizeof(long long));
-    double f_mhz = clk[0] / (ms * 1e3); // lower bound on clock (block 0 ran ~whole kernel)
+    static long long clk[2 * 4096];
+    static unsigned smid[4096];
+    cudaMemcpyFromSymbol(clk, g_clk, sizeof(long long) * 2 * blocks);
+    cudaMemcpyFromSymbol(smid, g_smid, sizeof(unsigned) * blocks);
+    long long lo = -1, hi = -1; // first start .. last end of the blocks on block 0's SM
+    for (int b = 0; b < blocks; ++b)
+        if (smid[b] == smid[0]) {
+            if (lo < 0 || clk[2 * b] < lo) lo = clk[2 * b];
+            if (hi < 0 || clk[2 * b + 1] > hi) hi = clk[2 * b + 1];
+        }
+    double f_mhz = double(hi - lo) / (ms * 1e3); // the timed loop spans ~the whole kernel
     double ops = (double)threads * blocks * iters * NCH;
     double per_clk_sm = ops / (ms * 1e-3) / (f_mhz * 1e6) / sms;
     printf("{\"op\": \"%s\", \"ms\": %.3f, \"f_mhz_est\": %.0f, \"ops_per_clk_per_sm\": %.2f, \"Gops\": %.1f}\n",

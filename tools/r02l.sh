@@ -1,0 +1,8 @@
+# single-bound two-item vote (MDG_SINGLE_X2): config-4 level-7 rounds, bench, tests
+export PYTHONUNBUFFERED=1
+O=gpurun_out
+python tools/ncu_target.py --n 300 --k 200 --seed 11 --c 7 --j 0 --cutoff 24 --reps 2 > $O/r02l_c7j0.log 2>&1
+python tools/ncu_target.py --n 300 --k 200 --seed 11 --c 7 --j 1 --cutoff 23 --reps 2 > $O/r02l_c7j1.log 2>&1
+python tools/ncu_target.py --n 256 --k 32 --seed 7 --c 9 --j 0 --cutoff 77 --reps 3 > $O/r02l_cfg3_c9.log 2>&1
+timeout 600 python bench.py --no-cpu-baseline > $O/r02l_bench.json 2> $O/r02l_bench.err; echo bench=$?
+timeout 1500 python -m pytest tests -m gpu -x -q > $O/r02l_pytest.log 2>&1; echo pytest=$?
