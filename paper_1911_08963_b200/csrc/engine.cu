@@ -2872,14 +2872,15 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
 }
 
 static TabArgs tab_args(Engine::Impl& im, const GammaDev& g, const PlanEntry& pe, uint32_t* yt,
-                        uint32_t k, uint32_t c) {
+                        uint32_t k, uint32_t c, bool want_fold = true) {
     TabArgs a{};
     a.rows = g.rows; a.ytab = yt; a.binom = im.binom; a.prefix = pe.d_prefix; a.tr = pe.d_tr;
     a.k = k; a.p = pe.plan.p; a.s = pe.plan.s; a.emin = pe.plan.emin;
     a.npiv = uint32_t(pe.plan.prefix.size() - 1);
     a.id_rows = g.id_rows; a.add_const = (g.id_rows == k) ? c : 0; a.tx = pe.plan.TX;
-    a.fold = sampled_fold_plan(im, uint32_t(&g - im.gammas.data()), k, c);
-    if (!im.prune) // exact weights only
+    if (want_fold) // (the histogram kernel weighs everything: no stage-1 plan to sample)
+        a.fold = sampled_fold_plan(im, uint32_t(&g - im.gammas.data()), k, c);
+    if (!im.prune || !want_fold) // exact weights only
         std::memset(a.fold.code, 0, sizeof a.fold.code);
     a.rd = pe.plan.rd ? 1u : 0u;
     static const bool no_pos = std::getenv("MDG_NO_POS_KEY") != nullptr; // tests: the tab_find path
@@ -2961,11 +2962,15 @@ RoundResult Engine::round_hist(uint32_t j, uint32_t c, uint64_t* hist) {
     const int XSh = stride_for(int(g.nw) + (g.hid ? 1 : 0));
     int hocc = 0;
     dispatch_nw_hid<HistOcc>(g.nw, g.hid, size_t(kTX) * XSh * 4 + size_t(kWarps) * 2 * nbins * 4, &hocc);
-    const PlanEntry& pe = im.plan(k_, c, g, plan_sms_, im.rd, false, /*tpb=*/4, std::max(1, hocc) * sms_);
+    static const uint32_t kHistTpb = [] { // tiles per resident block (MDG_HIST_TPB, tuning)
+        const char* e = std::getenv("MDG_HIST_TPB");
+        return e ? uint32_t(std::max(1, std::atoi(e))) : 4u;
+    }();
+    const PlanEntry& pe = im.plan(k_, c, g, plan_sms_, im.rd, false, kHistTpb, std::max(1, hocc) * sms_);
     uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
     unsigned long long* slot = im.take_slot();
     CK(cudaMemsetAsync(im.hist_dev, 0, nbins * 8, im.stream));
-    TabArgs a = tab_args(im, g, pe, yt, k_, c);
+    TabArgs a = tab_args(im, g, pe, yt, k_, c, /*want_fold=*/false);
     a.tile_lo = 0; a.tile_hi = pe.plan.tiles();
     a.evaluated = slot + 1; a.counter = slot + 2;
     a.nbins = nbins;

@@ -4,6 +4,7 @@
 // (cli.cpp:223-238) plus the new keys (witness, trace, levels, capped, ...).
 // Exit codes as the reference: 0 ok, 1 internal error, 2 invalid input or
 // config (cli.cpp:198-219).
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -19,7 +20,8 @@ namespace {
 int usage() {
     std::cerr << "usage:\n"
                  "  mindist mindist FILE [FILE ...] [--algorithm gpu|brute] [--kernel tab|rd] [--trials T]\n"
-                 "                       [--seed S] [--level-cap C] [--device D] [--exact-rounds]\n"
+                 "                       [--seed S] [--level-cap C] [--device D] [--devices D0,D1,..]\n"
+                 "                       [--split-min N] [--exact-rounds]\n"
                  "                       [--gamma-search host|gpu] [--pretty]\n"
                  "    accepted for the reference's command line (cli.cpp:264-277), validated as there\n"
                  "    and not used by the GPU engine: --algorithm basic|optimized|stack|saved|\n"
@@ -78,6 +80,7 @@ int main(int argc, char** argv) {
     mdg_config_default(&cfg);
     bool pretty = false;
     int device = 0;
+    std::vector<int> devices; // --devices: one process, several contexts (mdg_min_weight_multi)
     bool seed_given = false;
     bool brute = false;
     bool workers_given = false;
@@ -138,6 +141,19 @@ int main(int argc, char** argv) {
             cfg.level_cap = uint32_t(x);
         } else if (a == "--device" && parse_u64(v.c_str(), x)) {
             device = int(x);
+        } else if (a == "--devices") { // comma-separated CUDA devices (repeats allowed)
+            size_t p0 = 0;
+            while (p0 <= v.size()) {
+                const size_t p1 = std::min(v.find(',', p0), v.size());
+                if (!parse_u64(v.substr(p0, p1 - p0).c_str(), x)) {
+                    std::cerr << "error: bad option --devices " << v << "\n";
+                    return 2;
+                }
+                devices.push_back(int(x));
+                p0 = p1 + 1;
+            }
+        } else if (a == "--split-min" && parse_u64(v.c_str(), x)) {
+            cfg.split_min = x;
         } else {
             std::cerr << "error: bad option " << a << " " << v << "\n";
             return 2;
@@ -174,11 +190,30 @@ int main(int argc, char** argv) {
             return 2;
         }
     }
+    if (devices.size() > 1 && (brute || paths.size() > 1)) {
+        std::cerr << "error: --devices splits the rounds of ONE code (no --algorithm brute, one FILE)\n";
+        return 2;
+    }
     mdg_ctx* ctx = nullptr;
-    int rc = mdg_open(device, &ctx);
+    int rc = mdg_open(devices.empty() ? device : devices[0], &ctx);
     if (rc) return exit_code(rc);
     std::vector<mdg_run*> runs(paths.size(), nullptr);
-    if (brute) {
+    if (devices.size() > 1) { // rounds split across the contexts; rank 0's record is printed
+        std::vector<mdg_ctx*> ctxs{ctx};
+        for (size_t i = 1; i < devices.size() && rc == 0; ++i) {
+            mdg_ctx* c = nullptr;
+            rc = mdg_open(devices[i], &c);
+            if (rc == 0) ctxs.push_back(c);
+        }
+        std::vector<mdg_run*> all(ctxs.size(), nullptr);
+        if (rc == 0)
+            rc = mdg_min_weight_multi(ctxs.data(), uint32_t(ctxs.size()), Gs[0].data(), Gs[0].rows(),
+                                      Gs[0].cols(), &cfg, all.data());
+        for (size_t i = 1; i < all.size(); ++i)
+            if (all[i]) mdg_run_free(all[i]);
+        for (size_t i = 1; i < ctxs.size(); ++i) mdg_close(ctxs[i]);
+        runs[0] = all[0];
+    } else if (brute) {
         for (size_t f = 0; f < paths.size() && rc == 0; ++f)
             rc = mdg_brute_force(ctx, Gs[f].data(), Gs[f].rows(), Gs[f].cols(), 40, &runs[f]);
     } else if (paths.size() == 1) {

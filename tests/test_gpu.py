@@ -861,3 +861,27 @@ def test_reference_loop_drives_gpu_round(tmp_path):
         assert rec["rounds"] == case["rounds"], case["name"]
         assert (rec["m"], rec["k_last"], rec["g_final"]) == (case["m"], case["k_last"], case["g_final"])
         assert rec["d"] == (case["U_final"] if case.get("capped") else case["d"]), case["name"]
+
+
+def test_cli_devices_split(mdg, tmp_path):
+    """`mindist mindist FILE --devices 0,0 --split-min 1`: one process, two contexts (here on
+    the same GPU), every round split across them through the exchange group; the record has
+    the golden d / trace / levels and "devices": 2."""
+    import json
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "paper_1911_08963_b200", "bin", "mindist")
+    case = next(c for c in load_golden("configs") if c["name"] == "cfg2_s8")
+    g = case["gen"]
+    f = tmp_path / "cfg2_s8.txt"
+    f.write_text(mdg.serialize_matrix(mdg.gen_matrix(g["n"], g["k"], g["seed"], True), g["n"]))
+    r = subprocess.run([exe, "mindist", str(f), "--seed", str(g["seed"]), "--devices", "0,0",
+                        "--split-min", "1"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    rec = json.loads(r.stdout)
+    assert rec["d"] == case["d"] and rec["devices"] == 2 and rec["witness_ok"]
+    assert rec["levels"] == case["levels"]
+    r = subprocess.run([exe, "mindist", str(f), str(f), "--devices", "0,0", "--seed", "1"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2 and "--devices" in r.stderr
