@@ -373,8 +373,10 @@ static uint32_t shape_words(uint32_t k) {
     return kw <= 4 ? kw : kw <= 8 ? 8 : kw <= 16 ? 16 : kw <= 32 ? 32 : (kw + 63) / 64 * 64;
 }
 
+// `order` is left in the column order compute_gamma_matrices ends with on it (its pivot
+// column swaps, applied in the same sequence)
 static std::pair<uint32_t, uint32_t> block_shape(const std::vector<uint64_t>& cols, uint32_t KW, uint32_t n,
-                                                 uint32_t k, std::vector<uint32_t> order) {
+                                                 uint32_t k, std::vector<uint32_t>& order) {
     switch (KW) {
         case 1: return block_shape_w<1>(cols.data(), n, k, order);
         case 2: return block_shape_w<2>(cols.data(), n, k, order);
@@ -478,7 +480,7 @@ GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint6
             perms.push_back(std::move(perm));
             mk.emplace_back(0, 0);
         }
-        std::function<void(uint32_t)> work = [&](uint32_t i) {
+        std::function<void(uint32_t)> work = [&](uint32_t i) { // perms[t] -> its final order
             mk[t0 + i] = block_shape(cols, KW, n, k, perms[t0 + i]);
         };
         if (pool && t1 - t0 >= 8)
@@ -492,6 +494,10 @@ GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint6
                 win = t;
             }
     }
+    // the winner is systematized on its FINAL column order (block_shape applied the pivot swaps):
+    // every block's pivots are then in place, so gamma_blocks does no column swaps (each one
+    // costs a pass over all rows of the matrix and of every earlier snapshot) -- the same Gamma
+    // set and column_perm as systematizing the trial order itself
     GammaSet cand = win < 0 ? compute_gamma_matrices(G) : gamma_for_permutation(G, perms[size_t(win)]);
     if (cand.m() != bm || cand.k_last != bk)
         throw std::logic_error("best_gamma_over_permutations: block scan disagrees with the systematization");

@@ -885,3 +885,49 @@ def test_cli_devices_split(mdg, tmp_path):
     r = subprocess.run([exe, "mindist", str(f), str(f), "--devices", "0,0", "--seed", "1"],
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 2 and "--devices" in r.stderr
+
+
+def test_group_abi_driven_by_caller(mdg):
+    """The exchange group through its own C ABI (mdg_group_create / mdg_group_attach /
+    mdg_group_reduce_min): the caller drives each member from its own thread with
+    mdg_min_weight_dist(..., reduce_min = mdg_group_reduce_min); every member's record equals
+    the golden, and detaching restores single-context runs."""
+    import ctypes as C
+    import threading
+    case = next(c for c in load_golden("configs") if c["name"] == "cfg2_s1")
+    g = case["gen"]
+    G = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
+    world = 2
+    devs = [mdg.Device(0) for _ in range(world)]
+    grp = C.c_void_p()
+    L = mdg.lib()
+    assert L.mdg_group_create(world, C.byref(grp)) == 0
+    try:
+        for r, d in enumerate(devs):
+            assert L.mdg_group_attach(d.handle, grp, r) == 0
+        out = [None] * world
+        errs = []
+
+        def member(r):
+            try:
+                out[r] = mdg.min_weight_dist(G, g["n"], r, world, "group", trials=10, seed=g["seed"],
+                                             device=devs[r], split_min=1)
+            except Exception as e:  # surfaced below
+                errs.append(e)
+
+        ts = [threading.Thread(target=member, args=(r,)) for r in range(world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join(timeout=300)
+        assert not errs, errs
+        for r in range(world):
+            _check_run(out[r], case, f"group rank {r}", exact=False)
+        for d in devs:
+            assert L.mdg_group_attach(d.handle, None, 0) == 0
+        solo = mdg.min_weight(G, g["n"], 10, g["seed"], device=devs[0])
+        _check_run(solo, case, "after detach", exact=False)
+    finally:
+        L.mdg_group_free(grp)
+        for d in devs:
+            d.close()
