@@ -43,9 +43,10 @@ def main():
     dev = mdg.Device(0)
     out = {"device": "B200", "rows": []}
     cfgs = {c["name"]: c for c in gold("configs")}
-    cap6 = {}
-    if os.path.exists(os.path.join(GOLD, "configs_cap4_6.json")):
-        cap6 = {c["name"]: c for c in gold("configs_cap4_6")}
+    capped = {}
+    for cap in (6, 7):
+        if os.path.exists(os.path.join(GOLD, f"configs_cap4_{cap}.json")):
+            capped[cap] = {c["name"]: c for c in gold(f"configs_cap4_{cap}")}.get("cfg4")
     for name in ["cfg1"] + [f"cfg2_s{s}" for s in range(1, 9)] + ["cfg3"]:
         c = cfgs[name]
         g = c["gen"]
@@ -63,7 +64,7 @@ def main():
     c4 = cfgs["cfg4"]
     for cap in sorted({5, 6, a.cap4}):
         r, wall = run_code(dev, 300, 200, 11, cap, False, reps=1 if cap >= 7 else 2)
-        ref = c4 if cap == 5 else cap6.get("cfg4") if cap == 6 else None
+        ref = c4 if cap == 5 else capped.get(cap)
         ok = None if ref is None else (r.d == ref["U_final"] and r.levels == ref["levels"])
         out["rows"].append({
             "config": f"cfg4_cap{cap}", "mode": "bounded", "U_at_cap": r.d, "capped": r.capped,
@@ -114,6 +115,14 @@ def main():
                         "flavor": "v3", "threads": 1, "seconds": dt, "codewords": tot_cw,
                         "cw_per_s": 2 * tot_cw / dt})
             print(json.dumps(cpu[-1]), flush=True)
+            c7 = capped.get(7)
+            if c7 and "level7_rounds" in c7: # measured while pinning (oracle/make_cfg4_c7.py)
+                for j, v in sorted(c7["level7_rounds"].items()):
+                    cpu.append({"config": f"cfg4 level-7 round j={j}", "engine": v["engine"],
+                                "flavor": "v3", "threads": "see engine", "seconds": v["seconds"],
+                                "codewords": v["combinations"],
+                                "cw_per_s": v["combinations"] / v["seconds"],
+                                "where": "the dev container (8 vCPU), not the B200 box"})
             out["cpu_reference"] = cpu
     out["cpu"] = subprocess.run(["bash", "-c", "lscpu | grep 'Model name'; nproc"], capture_output=True,
                                 text=True).stdout
