@@ -1470,7 +1470,10 @@ __global__ void __launch_bounds__(kThreads) tab_find(TabArgs a) {
 // smem bins are flushed into the u64 global histogram before any could wrap (a block counts
 // at most 2^32 - 1 codewords between flushes).
 template <int NW, bool HID>
-__global__ void __launch_bounds__(kThreads) tab_hist(TabArgs a) {
+#ifndef MDG_HIST_MINBLK
+#define MDG_HIST_MINBLK 1
+#endif
+__global__ void __launch_bounds__(kThreads, MDG_HIST_MINBLK) tab_hist(TabArgs a) {
     constexpr int R = r_for(NW);
     constexpr int YC = R * kThreads;
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));

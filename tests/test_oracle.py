@@ -84,3 +84,23 @@ def test_lower_bound_spot_values():
     assert port.lib().mdo_singleton_upper(7, 4) == 4
     assert port.lib().mdo_singleton_upper(23, 12) == 12
     assert port.lib().mdo_singleton_upper(5, 5) == 1
+
+
+def test_cfg4_cap7_golden_consistent():
+    """configs_cap4_7.json (the reference's cap-6 trace + its level-7 rounds, oracle/
+    make_cfg4_c7.py) extends configs_cap4_6.json exactly, and its level-7 (L, U) entry is the
+    run_bz_loop replay (engines.cpp:447-476) with the oracle's lower_bound (gamma.cpp:96-100);
+    the Gamma set is the one the oracle restatement builds from the config-4 input."""
+    c6 = next(c for c in load_golden("configs_cap4_6") if c["name"] == "cfg4")
+    c7 = next(c for c in load_golden("configs_cap4_7") if c["name"] == "cfg4")
+    assert c7["rounds"][:len(c6["rounds"])] == c6["rounds"]
+    assert c7["levels"][:len(c6["levels"])] == c6["levels"]
+    assert c7["gamma_hash"] == c6["gamma_hash"] and c7["column_perm"] == c6["column_perm"]
+    U, L = c6["U_final"], c6["L_final"]
+    for j in range(c7["m"]):
+        w = c7["level7_rounds"][str(j)]["w"]
+        assert c7["level7_rounds"][str(j)]["combinations"] == 2283896214600  # C(200, 7)
+        U = min(U, w)
+        assert c7["rounds"][len(c6["rounds"]) + j] == [7, j, w, U]
+    L = max(L, int(port.lib().mdo_lower_bound(c7["m"], 7, c7["k"], c7["k_last"])))
+    assert c7["levels"][-1] == [7, L, U] and (U, L) == (c7["U_final"], c7["L_final"]) == (22, 8)
