@@ -2134,9 +2134,10 @@ constexpr int kNcclMin = 3;    // ncclMin
 // Members whose enqueue decisions diverge (a bug: the loop is deterministic) time out.
 struct ExchangeGroup {
     explicit ExchangeGroup(uint32_t world, double timeout_s)
-        : world(world), timeout_s(timeout_s), slots(world, nullptr), events(world, nullptr) {}
+        : world(world), timeout_s(timeout_s), slots(world, nullptr), events(world, nullptr),
+          tags(world, 0), loops(world, 0), left(world, 0) {}
     const uint32_t world;
-    const double timeout_s;
+    const double timeout_s; // <= 0: wait as long as the other members run (a split round may take hours)
     std::mutex mu;
     std::condition_variable cv;
     uint64_t generation = 0;
@@ -2145,6 +2146,9 @@ struct ExchangeGroup {
     std::string why;
     std::vector<unsigned long long*> slots;
     std::vector<cudaEvent_t> events;
+    std::vector<uint64_t> tags;  // (c << 32 | j) of the split round each member arrived with
+    std::vector<uint64_t> loops; // level loops each member has entered
+    std::vector<uint64_t> left;  // the last loop each member has left
     std::vector<int> devices;
     // shared round keys (tile results of every member, polled at every tile fetch): a ring on
     // rank 0's device, entry i % kRing for the i-th split round; rank 0 resets an entry after
@@ -2163,25 +2167,58 @@ struct ExchangeGroup {
             cudaSetDevice(cur);
         }
     }
+    void fail(const std::string& reason) { // with mu held
+        if (!aborted) why = reason;
+        aborted = true;
+        cv.notify_all();
+    }
+    // a member starts / ends a level loop: a member still waiting for the others at a split
+    // round of loop L while one of them has left loop L has diverged (it enqueued a split round
+    // the other never will) -- fail at once instead of waiting forever
+    void enter(uint32_t rank) {
+        std::lock_guard<std::mutex> lk(mu);
+        ++loops[rank];
+    }
+    void leave(uint32_t rank) {
+        std::lock_guard<std::mutex> lk(mu);
+        left[rank] = loops[rank];
+        cv.notify_all();
+    }
 
-    // publish (slot, ev) of `rank`, wait for every member of this round; copies out all
-    void exchange(uint32_t rank, unsigned long long* slot, cudaEvent_t ev,
+    // publish (slot, ev) of `rank` for split round (c, j), wait for every member of this round;
+    // copies out all. Members must arrive with the same (c, j): their enqueue sequences are
+    // identical by construction, so a mismatch is a bug -- fail loudly.
+    void exchange(uint32_t rank, uint32_t c, uint32_t j, unsigned long long* slot, cudaEvent_t ev,
                   std::vector<unsigned long long*>& all_slots, std::vector<cudaEvent_t>& all_events) {
         std::unique_lock<std::mutex> lk(mu);
         if (aborted) throw std::runtime_error("exchange group aborted: " + why);
         slots[rank] = slot;
         events[rank] = ev;
-        const uint64_t gen = generation;
+        tags[rank] = (uint64_t(c) << 32) | j;
+        const uint64_t gen = generation, loop = loops[rank];
+        auto departed = [&] {
+            for (uint32_t r = 0; r < world; ++r)
+                if (r != rank && left[r] == loop && loops[r] == loop) return true;
+            return false;
+        };
         if (++arrived == world) {
             arrived = 0;
             ++generation;
+            for (uint32_t r = 0; r < world; ++r)
+                if (tags[r] != tags[rank])
+                    fail("members diverged: rank " + std::to_string(r) + " is at another split round");
             cv.notify_all();
-        } else if (!cv.wait_for(lk, std::chrono::duration<double>(timeout_s),
-                                [&] { return generation != gen || aborted; })) {
-            aborted = true;
-            why = "member " + std::to_string(rank) + " timed out at a split round (diverged loop?)";
-            cv.notify_all();
-            throw std::runtime_error("exchange group: " + why);
+        } else {
+            auto ready = [&] { return generation != gen || aborted || departed(); };
+            if (timeout_s > 0) {
+                if (!cv.wait_for(lk, std::chrono::duration<double>(timeout_s), ready))
+                    fail("member " + std::to_string(rank) + " timed out at a split round");
+            } else {
+                cv.wait(lk, ready);
+            }
+            if (generation == gen && !aborted)
+                fail("members diverged: a member left the level loop while rank " + std::to_string(rank) +
+                     " waits at a split round");
         }
         if (aborted) throw std::runtime_error("exchange group aborted: " + why);
         all_slots = slots;
@@ -2189,15 +2226,17 @@ struct ExchangeGroup {
     }
     void abort(const std::string& reason) {
         std::lock_guard<std::mutex> lk(mu);
-        if (!aborted) why = reason;
-        aborted = true;
-        cv.notify_all();
+        fail(reason);
     }
 };
 
 std::shared_ptr<ExchangeGroup> make_exchange_group(uint32_t world, double timeout_s) {
     if (world < 1 || world > uint32_t(kMaxGroup))
         throw std::invalid_argument("exchange group: 1 <= world <= 16");
+    if (timeout_s < 0) { // default: MDG_GROUP_TIMEOUT seconds, else no timeout
+        const char* e = std::getenv("MDG_GROUP_TIMEOUT");
+        timeout_s = e ? std::atof(e) : 0.0;
+    }
     return std::make_shared<ExchangeGroup>(world, timeout_s);
 }
 void abort_exchange_group(ExchangeGroup& g, const std::string& reason) { g.abort(reason); }
@@ -3061,6 +3100,12 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
         throw std::invalid_argument("chain_loop: no NCCL communicator or exchange group attached");
     if (impl_->group && (impl_->group->world != world || impl_->group_rank != rank))
         throw std::invalid_argument("chain_loop: rank / world differ from the attached exchange group");
+    struct GroupLoop { // enter / leave the group's level loop (see ExchangeGroup::enter)
+        ExchangeGroup* g;
+        uint32_t r;
+        GroupLoop(ExchangeGroup* g, uint32_t r) : g(g), r(r) { if (g) g->enter(r); }
+        ~GroupLoop() { if (g) g->leave(r); }
+    } group_loop(allreduce && !impl_->comm ? impl_->group.get() : nullptr, rank);
     CK(cudaSetDevice(device_));
     Impl& im = *impl_;
     // host work per check: ~2e8 codewords (~0.1 ms of device time) between looks at `done`
@@ -3228,7 +3273,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
                 CK(cudaEventRecord(im.group_ev, im.stream));
                 std::vector<unsigned long long*> all;
                 std::vector<cudaEvent_t> evs;
-                im.group->exchange(rank, slot, im.group_ev, all, evs);
+                im.group->exchange(rank, g, j, slot, im.group_ev, all, evs);
                 GroupKeys gk{};
                 gk.n = world;
                 for (uint32_t r = 0; r < world; ++r) {

@@ -70,7 +70,8 @@ struct TabPlan {
 // In-process exchange group (engine.cu): `world` engines in one process reduce each split
 // round's key through stream-ordered events and a min kernel instead of NCCL.
 struct ExchangeGroup;
-std::shared_ptr<ExchangeGroup> make_exchange_group(uint32_t world, double timeout_s = 120.0);
+// timeout_s < 0: MDG_GROUP_TIMEOUT seconds if set, else none (0 = none)
+std::shared_ptr<ExchangeGroup> make_exchange_group(uint32_t world, double timeout_s = -1.0);
 void abort_exchange_group(ExchangeGroup& g, const std::string& reason);
 
 class Engine {

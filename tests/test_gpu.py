@@ -931,3 +931,43 @@ def test_group_abi_driven_by_caller(mdg):
         L.mdg_group_free(grp)
         for d in devs:
             d.close()
+
+
+def test_group_divergence_fails_fast(mdg):
+    """Members whose level loops diverge (here: different split_min, so they enqueue different
+    split rounds) fail with an error instead of hanging: a (c, j) mismatch at a barrier, or a
+    member leaving the loop while another waits at a split round."""
+    import ctypes as C
+    import threading
+    import time
+    G = mdg.gen_matrix(128, 64, 1, True)
+    L = mdg.lib()
+    for mins in ((1, 10**6), (1, 1 << 62)):
+        devs = [mdg.Device(0) for _ in range(2)]
+        grp = C.c_void_p()
+        assert L.mdg_group_create(2, C.byref(grp)) == 0
+        results = [None, None]
+        try:
+            for r, d in enumerate(devs):
+                assert L.mdg_group_attach(d.handle, grp, r) == 0
+
+            def member(r):
+                try:
+                    results[r] = mdg.min_weight_dist(G, 128, r, 2, "group", trials=10, seed=1,
+                                                     device=devs[r], split_min=mins[r])
+                except Exception as e:
+                    results[r] = e
+
+            t0 = time.time()
+            ts = [threading.Thread(target=member, args=(r,)) for r in range(2)]
+            for t in ts:
+                t.start()
+            for t in ts:
+                t.join(timeout=120)
+            assert not any(t.is_alive() for t in ts), "diverged members hung"
+            assert time.time() - t0 < 60
+            assert isinstance(results[0], mdg.MdgError) and "diverged" in str(results[0]), results
+        finally:
+            L.mdg_group_free(grp)
+            for d in devs:
+                d.close()
