@@ -1470,10 +1470,11 @@ __global__ void __launch_bounds__(kThreads) tab_find(TabArgs a) {
 // smem bins are flushed into the u64 global histogram before any could wrap (a block counts
 // at most 2^32 - 1 codewords between flushes).
 template <int NW, bool HID>
-#ifndef MDG_HIST_MINBLK
-#define MDG_HIST_MINBLK 1
-#endif
+#ifdef MDG_HIST_MINBLK // tuning builds only: a minimum of resident blocks (5 / 6 measured slower)
 __global__ void __launch_bounds__(kThreads, MDG_HIST_MINBLK) tab_hist(TabArgs a) {
+#else
+__global__ void __launch_bounds__(kThreads) tab_hist(TabArgs a) {
+#endif
     constexpr int R = r_for(NW);
     constexpr int YC = R * kThreads;
     constexpr int XS = stride_for(NW + (HID ? 1 : 0));
@@ -2146,6 +2147,11 @@ struct ExchangeGroup {
     std::string why;
     std::vector<unsigned long long*> slots;
     std::vector<cudaEvent_t> events;
+    // what each barrier handed out, by generation parity: a member woken late from barrier g
+    // must not read `slots` / `events` -- a fast member may already have published round g + 1
+    // there. Barrier g + 1 needs the late member, so snapshot g stays valid until it has read it.
+    std::vector<unsigned long long*> snap_slots[2];
+    std::vector<cudaEvent_t> snap_events[2];
     std::vector<uint64_t> tags;  // (c << 32 | j) of the split round each member arrived with
     std::vector<uint64_t> loops; // level loops each member has entered
     std::vector<uint64_t> left;  // the last loop each member has left
@@ -2203,6 +2209,8 @@ struct ExchangeGroup {
         };
         if (++arrived == world) {
             arrived = 0;
+            snap_slots[gen & 1] = slots;
+            snap_events[gen & 1] = events;
             ++generation;
             for (uint32_t r = 0; r < world; ++r)
                 if (tags[r] != tags[rank])
@@ -2221,8 +2229,8 @@ struct ExchangeGroup {
                      " waits at a split round");
         }
         if (aborted) throw std::runtime_error("exchange group aborted: " + why);
-        all_slots = slots;
-        all_events = events;
+        all_slots = snap_slots[gen & 1];
+        all_events = snap_events[gen & 1];
     }
     void abort(const std::string& reason) {
         std::lock_guard<std::mutex> lk(mu);
@@ -3478,7 +3486,8 @@ void Engine::group_attach(std::shared_ptr<ExchangeGroup> g, uint32_t rank) {
         g->devices.push_back(device_);
         if (rank == 0 && !g->ring && !std::getenv("MDG_NO_SHARED_BOUND")) {
             CK(cudaMalloc(&g->ring, ExchangeGroup::kRing * sizeof(unsigned long long)));
-            CK(cudaMemset(g->ring, 0xFF, ExchangeGroup::kRing * sizeof(unsigned long long)));
+            CK(cudaMemsetAsync(g->ring, 0xFF, ExchangeGroup::kRing * sizeof(unsigned long long), im.stream));
+            CK(cudaStreamSynchronize(im.stream)); // before any member's (non-blocking) stream uses it
             g->ring_device = device_;
         }
     }

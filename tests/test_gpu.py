@@ -355,6 +355,25 @@ def test_min_weight_multi_group_split(mdg, world, shared, monkeypatch):
             d.close()
 
 
+def test_min_weight_multi_group_split_rd(mdg):
+    """The split path with the revolving-door kernel's plans (rd tiles are revolving-door rank
+    ranges of the prefixes; tab_split cuts them the same way): two contexts, every round split,
+    golden traces on both ranks."""
+    devs = [mdg.Device(0) for _ in range(2)]
+    try:
+        for name in ("cfg1", "cfg2_s8", "cfg3"):
+            case = next(c for c in load_golden("configs") if c["name"] == name)
+            g = case["gen"]
+            rows = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
+            runs = mdg.min_weight_multi(rows, g["n"], devs, trials=10, seed=g["seed"],
+                                        kernel=mdg.KERNEL_RD, split_min=1)
+            for r, res in enumerate(runs):
+                _check_run(res, case, f"rd {name} rank{r}", exact=False)
+    finally:
+        for d in devs:
+            d.close()
+
+
 def test_min_weight_multi_errors(mdg):
     """Argument checks of the single-process multi front door, and a member failure (a level
     beyond the device limit would be hit by every rank at once; here a bad context list)
