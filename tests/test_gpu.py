@@ -374,6 +374,26 @@ def test_min_weight_multi_group_split_rd(mdg):
             d.close()
 
 
+def test_min_weight_multi_group_stress(mdg):
+    """Many short split rounds through a four-member exchange group (every round of config 1
+    and config 2 seed 8 split, 12 runs): members that run ahead of the others must never make a
+    slow member read the next round's slots (the barrier snapshots them); every rank's trace
+    equals the golden every time."""
+    devs = [mdg.Device(0) for _ in range(4)]
+    try:
+        for name in ("cfg1", "cfg2_s8"):
+            case = next(c for c in load_golden("configs") if c["name"] == name)
+            g = case["gen"]
+            rows = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
+            for _ in range(6):
+                for r, res in enumerate(mdg.min_weight_multi(rows, g["n"], devs, trials=10,
+                                                             seed=g["seed"], split_min=1)):
+                    _check_run(res, case, f"stress {name} rank{r}", exact=False)
+    finally:
+        for d in devs:
+            d.close()
+
+
 def test_min_weight_multi_errors(mdg):
     """Argument checks of the single-process multi front door, and a member failure (a level
     beyond the device limit would be hit by every rank at once; here a bad context list)
