@@ -2535,13 +2535,52 @@ void Engine::load(uint32_t m, uint32_t k, uint32_t n, const uint64_t* rows, cons
                                                     " lacks its identity block");
                 }
         }
+        // A partial Gamma's rows [rk, k) usually still own a unit column of the previous
+        // block's identity (the last block's row operations add pivot rows, whose earlier
+        // identity bits are the pivots' own: gamma.cpp:57-62), so every row owns exactly one
+        // weight-1 column. Then |S| counts all of them and the Gamma is compacted like a
+        // full-rank one (no per-entry identity counts; config 4's Gamma_1: 7 words + counts
+        // -> 4 words). Otherwise only the identity block is elided (per-entry counts, HID).
+        std::vector<uint32_t> extra; // unit column owned by row rk + i
+        if (ranks && rk > 0 && rk < k && !getenv("MDG_NO_UNIT_ELISION")) {
+            std::vector<int32_t> owner(n, -1); // row of a weight-1 column, -2 heavier, -1 empty
+            for (uint32_t r = 0; r < k; ++r) {
+                const uint64_t* row = G + size_t(r) * W;
+                for (uint32_t col = 0; col < n; ++col)
+                    if ((row[col / 64] >> (col % 64)) & 1u) owner[col] = owner[col] == -1 ? int32_t(r) : -2;
+            }
+            extra.assign(k - rk, UINT32_MAX);
+            for (uint32_t col = 0; col < n; ++col) {
+                if (col >= off && col < off + rk) continue;
+                const int32_t r = owner[col];
+                if (r >= int32_t(rk) && extra[r - rk] == UINT32_MAX) extra[r - rk] = col;
+            }
+            for (uint32_t x : extra)
+                if (x == UINT32_MAX) { extra.clear(); break; }
+        }
+        const bool all_unit = !extra.empty();
+        std::vector<uint8_t> elide(n, 0);
+        if (ranks)
+            for (uint32_t t = 0; t < rk; ++t) elide[off + t] = 1;
+        for (uint32_t col : extra) elide[col] = 1;
         GammaDev gd;
-        gd.id_rows = rk;
-        gd.n_compact = n - rk;
+        gd.id_rows = all_unit ? k : rk;
+        gd.n_compact = n - rk - uint32_t(extra.size());
         gd.nw = template_width(std::max<uint32_t>(1, (gd.n_compact + 31) / 32)); // zero-padded
-        gd.hid = rk > 0 && rk < k;
+        gd.hid = rk > 0 && rk < k && !all_unit;
         auto& hr = host[j];
         hr.assign(size_t(k) * gd.nw, 0);
+        if (all_unit) { // compacted row = the non-elided columns in order (bit by bit: k x n)
+            for (uint32_t r = 0; r < k; ++r) {
+                const uint64_t* row = G + size_t(r) * W;
+                uint32_t* dst = hr.data() + size_t(r) * gd.nw;
+                for (uint32_t col = 0, p = 0; col < n; ++col) {
+                    if (elide[col]) continue;
+                    if ((row[col / 64] >> (col % 64)) & 1u) dst[p / 32] |= 1u << (p % 32);
+                    ++p;
+                }
+            }
+        }
         // compacted row = bits [0, off) then bits [off + rk, n): two word-level bit-range copies
         auto get64 = [&](const uint64_t* row, uint32_t pos) -> uint64_t { // 64 bits from pos (0-padded)
             const uint32_t w = pos / 64, sh = pos % 64;
@@ -2550,7 +2589,7 @@ void Engine::load(uint32_t m, uint32_t k, uint32_t n, const uint64_t* rows, cons
             return v;
         };
         const uint32_t cut = ranks ? rk : 0, head = ranks ? off : n;
-        for (uint32_t r = 0; r < k; ++r) {
+        for (uint32_t r = 0; r < k && !all_unit; ++r) {
             const uint64_t* row = G + size_t(r) * W;
             uint32_t* dst = hr.data() + size_t(r) * gd.nw;
             auto put = [&](uint32_t from, uint32_t len, uint32_t to) { // bits [from, from+len) -> to

@@ -1010,3 +1010,41 @@ def test_group_divergence_fails_fast(mdg):
             L.mdg_group_free(grp)
             for d in devs:
                 d.close()
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_unit_column_elision_vs_oracle(mdg, device, kernel, monkeypatch):
+    """A partial Gamma whose rows [rank, k) each still own a weight-1 column (the previous
+    block's identity, untouched by the last block's row operations) is compacted like a
+    full-rank one (|S| + popcount of the non-unit columns). Per-round minima, evaluated counts
+    and witnesses equal the oracle's on the uncompacted Gammas, with the elision on and off
+    (MDG_NO_UNIT_ELISION), on config 4 and on partial blocks of other shapes, including
+    sparse codes whose last rows may own no unit column (the identity-only fallback)."""
+    device.set_kernel(kernel)
+    rng = np.random.default_rng(99)
+    codes = [(mdg.gen_matrix(n, k, s, True), n) for (n, k, s) in
+             [(300, 200, 11), (70, 40, 2), (45, 40, 6), (130, 64, 11), (301, 150, 6), (33, 20, 3)]]
+    while len(codes) < 14:
+        k = int(rng.integers(6, 20))
+        n = int(rng.integers(k + 2, 2 * k))
+        codes.append((_sparse_code(rng, k, n, float(rng.choice([0.2, 0.5]))), n))
+    partial = 0
+    for G, n in codes:
+        gs = mdg.GammaSet.build(G, n, 3, 1)
+        partial += gs.ranks[-1] < gs.gamma(0).shape[0]
+        for off in (False, True):
+            if off:
+                monkeypatch.setenv("MDG_NO_UNIT_ELISION", "1")
+            else:
+                monkeypatch.delenv("MDG_NO_UNIT_ELISION", raising=False)
+            device.load_gset(gs)
+            j = gs.m - 1
+            g = gs.gamma(j)
+            for c in range(1, 4 if n > 100 else 5):
+                w, combos = port.round_min(g, n, c)
+                out = device.round(j, c)
+                assert (out.min_weight, out.evaluated) == (w, combos), (n, off, c, kernel)
+                idx = device.round_witness(j, c, out)
+                assert popcount_rows(g, idx)[0] == w
+    monkeypatch.delenv("MDG_NO_UNIT_ELISION", raising=False)
+    assert partial >= 6
