@@ -1469,6 +1469,36 @@ __global__ void __launch_bounds__(kThreads) tab_find(TabArgs a) {
 // from the popcounts (popsum_mad: the FMA pipe is idle, the ALU pipe carries the LOP3s); the
 // smem bins are flushed into the u64 global histogram before any could wrap (a block counts
 // at most 2^32 - 1 codewords between flushes).
+//
+// Chain basis. popsum's carry-save chain folds words (ones, v[2i+1], v[2i+2]) into a new ones
+// word S_{i+1} = v[0] ^ ... ^ v[2i+2] and a carry. XOR is linear, so when both sides of the tile
+// store S_{i+1} in place of word 2i+2 (to_chain_basis, once per item per tile), X' ^ Y' yields
+// the chain's ones words directly and each carry is ONE LOP3 of (ones before, v[2i+1], ones
+// after): maj(a, b, t ^ a ^ b), LUT 0xD4 -- one LOP3 per chain step instead of two (NW = 8:
+// 13 LOP3 per codeword instead of 16, 27 instead of 30 instructions).
+#ifndef MDG_HIST_CHAIN
+#define MDG_HIST_CHAIN 1
+#endif
+template <int N>
+__device__ __forceinline__ void to_chain_basis(uint32_t* v) {
+#pragma unroll
+    for (int i = 0; i < (N - 1) / 2; ++i) v[2 + 2 * i] ^= v[2 * i] ^ v[1 + 2 * i];
+}
+template <int N>
+__device__ __forceinline__ uint32_t popsum_chain_mad(const uint32_t (&v)[N], uint32_t acc, const uint32_t* s) {
+    if constexpr (N < 3) {
+        return popsum_mad<N>(v, acc, s);
+    } else {
+        constexpr int M = (N - 1) / 2;
+        uint32_t carries[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) carries[i] = lop3<0xD4>(v[2 * i], v[1 + 2 * i], v[2 + 2 * i]);
+        acc = mad_u32(__popc(v[2 * M]), s[0], acc);
+        if constexpr ((N - 1) % 2 == 1) acc = mad_u32(__popc(v[N - 1]), s[0], acc);
+        return popsum_mad<M>(carries, acc, s + 1);
+    }
+}
+
 template <int NW, bool HID>
 #ifdef MDG_HIST_MINBLK // tuning builds only: a minimum of resident blocks (5 / 6 measured slower)
 __global__ void __launch_bounds__(kThreads, MDG_HIST_MINBLK) tab_hist(TabArgs a) {
@@ -1531,10 +1561,17 @@ __global__ void __launch_bounds__(kThreads) tab_hist(TabArgs a) {
         __syncthreads();
         if (ti.stop) break;
         if (flush_now) flush();
-        if (threadIdx.x < ti.nx) build_smem_item<NW, HID>(a, ti, threadIdx.x, xs + threadIdx.x * XS);
+        if (threadIdx.x < ti.nx) {
+            build_smem_item<NW, HID>(a, ti, threadIdx.x, xs + threadIdx.x * XS);
+            if (MDG_HIST_CHAIN) to_chain_basis<NW>(xs + threadIdx.x * XS);
+        }
         uint32_t Y[R][NW], idY[R];
         bool valid[R];
         load_suffixes<NW, HID>(a, ti, Y, idY, valid);
+        if (MDG_HIST_CHAIN) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) to_chain_basis<NW>(Y[r]);
+        }
         uint32_t base[R]; // the item's bin row: real bins + weight offset, or the scratch copy
 #pragma unroll
         for (int r = 0; r < R; ++r) base[r] = (valid[r] ? sreal : sjunk) + 4u * (a.add_const + (HID ? idY[r] : 0u));
@@ -1549,7 +1586,8 @@ __global__ void __launch_bounds__(kThreads) tab_hist(TabArgs a) {
 #pragma unroll
                 for (int w = 0; w < NW; ++w) v[w] = X[w] ^ Y[r][w];
                 const uint32_t b0 = HID ? mad_u32(X[NW], sc[0], base[r]) : base[r];
-                asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(popsum_mad<NW>(v, b0, sc)));
+                asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(
+                    MDG_HIST_CHAIN ? popsum_chain_mad<NW>(v, b0, sc) : popsum_mad<NW>(v, b0, sc)));
             }
         }
         __syncthreads();
@@ -1738,9 +1776,13 @@ void dispatch_nw_hid(uint32_t nw, bool hid, Args&&... args) {
         if (hid) F<N, true>::run(args...); else F<N, false>::run(args...);       \
         break;
     switch (nw) {
+#ifdef MDG_DEV_FEW_WIDTHS // tuning builds only (tools/build_variant.sh): compiles in a minute
+        MDG_CASE(2) MDG_CASE(4) MDG_CASE(7) MDG_CASE(8)
+#else
         MDG_CASE(1) MDG_CASE(2) MDG_CASE(3) MDG_CASE(4) MDG_CASE(5) MDG_CASE(6) MDG_CASE(7)
         MDG_CASE(8) MDG_CASE(10) MDG_CASE(12) MDG_CASE(14) MDG_CASE(16) MDG_CASE(20)
         MDG_CASE(24) MDG_CASE(28) MDG_CASE(32)
+#endif
         default: throw std::invalid_argument("row width beyond the device limit");
     }
 #undef MDG_CASE
@@ -2913,6 +2955,14 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
         return 1.0 - q;
     };
     const int GR = std::min(R, 4);
+    // A vote group that falls through costs far more than its exact weights' pipe time: the
+    // branch, the dependent carry-save -> POPC -> add -> min chain and the warp-wide wait showed
+    // 7-9 x the stage-1 time per codeword on config 4's NW = 4 rounds (two-word fold at T = 12..15
+    // against the three-word fold, profiles/r02f_fold_calibration.txt), 3 x the modelled `exact`.
+    static const double kFallPenalty = [] {
+        const char* e = std::getenv("MDG_FALL_PENALTY");
+        return e ? std::max(0.1, std::atof(e)) : 3.0;
+    }();
     int last = -2;
     std::string dbg;
     const auto tp1 = std::chrono::steady_clock::now();
@@ -2931,14 +2981,14 @@ static FoldPlan compute_fold_plan(const Engine::Impl& im, uint32_t j, uint32_t k
             const Opt& o = opts[i];
             const double adds = (o.G + 1) / 2;
             const double f1 = fall(c1[i][T], 32 * GR);
-            const double single = std::max(o.fw + adds + 1.4, 4.0 * o.G) + f1 * exact;
+            const double single = std::max(o.fw + adds + 1.4, 4.0 * o.G) + f1 * kFallPenalty * exact;
             if (single < best) best = single, code = o.code;
             if (!pairs || o.G != 1 || o.fw != 2) continue; // pair2_bits: one 2-word group
             const double f2 = fall(c2[i][T], 32 * (GP / 2));
             // a fall-through group takes the single bounds (folds already computed: POPCs only)
             // 3 LOP3 per pair (pair2_bits)
             const double pair = std::max(1.5 + 0.5 * adds + 0.9, 2.0 * o.G) +
-                                f2 * (std::max(adds + 1.4, 4.0 * o.G) + f1 * exact);
+                                f2 * (std::max(adds + 1.4, 4.0 * o.G) + f1 * kFallPenalty * exact);
             if (pair < best) best = pair, code = o.code | kFoldPair;
         }
         fp.code[T] = uint8_t(code);
