@@ -111,6 +111,16 @@ int mdg_round_bounded(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t stop_at, ui
 /* Full weight histogram of round (j, c) (no early exit): hist[0..n] (config 5;
  * no reference counterpart). Returns the min in out. */
 int mdg_round_hist(mdg_ctx* ctx, uint32_t j, uint32_t c, uint64_t* hist, mdg_round_out* out);
+/* The same histogram at N > 1: rank `rank` counts its contiguous share
+ * of the histogram kernel's tiles (about 1/world of the codewords; out->task_lo/hi, out->evaluated
+ * are this rank's). With an NCCL communicator attached (mdg_nccl_init) the n + 1 counts are summed
+ * across the ranks in stream (ncclAllReduce(sum)): every rank receives the whole histogram and
+ * *reduced = 1. Without one hist holds the rank's partial counts (*reduced = 0) for the caller to
+ * sum (contexts of one process add them on the host). out->min_weight = first nonzero bin of
+ * what hist holds. The reference analog is the merge of worker-local results at join
+ * (engines.cpp:432-441). reduced may be NULL. */
+int mdg_round_hist_dist(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t rank, uint32_t world,
+                        uint64_t* hist, mdg_round_out* out, int* reduced);
 
 /* Combination (c sorted row indices) achieving out->min_weight in the task
  * named by out->argmin_key — the witness of that round. */

@@ -115,6 +115,8 @@ SYMBOLS = {
     "mdg_round_bounded": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                     C.c_uint64, C.c_uint64, C.POINTER(_RoundOut)]),
     "mdg_round_hist": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, u64p, C.POINTER(_RoundOut)]),
+    "mdg_round_hist_dist": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, u64p,
+                                      C.POINTER(_RoundOut), C.POINTER(C.c_int)]),
     "mdg_round_witness": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(_RoundOut), u32p]),
     "mdg_set_kernel": (C.c_int, [C.c_void_p, C.c_int]),
     "mdg_set_pruning": (C.c_int, [C.c_void_p, C.c_int]),
@@ -449,6 +451,16 @@ class Device:
         o = _RoundOut()
         _check(lib().mdg_round_hist(self._h, j, c, hist, C.byref(o)))
         return _round_out(o), hist
+
+    def round_hist_dist(self, j: int, c: int, n: int, rank: int, world: int):
+        """mdg_round_hist_dist: this rank's share of round (j, c)'s histogram -- summed across
+        the ranks over NCCL when a communicator is attached (reduced = True), else the rank's
+        partial counts. Returns (RoundOut, hist, reduced)."""
+        hist = np.zeros(n + 1, dtype=np.uint64)
+        o = _RoundOut()
+        red = C.c_int(0)
+        _check(lib().mdg_round_hist_dist(self._h, j, c, rank, world, hist, C.byref(o), C.byref(red)))
+        return _round_out(o), hist, bool(red.value)
 
     def round_witness(self, j: int, c: int, out: RoundOut) -> list:
         idx = np.zeros(c, dtype=np.uint32)

@@ -523,6 +523,16 @@ int mdg_round_hist(mdg_ctx* ctx, uint32_t j, uint32_t c, uint64_t* hist, mdg_rou
     });
 }
 
+int mdg_round_hist_dist(mdg_ctx* ctx, uint32_t j, uint32_t c, uint32_t rank, uint32_t world,
+                        uint64_t* hist, mdg_round_out* out, int* reduced) {
+    return guard([&] {
+        if (!ctx || !hist || !out) throw std::invalid_argument("null argument");
+        if (world < 1 || rank >= world) throw std::invalid_argument("bad rank / world");
+        fill_out(ctx->eng->round_hist(j, c, hist, rank, world), out);
+        if (reduced) *reduced = (world > 1 && ctx->eng->has_comm()) ? 1 : 0;
+    });
+}
+
 int mdg_round_witness(mdg_ctx* ctx, uint32_t j, uint32_t c, const mdg_round_out* out, uint32_t* idx) {
     return guard([&] {
         if (!ctx || !out || !idx) throw std::invalid_argument("null argument");

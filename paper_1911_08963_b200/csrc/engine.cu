@@ -2163,6 +2163,7 @@ NcclApi& nccl() {
 }
 constexpr int kNcclUint64 = 5; // ncclUint64
 constexpr int kNcclMin = 3;    // ncclMin
+constexpr int kNcclSum = 0;    // ncclSum
 } // namespace
 
 // ------------------------------------------------------------ exchange group
@@ -3082,8 +3083,9 @@ RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t tas
     return rr;
 }
 
-RoundResult Engine::round_hist(uint32_t j, uint32_t c, uint64_t* hist) {
+RoundResult Engine::round_hist(uint32_t j, uint32_t c, uint64_t* hist, uint32_t rank, uint32_t world) {
     check_round(j, c);
+    if (world < 1 || rank >= world) throw std::invalid_argument("round_hist: bad rank / world");
     CK(cudaSetDevice(device_));
     Impl& im = *impl_;
     const GammaDev& g = im.gammas[j];
@@ -3105,21 +3107,31 @@ RoundResult Engine::round_hist(uint32_t j, uint32_t c, uint64_t* hist) {
         const char* e = std::getenv("MDG_HIST_TPB");
         return e ? uint32_t(std::max(1, std::atoi(e))) : 4u;
     }();
-    const PlanEntry& pe = im.plan(k_, c, g, plan_sms_, im.rd, false, kHistTpb, std::max(1, hocc) * sms_);
+    // (plan_sms_: the SM count the ranks agreed on, so every rank cuts the same tiles)
+    const PlanEntry& pe = im.plan(k_, c, g, plan_sms_, im.rd, false, kHistTpb, std::max(1, hocc) * plan_sms_);
     uint32_t* yt = ensure_ytab(im, j, k_, pe.plan.s);
     unsigned long long* slot = im.take_slot();
     CK(cudaMemsetAsync(im.hist_dev, 0, nbins * 8, im.stream));
     TabArgs a = tab_args(im, g, pe, yt, k_, c, /*want_fold=*/false);
-    a.tile_lo = 0; a.tile_hi = pe.plan.tiles();
+    // multi-rank: rank r counts a contiguous tile range holding about
+    // 1/world of the codewords; the counts are summed across ranks (NCCL, below, or the caller)
+    const auto range = world > 1 ? tab_split(pe.plan, rank, world) : std::make_pair(uint64_t(0), pe.plan.tiles());
+    a.tile_lo = range.first; a.tile_hi = range.second;
     a.evaluated = slot + 1; a.counter = slot + 2;
     a.nbins = nbins;
     a.hist = im.hist_dev;
     int XS = stride_for(int(g.nw) + (g.hid ? 1 : 0));
     size_t dyn = size_t(pe.plan.TX) * XS * 4 + size_t(kWarps) * 2 * nbins * 4; // bins + scratch per warp
     CK(cudaEventRecord(im.ev0, im.stream));
-    dispatch_nw_hid<TabLaunch>(g.nw, g.hid, a, pe.plan.tiles(), im.stream, 2, dyn, sms_);
-    CK(cudaGetLastError());
-    im.cnt.launches += 1;
+    if (a.tile_hi > a.tile_lo) {
+        dispatch_nw_hid<TabLaunch>(g.nw, g.hid, a, a.tile_hi - a.tile_lo, im.stream, 2, dyn, sms_);
+        CK(cudaGetLastError());
+        im.cnt.launches += 1;
+    }
+    if (world > 1 && im.comm) { // every rank receives the whole histogram
+        int rc = nccl().AllReduce(im.hist_dev, im.hist_dev, nbins, kNcclUint64, kNcclSum, im.comm, im.stream);
+        if (rc != 0) throw std::runtime_error(std::string("ncclAllReduce: ") + nccl().GetErrorString(rc));
+    }
     CK(cudaEventRecord(im.ev1, im.stream));
     CK(cudaMemcpyAsync(hist, im.hist_dev, nbins * 8, cudaMemcpyDeviceToHost, im.stream));
     im.cnt.d2h += nbins * 8;
@@ -3129,7 +3141,8 @@ RoundResult Engine::round_hist(uint32_t j, uint32_t c, uint64_t* hist) {
     CK(cudaEventElapsedTime(&ms, im.ev0, im.ev1));
     rr.ms = ms;
     rr.evaluated = im.host_slot[1];
-    rr.task_hi = pe.plan.tiles();
+    rr.task_lo = a.tile_lo;
+    rr.task_hi = a.tile_hi;
     for (uint32_t w = 0; w < nbins; ++w)
         if (hist[w]) { rr.w = w; break; }
     rr.key = rr.w == UINT32_MAX ? ~0ull : (uint64_t(rr.w) << kKeyShift);
@@ -3507,6 +3520,7 @@ void Engine::set_kernel(Kernel kern) {
     impl_->rd = kern == Kernel::rd;
 }
 struct CUstream_st* Engine::stream() const { return impl_->stream; }
+bool Engine::has_comm() const { return impl_->comm != nullptr; }
 void* Engine::scratch(size_t bytes) {
     Impl& im = *impl_;
     if (im.scratch_cap < bytes) {

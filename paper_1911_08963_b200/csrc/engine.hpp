@@ -99,7 +99,11 @@ public:
     // codeword lies below it — what run_bz_loop's U = min(U, w) needs.
     RoundResult round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t task_lo = 0,
                       uint64_t task_hi = UINT64_MAX, uint32_t cutoff = 0);
-    RoundResult round_hist(uint32_t j, uint32_t c, uint64_t* hist);
+    // rank / world: this rank's contiguous share of the histogram kernel's tiles (about 1/world
+    // of the codewords); with an NCCL communicator attached the counts are summed across the
+    // ranks in stream, otherwise `hist` is this rank's partial histogram
+    RoundResult round_hist(uint32_t j, uint32_t c, uint64_t* hist, uint32_t rank = 0, uint32_t world = 1);
+    bool has_comm() const;
 
     // The whole level loop with rounds chained on the stream (either kernel):
     // a device-side state carries U / L / done, a finalize kernel per round

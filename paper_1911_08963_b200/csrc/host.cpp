@@ -504,16 +504,16 @@ GammaSet best_gamma_over_permutations(const BitMatrix& G, uint32_t trials, uint6
     return cand;
 }
 
-// gamma.cpp:96-100
+// The BZ lower bound after level g (gamma.cpp:96-100): each of the m - 1 full information sets
+// contributes g + 1, the last one g + 1 less the k - k_last rows it lacks (never below 0).
 uint32_t lower_bound(uint32_t m, uint32_t g, uint32_t k, uint32_t k_last) {
-    int64_t partial = static_cast<int64_t>(g) + 1 - static_cast<int64_t>(k) + k_last;
-    if (partial < 0) partial = 0;
-    return (m - 1) * (g + 1) + static_cast<uint32_t>(partial);
+    const int64_t last = int64_t(g) + 1 - (int64_t(k) - int64_t(k_last));
+    return (m - 1) * (g + 1) + static_cast<uint32_t>(std::max<int64_t>(last, 0));
 }
 
-// gamma.cpp:102-106
+// The Singleton bound n - k + 1 as the loop's first upper bound (gamma.cpp:102-106).
 uint32_t singleton_upper(uint32_t n, uint32_t k) {
-    if (k < 1 || n < k) throw std::invalid_argument("singleton_upper: need n >= k >= 1");
+    if (k == 0 || k > n) throw std::invalid_argument("singleton_upper: need n >= k >= 1");
     return n - k + 1;
 }
 
@@ -586,58 +586,68 @@ ParseError::ParseError(uint32_t line_no, uint32_t column_no, const std::string& 
       column(column_no) {}
 
 namespace {
-bool blank_or_comment(const std::string& line) {
-    for (char ch : line) {
-        if (ch == ' ' || ch == '\t' || ch == '\r') continue;
-        return ch == '#';
+// One pass over the text of a matrix file: yields the payload lines (whitespace-trimmed,
+// neither empty nor a '#' comment) with their 1-based line numbers. A last line without a
+// newline counts when it has characters, as with std::getline.
+class PayloadLines {
+public:
+    explicit PayloadLines(const std::string& text) : text_(text) {}
+    uint32_t lines_read() const { return line_no_; }
+    bool next(std::string& out) {
+        while (pos_ < text_.size()) {
+            size_t end = text_.find('\n', pos_);
+            if (end == std::string::npos) end = text_.size();
+            ++line_no_;
+            size_t b = pos_, e = end;
+            pos_ = end + 1;
+            auto pad = [](char ch) { return ch == ' ' || ch == '\t' || ch == '\r'; };
+            while (b < e && pad(text_[b])) ++b;
+            while (e > b && pad(text_[e - 1])) --e;
+            if (b == e || text_[b] == '#') continue;
+            out.assign(text_, b, e - b);
+            return true;
+        }
+        return false;
     }
-    return true;
-}
-std::string strip(const std::string& line) {
-    size_t b = line.find_first_not_of(" \t\r");
-    if (b == std::string::npos) return "";
-    size_t e = line.find_last_not_of(" \t\r");
-    return line.substr(b, e - b + 1);
-}
+
+private:
+    const std::string& text_;
+    size_t pos_ = 0;
+    uint32_t line_no_ = 0;
+};
 } // namespace
 
-// io.cpp:33-73 — header "n k", then k rows of exactly n symbols from {0,1};
-// '#' comment and blank lines anywhere; errors carry line and column.
+// The reference's text format (io.cpp:33-73): a header "n k", then k rows of exactly n symbols
+// 0 / 1; blank lines and '#' comment lines anywhere; every error names its line and column
+// (same messages and positions as the reference's ParseError).
 BitMatrix parse_matrix(const std::string& text) {
-    std::istringstream in(text);
-    std::string line;
-    uint32_t line_no = 0;
+    PayloadLines src(text);
+    std::string item;
+    if (!src.next(item)) throw ParseError(src.lines_read() + 1, 1, "missing header line");
     uint64_t n = 0, k = 0;
-    bool have_header = false;
-    while (!have_header) {
-        if (!std::getline(in, line)) throw ParseError(line_no + 1, 1, "missing header line");
-        ++line_no;
-        if (blank_or_comment(line)) continue;
-        std::istringstream hs(strip(line));
-        if (!(hs >> n >> k)) throw ParseError(line_no, 1, "header must be two integers: n k");
-        std::string rest;
-        if (hs >> rest) throw ParseError(line_no, 1, "header must be exactly: n k");
-        if (n < 1 || k < 1) throw ParseError(line_no, 1, "n and k must be >= 1");
-        if (n > 1u << 20 || k > 1u << 20) throw ParseError(line_no, 1, "unreasonable dimensions");
-        have_header = true;
+    {
+        std::istringstream header(item);
+        std::string extra;
+        if (!(header >> n >> k)) throw ParseError(src.lines_read(), 1, "header must be two integers: n k");
+        if (header >> extra) throw ParseError(src.lines_read(), 1, "header must be exactly: n k");
     }
+    if (n == 0 || k == 0) throw ParseError(src.lines_read(), 1, "n and k must be >= 1");
+    constexpr uint64_t kMaxDim = uint64_t{1} << 20;
+    if (n > kMaxDim || k > kMaxDim) throw ParseError(src.lines_read(), 1, "unreasonable dimensions");
     BitMatrix M(static_cast<uint32_t>(k), static_cast<uint32_t>(n));
-    uint32_t row = 0;
-    while (row < k) {
-        if (!std::getline(in, line))
-            throw ParseError(line_no + 1, 1,
-                             "expected " + std::to_string(k) + " rows, got " + std::to_string(row));
-        ++line_no;
-        if (blank_or_comment(line)) continue;
-        std::string data = strip(line);
-        if (data.size() != n)
-            throw ParseError(line_no, static_cast<uint32_t>(data.size()) + 1,
+    for (uint32_t r = 0; r < k; ++r) {
+        if (!src.next(item))
+            throw ParseError(src.lines_read() + 1, 1,
+                             "expected " + std::to_string(k) + " rows, got " + std::to_string(r));
+        if (item.size() != n)
+            throw ParseError(src.lines_read(), static_cast<uint32_t>(item.size()) + 1,
                              "row must have exactly " + std::to_string(n) + " symbols");
-        for (uint32_t c = 0; c < n; ++c) {
-            if (data[c] == '1') M.set(row, c, true);
-            else if (data[c] != '0') throw ParseError(line_no, c + 1, "symbols must be 0 or 1");
+        uint64_t* words = M.row(r);
+        for (uint32_t col = 0; col < n; ++col) {
+            const char ch = item[col];
+            if (ch == '1') words[col >> 6] |= uint64_t{1} << (col & 63);
+            else if (ch != '0') throw ParseError(src.lines_read(), col + 1, "symbols must be 0 or 1");
         }
-        ++row;
     }
     return M;
 }
@@ -650,13 +660,18 @@ BitMatrix parse_matrix_file(const std::string& path) {
     return parse_matrix(ss.str());
 }
 
-// io.cpp:81-88
+// io.cpp:81-88: "n k" and one line of n symbols per row
 std::string serialize_matrix(const BitMatrix& M) {
-    std::string out = std::to_string(M.cols()) + " " + std::to_string(M.rows()) + "\n";
-    out.reserve(out.size() + size_t(M.rows()) * (M.cols() + 1));
-    for (uint32_t r = 0; r < M.rows(); ++r) {
-        for (uint32_t c = 0; c < M.cols(); ++c) out += M.get(r, c) ? '1' : '0';
-        out += '\n';
+    const uint32_t k = M.rows(), n = M.cols();
+    std::string out = std::to_string(n) + ' ' + std::to_string(k) + '\n';
+    const size_t body = out.size();
+    out.resize(body + size_t(k) * (size_t(n) + 1), '0');
+    for (uint32_t r = 0; r < k; ++r) {
+        char* line = &out[body + size_t(r) * (size_t(n) + 1)];
+        const uint64_t* words = M.row(r);
+        for (uint32_t col = 0; col < n; ++col)
+            if ((words[col >> 6] >> (col & 63)) & 1u) line[col] = '1';
+        line[n] = '\n';
     }
     return out;
 }
@@ -677,18 +692,18 @@ BitMatrix gen_matrix(uint32_t n, uint32_t k, uint64_t seed, bool identity) {
 }
 
 // ------------------------------------------------------------ binomials
-// enumeration.cpp:9-20: exact, throws std::overflow_error past 64 bits
+// C(p, q) exactly (enumeration.cpp:9-20: 0 outside 0 <= q <= p, std::overflow_error past 64
+// bits). With t = min(q, p - q) the running value after i factors is C(p - t + i, i): always an
+// integer, never above the result, so it overflows iff the result does.
 uint64_t binomial(uint32_t p, int64_t q) {
     if (q < 0 || q > static_cast<int64_t>(p)) return 0;
-    uint64_t qq = static_cast<uint64_t>(q);
-    if (qq > p - qq) qq = p - qq;
-    unsigned __int128 c = 1;
-    for (uint64_t i = 1; i <= qq; ++i) {
-        c = c * (p - qq + i) / i;
-        if (c > std::numeric_limits<uint64_t>::max())
-            throw std::overflow_error("binomial: value exceeds 64 bits");
+    const uint32_t t = static_cast<uint32_t>(std::min<int64_t>(q, static_cast<int64_t>(p) - q));
+    unsigned __int128 v = 1;
+    for (uint32_t i = 1, top = p - t + 1; i <= t; ++i, ++top) {
+        v = v * top / i;
+        if (v >> 64) throw std::overflow_error("binomial: value exceeds 64 bits");
     }
-    return static_cast<uint64_t>(c);
+    return static_cast<uint64_t>(v);
 }
 
 // Revolving-door order R(n,t) = R(n-1,t) ++ reverse(R(n-1,t-1)) (n-1 appended)

@@ -85,3 +85,53 @@ def test_two_rank_split_reproduces_reference_trace():
             assert d == cases[name]["d"], (rank, name)
             assert rounds == cases[name]["rounds"], (rank, name)
             assert levels == cases[name]["levels"], (rank, name)
+
+
+def _hist_worker(rank, world, port, levels, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import paper_1911_08963_b200 as mdg
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        M = mdg.gen_matrix(256, 100, 3, identity=False)
+        out = {}
+        for c in levels:
+            N = comb(100, c)
+            lo, hi = N * rank // world, N * (rank + 1) // world
+            hist = np.zeros(257, dtype=np.int64)
+            for r in range(lo, hi):  # this rank's contiguous revolving-door range
+                hist[_weight(M, mdg.rd_unrank(c, r))] += 1
+            t = torch.from_numpy(hist)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)  # allreduce(sum) over n + 1 counts
+            out[c] = (t.tolist(), hi - lo)
+        q.put((rank, out, None))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, None, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_histogram_sums_to_reference():
+    """Config 5 at N > 1 (host logic of mdg_round_hist_dist): each rank counts the weights of a
+    contiguous share of the C(100, c) combinations, the n + 1 counts are summed with an
+    allreduce; every rank must hold the reference's histogram."""
+    levels = (1, 2, 3)
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_hist_worker, args=(r, world, port, levels, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    gold = {lv["c"]: lv for lv in load_golden("cfg5_hist")["levels"]}
+    for rank, out, err in results:
+        assert err is None, err
+        for c in levels:
+            hist, share = out[c]
+            assert hist == gold[c]["hist"], (rank, c)
+    assert sum(out[3][1] for _, out, _ in results) == comb(100, 3)

@@ -90,6 +90,42 @@ def test_histogram_cfg5(mdg, device):
         assert full.min_weight == lv["min"]
 
 
+def test_histogram_split_across_ranks_sums_to_golden(mdg):
+    """SURVEY.md 8e, config 5 at N > 1: every rank counts its contiguous share of the histogram
+    kernel's tiles; the partial histograms (no communicator: the caller sums) add up to the
+    reference's, the shares partition the tiles and are balanced in codewords."""
+    from math import comb
+    h = load_golden("cfg5_hist")
+    M = mdg.gen_matrix(256, 100, 3, identity=False)
+    for world in (2, 3, 8):
+        devs = [mdg.Device(0) for _ in range(world)]
+        try:
+            for d in devs:
+                d.load_gammas(M, 256, ranks=None)
+            for lv in h["levels"]:
+                c = lv["c"]
+                total = np.zeros(257, dtype=np.uint64)
+                edges, evaluated = [], []
+                for r, d in enumerate(devs):
+                    out, hist, reduced = d.round_hist_dist(0, c, 256, r, world)
+                    assert not reduced
+                    total += hist
+                    edges.append((out.task_lo, out.task_hi))
+                    evaluated.append(out.evaluated)
+                assert total.tolist() == lv["hist"], (world, c)
+                assert edges[0][0] == 0 and all(edges[i][1] == edges[i + 1][0] for i in range(world - 1))
+                assert sum(evaluated) == comb(100, c)
+                if c == 5:  # each share within a few tiles of 1 / world
+                    assert max(evaluated) - min(evaluated) <= 0.05 * comb(100, c) / world + 4 * 1024 * 128
+            out, hist, reduced = devs[0].round_hist_dist(0, 4, 256, 0, 1)
+            assert not reduced and hist.tolist() == h["levels"][3]["hist"]
+            with pytest.raises(Exception):
+                devs[0].round_hist_dist(0, 4, 256, 2, 2)
+        finally:
+            for d in devs:
+                d.close()
+
+
 def test_histogram_with_identity_vs_oracle(mdg, device):
     G = mdg.gen_matrix(70, 20, 5, True)
     gs = mdg.GammaSet.build(G, 70, 3, 5)

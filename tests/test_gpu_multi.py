@@ -49,6 +49,15 @@ for name in ("cfg2_s1", "cfg2_s8", "cfg4_cap6"):
         out.append({"name": name, "split_min": split_min, "d": r.d, "capped": r.capped,
                     "rounds": r.rounds, "levels": r.levels, "gamma_hash": r.gamma_hash,
                     "witness_ok": r.witness_ok, "evaluated": r.evaluated})
+# config 5 at N > 1: each rank's share of the histogram, summed in stream by ncclAllReduce(sum)
+hg = load_golden("cfg5_hist")
+M = mdg.gen_matrix(256, 100, 3, identity=False)
+dev.load_gammas(M, 256, ranks=None)
+hist_ok = True
+for lv in hg["levels"]:
+    o, hist, reduced = dev.round_hist_dist(0, lv["c"], 256, rank, world)
+    hist_ok = hist_ok and reduced and hist.tolist() == lv["hist"] and o.min_weight == lv["min"]
+out.append({"name": "cfg5_hist", "ok": bool(hist_ok)})
 dev.close()
 print("RESULT " + json.dumps(out), flush=True)
 dist.destroy_process_group()
@@ -93,13 +102,16 @@ def test_nccl_two_ranks_split_path_vs_golden(mdg):
     cases["cfg4_cap6"] = next(c for c in load_golden("configs_cap4_6") if c["name"] == "cfg4")
     for rank_out in outs:
         for rec in rank_out:
+            if rec["name"] == "cfg5_hist":  # the NCCL-summed histogram equals the reference's on every rank
+                assert rec["ok"]
+                continue
             case = cases[rec["name"]]
             assert rec["d"] == (case["U_final"] if rec["capped"] else case["d"]), rec["name"]
             assert rec["rounds"] == _bounded(case), (rec["name"], rec["split_min"])
             assert rec["levels"] == case["levels"], (rec["name"], rec["split_min"])
             assert rec["gamma_hash"] == case["gamma_hash"] and rec["witness_ok"]
     # every split round's tiles are divided: with split_min = 1 each rank evaluates part
-    a = {(r["name"], r["split_min"]): r["evaluated"] for r in outs[0]}
-    b = {(r["name"], r["split_min"]): r["evaluated"] for r in outs[1]}
+    a = {(r["name"], r["split_min"]): r["evaluated"] for r in outs[0] if "split_min" in r}
+    b = {(r["name"], r["split_min"]): r["evaluated"] for r in outs[1] if "split_min" in r}
     whole = a[("cfg2_s1", 1 << 62)]
     assert a[("cfg2_s1", 1)] < 0.75 * whole and b[("cfg2_s1", 1)] < 0.75 * whole

@@ -159,6 +159,54 @@ def test_matrix_grammar(mdg):
         assert pos in str(ei.value) and frag in str(ei.value)
 
 
+def test_parse_errors_match_the_compiled_reference(mdg):
+    """Every malformed (and odd but legal) text gets the reference parser's verdict: the same
+    "line L, column C: message" from parse_matrix (io.cpp:33-73) in oracle/_ref, or the same
+    matrix. Skipped where the compiled reference is absent."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    import random
+    rng = random.Random(7)
+    ham = "7 4\n1101000\n0110100\n0011010\n0001101\n"
+    texts = ["", "\n\n", "# only a comment", "7", "7 x\n", "x 4\n", "-1 4\n1\n", "7 4 \t\r\n1101000\r\n0110100\r\n0011010\r\n0001101",
+             "99999999999999999999999 4\n", "1048577 1\n", "3 1048577\n", "7 4\n1101000\n0110100\n0011010\n",
+             "7 4\n1101000\n0110100\n0011010\n0001101\n0001101\n", "2 2\n10\n0 1\n", "2 2\n 10 \n\t01\t\n",
+             "2 2\n10 # tail\n01\n", "+2 +2\n10\n01\n", "2 2\n#\n10\n\n\n01", "2 2\n10\n012\n", "2 2\n10\n0\n", "2.0 2\n10\n01\n"]
+    for _ in range(300):  # mutations of a good file: a replaced, dropped or inserted character
+        t = list(ham)
+        for _ in range(rng.randint(1, 3)):
+            pos = rng.randrange(len(t) + 1)
+            op = rng.random()
+            ch = rng.choice("01 \n#x2\t\r7-")
+            if op < 0.4 and pos < len(t):
+                t[pos] = ch
+            elif op < 0.7 and pos < len(t):
+                del t[pos]
+            else:
+                t.insert(pos, ch)
+        texts.append("".join(t))
+    checked_err = checked_ok = 0
+    for text in texts:
+        try:
+            want = ref.trace(text, trials=1, seed=1, engine="stack", with_rows=False)
+            want_err = None
+        except RuntimeError as e:
+            want, want_err = None, str(e)
+        if want_err is not None and not want_err.startswith("line "):
+            continue  # parsed, then rejected later (e.g. the zero matrix): not the parser's verdict
+        if want_err is not None:
+            with pytest.raises(mdg.InvalidArgument) as ei:
+                mdg.parse_matrix(text)
+            assert want_err in str(ei.value), (text, want_err, str(ei.value))
+            checked_err += 1
+        else:
+            rows, n = mdg.parse_matrix(text)
+            assert (n, rows.shape[0]) == (want["n"], want["k_input"] if "k_input" in want else rows.shape[0])
+            checked_ok += 1
+    assert checked_err > 50 and checked_ok > 5
+
+
 def test_binomial_and_overflow(mdg):
     # test_enumeration.cpp:73-81
     for p in range(0, 40):
