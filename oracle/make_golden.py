@@ -8,6 +8,7 @@ writes the golden vectors the parity tests compare against:
                  column_perm, Gamma hashes), per-round minima and per-level
                  (L, U) trace, d. Config 4 is level-capped.
   cfg5_hist.json config 5: per-level min weight and full weight histogram.
+  cfg5_hist_c6.json  the same matrix at level 6 (--only cfg5_hist_c6; 1.19e9 codewords).
   kats.json      reference known-answer codes (acceptance_main.cpp:90-125,
                  test_engines.cpp:227-255): traces + brute-force d.
   seeded.json    acceptance criterion 1's 200 seeded codes
@@ -84,7 +85,7 @@ def do_configs(workers, cap4):
     return out
 
 
-def do_hist():
+def do_hist(cmax=5):
     text = ref.gen(256, 100, 3, identity=False)
     import subprocess
     exe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref", "mdref_v3")
@@ -92,12 +93,20 @@ def do_hist():
     with open(path, "w") as f:
         f.write(text)
     t0 = time.time()
-    js = json.loads(subprocess.run([exe, "hist", path, "--cmax", "5"], check=True,
+    js = json.loads(subprocess.run([exe, "hist", path, "--cmax", str(cmax)], check=True,
                                    capture_output=True, text=True).stdout)
     js.update(name="cfg5", matrix_hash=matrix_hash(text),
               gen={"n": 256, "k": 100, "seed": 3, "identity": False})
     print(f"cfg5: mins={[lv['min'] for lv in js['levels']]} {time.time() - t0:.1f}s", flush=True)
     return js
+
+
+def do_hist_c6():
+    """Level 6 of config 5's matrix (1,192,052,400 codewords, ~3 min on one core): the histogram
+    kernel's large parity case. Only the level-6 record is kept."""
+    js = do_hist(6)
+    return {"n": js["n"], "k": js["k"], "level": js["levels"][5], "name": "cfg5_c6",
+            "matrix_hash": js["matrix_hash"], "gen": js["gen"]}
 
 
 def do_kats():
@@ -170,11 +179,12 @@ def main():
         "seeded": lambda: do_seeded(),
         "rounds": lambda: do_rounds(),
         "cfg5_hist": lambda: do_hist(),
+        "cfg5_hist_c6": lambda: do_hist_c6(),
         "configs": lambda: do_configs(a.workers, a.cap4),
     }
     for name, fn in jobs.items():
-        if a.only and name != a.only:
-            continue
+        if (a.only and name != a.only) or (not a.only and name == "cfg5_hist_c6"):
+            continue  # the level-6 histogram only on request (--only cfg5_hist_c6)
         data = fn()
         fname = name if not (name == "configs" and a.cap4 != 5) else f"configs_cap4_{a.cap4}"
         with open(os.path.join(GOLD, fname + ".json"), "w") as f:

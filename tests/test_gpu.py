@@ -90,6 +90,23 @@ def test_histogram_cfg5(mdg, device):
         assert full.min_weight == lv["min"]
 
 
+def test_histogram_level6_vs_reference(mdg, device):
+    """The histogram kernel at its steady-state size: level 6 of config 5's matrix, all
+    C(100, 6) = 1,192,052,400 codewords, bit-exact against the reference's histogram -- whole
+    and as the sum of three ranks' shares."""
+    lv = load_golden("cfg5_hist_c6")["level"]
+    rows = mdg.gen_matrix(256, 100, 3, identity=False)
+    device.load_gammas(rows, 256, ranks=None)
+    out, hist = device.round_hist(0, 6, 256)
+    assert hist.tolist() == lv["hist"] and out.min_weight == lv["min"] == 81
+    assert out.evaluated == lv["count"] == comb(100, 6)
+    total = np.zeros(257, dtype=np.uint64)
+    for r in range(3):
+        o, h, reduced = device.round_hist_dist(0, 6, 256, r, 3)
+        total += h
+    assert total.tolist() == lv["hist"]
+
+
 def test_histogram_split_across_ranks_sums_to_golden(mdg):
     """SURVEY.md 8e, config 5 at N > 1: every rank counts its contiguous share of the histogram
     kernel's tiles; the partial histograms (no communicator: the caller sums) add up to the
