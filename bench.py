@@ -27,7 +27,7 @@ codes. Metric: codewords evaluated per second (BASELINE.json `metric`).
            separate pass with one loop at a time): achieved
            codewords/s vs the integer issue-rate roofline of its op mix: ALU pipe
            (LOP3, 64/clk/SM) and XU pipe (POPC, 16/clk/SM) rates measured on B200
-           (profiles/r01_pipes_microbench.jsonl) over the ops per codeword ncu counts.
+           (profiles/r02_pipes_microbench.jsonl) over the ops per codeword ncu counts.
 * cpu_baseline — the reference's own engine (oracle/_ref, unmodified sources)
            on this host's cores, one code of the same workload.
 
@@ -50,15 +50,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 N, K, SEEDS = 128, 64, list(range(1, 9))
-POPC_PER_S_MEASURED = 4642.3e9   # profiles/r01_pipes_microbench.jsonl (B200, 148 SMs): XU pipe
+POPC_PER_S_MEASURED = 4642.3e9   # profiles/r02_pipes_microbench.jsonl (B200, 148 SMs): XU pipe
 ALU_PER_S_MEASURED = 18146.5e9   # same file: LOP3 on the ALU pipe (64/clk/SM)
 # Pipe operations the bound-pruned level-7 round kernel executes per codeword, from the committed
-# ncu capture of that launch (profiles/r01m_tab_round_c7_ncu.txt: tab_round<2,false> on the
+# ncu capture of that launch (profiles/r02f_tab_round_c7_ncu.txt: tab_round<2,false> on the
 # config-2 seed-1 level-7 round at the loop's U = 16): ALU-pipe ops (3 LOP3 per pair bound,
 # vote min / compare, loop) and XU ops (POPC). The ALU pipe binds (83 % busy, XU 80 %).
-ALU_PER_CW_PRUNED = 2.320
+ALU_PER_CW_PRUNED = 2.321
 XU_PER_CW_PRUNED = 0.561
-DRAM_BYTES_PER_LAUNCH = 4244480  # same capture: dram__bytes_read.sum + dram__bytes_write.sum
+DRAM_BYTES_PER_LAUNCH = 4246272  # same capture: dram__bytes_read.sum + dram__bytes_write.sum
 WORKLOAD = "cfg2: random [128,64] codes G=(I|A), mt19937_64 seeds 1..8, BZ to termination (exact d)"
 
 
@@ -256,6 +256,7 @@ def strong_leg(mdg, torch, dist, rank, world, local, kernel, barrier, warm=1, st
             "ranks": world, "scaling": "strong", "steps": steps,
             "ms_per_run": tot / steps, "codewords": int(r.combinations),
             "cw_per_s": r.combinations / (tot / steps * 1e-3),
+            "h2d_bytes_per_run": int(r.h2d_bytes), "d2h_bytes_per_run": int(r.d2h_bytes),
             "levels": r.levels, "parity_cap6_vs_reference": bool(parity6),
             "parity_cap7_vs_reference": parity7,
             "path": "mdg_min_weight_dist (NCCL)" if world > 1 else "mdg_min_weight"}
@@ -545,7 +546,7 @@ def main():
                            f"1.81e13 LOP3/s / {ALU_PER_CW_PRUNED} ALU ops per codeword, XU pipe 16/clk/SM = "
                            f"4.64e12 POPC/s / {XU_PER_CW_PRUNED} POPC per codeword); rates measured on B200 "
                            "(tools/pipes_microbench.cu), ops per codeword from ncu "
-                           "(profiles/r01m_tab_round_c7_ncu.txt)"),
+                           "(profiles/r02f_tab_round_c7_ncu.txt)"),
             "peak_alu": peak_alu / 1e9, "peak_xu": peak_xu / 1e9,
             "op_mix_per_codeword": ("stage 1: one bound per pair of codewords, popc(fold_a & fold_b) with "
                                     "fold = OR of the words of X ^ Y, built in 3 LOP3 from per-pair constants "
@@ -572,7 +573,7 @@ def main():
                                     "roofline of that fixed unit, 4.64e12 POPC/s / 2; `frac` above is the "
                                     "pruned kernel's issue efficiency on its own op mix, which a better "
                                     "pruning stage can lower"),
-            "traffic_note": "DRAM 4.24 MB per launch (the tables, read once), 0.6% of HBM bandwidth: compute-bound",
+            "traffic_note": "DRAM 4.25 MB per launch (the tables, read once), 0.6% of HBM bandwidth: compute-bound",
             "hbm_check": hbm_check(achieved),
         }
         if clocks.get("sm_mhz"):
@@ -595,8 +596,13 @@ def main():
             except Exception as e:  # reported, never fatal
                 cpu = {"value": None, "unit": "cw/s", "cores": 0, "kind": "unavailable",
                        "sample": str(e)[:200]}
+        e2e_weak = {"value": e2e_value, "unit": "cw/s", "h2d_bytes_per_step": h2d // args.steps,
+                    "d2h_bytes_per_step": d2h // args.steps, "ms_per_step": tot_e2e / args.steps,
+                    "workload": WORKLOAD,
+                    "path": "mdg_min_weight_batch (C ABI) from pinned host matrices: row basis + Gamma "
+                            "search + H2D + level loop + witness + D2H"}
         weak = {"value": value, "unit": "cw/s", "ms_per_step": tot_ms / args.steps,
-                "workload": WORKLOAD, "scaling": "weak",
+                "workload": WORKLOAD, "scaling": "weak", "e2e": e2e_weak,
                 "parallelism": (f"{world} ranks, each running the eight-code step ({args.streams} "
                                 "codes in flight per GPU); independent codes, no data-path collective"
                                 if world > 1 else
@@ -629,13 +635,16 @@ def main():
             "weak_step": weak if world > 1 else None,
             "strong": strong,
             "configs": configs,
-            "e2e": {"value": e2e_value, "unit": "cw/s", "h2d_bytes_per_step": h2d // args.steps,
-                    "d2h_bytes_per_step": d2h // args.steps,
-                    "ms_per_step": tot_e2e / args.steps,
-                    "workload": WORKLOAD,
-                    "path": "mdg_min_weight_batch (C ABI)" +
-                            " from pinned host matrices: row basis + Gamma search + H2D + level loop"
-                            " + witness + D2H"},
+            # N > 1: the strong leg IS the front-door call on a host matrix (row basis, Gamma
+            # search, H2D, split level loop, witness, D2H inside its timed region), so the
+            # headline is its own end-to-end number; the eight-code e2e stays in weak_step
+            "e2e": ({"value": strong["cw_per_s"], "unit": "cw/s",
+                     "h2d_bytes_per_step": strong["h2d_bytes_per_run"],
+                     "d2h_bytes_per_step": strong["d2h_bytes_per_run"],
+                     "ms_per_step": strong["ms_per_run"], "workload": strong["workload"],
+                     "path": "mdg_min_weight_dist (C ABI) from the host matrix, per rank: row basis + Gamma "
+                             "search + H2D + split level loop (NCCL) + witness + D2H"}
+                    if headline_strong else e2e_weak),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "clocks": clocks,

@@ -352,10 +352,13 @@ __global__ void tables_build(const __grid_constant__ TableJobs J, const uint64_t
 // the fast path (U <= L) and termination (L >= U) exactly as the host loop.
 struct ChainState {
     uint32_t U, L, done, exact;
+    uint32_t run, pad;     // run: the chain_loop call's id, stamped into every record it closes
+    unsigned long long t0; // %globaltimer at the loop's start (chain_stamp)
 };
 struct ChainRec {
     uint32_t c, j, w, U_after, bounded, ran, L_after, level_end;
     unsigned long long key, evaluated, t_ns; // t_ns: %globaltimer when the round closed
+    unsigned long long run;                  // ChainState::run of the loop that closed the round
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -374,6 +377,7 @@ __device__ __forceinline__ void finalize_round(ChainState* st, const unsigned lo
     ChainRec r{};
     r.c = c;
     r.j = j;
+    r.run = st->run;
     r.t_ns = globaltimer_ns();
     if (st->done || st->U <= st->L) { // fast path: the round is not run, the loop ends
         st->done = 1;
@@ -2398,7 +2402,16 @@ struct PlanEntry {
     uint8_t* d_tr = nullptr; // per-pivot orientation (null: all normal)
 };
 
-constexpr int kSlots = 4096; // per-round scratch slots {best key, evaluated, counter, find, blocks done}
+// per-round scratch slots {best key, evaluated, counter, find, blocks done}: a ring of kSlots
+// (MDG_SLOTS shrinks it so tests wrap it often), re-initialized by one kernel per wrap
+constexpr int kSlots = 4096;
+static int ring_slots() {
+    static const int n = [] {
+        const char* e = std::getenv("MDG_SLOTS");
+        return e ? std::max(2 * (kMaxFuse + 2), std::min(kSlots, std::atoi(e))) : kSlots;
+    }();
+    return n;
+}
 
 struct Engine::Impl {
     cudaStream_t stream = nullptr;
@@ -2422,7 +2435,9 @@ struct Engine::Impl {
     uint64_t* binom = nullptr;
     unsigned long long* slots = nullptr;
     unsigned long long* host_slot = nullptr; // pinned, 4 words
-    int next_slot = kSlots;                  // forces an init on first use
+    int nslots = ring_slots();
+    int next_slot = kSlots;                  // >= nslots: forces an init on first use
+    uint32_t chain_runs = 0;                 // chain_loop calls so far (ChainState::run)
     unsigned long long* hist_dev = nullptr;
     size_t hist_cap = 0;
     std::vector<GammaDev> gammas;
@@ -2453,13 +2468,22 @@ struct Engine::Impl {
         return evpool[i];
     }
 
-    unsigned long long* take_slot() {
-        if (next_slot >= kSlots) {
-            init_slots<<<(kSlots + 255) / 256, 256, 0, stream>>>(slots, kSlots);
+    // The ring is re-initialized (in stream order) when it wraps, so a slot must be USED by a
+    // launch enqueued before the next re-initialization: a launch that needs several slots
+    // reserves them first, so the wrap cannot fall between its take_slot calls. (Taken one by
+    // one, a fused level's first slots could predate the re-initialization that its launch
+    // then followed: they were written after it and stayed dirty for the ring's next cycle --
+    // a stale lighter key then won that later round's atomicMin.)
+    void reserve_slots(int n) {
+        if (next_slot + n > nslots) {
+            init_slots<<<(nslots + 255) / 256, 256, 0, stream>>>(slots, nslots);
             CK(cudaGetLastError());
             cnt.launches += 1;
             next_slot = 0;
         }
+    }
+    unsigned long long* take_slot() {
+        reserve_slots(1);
         return slots + 8 * size_t(next_slot++);
     }
     void read_slot(unsigned long long* slot) {
@@ -3181,7 +3205,13 @@ std::vector<uint32_t> Engine::witness(uint32_t j, uint32_t c, const RoundResult&
         im.read_slot(slot);
         CK(cudaStreamSynchronize(im.stream));
         uint64_t f = im.host_slot[3];
-        if (f == ~0ull) throw std::logic_error("witness: winning tile holds no codeword of the round minimum");
+        if (f == ~0ull) {
+            char buf[160];
+            std::snprintf(buf, sizeof buf, " (key 0x%llx, plan tag %u, task %llu of %llu, weight %u, slot %d)",
+                          (unsigned long long)rr.key, rr.plan_tag, (unsigned long long)task,
+                          (unsigned long long)pe.plan.tiles(), target, im.next_slot);
+            throw std::logic_error(std::string("witness: winning tile holds no codeword of the round minimum") + buf);
+        }
         tab_decode(pe.plan, task, uint32_t(f >> 32), uint32_t(f & 0xFFFFFFFFu), idx.data());
     }
     // the decoded rows must have the key's weight (compacted XOR + identity rows), else the
@@ -3220,8 +3250,9 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
     Impl& im = *impl_;
     // host work per check: ~2e8 codewords (~0.1 ms of device time) between looks at `done`
     constexpr double kCheckWork = 2e8;
-    ChainState init{U0, L0 < 1 ? 1u : L0, 0u, exact ? 1u : 0u};
+    ChainState init{U0, L0 < 1 ? 1u : L0, 0u, exact ? 1u : 0u, 0u, 0u, 0ull};
     init.done = init.U <= init.L ? 1u : 0u;
+    init.run = ++im.chain_runs;
     *im.h_state = init;
     CK(cudaMemcpyAsync(im.d_state, im.h_state, sizeof(ChainState), cudaMemcpyHostToDevice, im.stream));
     im.cnt.h2d += sizeof(ChainState);
@@ -3234,8 +3265,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
     ChainResult res;
     size_t nrec = 0;
     double pending = 0;
-    unsigned long long* t0_slot = im.take_slot();
-    chain_stamp<<<1, 32, 0, im.stream>>>(t0_slot);
+    chain_stamp<<<1, 32, 0, im.stream>>>(&im.d_state->t0);
     CK(cudaGetLastError());
     im.cnt.launches += 1;
     // Tables: those of the first levels in one launch up front (while the levels add up to
@@ -3303,6 +3333,9 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
         if (fuse_level) {
             const GammaDev& g0 = im.gammas[0];
             const PlanEntry& pe = im.plan(k_, g, g0, plan_sms_);
+#ifndef MDG_NO_SLOT_RESERVE // (test builds only: reproduces the round-2 ring hazard)
+            im.reserve_slots(int(m_) + 1); // the m rounds' slots + the scheduler's: one ring cycle
+#endif
             LevelDesc L{};
             L.m = m_;
             L.T = pe.plan.tiles();
@@ -3323,6 +3356,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
                 r.add_const = aj.add_const;
             }
             unsigned long long* ls = im.take_slot(); // shared counter + blocks done
+
             a.st = im.d_state;
             a.counter = ls + 2;
             a.blocks_done = ls + 4;
@@ -3424,10 +3458,8 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
     std::vector<ChainRec> recs(nrec);
     if (nrec)
         CK(cudaMemcpyAsync(recs.data(), im.d_recs, nrec * sizeof(ChainRec), cudaMemcpyDeviceToHost, im.stream));
-    unsigned long long t_start = 0;
-    CK(cudaMemcpyAsync(im.host_slot, t0_slot, 8, cudaMemcpyDeviceToHost, im.stream));
     CK(cudaStreamSynchronize(im.stream));
-    t_start = im.host_slot[0];
+    const unsigned long long t_start = im.h_state->t0;
     im.cnt.d2h += sizeof(ChainState) + nrec * sizeof(ChainRec);
     res.U = im.h_state->U;
     res.L = im.h_state->L;
@@ -3440,6 +3472,12 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
     unsigned long long prev = t_start;
     for (size_t i = 0; i < nrec; ++i) {
         const ChainRec& r = recs[i];
+        // every enqueued round must have been closed by THIS loop (its last block / finalize
+        // launch): a record left over from an earlier loop would be a silent wrong trace
+        if (r.run != init.run)
+            throw std::logic_error("chain_loop: round record " + std::to_string(i) + " was not closed on the device (run " +
+                                   std::to_string(r.run) + ", expected " + std::to_string(init.run) + "; c " +
+                                   std::to_string(r.c) + ", j " + std::to_string(r.j) + ")");
         const double ms = r.t_ns > prev ? double(r.t_ns - prev) * 1e-6 : 0.0;
         prev = r.t_ns;
         if (!r.ran) continue;
@@ -3494,6 +3532,7 @@ Engine::BruteResult Engine::brute_force(uint32_t k, uint32_t n, const uint64_t* 
     unsigned long long* fslot = im.take_slot();
     sa.tile_lo = key & ((uint64_t{1} << kKeyShift) - 1);
     sa.tile_hi = sa.tile_lo + 1;
+    sa.best_key = fslot; sa.evaluated = fslot + 1; sa.counter = fslot + 2; // (unused by the search)
     sa.find_out = fslot + 3;
     sa.find_target = br.d;
     dispatch_nw_hid<SpanLaunch>(g.nw, false, g.rows, a_rows, b_rows, ta, tb, sa, 2, im.stream, sms_);

@@ -1101,3 +1101,60 @@ def test_unit_column_elision_vs_oracle(mdg, device, kernel, monkeypatch):
                 assert popcount_rows(g, idx)[0] == w
     monkeypatch.delenv("MDG_NO_UNIT_ELISION", raising=False)
     assert partial >= 6
+
+
+_RING_WORKER = r"""
+import os, sys
+import numpy as np
+sys.path.insert(0, %(root)r)
+import paper_1911_08963_b200 as mdg
+from oracle import port
+rng = np.random.default_rng(%(seed)d)
+dev = mdg.Device(0)
+checked = bad = 0
+while checked < %(count)d:
+    k = int(rng.integers(3, 15)); n = int(rng.integers(k + 1, 4 * k + 20))
+    dens = float(rng.choice([0.1, 0.25, 0.5]))
+    dense = (rng.random((k, n)) < dens).astype(np.uint64)
+    rows = np.zeros((k, (n + 63) // 64), dtype=np.uint64)
+    for c in range(n):
+        rows[:, c // 64] |= dense[:, c] << np.uint64(c %% 64)
+    if port.rank(rows, n) != k:
+        continue
+    s = int(rng.integers(0, 1000))
+    ref = port.min_weight(rows, n, 10, s)
+    for kernel in (0, 1):
+        for exact in (True, False):
+            r = mdg.min_weight(rows, n, 10, s, kernel=kernel, device=dev, exact_rounds=exact)
+            U, want = n - k + 1, []
+            for c, j, w, u in ref.rounds:
+                want.append([c, j, w if exact else min(w, U), u])
+                U = u
+            if not (r.d == ref.d and r.levels == ref.levels and r.rounds == want and r.witness_ok):
+                bad += 1
+    checked += 1
+dev.close()
+print("RESULT", checked, bad, flush=True)
+"""
+
+
+@pytest.mark.parametrize("slots", [40, 61, 0])
+def test_slot_ring_wraps_keep_rounds_clean(slots):
+    """Hundreds of BZ runs on ONE context so the ring of per-round scratch slots wraps at every
+    alignment (MDG_SLOTS shrinks the ring: it then wraps every few levels): a fused level whose
+    slots straddled the wrap once left its first slots dirty for the ring's next cycle, and a
+    stale lighter key then won a later round's atomicMin (a wrong d after ~2,400 runs on one
+    context; found by tools/forced_sweep.py). d, both traces and the witness against the oracle."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT as ROOT_DIR
+    env = dict(os.environ)
+    if slots:
+        env["MDG_SLOTS"] = str(slots)
+    script = _RING_WORKER % {"root": ROOT_DIR, "seed": 11 + slots, "count": 150 if slots else 60}
+    p = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = next(ln for ln in p.stdout.splitlines() if ln.startswith("RESULT"))
+    _, checked, bad = line.split()
+    assert int(bad) == 0 and int(checked) >= 60, line
