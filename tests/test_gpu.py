@@ -1162,3 +1162,22 @@ def test_slot_ring_wraps_keep_rounds_clean(slots, seed, kmax):
     line = next(ln for ln in p.stdout.splitlines() if ln.startswith("RESULT"))
     _, checked, bad = line.split()
     assert int(bad) == 0 and int(checked) == 300, line
+
+
+@pytest.mark.parametrize("slots,seed", [(0, 21), (40, 22)])
+def test_soak_mixed_calls_on_one_context(slots, seed):
+    """tools/soak.py: a random mix of every public call (front door, batch, resident loops,
+    single / bounded / split rounds, witnesses, histograms whole and split, brute force,
+    rank-deficient inputs) on ONE long-lived context, each result against the C oracle; once
+    with the scratch ring shrunk so it wraps every few launches."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT as ROOT_DIR
+    env = dict(os.environ)
+    if slots:
+        env["MDG_SLOTS"] = str(slots)
+    p = subprocess.run([sys.executable, os.path.join(ROOT_DIR, "tools", "soak.py"), "400", str(seed)],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, (p.stdout[-1500:], p.stderr[-1500:])
+    assert "400 operations, 0 failures" in p.stdout
