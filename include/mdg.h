@@ -266,6 +266,21 @@ int mdg_nccl_unique_id(uint8_t id[128]);
 int mdg_nccl_init(mdg_ctx* ctx, const uint8_t id[128], uint32_t rank, uint32_t world);
 int mdg_nccl_reduce_min(void* ctx, uint64_t* keys, uint32_t count); /* mdg_reduce_fn; user = ctx */
 
+/* Cross-process shared bound ("a system-scope atomicMin into a peer-mapped
+ * word ... also polled by every block for early exit"; the reference merges worker-local minima
+ * only at join, parallel.cpp:20-31). Rank 0 creates a small ring of round-key words in its
+ * device memory and passes the 64-byte CUDA IPC handle to the other ranks (any transport: the
+ * NCCL / MPI / torch.distributed bootstrap), which map it (same GPU, or peers with native
+ * atomics over NVLink). From then on every split round of mdg_min_weight_dist / mdg_bz_loop_
+ * device_dist -- the chained NCCL loop and the callback loop alike -- also publishes each tile
+ * result into the round's shared word and polls it at every tile fetch: one rank's find lowers
+ * the others' pruning bound and fires their early exit. Results are unchanged (the round's key
+ * is still the reduction of the ranks' own keys); MDG_NO_SHARED_BOUND disables it. Every rank
+ * must create / open before the first split round and run the same sequence of split rounds. */
+int mdg_shared_bound_create(mdg_ctx* ctx, uint8_t handle[64]);
+int mdg_shared_bound_open(mdg_ctx* ctx, const uint8_t handle[64]);
+int mdg_shared_bound_close(mdg_ctx* ctx);
+
 /* In-process exchange group: `world` contexts in ONE process (on one device,
  * or on devices with peer access), each driven by its own thread, run the
  * same level loop; a split round's key is min-reduced by a stream-ordered

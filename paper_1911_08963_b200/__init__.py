@@ -115,6 +115,9 @@ SYMBOLS = {
     "mdg_round_bounded": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                     C.c_uint64, C.c_uint64, C.POINTER(_RoundOut)]),
     "mdg_round_hist": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, u64p, C.POINTER(_RoundOut)]),
+    "mdg_shared_bound_create": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8)]),
+    "mdg_shared_bound_open": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8)]),
+    "mdg_shared_bound_close": (C.c_int, [C.c_void_p]),
     "mdg_round_hist_dist": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, u64p,
                                       C.POINTER(_RoundOut), C.POINTER(C.c_int)]),
     "mdg_round_witness": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(_RoundOut), u32p]),
@@ -461,6 +464,20 @@ class Device:
         red = C.c_int(0)
         _check(lib().mdg_round_hist_dist(self._h, j, c, rank, world, hist, C.byref(o), C.byref(red)))
         return _round_out(o), hist, bool(red.value)
+
+    def shared_bound_create(self) -> bytes:
+        """Rank 0 of a multi-process run: create the shared round-key ring; returns its 64-byte
+        CUDA IPC handle for the other ranks' shared_bound_open (mdg_shared_bound_create)."""
+        buf = (C.c_uint8 * 64)()
+        _check(lib().mdg_shared_bound_create(self._h, buf))
+        return bytes(buf)
+
+    def shared_bound_open(self, handle: bytes):
+        buf = (C.c_uint8 * 64).from_buffer_copy(handle)
+        _check(lib().mdg_shared_bound_open(self._h, buf))
+
+    def shared_bound_close(self):
+        _check(lib().mdg_shared_bound_close(self._h))
 
     def round_witness(self, j: int, c: int, out: RoundOut) -> list:
         idx = np.zeros(c, dtype=np.uint32)

@@ -191,10 +191,11 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
             rr = eng.round(j, g, stop_at, 0, UINT64_MAX, cutoff);
         } else {
             const auto [lo, hi] = eng.split_range(j, g, rank, world);
-            rr = eng.round(j, g, stop_at, lo, hi, cutoff);
+            rr = eng.round(j, g, stop_at, lo, hi, cutoff, /*shared_bound=*/true);
             uint64_t key = rr.key;
             int rc = reduce(user, &key, 1);
             if (rc != 0) throw std::runtime_error("mdg: cross-rank reduction failed");
+            eng.shared_bound_advance(); // every rank has finished the round: the owner frees its word
             rr.key = key;
             rr.bounded = false;
             rr.w = key == ~0ull ? UINT32_MAX : uint32_t(key >> kKeyShift);
@@ -520,6 +521,27 @@ int mdg_round_hist(mdg_ctx* ctx, uint32_t j, uint32_t c, uint64_t* hist, mdg_rou
     return guard([&] {
         if (!ctx || !hist || !out) throw std::invalid_argument("null argument");
         fill_out(ctx->eng->round_hist(j, c, hist), out);
+    });
+}
+
+int mdg_shared_bound_create(mdg_ctx* ctx, uint8_t handle[64]) {
+    return guard([&] {
+        if (!ctx || !handle) throw std::invalid_argument("null argument");
+        ctx->eng->shared_bound_create(handle);
+    });
+}
+
+int mdg_shared_bound_open(mdg_ctx* ctx, const uint8_t handle[64]) {
+    return guard([&] {
+        if (!ctx || !handle) throw std::invalid_argument("null argument");
+        ctx->eng->shared_bound_open(handle);
+    });
+}
+
+int mdg_shared_bound_close(mdg_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) throw std::invalid_argument("null ctx");
+        ctx->eng->shared_bound_close();
     });
 }
 

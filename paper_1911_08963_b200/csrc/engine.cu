@@ -2438,6 +2438,22 @@ struct Engine::Impl {
     int nslots = ring_slots();
     int next_slot = kSlots;                  // >= nslots: forces an init on first use
     uint32_t chain_runs = 0;                 // chain_loop calls so far (ChainState::run)
+    // Cross-process shared bound (one process per GPU): a ring of round-key words in rank 0's
+    // device memory, mapped into the other ranks through a CUDA IPC handle. Entry i % kXRing
+    // serves the i-th split round; the owner resets it after that round's reduction.
+    static constexpr uint32_t kXRing = 64;
+    unsigned long long* xring = nullptr;
+    bool xowner = false;
+    uint64_t xround = 0; // split rounds so far (the same on every rank)
+    unsigned long long* xword() const {
+        static const bool off = std::getenv("MDG_NO_SHARED_BOUND") != nullptr;
+        return (xring && !off) ? xring + xround % kXRing : nullptr;
+    }
+    void xadvance() { // after a split round's reduction (every rank has finished the round)
+        if (!xring) return;
+        if (xowner) CK(cudaMemsetAsync(xring + xround % kXRing, 0xFF, sizeof(unsigned long long), stream));
+        ++xround;
+    }
     unsigned long long* hist_dev = nullptr;
     size_t hist_cap = 0;
     std::vector<GammaDev> gammas;
@@ -2560,6 +2576,9 @@ Engine::~Engine() {
         try { nccl().CommDestroy(impl_->comm); } catch (...) {}
     }
     if (impl_->group_ev) cudaEventDestroy(impl_->group_ev);
+    if (impl_->xring) {
+        if (impl_->xowner) cudaFree(impl_->xring); else cudaIpcCloseMemHandle(impl_->xring);
+    }
     cudaFree(impl_->red_dev);
     cudaFree(impl_->scratch);
     cudaFree(impl_->d_state);
@@ -3064,7 +3083,7 @@ uint64_t Engine::tasks(uint32_t j, uint32_t c) {
 }
 
 RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t task_lo, uint64_t task_hi,
-                          uint32_t cutoff) {
+                          uint32_t cutoff, bool shared_bound) {
     check_round(j, c);
     CK(cudaSetDevice(device_));
     Impl& im = *impl_;
@@ -3083,6 +3102,7 @@ RoundResult Engine::round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t tas
     a.cutoff = cutoff;
     a.tile_lo = lo; a.tile_hi = hi;
     a.best_key = slot; a.evaluated = slot + 1; a.counter = slot + 2;
+    if (shared_bound) a.shared_key = im.xword(); // a split round of a multi-process run
     CK(cudaEventRecord(im.ev0, im.stream));
     if (hi > lo) {
         dispatch_nw_hid<TabLaunch>(g.nw, g.hid, a, hi - lo, im.stream, 0, size_t(0), sms_);
@@ -3390,6 +3410,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
             a.best_key = slot; a.evaluated = slot + 1; a.counter = slot + 2;
             if (split && !im.comm && im.group && im.group->ring && im.group->ring_ok) // group: shared key
                 a.shared_key = im.group->ring + im.group_round % ExchangeGroup::kRing;
+            if (split && im.comm) a.shared_key = im.xword(); // processes: the IPC-mapped word, if any
             const bool fuse = !split && a.tile_hi > a.tile_lo;
             if (fuse) { // the round kernel's last block closes the round: one launch per round
                 a.fin_st = im.d_state;
@@ -3413,6 +3434,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
             if (split && im.comm) {
                 int rc = nccl().AllReduce(slot, slot, 1, kNcclUint64, kNcclMin, im.comm, im.stream);
                 if (rc != 0) throw std::runtime_error(std::string("ncclAllReduce: ") + nccl().GetErrorString(rc));
+                im.xadvance(); // the owner frees the shared word (stream order: after the reduction)
             } else if (split) { // in-process exchange group
                 CK(cudaEventRecord(im.group_ev, im.stream));
                 std::vector<unsigned long long*> all;
@@ -3560,6 +3582,44 @@ void Engine::set_kernel(Kernel kern) {
 }
 struct CUstream_st* Engine::stream() const { return impl_->stream; }
 bool Engine::has_comm() const { return impl_->comm != nullptr; }
+
+static_assert(sizeof(cudaIpcMemHandle_t) == 64, "mdg_shared_bound handles are 64 bytes");
+void Engine::shared_bound_create(uint8_t handle[64]) {
+    CK(cudaSetDevice(device_));
+    Impl& im = *impl_;
+    shared_bound_close();
+    CK(cudaMalloc(&im.xring, Impl::kXRing * sizeof(unsigned long long)));
+    CK(cudaMemset(im.xring, 0xFF, Impl::kXRing * sizeof(unsigned long long)));
+    im.xowner = true;
+    im.xround = 0;
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, im.xring));
+    std::memcpy(handle, &h, sizeof h);
+}
+void Engine::shared_bound_open(const uint8_t handle[64]) {
+    CK(cudaSetDevice(device_));
+    Impl& im = *impl_;
+    shared_bound_close();
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    im.xring = static_cast<unsigned long long*>(p);
+    im.xowner = false;
+    im.xround = 0;
+}
+void Engine::shared_bound_close() {
+    Impl& im = *impl_;
+    if (!im.xring) return;
+    CK(cudaSetDevice(device_));
+    CK(cudaStreamSynchronize(im.stream));
+    if (im.xowner) CK(cudaFree(im.xring)); else CK(cudaIpcCloseMemHandle(im.xring));
+    im.xring = nullptr;
+    im.xowner = false;
+    im.xround = 0;
+}
+void Engine::shared_bound_advance() { impl_->xadvance(); }
+bool Engine::has_shared_bound() const { return impl_->xring != nullptr; }
 void* Engine::scratch(size_t bytes) {
     Impl& im = *impl_;
     if (im.scratch_cap < bytes) {

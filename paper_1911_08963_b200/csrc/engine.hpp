@@ -97,13 +97,26 @@ public:
     // cutoff: only weights < cutoff matter (0 = the exact round minimum). With a
     // cutoff the result is min(true minimum, cutoff) and `bounded` is set when no
     // codeword lies below it — what run_bz_loop's U = min(U, w) needs.
+    // shared_bound: a split round of a multi-process run -- publish / poll the ranks' common
+    // round key (shared_bound_create / _open), if one is mapped
     RoundResult round(uint32_t j, uint32_t c, uint32_t stop_at, uint64_t task_lo = 0,
-                      uint64_t task_hi = UINT64_MAX, uint32_t cutoff = 0);
+                      uint64_t task_hi = UINT64_MAX, uint32_t cutoff = 0, bool shared_bound = false);
     // rank / world: this rank's contiguous share of the histogram kernel's tiles (about 1/world
     // of the codewords); with an NCCL communicator attached the counts are summed across the
     // ranks in stream, otherwise `hist` is this rank's partial histogram
     RoundResult round_hist(uint32_t j, uint32_t c, uint64_t* hist, uint32_t rank = 0, uint32_t world = 1);
     bool has_comm() const;
+    // Cross-process shared bound: rank 0 creates a ring of round-key words
+    // and hands its CUDA IPC handle to the other ranks (one process per GPU), which map it.
+    // In every split round each tile result is also atomicMin_system-ed into the round's word
+    // and every tile fetch polls it: one rank's find prunes and stops the others. The round's
+    // result stays the reduction of the ranks' own keys. advance(): after a split round's
+    // reduction (host-loop callers; the chained NCCL loop does it in stream).
+    void shared_bound_create(uint8_t handle[64]);
+    void shared_bound_open(const uint8_t handle[64]);
+    void shared_bound_close();
+    void shared_bound_advance();
+    bool has_shared_bound() const;
 
     // The whole level loop with rounds chained on the stream (either kernel):
     // a device-side state carries U / L / done, a finalize kernel per round

@@ -1181,3 +1181,88 @@ def test_soak_mixed_calls_on_one_context(slots, seed):
                        env=env, capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, (p.stdout[-1500:], p.stderr[-1500:])
     assert "400 operations, 0 failures" in p.stdout
+
+
+_XB_WORKER = r"""
+import json, os, sys
+sys.path.insert(0, %(root)r)
+sys.path.insert(0, os.path.join(%(root)r, "tests"))
+import numpy as np
+import torch.distributed as dist
+import paper_1911_08963_b200 as mdg
+from conftest import load_golden
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+dist.init_process_group("gloo", rank=rank, world_size=world)
+dev = mdg.Device(0)
+h = [dev.shared_bound_create() if rank == 0 else None]
+dist.broadcast_object_list(h, src=0)
+if rank != 0:
+    dev.shared_bound_open(h[0])
+dist.barrier()
+
+def red(keys):  # element-wise u64 min over the ranks (the callback loop: one exchange per split round)
+    out = [None] * world
+    dist.all_gather_object(out, keys.copy())
+    return np.minimum.reduce(out)
+
+cases = {c["name"]: c for c in load_golden("configs")}
+out = []
+for name in ("cfg1", "cfg2_s8", "cfg2_s1"):
+    case = cases[name]
+    g = case["gen"]
+    G = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
+    for split_min in (1, 10**6):
+        r = mdg.min_weight_dist(G, g["n"], rank, world, red, trials=10, seed=g["seed"], device=dev,
+                                split_min=split_min)
+        out.append({"name": name, "split_min": split_min, "d": r.d, "rounds": r.rounds, "levels": r.levels,
+                    "gamma_hash": r.gamma_hash, "witness_ok": r.witness_ok, "evaluated": r.evaluated})
+dist.barrier()
+dev.shared_bound_close()
+dev.close()
+print("RESULT " + json.dumps(out), flush=True)
+dist.destroy_process_group()
+"""
+
+
+def test_shared_bound_across_processes():
+    """SURVEY.md 8e (i) across processes: two processes on this GPU share the round-key ring
+    through a CUDA IPC handle (mdg_shared_bound_create / _open); every split round publishes its
+    tile results there and polls it. d, traces, Gamma set and witness equal the goldens on both
+    ranks, with the shared bound on and off (MDG_NO_SHARED_BOUND); with it the ranks together
+    evaluate no more codewords than without (one rank's find stops the other)."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    from conftest import ROOT as ROOT_DIR
+    cases = {c["name"]: c for c in load_golden("configs")}
+    totals = {}
+    for off in (False, True):
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port_no = sk.getsockname()[1]
+        procs = []
+        for r in range(2):
+            env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+            if off:
+                env["MDG_NO_SHARED_BOUND"] = "1"
+            procs.append(subprocess.Popen([sys.executable, "-c", _XB_WORKER % {"root": ROOT_DIR}], env=env,
+                                          stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+        outs = []
+        for p in procs:
+            o, e = p.communicate(timeout=600)
+            assert p.returncode == 0, e[-2000:]
+            outs.append(json.loads(next(ln for ln in o.splitlines() if ln.startswith("RESULT "))[7:]))
+        for rank_out in outs:
+            for rec in rank_out:
+                case = cases[rec["name"]]
+                U, want = case["n"] - case["k"] + 1, []
+                for c, j, w, ua in case["rounds"]:
+                    want.append([c, j, min(w, U), ua])
+                    U = ua
+                assert rec["d"] == case["d"] and rec["rounds"] == want and rec["levels"] == case["levels"], rec["name"]
+                assert rec["gamma_hash"] == case["gamma_hash"] and rec["witness_ok"], rec["name"]
+        totals[off] = sum(rec["evaluated"] for rank_out in outs for rec in rank_out if rec["split_min"] == 1)
+    print(f"codewords evaluated over the split runs, both ranks: shared bound {totals[False]}, off {totals[True]}")
+    assert totals[False] <= totals[True] * 1.01, totals
