@@ -1,6 +1,6 @@
 """Randomized soak of ONE long-lived context (development tool): a random mix of the public calls
 -- front door (both kernels, both round modes, level caps), batch front door, device-resident
-loops, single rounds (whole, bounded, split into task ranges), witnesses, histograms (whole and
+loops, one code split across several contexts (exchange group), single rounds (whole, bounded, split into task ranges), witnesses, histograms (whole and
 split across ranks), brute force -- on random codes, every result against the C oracle. Meant to
 be run with MDG_SLOTS small as well (the scratch ring then wraps every few launches).
 Usage: python tools/soak.py ITERATIONS SEED"""
@@ -16,6 +16,7 @@ from oracle import port  # noqa: E402
 iters, seed = int(sys.argv[1]), int(sys.argv[2])
 rng = np.random.default_rng(seed)
 dev = mdg.Device(0)
+group = [mdg.Device(0) for _ in range(3)]  # long-lived members of the in-process exchange group
 bad = []
 
 
@@ -56,7 +57,7 @@ def check(ok, what):
 
 
 for it in range(iters):
-    op = int(rng.integers(0, 8))
+    op = int(rng.integers(0, 9))
     try:
         if op == 0:  # front door
             rows, n, k = rand_code()
@@ -124,6 +125,17 @@ for it in range(iters):
             rows, n, k = rand_code(14)
             r = mdg.brute_force(rows, n, device=dev)
             check(r.d == port.brute(rows, n) and r.witness_ok, ("brute", it, n, k))
+        elif op == 8:  # one code split across 2-3 contexts (exchange group), every round or some
+            rows, n, k = rand_code()
+            s = int(rng.integers(0, 1000))
+            world = int(rng.integers(2, 4))
+            split_min = int(rng.choice([1, 200, 5000]))
+            ref = port.min_weight(rows, n, 10, s)
+            runs = mdg.min_weight_multi(rows, n, group[:world], trials=10, seed=s, split_min=split_min,
+                                        kernel=int(rng.integers(0, 2)))
+            for r in runs:
+                check(r.d == ref.d and r.rounds == expect_rounds(ref, n, k, False) and r.levels == ref.levels and
+                      r.witness_ok, ("multi", it, n, k, s, world, split_min))
         else:  # rank-deficient input through the front door
             rows, n, k = rand_code(12, full_rank=False)
             extra = rows[rng.integers(0, k, size=3)]
