@@ -53,7 +53,7 @@ N, K, SEEDS = 128, 64, list(range(1, 9))
 POPC_PER_S_MEASURED = 4642.3e9   # profiles/r02_pipes_microbench.jsonl (B200, 148 SMs): XU pipe
 ALU_PER_S_MEASURED = 18146.5e9   # same file: LOP3 on the ALU pipe (64/clk/SM)
 # Pipe operations the bound-pruned level-7 round kernel executes per codeword, from the committed
-# ncu capture of that launch (profiles/r02f_tab_round_c7_ncu.txt: tab_round<2,false> on the
+# ncu capture of that launch (profiles/r02g_tab_round_c7_ncu.txt: tab_round<2,false> on the
 # config-2 seed-1 level-7 round at the loop's U = 16): ALU-pipe ops (3 LOP3 per pair bound,
 # vote min / compare, loop) and XU ops (POPC). The ALU pipe binds (83 % busy, XU 80 %).
 ALU_PER_CW_PRUNED = 2.321
@@ -546,7 +546,7 @@ def main():
                            f"1.81e13 LOP3/s / {ALU_PER_CW_PRUNED} ALU ops per codeword, XU pipe 16/clk/SM = "
                            f"4.64e12 POPC/s / {XU_PER_CW_PRUNED} POPC per codeword); rates measured on B200 "
                            "(tools/pipes_microbench.cu), ops per codeword from ncu "
-                           "(profiles/r02f_tab_round_c7_ncu.txt)"),
+                           "(profiles/r02g_tab_round_c7_ncu.txt)"),
             "peak_alu": peak_alu / 1e9, "peak_xu": peak_xu / 1e9,
             "op_mix_per_codeword": ("stage 1: one bound per pair of codewords, popc(fold_a & fold_b) with "
                                     "fold = OR of the words of X ^ Y, built in 3 LOP3 from per-pair constants "
