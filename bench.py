@@ -630,6 +630,8 @@ def main():
                                     "is the exact-weight kernel on a fixed unit)"),
                        "l2": "flushed between steps (256 MiB write); working set < 1 MiB",
                        "codewords_per_step": cw_total // args.steps,
+                       "ms_step_min_median_max": [min(ms_steps), statistics.median(ms_steps), max(ms_steps)],
+                       "e2e_ms_step_min_median_max": [min(e2e_ms), statistics.median(e2e_ms), max(e2e_ms)],
                        "ms_per_code_amortized": tot_ms / args.steps / len(SEEDS),
                        "d": expect_d},
             "weak_step": weak if world > 1 else None,
