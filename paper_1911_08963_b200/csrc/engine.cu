@@ -385,7 +385,7 @@ __device__ __forceinline__ void finalize_round(ChainState* st, const unsigned lo
         volatile uint32_t* p = st->progress;
         // posted writes, no fence: the host only polls them opportunistically (a system-scope
         // fence here cost ~2 % of the eight-code bench: it sits between a level and the next)
-        if (st->done) p[1] = 1u;
+        if (st->done) p[1] = st->run; // tagged with the loop's id: a straggler of an earlier loop cannot end this one
         if (levels_closed) p[0] = levels_closed;
     };
     if (st->done || st->U <= st->L) { // fast path: the round is not run, the loop ends
@@ -3302,6 +3302,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
         return e ? uint32_t(std::max(0, std::atoi(e))) : 0u;
     }();
     volatile uint32_t* prog = nullptr;
+    bool stopped_on_progress = false;
     if (!allreduce) {
         im.h_progress[0] = 0; // the stream is idle of earlier loops' writers (each loop ends synchronized)
         im.h_progress[1] = 0;
@@ -3360,14 +3361,15 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
         if (level_cap && g > level_cap) break;
         if (prog) { // stop on `done`; optionally at most kAhead levels beyond the last closed one
             const auto t_wait = std::chrono::steady_clock::now();
-            while (kAhead > 0 && !prog[1] && g > prog[0] + kAhead) {
+            while (kAhead > 0 && prog[1] != init.run && g > prog[0] + kAhead) {
                 if (std::chrono::steady_clock::now() - t_wait > std::chrono::milliseconds(2)) {
                     CK(cudaStreamSynchronize(im.stream)); // a long level: block instead of spinning
                     break;
                 }
             }
-            if (prog[1]) { // closed on the device: nothing more to enqueue
+            if (prog[1] == init.run) { // closed on the device: nothing more to enqueue
                 done = true;
+                stopped_on_progress = true;
                 break;
             }
         }
@@ -3537,6 +3539,8 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
     res.L = im.h_state->L;
     res.plan_tag = plan_tag(im.rd, im.prune);
     res.done = im.h_state->done != 0;
+    if (stopped_on_progress && !res.done)
+        throw std::logic_error("chain_loop: the progress word reported termination but the loop state is not done");
     // run_bz_loop: capped when the loop reaches level cap + 1 (<= k) without being done
     res.capped = !res.done && level_cap && level_cap < k_ && g > level_cap;
     // per-round device time: between consecutive round closes (device clock;

@@ -1164,12 +1164,13 @@ def test_slot_ring_wraps_keep_rounds_clean(slots, seed, kmax):
     assert int(bad) == 0 and int(checked) == 300, line
 
 
-@pytest.mark.parametrize("slots,seed", [(0, 21), (40, 22)])
-def test_soak_mixed_calls_on_one_context(slots, seed):
+@pytest.mark.parametrize("slots,seed,ahead", [(0, 21, 0), (40, 22, 0), (0, 23, 1)])
+def test_soak_mixed_calls_on_one_context(slots, seed, ahead):
     """tools/soak.py: a random mix of every public call (front door, batch, resident loops,
     single / bounded / split rounds, witnesses, histograms whole and split, brute force,
-    rank-deficient inputs) on ONE long-lived context, each result against the C oracle; once
-    with the scratch ring shrunk so it wraps every few launches."""
+    rank-deficient inputs, one code split across several contexts) on ONE long-lived context,
+    each result against the C oracle; once with the scratch ring shrunk so it wraps every few
+    launches, once with at most one level in flight beyond the last closed one."""
     import os
     import subprocess
     import sys
@@ -1177,6 +1178,8 @@ def test_soak_mixed_calls_on_one_context(slots, seed):
     env = dict(os.environ)
     if slots:
         env["MDG_SLOTS"] = str(slots)
+    if ahead:  # the chained loop's levels-in-flight throttle (off by default)
+        env["MDG_LEVELS_AHEAD"] = str(ahead)
     p = subprocess.run([sys.executable, os.path.join(ROOT_DIR, "tools", "soak.py"), "400", str(seed)],
                        env=env, capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, (p.stdout[-1500:], p.stderr[-1500:])
