@@ -24,6 +24,9 @@ def rand_code(kmax=20, full_rank=True):
     while True:
         k = int(rng.integers(2, kmax))
         n = int(rng.integers(k + 1, 4 * k + 24))
+        if rng.random() < 0.15:  # a wide code: every row width of the kernels (up to 32 words)
+            k = int(rng.integers(2, min(kmax, 9)))
+            n = int(rng.integers(100, 1025))
         dens = float(rng.choice([0.08, 0.25, 0.5]))
         dense = (rng.random((k, n)) < dens).astype(np.uint64)
         rows = np.zeros((k, (n + 63) // 64), dtype=np.uint64)
