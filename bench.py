@@ -53,7 +53,7 @@ N, K, SEEDS = 128, 64, list(range(1, 9))
 POPC_PER_S_MEASURED = 4642.3e9   # profiles/r02_pipes_microbench.jsonl (B200, 148 SMs): XU pipe
 ALU_PER_S_MEASURED = 18146.5e9   # same file: LOP3 on the ALU pipe (64/clk/SM)
 # Pipe operations the bound-pruned level-7 round kernel executes per codeword, from the committed
-# ncu capture of that launch (profiles/r02g_tab_round_c7_ncu.txt: tab_round<2,false> on the
+# ncu capture of that launch (profiles/r02h_tab_round_c7_ncu.txt: tab_round<2,false> on the
 # config-2 seed-1 level-7 round at the loop's U = 16): ALU-pipe ops (3 LOP3 per pair bound,
 # vote min / compare, loop) and XU ops (POPC). The ALU pipe binds (83 % busy, XU 80 %).
 ALU_PER_CW_PRUNED = 2.321
@@ -386,14 +386,19 @@ def main():
 
     def device_step():
         """This rank's level loops over the resident Gamma sets: with --streams > 1 up to that
-        many codes run at once, each context on its own stream (ctypes releases the GIL);
+        many codes run at once, each context on its own stream (mdg_bz_loop_device_batch);
         CUDA events on the torch stream bracket the whole step."""
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
         if args.streams <= 1:
             runs = [one_loop(x) for x in range(len(devs))]
-        else:
+        elif os.environ.get("MDG_BENCH_PYTHON_POOL"):  # the former path: Python threads over bz_loop
             runs = list(pool.map(one_loop, range(len(devs))))
+        else:  # mdg_bz_loop_device_batch: the library's own worker threads
+            runs = mdg.bz_loop_batch(devs, gsets, kernel=kernel, streams=args.streams)
+            for x, r in enumerate(runs):
+                if r.d != expect_d[mine[x]] or not r.witness_ok:
+                    raise SystemExit(f"parity failure on seed {SEEDS[mine[x]]}: d={r.d}")
         ev1.record()
         torch.cuda.synchronize()
         return ev0.elapsed_time(ev1), sum(r.evaluated for r in runs), sum(r.launches for r in runs)
@@ -546,7 +551,7 @@ def main():
                            f"1.81e13 LOP3/s / {ALU_PER_CW_PRUNED} ALU ops per codeword, XU pipe 16/clk/SM = "
                            f"4.64e12 POPC/s / {XU_PER_CW_PRUNED} POPC per codeword); rates measured on B200 "
                            "(tools/pipes_microbench.cu), ops per codeword from ncu "
-                           "(profiles/r02g_tab_round_c7_ncu.txt)"),
+                           "(profiles/r02h_tab_round_c7_ncu.txt)"),
             "peak_alu": peak_alu / 1e9, "peak_xu": peak_xu / 1e9,
             "op_mix_per_codeword": ("stage 1: one bound per pair of codewords, popc(fold_a & fold_b) with "
                                     "fold = OR of the words of X ^ Y, built in 3 LOP3 from per-pair constants "

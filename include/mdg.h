@@ -233,6 +233,12 @@ int mdg_min_weight_batch(mdg_ctx* ctx, uint32_t count, const uint64_t* const* G,
 /* The level loop over the Gamma set already loaded into ctx (mdg_load_gset):
  * the device-resident variant of the front door (no Gamma search, no upload). */
 int mdg_bz_loop_device(mdg_ctx* ctx, const mdg_gset* gs, const mdg_config* cfg, mdg_run** out);
+/* mdg_bz_loop_device for `count` codes at once: code i's Gamma set gs[i] is resident in ctxs[i]
+ * (distinct contexts, one device or several), up to `streams` loops in flight from the
+ * library's own worker threads (0 = 4). out[i] equals mdg_bz_loop_device(ctxs[i], gs[i], cfg).
+ * No reference counterpart (one matrix per call there); cfg NULL = defaults for all. */
+int mdg_bz_loop_device_batch(mdg_ctx* const* ctxs, const mdg_gset* const* gs, uint32_t count,
+                             const mdg_config* cfg, uint32_t streams, mdg_run** out);
 int mdg_bz_loop_device_dist(mdg_ctx* ctx, const mdg_gset* gs, const mdg_config* cfg,
                             uint32_t rank, uint32_t world, mdg_reduce_fn reduce_min, void* user,
                             mdg_run** out);

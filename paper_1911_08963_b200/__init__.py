@@ -25,7 +25,7 @@ import numpy as np
 __all__ = [
     "MdgError", "InvalidArgument", "OverflowError_", "CudaFailure", "lib", "Device", "GammaSet",
     "RoundOut", "RunResult", "min_weight", "min_weight_dist", "min_weight_multi", "run_bz_loop", "lower_bound",
-    "singleton_upper", "brute_force", "nccl_unique_id", "parse_matrix", "serialize_matrix", "gen_matrix", "binomial",
+    "singleton_upper", "brute_force", "bz_loop_batch", "nccl_unique_id", "parse_matrix", "serialize_matrix", "gen_matrix", "binomial",
     "rd_unrank", "rd_rank", "hash_rows", "rank_of", "words", "KERNEL_TAB", "KERNEL_RD",
 ]
 
@@ -147,6 +147,8 @@ SYMBOLS = {
                                       C.c_void_p, C.POINTER(C.c_void_p)]),
     "mdg_min_weight_batch": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.POINTER(C.c_uint64)), u32p, u32p,
                                        C.POINTER(_Config), C.c_uint32, C.POINTER(C.c_void_p)]),
+    "mdg_bz_loop_device_batch": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_uint32,
+                                           C.POINTER(_Config), C.c_uint32, C.POINTER(C.c_void_p)]),
     "mdg_bz_loop_device": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(_Config),
                                      C.POINTER(C.c_void_p)]),
     "mdg_bz_loop_device_dist": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(_Config), C.c_uint32,
@@ -707,6 +709,22 @@ def min_weight_dist(G: np.ndarray, n: int, rank: int, world: int,
                                      C.byref(cfg), rank, world, fn, user, C.byref(h)))
     del keep
     return _collect(h)
+
+
+def bz_loop_batch(devices: list, gsets: list, level_cap: int = 0, kernel: int = KERNEL_TAB,
+                  witness: bool = True, exact_rounds: bool = False, streams: int = 4) -> list:
+    """Device-resident level loops of many codes at once (mdg_bz_loop_device_batch): gsets[i] is
+    loaded in devices[i] (distinct Device objects), up to `streams` loops in flight from the
+    library's worker threads. Returns one RunResult per code, each equal to Device.bz_loop's."""
+    count = len(devices)
+    if len(gsets) != count:
+        raise InvalidArgument("bz_loop_batch: one Gamma set per device")
+    cfg = _config(0, 0, level_cap, kernel, witness, exact_rounds)
+    ctxs = (C.c_void_p * max(1, count))(*[d.handle.value for d in devices])
+    gss = (C.c_void_p * max(1, count))(*[g._h.value for g in gsets])
+    hs = (C.c_void_p * max(1, count))()
+    _check(lib().mdg_bz_loop_device_batch(ctxs, gss, count, C.byref(cfg), streams, hs))
+    return [_collect(C.c_void_p(hs[i])) for i in range(count)]
 
 
 def min_weight_multi(G: np.ndarray, n: int, devices: list, trials: int = 10, seed: int = 0,

@@ -6,7 +6,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
 #include <exception>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <memory>
 #include <optional>
@@ -745,6 +748,83 @@ int mdg_min_weight_dist(mdg_ctx* ctx, const uint64_t* G, uint32_t k, uint32_t n,
     });
 }
 
+namespace {
+// Workers of the batch front doors, kept between calls (spawning three threads per call cost
+// ~0.1 ms of a 2 ms eight-code step). run(S, fn) runs fn(0) on the caller and fn(1..S-1) on pool
+// threads and returns when all are done; a second batch call arriving meanwhile spawns its own
+// threads instead of waiting.
+class BatchPool {
+public:
+    static BatchPool& get() {
+        static BatchPool p;
+        return p;
+    }
+    void run(uint32_t S, const std::function<void(uint32_t)>& fn) {
+        if (S <= 1) {
+            fn(0);
+            return;
+        }
+        std::unique_lock<std::mutex> busy(busy_, std::try_to_lock);
+        if (!busy.owns_lock()) { // pool in use by another caller: plain threads
+            std::vector<std::thread> th;
+            for (uint32_t w = 1; w < S; ++w) th.emplace_back(fn, w);
+            fn(0);
+            for (auto& t : th) t.join();
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            while (workers_.size() + 1 < S) workers_.emplace_back([this, id = uint32_t(workers_.size() + 1)] { loop(id); });
+            fn_ = &fn;
+            want_ = S;
+            pending_ = S - 1;
+            ++epoch_;
+        }
+        cv_.notify_all();
+        fn(0);
+        std::unique_lock<std::mutex> lk(m_);
+        done_.wait(lk, [this] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+
+private:
+    BatchPool() = default;
+    ~BatchPool() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+    void loop(uint32_t id) {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(uint32_t)>* fn = nullptr;
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return stop_ || (epoch_ != seen && id < want_); });
+                if (stop_) return;
+                seen = epoch_;
+                fn = fn_;
+            }
+            (*fn)(id);
+            {
+                std::lock_guard<std::mutex> lk(m_);
+                if (--pending_ == 0) done_.notify_one();
+            }
+        }
+    }
+    std::mutex busy_, m_;
+    std::condition_variable cv_, done_;
+    std::vector<std::thread> workers_;
+    const std::function<void(uint32_t)>* fn_ = nullptr;
+    uint32_t want_ = 0, pending_ = 0;
+    uint64_t epoch_ = 0;
+    bool stop_ = false;
+};
+} // namespace
+
 int mdg_min_weight_batch(mdg_ctx* ctx, uint32_t count, const uint64_t* const* G, const uint32_t* k,
                          const uint32_t* n, const mdg_config* cfg, uint32_t streams,
                          mdg_run** out) {
@@ -767,7 +847,7 @@ int mdg_min_weight_batch(mdg_ctx* ctx, uint32_t count, const uint64_t* const* G,
         static const bool timing = std::getenv("MDG_TIMING") != nullptr;
         const auto t_batch = std::chrono::steady_clock::now();
         std::atomic<uint32_t> next{0};
-        auto worker = [&](uint32_t w) {
+        const std::function<void(uint32_t)> worker = [&](uint32_t w) {
             Engine& eng = w == 0 ? *ctx->eng : *ctx->extra[w - 1];
             try {
                 for (uint32_t i; (i = next.fetch_add(1)) < count;) {
@@ -788,10 +868,45 @@ int mdg_min_weight_batch(mdg_ctx* ctx, uint32_t count, const uint64_t* const* G,
                 next.store(count); // stop handing out codes
             }
         };
-        std::vector<std::thread> th;
-        for (uint32_t w = 1; w < S; ++w) th.emplace_back(worker, w);
-        worker(0);
-        for (auto& t : th) t.join();
+        BatchPool::get().run(S, worker);
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+        for (uint32_t i = 0; i < count; ++i) out[i] = runs[i].release();
+    });
+}
+
+int mdg_bz_loop_device_batch(mdg_ctx* const* ctxs, const mdg_gset* const* gs, uint32_t count,
+                             const mdg_config* cfg, uint32_t streams, mdg_run** out) {
+    return guard([&] {
+        if (count && (!ctxs || !gs || !out)) throw std::invalid_argument("null argument");
+        for (uint32_t i = 0; i < count; ++i) {
+            if (!ctxs[i] || !gs[i]) throw std::invalid_argument("null context or Gamma set");
+            for (uint32_t q = 0; q < i; ++q)
+                if (ctxs[q] == ctxs[i]) throw std::invalid_argument("one context per code: contexts must be distinct");
+            out[i] = nullptr;
+        }
+        mdg_config c;
+        mdg_config_default(&c);
+        if (cfg) c = *cfg;
+        const uint32_t S = std::max(1u, std::min(streams ? streams : 4u, std::max(count, 1u)));
+        std::vector<std::unique_ptr<mdg_run>> runs(count);
+        std::vector<std::exception_ptr> errs(S);
+        std::atomic<uint32_t> next{0};
+        const std::function<void(uint32_t)> worker = [&](uint32_t w) {
+            try {
+                for (uint32_t i; (i = next.fetch_add(1)) < count;) {
+                    auto t0 = std::chrono::steady_clock::now();
+                    auto run = std::make_unique<mdg_run>();
+                    run_device_loop(*ctxs[i]->eng, gs[i]->gs, c, 0, 1, nullptr, nullptr, *run);
+                    run->wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                    runs[i] = std::move(run);
+                }
+            } catch (...) {
+                errs[w] = std::current_exception();
+                next.store(count);
+            }
+        };
+        BatchPool::get().run(S, worker);
         for (auto& e : errs)
             if (e) std::rethrow_exception(e);
         for (uint32_t i = 0; i < count; ++i) out[i] = runs[i].release();

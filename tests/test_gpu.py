@@ -611,6 +611,36 @@ def test_min_weight_batch_equals_single(mdg, device, streams):
     assert mdg.min_weight_batch([], 80, device=device) == []
 
 
+def test_bz_loop_batch_equals_single(mdg):
+    """mdg_bz_loop_device_batch: the resident loops of eight config-2 codes (and a mixed set)
+    through the library's worker pool equal the per-code loops; repeated calls reuse the pool."""
+    cases = {c["name"]: c for c in load_golden("configs")}
+    names = [f"cfg2_s{s}" for s in range(1, 9)] + ["cfg1", "cfg3"]
+    devs, gsets = [], []
+    for name in names:
+        g = cases[name]["gen"]
+        G = mdg.gen_matrix(g["n"], g["k"], g["seed"], True)
+        gs = mdg.GammaSet.build(G, g["n"], 10, g["seed"])
+        d = mdg.Device(0)
+        d.load_gset(gs)
+        devs.append(d)
+        gsets.append(gs)
+    try:
+        for streams in (1, 3, 4, 16):
+            for kernel in KERNELS:
+                runs = mdg.bz_loop_batch(devs, gsets, kernel=kernel, streams=streams)
+                for name, r in zip(names, runs):
+                    _check_run(r, cases[name], name, exact=False)
+        single = [d.bz_loop(gs) for d, gs in zip(devs, gsets)]
+        for a, b in zip(single, mdg.bz_loop_batch(devs, gsets)):
+            assert (a.d, a.rounds, a.levels, a.witness_ok) == (b.d, b.rounds, b.levels, b.witness_ok)
+        with pytest.raises(mdg.InvalidArgument):
+            mdg.bz_loop_batch([devs[0], devs[0]], gsets[:2])
+    finally:
+        for d in devs:
+            d.close()
+
+
 def test_pruning_off_same_minima(mdg, device):
     """mdg_set_pruning(0) (every codeword's weight exact) returns the same round minima."""
     for (n, k, seed) in [(128, 64, 1), (300, 200, 11), (256, 32, 7)]:
