@@ -6,8 +6,9 @@ step = the full Brouwer–Zimmermann run to termination (exact d) of all eight
 codes. Metric: codewords evaluated per second (BASELINE.json `metric`).
 
 * value  — N = 1: device-resident: the level loops over Gamma sets already in
-           HBM (mdg_bz_loop_device, one context per code, --streams codes in
-           flight), CUDA events around each whole step (host gaps included);
+           HBM (mdg_bz_loop_device_batch: one context per code, --streams codes
+           in flight from the library's worker threads), CUDA events around each
+           whole step (host gaps included);
            codewords / time. N > 1 (torchrun): the strong leg below is the
            headline ("scaling": "strong"); the eight-code step, run by every rank
            on its own GPU (independent codes, no collective), moves to
@@ -17,8 +18,10 @@ codes. Metric: codewords evaluated per second (BASELINE.json `metric`).
            key min-reduced by an in-stream NCCL allreduce(min)
            (mdg_min_weight_dist); N = 1 is its baseline. Parity
            flags against the reference's cap-6 and cap-7 traces.
-* configs — N = 1: time-to-d of configs 1, 3, 4 (caps 5, 6) and the config-5
-           histograms, each with a parity flag against the reference goldens.
+* configs — N = 1: time-to-d of configs 1, 3, 4 (caps 5, 6), the config-5
+           histograms and the histogram of level 6 of the same matrix (1.19e9
+           codewords: the kernel's steady state), each with a parity flag against
+           the reference goldens.
 * e2e    — the public front door from host matrices (mdg_min_weight_batch over
            the rank's codes): row basis +
            Gamma search on the host, H2D of the Gammas, the device loop, D2H of
