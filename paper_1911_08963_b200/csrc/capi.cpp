@@ -265,7 +265,7 @@ void run_device_loop(Engine& eng, const GammaSet& gs, const mdg_config& cfg, uin
             rr.evaluated = r.evaluated;
             rr.combinations = rs.combinations;
             rr.ms = r.ms;
-            rr.plan_tag = cr.plan_tag;
+            rr.plan_tag = r.plan_tag;
             log.push_back({r.j, r.c, rr});
         }
         er.d = cr.U;

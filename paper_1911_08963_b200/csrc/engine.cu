@@ -1931,8 +1931,12 @@ uint32_t tab_tx() { return kTX; }
 
 static uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
-// RoundResult::plan_tag: bit 0 valid, bit 1 pruning on, bit 2 revolving-door plan
-static uint32_t plan_tag(bool rd, bool prune) { return 1u | (prune ? 2u : 0u) | (rd ? 4u : 0u); }
+// RoundResult::plan_tag: bit 0 valid, bit 1 pruning on, bit 2 revolving-door plan, bits 4..8 the
+// number of rounds m of the fused level the round ran in (0: a launch of its own) -- a fused
+// level plans its tiles for 1/m of the resident blocks per round
+static uint32_t plan_tag(bool rd, bool prune, uint32_t fused_m = 0) {
+    return 1u | (prune ? 2u : 0u) | (rd ? 4u : 0u) | ((fused_m & 31u) << 4);
+}
 
 // saturating Pascal table C(x, t), x <= kMaxK, t <= kMaxC (host and device copies)
 static const std::vector<uint64_t>& binom_table() {
@@ -2532,13 +2536,30 @@ struct Engine::Impl {
         return plan(k, c, g, sms, rd, prune);
     }
     // the tile plan of an explicit variant (a round's witness is decoded with the plan it ran on)
+    // fused_m > 1: the plan of one round of a fused level of m rounds. The level's tile space is
+    // its m rounds' tiles back to back, so each round needs only 1/m of the tiles that keep the
+    // resident blocks busy: larger tiles, fewer tile prologues (config 3, eight Gammas of 32 rows:
+    // TX 16 -> 128 at level 9)
     const PlanEntry& plan(uint32_t k, uint32_t c, const GammaDev& g, int sms, bool rd, bool prune,
-                          uint32_t tpb = 0, int resident_override = 0) {
-        auto key = std::make_tuple(k, c, g.nw, g.hid, rd, prune, tpb);
+                          uint32_t tpb = 0, int resident_override = 0, uint32_t fused_m = 0) {
+        if (fused_m < 2) fused_m = 0;
+        auto key = std::make_tuple(k, c, g.nw, g.hid, rd, prune, tpb | (fused_m << 24));
         auto it = plans.find(key);
         if (it != plans.end()) return it->second;
         PlanEntry pe;
-        const int res = resident_override ? resident_override : resident(g.nw, g.hid, sms);
+        int res = resident_override ? resident_override : resident(g.nw, g.hid, sms);
+        if (fused_m) {
+            // tiles per resident block over the whole level (the plan aims for 2 per round): 2 for
+            // two or three rounds, 4 from four rounds on -- measured (profiles/r02j_fused_tiles.txt):
+            // the eight-code config-2 step (m = 2) 2.02 -> 1.99 ms at 2 (2.02 at 4), config 3
+            // (m = 8, exact weights, tiles of very different lengths) 0.65 -> 0.62 ms at 4 (0.74 at 2)
+            static const int kFusedTiles = [] {
+                const char* e = std::getenv("MDG_FUSED_TILES");
+                return e ? std::max(1, std::atoi(e)) : 0;
+            }();
+            const int tiles = kFusedTiles ? kFusedTiles : (fused_m >= 4 ? 4 : 2);
+            res = std::max(1, res * tiles / (2 * int(fused_m)));
+        }
         pe.plan = make_tab_plan(k, c, g.nw, uint32_t(res), rd, tpb ? tpb : (prune ? 0u : 8u));
         const size_t pb = pe.plan.prefix.size() * 8, tb = pe.plan.tr.size();
         pe.d_prefix = static_cast<uint64_t*>(plan_arena.alloc(pb + tb));
@@ -3221,7 +3242,8 @@ std::vector<uint32_t> Engine::witness(uint32_t j, uint32_t c, const RoundResult&
     // whatever kernel / pruning setting is current: the plans differ
     const bool tagged = (rr.plan_tag & 1u) != 0;
     const PlanEntry& pe = im.plan(k_, c, g, plan_sms_, tagged ? (rr.plan_tag & 4u) != 0 : im.rd,
-                                  tagged ? (rr.plan_tag & 2u) != 0 : im.prune);
+                                  tagged ? (rr.plan_tag & 2u) != 0 : im.prune, 0, 0,
+                                  tagged ? (rr.plan_tag >> 4) & 31u : 0u);
     if (task >= pe.plan.tiles()) throw std::invalid_argument("witness: key names no task of this round");
     if (pos) { // the kernel named the position: smem-side index << 11 | register-side index
         const uint32_t p = uint32_t(rr.key & ((1u << kPosBits) - 1));
@@ -3343,6 +3365,8 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
     }
     uint32_t g = 1;
     bool done = init.done != 0;
+    std::vector<uint32_t> rec_tag; // per enqueued round: the plan it runs on (plan_tag)
+    static const bool fuse_tiles = std::getenv("MDG_NO_FUSED_TILES") == nullptr; // A/B switch
     uint64_t after_round = ~0ull; // launch count right after the last round launch
     bool synced = false;          // a host copy was enqueued since that launch
     // NVTX: one range per level's host enqueue (header-only NVTX3: no-ops unless a profiler
@@ -3404,7 +3428,9 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
             fuse_level = im.gammas[j].nw == im.gammas[0].nw && im.gammas[j].hid == im.gammas[0].hid;
         if (fuse_level) {
             const GammaDev& g0 = im.gammas[0];
-            const PlanEntry& pe = im.plan(k_, g, g0, plan_sms_);
+            const uint32_t fm = fuse_tiles ? m_ : 0u;
+            const PlanEntry& pe = im.plan(k_, g, g0, plan_sms_, im.rd, im.prune, 0, 0, fm);
+            for (uint32_t j = 0; j < m_; ++j) rec_tag.push_back(plan_tag(im.rd, im.prune, fm));
 #ifndef MDG_NO_SLOT_RESERVE // (test builds only: reproduces the round-2 ring hazard)
             im.reserve_slots(int(m_) + 1); // the m rounds' slots + the scheduler's: one ring cycle
 #endif
@@ -3516,6 +3542,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
                 im.cnt.launches += 1;
             }
             ++nrec;
+            rec_tag.push_back(plan_tag(im.rd, im.prune));
             pending += double(binomial(k_, g)) / (split ? world : 1);
         }
         ++g;
@@ -3558,7 +3585,7 @@ Engine::ChainResult Engine::chain_loop(uint32_t U0, uint32_t L0, uint32_t level_
         prev = r.t_ns;
         if (!r.ran) continue;
         res.rounds.push_back({r.c, r.j, r.w, r.U_after, r.bounded, r.L_after, r.level_end, r.key,
-                              r.evaluated, ms});
+                              r.evaluated, ms, rec_tag[i]});
     }
     return res;
 }

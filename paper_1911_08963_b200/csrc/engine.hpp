@@ -127,6 +127,7 @@ public:
         uint32_t c, j, w, U_after, bounded, L_after, level_end;
         uint64_t key, evaluated;
         double ms;
+        uint32_t plan_tag; // the tile plan this round ran on (a fused level's rounds use larger tiles)
     };
     struct ChainResult {
         uint32_t U = 0, L = 0;
